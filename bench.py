@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the Burger permutation-map hot path on B200.
+
+Metric (BASELINE.json): "state entries/sec and achieved HBM GB/s (fraction of
+8 TB/s) for map+gather at M=32".  Workload: config 5 (M = 32, 64 random
+NOT/CNOT/CCNOT gates, seed 4, complex64 Gaussian normalised state).
+
+One step = the whole hot path over the 2^32-entry state: qsim_build_map
+(materialise perm, uint32) then qsim_apply_map (k2[i] = k1[perm[i]]).  The
+fused mode (qsim_run_fused: the map recomputed in registers, no perm) is
+timed in its own loop and reported under "modes".  Inputs are larger than L2
+(80 GiB working set vs 126 MB L2), so no flush is needed between steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
+    python bench.py --impl reference      # the oracle, timed on host cores
+
+With torchrun (N > 1) every rank runs its own replica of the workload on its
+own GPU (no data-path collective; "scaling": "weak"); timing is the max over
+ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "state entries/sec and achieved HBM GB/s (fraction of 8 TB/s) for map+gather at M=32"
+FALLBACK_HBM_GBS = 6650.0       # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qsim", choices=["qsim", "reference"])
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-log2", type=int, default=28,
+                    help="outputs in the oracle's bounded sample (log2)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str, kernel: str):
+    """dram read+write bytes per launch from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config, {}).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self._stop = [], 0, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        rs = [n for b, n in self.REASONS.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": rs, "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------ cpu baseline
+def cpu_oracle_rate(gates, k1_host: np.ndarray, start: int, count: int, threads: int):
+    """The oracle as it stands (build then apply, single-threaded C) over the
+    output portion [start, start+count), split across `threads` host threads
+    on disjoint sub-ranges (ctypes releases the GIL).  Returns (entries/s, s)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+
+    per = (count + threads - 1) // threads
+    out = np.empty(count, dtype=k1_host.dtype)
+
+    def work(t):
+        a = start + t * per
+        b = min(start + count, a + per)
+        if a >= b:
+            return
+        perm = oracle.build_map(gates, k1_host.shape[0].bit_length() - 1, a, b - a)
+        out[a - start:b - start] = oracle.apply_map(perm, k1_host)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(work, range(threads)))
+    dt = time.perf_counter() - t0
+    return count / dt, dt
+
+
+# ----------------------------------------------------------------- main arm
+def run_qsim(args):
+    import torch
+    import paper_quant_ph_0308158_b200 as q
+    import workloads as wl
+
+    world, rank, local = dist_setup()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    cfg = wl.CONFIGS[args.config]
+    gates, M, N = cfg.gates(), cfg.M, cfg.N
+    e = 8 if cfg.dtype == "c64" else 16
+    stream = torch.cuda.Stream(dev)
+
+    # ---- inputs: seeded on the host (pinned), copied once to HBM
+    t_setup = time.perf_counter()
+    k1_host = torch.empty(N * e, dtype=torch.uint8, pin_memory=True)
+    wl.fill_state(cfg.state, k1_host.data_ptr())
+    k1 = torch.empty(N * e, dtype=torch.uint8, device=dev)
+    k1.copy_(k1_host, non_blocking=True)
+    perm = torch.empty(N, dtype=torch.int32, device=dev)
+    k2 = torch.empty(N * e, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    t_setup = time.perf_counter() - t_setup
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def timed_loop(step_fn, steps, warmup, per_kernel=None):
+        for _ in range(warmup):
+            step_fn(None)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        marks = [] if per_kernel else None
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        launches = 0
+        with torch.cuda.stream(stream):
+            t0.record(stream)
+            for _ in range(steps):
+                launches += step_fn(marks)
+            t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        kern = {}
+        if marks:
+            for name, a, b in marks:
+                kern.setdefault(name, []).append(a.elapsed_time(b))
+        return ms, launches, kern
+
+    def ev():
+        x = torch.cuda.Event(enable_timing=True)
+        x.record(stream)
+        return x
+
+    def step_materialised(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.build_map(gates, M, perm, stream=stream)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            q.apply_map(perm, M, k1, k2, stream=stream, dtype=cfg.dtype)
+            n += q.last_launch_count()
+            c = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("build_map", a, b))
+                marks.append(("apply_map", b, c))
+        return n
+
+    def step_fused(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.run_fused(gates, M, k1, k2, stream=stream, dtype=cfg.dtype)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("run_fused", a, b))
+        return n
+
+    sampler = ClockSampler(local)
+    with sampler:
+        ms_mat, launches_mat, kern_mat = timed_loop(step_materialised, args.steps, args.warmup,
+                                                    per_kernel=True)
+        ms_fused, launches_fused, kern_fused = timed_loop(step_fused, args.steps, args.warmup,
+                                                          per_kernel=True)
+    clocks = sampler.summary()
+
+    # ---- end to end through the C ABI from pinned host buffers
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        k2_host = torch.empty(N * e, dtype=torch.uint8, pin_memory=True)
+        for _ in range(1):
+            q.run_host(gates, M, q.MATERIALISED, k1_host, k2_host, k1, k2, perm,
+                       stream=stream, dtype=cfg.dtype)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            q.run_host(gates, M, q.MATERIALISED, k1_host, k2_host, k1, k2, perm,
+                       stream=stream, dtype=cfg.dtype)
+        dt = time.perf_counter() - t0
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([dt], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e = {"value": world * N * args.e2e_steps / dt, "unit": "entries/s",
+               "h2d_bytes_per_step": N * e, "d2h_bytes_per_step": N * e,
+               "ms_per_step": 1e3 * dt / args.e2e_steps,
+               "path": "qsim_run_host: H2D k1 (pinned), build_map, apply_map, D2H k2, sync"}
+        del k2_host
+
+    # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import workloads as wl2
+        k1_np = k1_host.numpy().view(wl2.NP_DTYPE[cfg.dtype])
+        threads = os.cpu_count() or 1
+        count = min(N, 1 << args.cpu_sample_log2)
+        rate, dt = cpu_oracle_rate(gates, k1_np, 0, count, threads)
+        cpu = {"value": rate, "unit": "entries/s", "cores": threads, "kind": "oracle",
+               "seconds": dt,
+               "sample": f"output entries [0, 2^{args.cpu_sample_log2}) of {args.config} "
+                         f"(build_map walk + apply gather, oracle C -O2, one thread per core "
+                         f"on disjoint sub-ranges)"}
+
+    if rank != 0:
+        return
+    hbm, hbm_src = peaks()
+    bytes_apply = N * (4 + 2 * e)          # read perm, gather k1, write k2
+    bytes_build = N * 4
+    bytes_fused = N * 2 * e
+    apply_ms = statistics.mean(kern_mat["apply_map"])
+    build_ms = statistics.mean(kern_mat["build_map"])
+    fused_ms = statistics.mean(kern_fused["run_fused"])
+    ms_step = ms_mat / args.steps
+    achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": world * N / (ms_step * 1e-3),
+        "unit": "entries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32",
+        "data": "synthetic (seeded counter-based Gaussian state, numpy PCG64 gate list)",
+        "config": {"workload": f"{args.config}: {cfg.description}", "M": M,
+                   "n_gates": int(gates.shape[0]), "state_dtype": "complex64" if e == 8 else
+                   "complex128", "step": "build_map + apply_map (materialised map+gather)",
+                   "l2": "inputs larger than L2 (k1, k2 %d GiB each; perm %d GiB)"
+                   % (N * e >> 30, N * 4 >> 30), "parallelism": f"replicas x{world}"},
+        "achieved_GBps": (bytes_build + bytes_apply) / (ms_step * 1e-3) / 1e9,
+        "frac_of_8TBps": (bytes_build + bytes_apply) / (ms_step * 1e-3) / 8e12,
+        "roofline": {"bound": "hbm", "kernel": "apply_map (k_apply)", "achieved": achieved,
+                     "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
+                     "frac": achieved / hbm, "frac_of_8TBps": achieved * 1e9 / 8e12,
+                     "traffic": ncu_traffic(args.config, "apply_map"),
+                     "algorithmic_bytes_per_launch": bytes_apply},
+        "modes": {
+            "build_map": {"ms": build_ms, "GBps": bytes_build / (build_ms * 1e-3) / 1e9,
+                          "entries_per_s": N / (build_ms * 1e-3), "bound": "alu/hbm"},
+            "apply_map": {"ms": apply_ms, "GBps": achieved, "entries_per_s": N / (apply_ms * 1e-3)},
+            "run_fused": {"ms": fused_ms, "GBps": bytes_fused / (fused_ms * 1e-3) / 1e9,
+                          "entries_per_s": N / (fused_ms * 1e-3),
+                          "frac_of_peak": bytes_fused / (fused_ms * 1e-3) / 1e9 / hbm},
+        },
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches_mat,
+        "gpu_launches_fused_loop": launches_fused,
+        "clocks": clocks,
+        "setup_s": t_setup,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The oracle (this tier's reference arm), timed on the host cores."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    import workloads as wl
+    cfg = wl.CONFIGS[args.config]
+    gates, N = cfg.gates(), cfg.N
+    k1 = np.empty(N, dtype=wl.NP_DTYPE[cfg.dtype])
+    wl.fill_state(cfg.state, k1.ctypes.data)
+    threads = os.cpu_count() or 1
+    count = min(N, 1 << 26)           # bounded sample per step
+    for _ in range(args.warmup):
+        cpu_oracle_rate(gates, k1, 0, min(count, 1 << 20), threads)
+    times = []
+    for s in range(args.steps):
+        start = (s * count) % N
+        _, dt = cpu_oracle_rate(gates, k1, start, count, threads)
+        times.append(dt)
+    ms = 1e3 * statistics.mean(times)
+    value = count / (ms * 1e-3)
+    sample = (f"each step: {count} consecutive outputs of {args.config} (of 2^{cfg.M}); "
+              f"oracle build walk + apply gather, one thread per core")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic", "config": {"workload": f"{args.config}: {cfg.description}",
+                                              "M": cfg.M, "n_gates": int(gates.shape[0])},
+            "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads,
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_qsim(a)

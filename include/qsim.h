@@ -1,0 +1,160 @@
+/*
+ * qsim.h -- C ABI of libqsim.so, the B200 (sm_100a) hot path of Burger,
+ * "New approaches to quantum computer simulation in a classical
+ * supercomputer" (arXiv quant-ph/0308158).
+ *
+ * Citations: "P:Lnn" = PAPER.md line nn (section); R-numbers are the
+ * readings of silent / garbled passages listed in DESIGN.md.
+ *
+ * The method:
+ *   - address bits a(M) ... a(1) index the 2^M entries of the state vector,
+ *     a(1) the LSB (P:L43 2(b)); here bit b (0-based) is a(b+1) (R3);
+ *   - each wiring-diagram step is a 0/1 matrix, symmetric, with one unity
+ *     per row: step k maps address x to f_k(x) = x with its target
+ *     bit toggled when all its control bits are 1 ("011 to 010"),
+ *     for NOT (0 controls), CNOT (1) and CCNOT / Toffoli (2) (R4, R5);
+ *   - the composite is U = U_n ... U_1, Step 1 (gates[0]) first (R1); row i
+ *     of U has its unity in column perm[i] = f_1(f_2(...f_n(i)...)) (R2);
+ *   - the state transform k2 = U k1 is k2[i] = k1[perm[i]],
+ *     computed "from top to bottom ... without special sorting".
+ *
+ * Conventions common to every call
+ *   - Status: every call returns QSIM_OK (0) or a negative qsim_status.
+ *     Arguments are validated completely BEFORE anything is enqueued, so an
+ *     error return means nothing ran.  QSIM_ECUDA means a CUDA API call
+ *     failed; qsim_last_error() gives the message (thread-local).
+ *   - Asynchrony: device work is enqueued on `stream` (a cudaStream_t; NULL
+ *     = legacy default stream) and the call returns without synchronising,
+ *     except qsim_run_host (see there).  Faults inside kernels surface at
+ *     the caller's next synchronisation.
+ *   - Ownership: all buffers are caller-owned.  The library allocates no
+ *     device memory.  `gates` is a host array read during the call (copied
+ *     into the launch's kernel-parameter bank); it may be freed on return.
+ *   - Device pointers (perm, k1, k2) must be 16-byte aligned
+ *     (QSIM_EINVAL otherwise) and must not overlap each other
+ *     (QSIM_EALIAS); all calls are out-of-place.
+ *   - Thread safety: reentrant; concurrent calls on different streams are
+ *     safe (no mutable module-scope device state).
+ */
+#ifndef QSIM_H
+#define QSIM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* One wiring-diagram step.  kind: 0 NOT, 1 CNOT, 2 CCNOT.
+ * target: 0-based bit b, i.e. address bit a(b+1).  c0 (CNOT, CCNOT) and
+ * c1 (CCNOT) are the control bits; slots a kind does not use are ignored.
+ * Valid: target < M, used controls < M, distinct from the target and from
+ * each other.                                                              */
+typedef struct qsim_gate {
+    uint8_t kind;
+    uint8_t target;
+    uint8_t c0;
+    uint8_t c1;
+} qsim_gate;
+
+typedef enum qsim_status {
+    QSIM_OK     = 0,
+    QSIM_EINVAL = -1, /* null / misaligned pointer, bad dtype / mode / kind */
+    QSIM_ERANGE = -2, /* M not in [1, 32], or range [start, start+count) not inside [0, 2^M) */
+    QSIM_EBIT   = -3, /* a bit >= M, target among controls, duplicate control */
+    QSIM_ECAP   = -4, /* n_gates < 0 or > QSIM_MAX_GATES */
+    QSIM_EALIAS = -5, /* device buffers overlap */
+    QSIM_ECUDA  = -6  /* a CUDA call failed; see qsim_last_error() */
+} qsim_status;
+
+typedef enum qsim_dtype {
+    QSIM_C64  = 0, /* complex64: 8 bytes per entry (2 x float32)  */
+    QSIM_C128 = 1  /* complex128: 16 bytes per entry (2 x float64) */
+} qsim_dtype;
+
+/* Largest gate list one launch accepts (the kernel-parameter bank holds
+ * 4 bytes per gate, <= 32 KB).                                             */
+#define QSIM_MAX_GATES 4096
+
+/* qsim_build_map -- materialise the composite ("save information
+ * about the unitary matrix"): perm[i] = f_1(...f_n(i)) for all i < 2^M.
+ *   gates   host, n_gates records (may be NULL when n_gates == 0: identity)
+ *   M       number of address bits, 1..32
+ *   perm    device, 2^M uint32 entries (written)                          */
+int qsim_build_map(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                   uint32_t *perm, void *stream);
+
+/* Same, for the "continuous portion" [start, start+count):
+ * perm_out[r] = perm[start + r].  count may be 0.                          */
+int qsim_build_map_range(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                         uint64_t start, uint64_t count, uint32_t *perm_out,
+                         void *stream);
+
+/* qsim_apply_map -- the state transform k2 = U k1 given the
+ * materialised map: k2[i] = k1[perm[i]] for all i < 2^M.  Entries are
+ * moved as raw bytes (bit-exact; -0.0 and NaN payloads preserved).
+ *   perm   device, 2^M uint32 (each < 2^M; a permutation if built above)
+ *   dtype  QSIM_C64 or QSIM_C128
+ *   k1     device, 2^M entries (read)     k2  device, 2^M entries (written)*/
+int qsim_apply_map(const uint32_t *perm, int32_t M, int32_t dtype,
+                   const void *k1, void *k2, void *stream);
+
+/* Range form: k2_out[r] = k1[perm_in[r]] for r < count; k1 holds all 2^M
+ * entries.  perm_in is typically perm + start of a full map.              */
+int qsim_apply_map_range(const uint32_t *perm_in, uint64_t count, int32_t M,
+                         int32_t dtype, const void *k1, void *k2_out,
+                         void *stream);
+
+/* qsim_run_fused -- k2[i] = k1[f_1(...f_n(i))] without storing the map:
+ * the memory-for-processing trade-off.  Same arguments as
+ * build + apply; no perm buffer.                                           */
+int qsim_run_fused(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                   int32_t dtype, const void *k1, void *k2, void *stream);
+
+/* Range form: k2_out[r] = k1[perm[start + r]], r < count.                 */
+int qsim_run_fused_range(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                         int32_t dtype, uint64_t start, uint64_t count,
+                         const void *k1, void *k2_out, void *stream);
+
+/* Walk algorithm selection for build / fused (ablation and tests).
+ *   QSIM_WALK_AUTO       library choice (bit-sliced)
+ *   QSIM_WALK_PER_LANE   one address per lane, 2 integer ops per gate
+ *   QSIM_WALK_BITSLICED  32 addresses per thread, one bit-plane word per
+ *                        address bit in shared memory, one logic op per gate */
+typedef enum qsim_walk {
+    QSIM_WALK_AUTO = 0,
+    QSIM_WALK_PER_LANE = 1,
+    QSIM_WALK_BITSLICED = 2
+} qsim_walk;
+
+int qsim_build_map_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                      uint64_t start, uint64_t count, uint32_t *perm_out,
+                      int32_t walk, void *stream);
+int qsim_run_fused_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                      int32_t dtype, uint64_t start, uint64_t count,
+                      const void *k1, void *k2_out, int32_t walk, void *stream);
+
+/* qsim_run_host -- the whole path from HOST buffers (end-to-end use):
+ * copies k1_host -> k1_dev, computes k2 (mode 0: build perm_dev, then
+ * apply; mode 1: fused, perm_dev unused and may be NULL), copies
+ * k2_dev -> k2_host, and SYNCHRONISES `stream` before returning.
+ *   k1_host, k2_host  host, 2^M entries each (pinned memory recommended)
+ *   k1_dev, k2_dev    device workspaces, 2^M entries each
+ *   perm_dev          device workspace, 2^M uint32 (mode 0)               */
+int qsim_run_host(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                  int32_t dtype, int32_t mode, const void *k1_host,
+                  void *k2_host, void *k1_dev, void *k2_dev,
+                  uint32_t *perm_dev, void *stream);
+
+/* Number of kernel launches the last successful call on this thread
+ * enqueued (for launch accounting in bench.py).                            */
+int32_t qsim_last_launch_count(void);
+
+const char *qsim_strerror(int32_t code);
+const char *qsim_last_error(void);
+int32_t qsim_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSIM_H */

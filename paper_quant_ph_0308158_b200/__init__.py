@@ -1,0 +1,176 @@
+"""B200-native hot path of Burger's permutation-map quantum-circuit simulator
+(arXiv quant-ph/0308158).
+
+A thin ctypes binding over ``libqsim.so`` (C ABI in ``include/qsim.h``):
+argument marshalling only -- every step of the path (the address walk and the
+gather) runs in the sm_100a kernels under ``csrc/``.  PyTorch supplies device
+memory and streams.  There is no CPU fallback: if the library is missing the
+import fails.
+
+    import paper_quant_ph_0308158_b200 as qsim
+    qsim.build_map(gates, M, perm)            # perm[i] = f_1(...f_n(i))
+    qsim.apply_map(perm, M, k1, k2)           # k2[i] = k1[perm[i]]
+    qsim.run_fused(gates, M, k1, k2)          # same k2, no perm buffer
+
+``gates`` is a uint8 array of shape (n, 4): (kind, target, c0, c1), kind
+0 NOT / 1 CNOT / 2 CCNOT, 0-based bits (bit b = a(b+1), a(1) the LSB),
+row 0 = Step 1 (applied first).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libqsim.so")
+
+OK, EINVAL, ERANGE, EBIT, ECAP, EALIAS, ECUDA = 0, -1, -2, -3, -4, -5, -6
+C64, C128 = 0, 1
+WALK_AUTO, WALK_PER_LANE, WALK_BITSLICED = 0, 1, 2
+MAX_GATES = 4096
+MATERIALISED, FUSED = 0, 1
+
+
+class QsimError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        lib = _lib
+        msg = lib.qsim_strerror(code).decode()
+        if code == ECUDA:
+            msg += ": " + lib.qsim_last_error().decode()
+        super().__init__(f"{where}: {msg} (status {code})")
+        self.code = code
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a). There is no CPU fallback.")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, u64, i32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int32
+    sig = {
+        "qsim_build_map": [vp, i32, i32, vp, vp],
+        "qsim_build_map_range": [vp, i32, i32, u64, u64, vp, vp],
+        "qsim_build_map_ex": [vp, i32, i32, u64, u64, vp, i32, vp],
+        "qsim_apply_map": [vp, i32, i32, vp, vp, vp],
+        "qsim_apply_map_range": [vp, u64, i32, i32, vp, vp, vp],
+        "qsim_run_fused": [vp, i32, i32, i32, vp, vp, vp],
+        "qsim_run_fused_range": [vp, i32, i32, i32, u64, u64, vp, vp, vp],
+        "qsim_run_fused_ex": [vp, i32, i32, i32, u64, u64, vp, vp, i32, vp],
+        "qsim_run_host": [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.qsim_strerror.argtypes = [i32]
+    lib.qsim_strerror.restype = ctypes.c_char_p
+    lib.qsim_last_error.argtypes = []
+    lib.qsim_last_error.restype = ctypes.c_char_p
+    lib.qsim_abi_version.restype = i32
+    lib.qsim_last_launch_count.restype = i32
+    return lib
+
+
+_lib = _load()
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+# ------------------------------------------------------------------ marshalling
+def _gates(gates):
+    g = np.ascontiguousarray(np.asarray(gates, dtype=np.uint8).reshape(-1, 4))
+    return g, (g.ctypes.data if g.shape[0] else None), int(g.shape[0])
+
+
+def _ptr(x) -> int | None:
+    """Device or host address of a torch tensor / numpy array / int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()                     # torch.Tensor
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dtype_code(x) -> int:
+    if isinstance(x, int):
+        return x
+    s = str(getattr(x, "dtype", x))
+    if "complex64" in s or s == "c64":
+        return C64
+    if "complex128" in s or s == "c128":
+        return C128
+    raise TypeError(f"state dtype must be complex64 or complex128, got {s}")
+
+
+def _check(rc: int, where: str) -> None:
+    if rc != OK:
+        raise QsimError(rc, where)
+
+
+# ---------------------------------------------------------------------- calls
+def build_map(gates, M: int, perm, stream=None) -> None:
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_build_map(gp, n, M, _ptr(perm), _stream(stream)), "qsim_build_map")
+
+
+def build_map_range(gates, M: int, start: int, count: int, perm_out, stream=None,
+                    walk: int = WALK_AUTO) -> None:
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_build_map_ex(gp, n, M, start, count, _ptr(perm_out), walk,
+                                  _stream(stream)), "qsim_build_map_ex")
+
+
+def apply_map(perm, M: int, k1, k2, stream=None, dtype=None) -> None:
+    code = _dtype_code(k1 if dtype is None else dtype)
+    _check(_lib.qsim_apply_map(_ptr(perm), M, code, _ptr(k1), _ptr(k2), _stream(stream)),
+           "qsim_apply_map")
+
+
+def apply_map_range(perm_in, count: int, M: int, k1, k2_out, stream=None, dtype=None) -> None:
+    code = _dtype_code(k1 if dtype is None else dtype)
+    _check(_lib.qsim_apply_map_range(_ptr(perm_in), count, M, code, _ptr(k1), _ptr(k2_out),
+                                     _stream(stream)), "qsim_apply_map_range")
+
+
+def run_fused(gates, M: int, k1, k2, stream=None, dtype=None) -> None:
+    g, gp, n = _gates(gates)
+    code = _dtype_code(k1 if dtype is None else dtype)
+    _check(_lib.qsim_run_fused(gp, n, M, code, _ptr(k1), _ptr(k2), _stream(stream)),
+           "qsim_run_fused")
+
+
+def run_fused_range(gates, M: int, start: int, count: int, k1, k2_out, stream=None,
+                    dtype=None, walk: int = WALK_AUTO) -> None:
+    g, gp, n = _gates(gates)
+    code = _dtype_code(k1 if dtype is None else dtype)
+    _check(_lib.qsim_run_fused_ex(gp, n, M, code, start, count, _ptr(k1), _ptr(k2_out), walk,
+                                  _stream(stream)), "qsim_run_fused_ex")
+
+
+def run_host(gates, M: int, mode: int, k1_host, k2_host, k1_dev, k2_dev, perm_dev=None,
+             stream=None, dtype=None) -> None:
+    """End to end from host buffers; returns after the stream is synchronised."""
+    g, gp, n = _gates(gates)
+    code = _dtype_code(k1_host if dtype is None else dtype)
+    _check(_lib.qsim_run_host(gp, n, M, code, mode, _ptr(k1_host), _ptr(k2_host), _ptr(k1_dev),
+                              _ptr(k2_dev), _ptr(perm_dev), _stream(stream)), "qsim_run_host")
+
+
+def last_launch_count() -> int:
+    return int(_lib.qsim_last_launch_count())

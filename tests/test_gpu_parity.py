@@ -1,0 +1,329 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle.
+
+Bit-exact throughout (pure index arithmetic and data movement; DESIGN.md
+"Parity bar").  Entries are compared as raw bytes / integer views, never as
+floats (R15).
+
+* small and medium sizes: every output compared with the oracle, both walk
+  algorithms, complex64 and complex128, ragged ranges, edge cases;
+* BASELINE.json configs: cfg1/cfg2 in full; cfg3/cfg4/cfg5 at full size in
+  the launch configuration bench.py uses, on sampled outputs the oracle
+  computes one by one, plus properties that hold at any size.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def q():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_native()
+    import paper_quant_ph_0308158_b200 as q
+    return q
+
+
+DEV = "cuda:0"
+WALKS = [1, 2]   # WALK_PER_LANE, WALK_BITSLICED
+
+
+def _to_dev(a: np.ndarray):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8)).to(DEV)
+
+
+def _perm_np(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _new_perm(count):
+    return torch.empty(max(count, 1), dtype=torch.int32, device=DEV)
+
+
+def _new_state(count, dtype):
+    return torch.empty(max(count, 1) * (8 if dtype == "c64" else 16), dtype=torch.uint8,
+                       device=DEV)
+
+
+# ------------------------------------------------------------- full compares
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 9, 10, 11, 13, 16])
+@pytest.mark.parametrize("walk", WALKS)
+def test_build_full_small(q, M, walk):
+    for seed, n in ((M, 0), (M + 1, 1), (M + 2, 37), (M + 3, 300)):
+        if M >= 3:
+            gates = wl.random_gates(n, M, seed)
+        else:
+            gates = wl.gates_array([wl.gate(wl.NOT, s % M) if M == 1 or s % 2
+                                    else wl.gate(wl.CNOT, s % 2, 1 - s % 2) for s in range(n)])
+        N = 1 << M
+        perm = _new_perm(N)
+        q.build_map_range(gates, M, 0, N, perm, walk=walk)
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(perm)[:N], oracle.build_map(gates, M)), (M, n, walk)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("M", [4, 12, 17])
+def test_apply_and_fused_full(q, M, dtype):
+    gates = wl.random_gates(64, M, 10 + M)
+    k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, M))
+    ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+    k1_d = _to_dev(k1)
+    perm = _new_perm(1 << M)
+    q.build_map(gates, M, perm)
+    k2 = torch.empty_like(k1_d)
+    q.apply_map(perm, M, k1_d, k2, dtype=dtype)
+    torch.cuda.synchronize()
+    assert k2.cpu().numpy().tobytes() == ref.tobytes()
+    for walk in WALKS:
+        k2f = torch.empty_like(k1_d)
+        q.run_fused_range(gates, M, 0, 1 << M, k1_d, k2f, dtype=dtype, walk=walk)
+        torch.cuda.synchronize()
+        assert k2f.cpu().numpy().tobytes() == ref.tobytes(), walk
+
+
+@pytest.mark.parametrize("walk", WALKS)
+def test_ragged_ranges(q, walk):
+    """Continuous portions with starts/ends off the 1024-entry tiles."""
+    M = 15
+    gates = wl.random_gates(90, M, 3)
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 4))
+    k1_d = _to_dev(k1)
+    perm_all = oracle.build_map(gates, M)
+    for start, count in ((0, 1), (1, 1), (5, 1023), (1023, 2), (1000, 3000), (4096, 4096),
+                         ((1 << M) - 7, 7), (123, 0), (0, 1 << M)):
+        pr = _new_perm(count)
+        q.build_map_range(gates, M, start, count, pr, walk=walk)
+        k2r = _new_state(count, "c64")
+        q.run_fused_range(gates, M, start, count, k1_d, k2r, dtype="c64", walk=walk)
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(pr)[:count], perm_all[start:start + count])
+        want = oracle.run_fused(gates, k1, start, count)
+        assert k2r.cpu().numpy()[:count * 8].tobytes() == want.tobytes()
+
+
+def test_apply_ragged_counts(q):
+    M = 12
+    k1 = wl.make_state(wl.StateSpec(M, "c128", wl.GAUSS, 8))
+    k1_d = _to_dev(k1)
+    perm = oracle.build_map(wl.random_gates(50, M, 8), M)
+    for count in (0, 1, 3, 4, 5, 1021, 4096):
+        p_d = torch.from_numpy(perm[:max(count, 1)].view(np.int32).copy()).to(DEV)
+        k2 = _new_state(count, "c128")
+        q.apply_map_range(p_d, count, M, k1_d, k2, dtype="c128")
+        torch.cuda.synchronize()
+        assert k2.cpu().numpy()[:count * 16].tobytes() == oracle.apply_map(perm[:count], k1).tobytes()
+
+
+def test_special_values_survive(q):
+    """-0.0, NaN payloads, denormals, inf: moved as bits (R15)."""
+    M = 11
+    N = 1 << M
+    k1 = wl.tagged_state("c64", N)
+    bits = k1.view(np.uint32).reshape(-1, 2)
+    bits[:8, 0] = [0x80000000, 0x7fc00001, 0xffc12345, 0x00000001, 0x7f800000, 0xff800000,
+                   0x7fbfffff, 0x80000001]
+    gates = wl.random_gates(33, M, 21)
+    ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+    k1_d = _to_dev(k1)
+    k2 = torch.empty_like(k1_d)
+    q.run_fused(gates, M, k1_d, k2, dtype="c64")
+    torch.cuda.synchronize()
+    assert k2.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_max_gates_and_capacity_buckets(q):
+    M = 14
+    for n in (63, 64, 65, 256, 257, 1024, 1025, q.MAX_GATES):
+        gates = wl.random_gates(n, M, n)
+        perm = _new_perm(1 << M)
+        q.build_map(gates, M, perm)
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(perm), oracle.build_map(gates, M)), n
+
+
+def test_determinism_and_streams(q):
+    M = 18
+    gates = wl.random_gates(64, M, 2)
+    outs = []
+    for i in range(3):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            p = _new_perm(1 << M)
+            q.build_map(gates, M, p, stream=s)
+        s.synchronize()
+        outs.append(_perm_np(p).copy())
+    assert all(np.array_equal(outs[0], o) for o in outs)
+
+
+# -------------------------------------------------------- BASELINE configs
+def test_cfg1_full(q):
+    cfg = wl.CONFIGS["cfg1"]
+    gates, k1 = cfg.gates(), wl.make_state(cfg.state)
+    perm_ref = oracle.build_map(gates, cfg.M)
+    assert perm_ref.tolist() == [0, 1, 7, 6, 4, 2, 3, 5]       # tests/golden/cfg1_perm.txt
+    k1_d = _to_dev(k1)
+    perm = _new_perm(8)
+    q.build_map(gates, cfg.M, perm)
+    k2, k2f = torch.empty_like(k1_d), torch.empty_like(k1_d)
+    q.apply_map(perm, cfg.M, k1_d, k2, dtype="c64")
+    q.run_fused(gates, cfg.M, k1_d, k2f, dtype="c64")
+    torch.cuda.synchronize()
+    ref = oracle.apply_map(perm_ref, k1)
+    assert np.array_equal(_perm_np(perm), perm_ref)
+    assert k2.cpu().numpy().tobytes() == ref.tobytes() == k2f.cpu().numpy().tobytes()
+
+
+def test_cfg2_full(q):
+    cfg = wl.CONFIGS["cfg2"]
+    gates, k1 = cfg.gates(), wl.make_state(cfg.state)
+    perm_ref = oracle.build_map(gates, cfg.M)
+    ref = oracle.apply_map(perm_ref, k1)
+    assert oracle.accumulate(gates, k1).tobytes() == ref.tobytes()
+    k1_d = _to_dev(k1)
+    perm = _new_perm(cfg.N)
+    q.build_map(gates, cfg.M, perm)
+    k2, k2f = torch.empty_like(k1_d), torch.empty_like(k1_d)
+    q.apply_map(perm, cfg.M, k1_d, k2, dtype="c64")
+    q.run_fused(gates, cfg.M, k1_d, k2f, dtype="c64")
+    torch.cuda.synchronize()
+    assert np.array_equal(_perm_np(perm), perm_ref)
+    assert k2.cpu().numpy().tobytes() == ref.tobytes()
+    assert k2f.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def _sample_indices(M, n=1 << 15, seed=0):
+    N = 1 << M
+    rng = np.random.default_rng(seed)
+    edges = [0, 1, 31, 32, 1023, 1024, 1025, N // 2 - 1, N // 2, N - 1025, N - 1024, N - 2, N - 1]
+    idx = np.concatenate([np.array(edges, dtype=np.uint64),
+                          rng.integers(0, N, size=n, dtype=np.uint64)])
+    return idx
+
+
+def _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d):
+    gates = cfg.gates()
+    idx = _sample_indices(cfg.M)
+    src = oracle.walk_many(gates, idx)
+    it = torch.from_numpy(idx.astype(np.int64)).to(DEV)
+    got_perm = perm_d.index_select(0, it).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got_perm.astype(np.uint64), src)
+    e = 8 if cfg.dtype == "c64" else 16
+    want = k1_host.view(np.uint8).reshape(-1, e)[src.astype(np.int64)]
+    for out in (k2_d, k2f_d):
+        if out is None:
+            continue
+        got = out.view(-1, e).index_select(0, it).cpu().numpy()
+        assert np.array_equal(got, want)
+
+
+def _full_config(q, name, fused):
+    cfg = wl.CONFIGS[name]
+    gates = cfg.gates()
+    e = 8 if cfg.dtype == "c64" else 16
+    k1_host = wl.make_state(cfg.state)
+    k1_d = torch.from_numpy(k1_host.view(np.uint8)).to(DEV)
+    perm_d = torch.empty(cfg.N, dtype=torch.int32, device=DEV)
+    k2_d = torch.empty(cfg.N * e, dtype=torch.uint8, device=DEV)
+    q.build_map(gates, cfg.M, perm_d)
+    q.apply_map(perm_d, cfg.M, k1_d, k2_d, dtype=cfg.dtype)
+    k2f_d = None
+    if fused:
+        k2f_d = torch.empty_like(k2_d)
+        q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype=cfg.dtype)
+    torch.cuda.synchronize()
+    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d)
+    if fused:
+        assert torch.equal(k2_d, k2f_d)          # materialised == fused, every byte
+    # perm(reverse G) o perm(G) == identity over all 2^M outputs (group identity)
+    rev_d = torch.empty_like(perm_d)
+    q.build_map(gates[::-1].copy(), cfg.M, rev_d)
+    p64 = perm_d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+    comp = rev_d.index_select(0, p64)
+    del p64
+    ident = torch.arange(cfg.N, device=DEV, dtype=torch.int64).to(torch.int32)
+    assert torch.equal(comp, ident)
+    return cfg
+
+
+def test_cfg3_full_size_sampled(q):
+    _full_config(q, "cfg3", fused=False)
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_sampled(q):
+    _full_config(q, "cfg4", fused=True)
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_sampled(q):
+    """M = 32: 2^32 entries, 16 GiB perm, 32 GiB k1 and k2 (BASELINE cfg5)."""
+    cfg = wl.CONFIGS["cfg5"]
+    gates = cfg.gates()
+    N = cfg.N
+    k1_host = np.empty(N, dtype=np.complex64)
+    wl.fill_state(cfg.state, k1_host.ctypes.data)
+    k1_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
+    chunk = 1 << 28
+    for s in range(0, N, chunk):
+        k1_d[s * 8:(s + chunk) * 8].copy_(torch.from_numpy(k1_host[s:s + chunk].view(np.uint8)))
+    perm_d = torch.empty(N, dtype=torch.int32, device=DEV)
+    k2_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
+    q.build_map(gates, cfg.M, perm_d)
+    q.apply_map(perm_d, cfg.M, k1_d, k2_d, dtype="c64")
+    torch.cuda.synchronize()
+    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, None)
+    # fused == materialised over all 2^32 entries, compared chunk-wise on device
+    k2f_d = torch.empty_like(k2_d)
+    q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype="c64")
+    torch.cuda.synchronize()
+    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2f_d, None)
+    for s in range(0, N * 8, 1 << 32):
+        assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
+    del k2f_d, k2_d, k1_d
+    # group identity at full size: perm(rev G)[perm(G)[i]] == i for all 2^32 i
+    rev_d = torch.empty_like(perm_d)
+    q.build_map(gates[::-1].copy(), cfg.M, rev_d)
+    for s in range(0, N, chunk):
+        p = perm_d[s:s + chunk].to(torch.int64) & 0xFFFFFFFF
+        comp = rev_d.index_select(0, p).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(comp, torch.arange(s, s + chunk, device=DEV, dtype=torch.int64))
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_tagged_gather_m32(q):
+    """Index-tagged k1 at M = 32 (re bits = j, im bits = ~j): k2's real bits
+    must equal perm[i] for every output (a gather check at full size that
+    needs no host copy of k1)."""
+    M, N = 32, 1 << 32
+    gates = wl.CONFIGS["cfg5"].gates()
+    host = np.empty(1 << 28, dtype=np.complex64)
+    k1_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
+    for s in range(0, N, 1 << 28):
+        wl.fill_tagged("c64", host.ctypes.data, s, 1 << 28)
+        k1_d[s * 8:(s + (1 << 28)) * 8].copy_(torch.from_numpy(host.view(np.uint8)))
+    k2_d = torch.empty_like(k1_d)
+    q.run_fused(gates, M, k1_d, k2_d, dtype="c64")
+    perm_d = torch.empty(N, dtype=torch.int32, device=DEV)
+    q.build_map(gates, M, perm_d)
+    torch.cuda.synchronize()
+    words = k2_d.view(torch.int32).view(-1, 2)
+    for s in range(0, N, 1 << 28):
+        w = words[s:s + (1 << 28)]
+        assert torch.equal(w[:, 0], perm_d[s:s + (1 << 28)])
+        assert torch.equal(w[:, 1], ~perm_d[s:s + (1 << 28)])
+    idx = _sample_indices(M, 4096, 5)
+    src = oracle.walk_many(gates, idx)
+    it = torch.from_numpy(idx.astype(np.int64)).to(DEV)
+    assert np.array_equal(words[:, 0].index_select(0, it).cpu().numpy().view(np.uint32)
+                          .astype(np.uint64), src)
+    torch.cuda.empty_cache()
