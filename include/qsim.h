@@ -134,17 +134,67 @@ int qsim_run_fused_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
                       int32_t dtype, uint64_t start, uint64_t count,
                       const void *k1, void *k2_out, int32_t walk, void *stream);
 
+/* ---- traversal plans (locality of the gather) ----------------------------
+ * The gather reads k1 at perm[i]; in natural output order the readers of one
+ * 128-byte line of k1 are scattered over the whole output range, so for a
+ * random circuit almost every read misses L2.  A plan orders the traversal:
+ * output i = sigma(c) for counter c = 0 .. 2^M-1, sigma a permutation of
+ * the address bits that keeps bits 0..4 in place (warps stay coalesced) and
+ * puts first the output bits in which the readers of one k1 line most often
+ * differ; CTAs take chunks of 2^chunk_log2 counters strictly in counter
+ * order from a device ticket, so the lines a chunk front touches stay in L2.
+ * The result is the same k2 bytes; only the order of work changes.
+ *
+ * qsim_plan_create samples the circuit on the host (inverse walk of 2048
+ * pseudo-random k1 lines, fixed seed: deterministic) and fills `plan`, a
+ * plain value owned by the caller.  chunk_log2 and blocks_per_sm may be
+ * edited before use (tuning).                                               */
+#define QSIM_WORKSPACE_BYTES 256
+
+typedef struct qsim_plan {
+    int32_t M;
+    int32_t dtype;          /* QSIM_C64 / QSIM_C128: a 128-B line holds 16 / 8 entries */
+    uint32_t chunk_log2;    /* counters per CTA chunk (default 16), within [10, M] */
+    int32_t blocks_per_sm;  /* resident CTAs per SM (default 2), 1..8          */
+    uint32_t flags;         /* bit 0: natural order (no sigma)                 */
+    uint32_t reserved;
+    uint8_t sigma[32];      /* counter bit k -> output bit sigma[k]            */
+    float change_freq[32];  /* per output bit: fraction of sampled k1 lines whose
+                               readers differ in that bit                     */
+} qsim_plan;
+
+int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
+                     qsim_plan *plan);
+
+/* qsim_apply_map_planned -- qsim_apply_map (the same k2, bit for bit) in the
+ * traversal order of `plan` (M and dtype are plan->M, plan->dtype).
+ *   workspace  device scratch of QSIM_WORKSPACE_BYTES (16-B aligned), reset
+ *              on `stream` by the call; must not be used by a concurrent
+ *              call.  NULL: grid-stride chunk order (slower, still correct).
+ * QSIM_EINVAL if the plan is malformed (sigma not a permutation of 0..M-1
+ * fixing bits 0..4, chunk_log2 or blocks_per_sm out of range).              */
+int qsim_apply_map_planned(const qsim_plan *plan, const uint32_t *perm, const void *k1,
+                           void *k2, void *workspace, void *stream);
+
+/* qsim_run_fused_planned -- qsim_run_fused (the same k2) with the walk done
+ * for the outputs in the plan's order; `gates` must be the circuit the plan
+ * was created from (same n_gates; the plan is not re-derived).              */
+int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_t n_gates,
+                           const void *k1, void *k2, void *workspace, void *stream);
+
 /* qsim_run_host -- the whole path from HOST buffers (end-to-end use):
- * copies k1_host -> k1_dev, computes k2 (mode 0: build perm_dev, then
- * apply; mode 1: fused, perm_dev unused and may be NULL), copies
- * k2_dev -> k2_host, and SYNCHRONISES `stream` before returning.
+ * copies k1_host -> k1_dev, computes k2 (mode 0: qsim_build_map into
+ * perm_dev, then the planned gather; mode 1: planned fused, perm_dev unused
+ * and may be NULL), copies k2_dev -> k2_host, and SYNCHRONISES `stream`
+ * before returning.  The plan is created inside the call.
  *   k1_host, k2_host  host, 2^M entries each (pinned memory recommended)
  *   k1_dev, k2_dev    device workspaces, 2^M entries each
- *   perm_dev          device workspace, 2^M uint32 (mode 0)               */
+ *   perm_dev          device workspace, 2^M uint32 (mode 0)
+ *   workspace         device, QSIM_WORKSPACE_BYTES (may be NULL)           */
 int qsim_run_host(const qsim_gate *gates, int32_t n_gates, int32_t M,
                   int32_t dtype, int32_t mode, const void *k1_host,
                   void *k2_host, void *k1_dev, void *k2_dev,
-                  uint32_t *perm_dev, void *stream);
+                  uint32_t *perm_dev, void *workspace, void *stream);
 
 /* Number of kernel launches the last successful call on this thread
  * enqueued (for launch accounting in bench.py).                            */

@@ -43,6 +43,17 @@ class QsimError(RuntimeError):
         self.code = code
 
 
+WORKSPACE_BYTES = 256
+
+
+class Plan(ctypes.Structure):
+    """qsim_plan (include/qsim.h): traversal order of the gather."""
+    _fields_ = [("M", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("chunk_log2", ctypes.c_uint32), ("blocks_per_sm", ctypes.c_int32),
+                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32)]
+
+
 def _load() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -59,8 +70,11 @@ def _load() -> ctypes.CDLL:
         "qsim_run_fused": [vp, i32, i32, i32, vp, vp, vp],
         "qsim_run_fused_range": [vp, i32, i32, i32, u64, u64, vp, vp, vp],
         "qsim_run_fused_ex": [vp, i32, i32, i32, u64, u64, vp, vp, i32, vp],
-        "qsim_run_host": [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp],
+        "qsim_run_host": [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp],
     }
+    sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
+    sig["qsim_apply_map_planned"] = [ctypes.POINTER(Plan), vp, vp, vp, vp, vp]
+    sig["qsim_run_fused_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp]
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -164,12 +178,43 @@ def run_fused_range(gates, M: int, start: int, count: int, k1, k2_out, stream=No
 
 
 def run_host(gates, M: int, mode: int, k1_host, k2_host, k1_dev, k2_dev, perm_dev=None,
-             stream=None, dtype=None) -> None:
+             workspace=None, stream=None, dtype=None) -> None:
     """End to end from host buffers; returns after the stream is synchronised."""
     g, gp, n = _gates(gates)
     code = _dtype_code(k1_host if dtype is None else dtype)
     _check(_lib.qsim_run_host(gp, n, M, code, mode, _ptr(k1_host), _ptr(k2_host), _ptr(k1_dev),
-                              _ptr(k2_dev), _ptr(perm_dev), _stream(stream)), "qsim_run_host")
+                              _ptr(k2_dev), _ptr(perm_dev), _ptr(workspace), _stream(stream)),
+           "qsim_run_host")
+
+
+def plan_create(gates, M: int, dtype="c64") -> Plan:
+    g, gp, n = _gates(gates)
+    plan = Plan()
+    _check(_lib.qsim_plan_create(gp, n, M, _dtype_code(dtype), ctypes.byref(plan)),
+           "qsim_plan_create")
+    return plan
+
+
+def apply_map_planned(plan: Plan, perm, k1, k2, workspace=None, stream=None) -> None:
+    """qsim_apply_map in the plan's traversal order (same k2 bytes)."""
+    _check(_lib.qsim_apply_map_planned(ctypes.byref(plan), _ptr(perm), _ptr(k1), _ptr(k2),
+                                       _ptr(workspace), _stream(stream)),
+           "qsim_apply_map_planned")
+
+
+def run_fused_planned(plan: Plan, gates, k1, k2, workspace=None, stream=None) -> None:
+    """qsim_run_fused in the plan's traversal order (same k2 bytes)."""
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_run_fused_planned(ctypes.byref(plan), gp, n, _ptr(k1), _ptr(k2),
+                                       _ptr(workspace), _stream(stream)),
+           "qsim_run_fused_planned")
+
+
+def workspace(device=None):
+    """A device workspace of WORKSPACE_BYTES for the planned calls."""
+    import torch
+    return torch.zeros(WORKSPACE_BYTES, dtype=torch.uint8,
+                       device=device if device is not None else "cuda")
 
 
 def last_launch_count() -> int:

@@ -1,10 +1,14 @@
 // qsim_api.cu -- the C ABI declared in include/qsim.h: argument validation,
-// gate packing into the kernel-parameter bank, launch configuration.
+// gate packing into the kernel-parameter bank, traversal plans, launch
+// configuration.
 //
-// Nothing here computes on the host beyond packing the gate list: every
-// step of the path (walk, gather) runs in the kernels of qsim_kernels.cuh.
+// The host never computes outputs: every step of the path (the address walk
+// and the gather) runs in the kernels of qsim_kernels.cuh.  The only host
+// arithmetic is packing the gate list and, in qsim_plan_create, sampling the
+// circuit to choose a traversal order.
 #include <cstdio>
 #include <cstring>
+#include <memory>
 
 #include "qsim.h"
 #include "qsim_kernels.cuh"
@@ -30,9 +34,11 @@ int cuda_fail(cudaError_t e, const char* what) {
 int sm_count() {
   static int n = 0;
   if (n == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      n = v;
+    else
       n = 148;
   }
   return n;
@@ -48,33 +54,45 @@ bool overlap(const void* a, uint64_t abytes, const void* b, uint64_t bbytes) {
 
 int elem_bytes(int32_t dtype) { return dtype == QSIM_C64 ? 8 : dtype == QSIM_C128 ? 16 : 0; }
 
-// Validate and pack the gate list (P:L43 semantics; readings R3-R5).
-template <int CAP>
-int pack_gates(const qsim_gate* gates, int32_t n, int32_t M, qsim::GateList<CAP>& out) {
-  out.n = (uint32_t)n;
-  for (int32_t k = 0; k < n; ++k) {
-    const qsim_gate& g = gates[k];
-    if (g.kind > 2) return QSIM_EINVAL;
-    if (g.target >= M) return QSIM_EBIT;
-    uint32_t c0 = 0, c1 = 0;
-    if (g.kind >= 1) {
-      if (g.c0 >= M || g.c0 == g.target) return QSIM_EBIT;
-      c0 = g.c0;
-    }
-    if (g.kind == 2) {
-      if (g.c1 >= M || g.c1 == g.target || g.c1 == g.c0) return QSIM_EBIT;
-      c1 = g.c1;
-    }
-    out.w[k] = (uint32_t)g.kind | ((uint32_t)g.target << 8) | (c0 << 16) | (c1 << 24);
-  }
-  return QSIM_OK;
-}
-
 int check_gates_args(const qsim_gate* gates, int32_t n, int32_t M) {
   if (M < 1 || M > 32) return QSIM_ERANGE;
   if (n < 0 || n > QSIM_MAX_GATES) return QSIM_ECAP;
   if (n > 0 && gates == nullptr) return QSIM_EINVAL;
   return QSIM_OK;
+}
+
+// Validate one gate (P:L43 step semantics; readings R3-R5).
+int check_gate(const qsim_gate& g, int32_t M) {
+  if (g.kind > 2) return QSIM_EINVAL;
+  if (g.target >= M) return QSIM_EBIT;
+  if (g.kind >= 1 && (g.c0 >= M || g.c0 == g.target)) return QSIM_EBIT;
+  if (g.kind == 2 && (g.c1 >= M || g.c1 == g.target || g.c1 == g.c0)) return QSIM_EBIT;
+  return QSIM_OK;
+}
+
+int check_gates(const qsim_gate* gates, int32_t n, int32_t M) {
+  int rc = check_gates_args(gates, n, M);
+  for (int32_t k = 0; rc == QSIM_OK && k < n; ++k) rc = check_gate(gates[k], M);
+  return rc;
+}
+
+// Pack for the kernels (gates already validated).  bitsliced: target |
+// c0 << 8 | c1 << 16 with absent controls = the all-ones plane; per-lane:
+// kind | target << 8 | c0 << 16 | c1 << 24 with absent controls = 0.
+template <int CAP>
+void pack_gates(const qsim_gate* gates, int32_t n, bool bitsliced, qsim::GateList<CAP>& out) {
+  out.n = (uint32_t)n;
+  for (int32_t k = 0; k < n; ++k) {
+    const qsim_gate& g = gates[k];
+    if (bitsliced) {
+      const uint32_t c0 = g.kind >= 1 ? g.c0 : qsim::kOnesPlane;
+      const uint32_t c1 = g.kind == 2 ? g.c1 : qsim::kOnesPlane;
+      out.w[k] = (uint32_t)g.target | (c0 << 8) | (c1 << 16);
+    } else {
+      const uint32_t c0 = g.kind >= 1 ? g.c0 : 0u, c1 = g.kind == 2 ? g.c1 : 0u;
+      out.w[k] = (uint32_t)g.kind | ((uint32_t)g.target << 8) | (c0 << 16) | (c1 << 24);
+    }
+  }
 }
 
 int check_range(int32_t M, uint64_t start, uint64_t count) {
@@ -83,33 +101,54 @@ int check_range(int32_t M, uint64_t start, uint64_t count) {
   return QSIM_OK;
 }
 
-// Launch the walk (MODE 0: write perm, MODE 1: fused gather) with the
-// gate list in a parameter bank sized for n.
+qsim::SigmaParams identity_sigma(int32_t M) {
+  qsim::SigmaParams sp;
+  for (int k = 0; k < 32; ++k) sp.sigma[k] = (uint8_t)k;
+  sp.chunk_log2 = 10;
+  sp.nbits = (uint32_t)M;
+  sp.ticket = nullptr;
+  return sp;
+}
+
+// Natural-order walk over [start, start+count): MODE 0 writes perm_out,
+// MODE 1 gathers k1 into k2_out (fused).
 template <int CAP, int MODE, typename T>
 int launch_walk_cap(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                     uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st) {
-  qsim::GateList<CAP> gl;
-  int rc = pack_gates<CAP>(gates, n, M, gl);
-  if (rc != QSIM_OK) return rc;
   if (count == 0) return QSIM_OK;
   const int sms = sm_count();
+  std::unique_ptr<qsim::GateList<CAP>> gl(new qsim::GateList<CAP>);
   if (walk == QSIM_WALK_PER_LANE) {
+    pack_gates<CAP>(gates, n, false, *gl);
     constexpr int APT = 4;
     const uint64_t threads = (count + APT - 1) / APT;
     uint64_t blocks = (threads + 255) / 256;
     const uint64_t cap = (uint64_t)sms * 8 * 16;
     if (blocks > cap) blocks = cap;
     qsim::k_walk_per_lane<CAP, MODE, T, APT><<<(unsigned)blocks, 256, 0, st>>>(
-        gl, start, count, perm_out, k1, k2_out);
+        *gl, start, count, perm_out, k1, k2_out);
     QSIM_CHECK_LAUNCH("k_walk_per_lane");
+    return QSIM_OK;
+  }
+  pack_gates<CAP>(gates, n, true, *gl);
+  const qsim::SigmaParams sp = identity_sigma(M);
+  const uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  uint64_t blocks = (te - tb + qsim::kBsWarps - 1) / qsim::kBsWarps;
+  const uint64_t cap = (uint64_t)sms * 2 * 16;
+  if (blocks > cap) blocks = cap;
+  const size_t smem = qsim::bs_smem_bytes((uint32_t)n);
+  if (MODE == 0) {
+    cudaFuncSetAttribute(qsim::k_build_bitsliced<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    qsim::k_build_bitsliced<CAP><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(
+        *gl, sp, start, start + count, tb, te, perm_out);
+    QSIM_CHECK_LAUNCH("k_build_bitsliced");
   } else {
-    const uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
-    uint64_t blocks = (te - tb + qsim::kBsWarps - 1) / qsim::kBsWarps;
-    const uint64_t cap = (uint64_t)sms * 6 * 32;
-    if (blocks > cap) blocks = cap;
-    qsim::k_walk_bitsliced<CAP, MODE, T><<<(unsigned)blocks, qsim::kBsThreads, 0, st>>>(
-        gl, start, start + count, tb, te, perm_out, k1, k2_out);
-    QSIM_CHECK_LAUNCH("k_walk_bitsliced");
+    cudaFuncSetAttribute(qsim::k_fused_bitsliced<CAP, T>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    qsim::k_fused_bitsliced<CAP, T><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(
+        *gl, sp, start, start + count, tb, te, k1, k2_out);
+    QSIM_CHECK_LAUNCH("k_fused_bitsliced");
   }
   return QSIM_OK;
 }
@@ -117,7 +156,6 @@ int launch_walk_cap(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start
 template <int MODE, typename T>
 int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                 uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st) {
-  if (walk < 0 || walk > 2) return QSIM_EINVAL;
   if (n <= 64)
     return launch_walk_cap<64, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st);
   if (n <= 256)
@@ -130,18 +168,20 @@ int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, ui
 
 int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                uint32_t* perm_out, int32_t walk, cudaStream_t st) {
-  int rc = check_gates_args(gates, n, M);
+  int rc = check_gates(gates, n, M);
   if (rc) return rc;
   if ((rc = check_range(M, start, count))) return rc;
+  if (walk < 0 || walk > 2) return QSIM_EINVAL;
   if (perm_out == nullptr || !aligned16(perm_out)) return QSIM_EINVAL;
   return launch_walk<0, uint2>(gates, n, M, start, count, perm_out, nullptr, nullptr, walk, st);
 }
 
 int fused_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, uint64_t start,
                uint64_t count, const void* k1, void* k2, int32_t walk, cudaStream_t st) {
-  int rc = check_gates_args(gates, n, M);
+  int rc = check_gates(gates, n, M);
   if (rc) return rc;
   if ((rc = check_range(M, start, count))) return rc;
+  if (walk < 0 || walk > 2) return QSIM_EINVAL;
   const int e = elem_bytes(dtype);
   if (e == 0) return QSIM_EINVAL;
   if (!k1 || !k2 || !aligned16(k1) || !aligned16(k2)) return QSIM_EINVAL;
@@ -171,15 +211,180 @@ int apply_impl(const uint32_t* perm, uint64_t count, int32_t M, int32_t dtype, c
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   if (dtype == QSIM_C64)
-    qsim::k_apply<uint2><<<(unsigned)blocks, 256, 0, st>>>(perm, count,
-                                                          static_cast<const uint2*>(k1),
-                                                          static_cast<uint2*>(k2));
+    qsim::k_apply<uint2><<<(unsigned)blocks, 256, 0, st>>>(
+        perm, count, static_cast<const uint2*>(k1), static_cast<uint2*>(k2));
   else
-    qsim::k_apply<uint4><<<(unsigned)blocks, 256, 0, st>>>(perm, count,
-                                                          static_cast<const uint4*>(k1),
-                                                          static_cast<uint4*>(k2));
+    qsim::k_apply<uint4><<<(unsigned)blocks, 256, 0, st>>>(
+        perm, count, static_cast<const uint4*>(k1), static_cast<uint4*>(k2));
   QSIM_CHECK_LAUNCH("k_apply");
   return QSIM_OK;
+}
+
+// ---- traversal plan (host analysis of the circuit; no output is computed)
+uint64_t plan_mix(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+// inverse map perm^-1(j) = f_n(...f_1(j)): Step 1 first
+uint32_t plan_inverse_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32_t x) {
+  for (int k = 0; k < n; ++k)
+    if ((~x & cm[k]) == 0u) x ^= tm[k];
+  return x;
+}
+
+int plan_validate(const qsim_plan* p) {
+  if (!p) return QSIM_EINVAL;
+  if (p->M < 1 || p->M > 32) return QSIM_ERANGE;
+  if (elem_bytes(p->dtype) == 0) return QSIM_EINVAL;
+  uint64_t seen = 0;
+  for (int k = 0; k < p->M; ++k) {
+    if (p->sigma[k] >= p->M) return QSIM_EINVAL;
+    seen |= 1ull << p->sigma[k];
+    if (k < 5 && p->sigma[k] != k) return QSIM_EINVAL;
+  }
+  if (seen != ((1ull << p->M) - 1)) return QSIM_EINVAL;
+  if (p->M >= 10 && (p->chunk_log2 < 10 || (int)p->chunk_log2 > p->M)) return QSIM_EINVAL;
+  if (p->blocks_per_sm < 1 || p->blocks_per_sm > 8) return QSIM_EINVAL;
+  return QSIM_OK;
+}
+
+bool plan_natural(const qsim_plan* p) { return (p->flags & 1u) || p->M < 10; }
+
+qsim::SigmaParams plan_params(const qsim_plan* p, void* workspace) {
+  qsim::SigmaParams sp;
+  std::memcpy(sp.sigma, p->sigma, 32);
+  sp.chunk_log2 = p->chunk_log2;
+  sp.nbits = (uint32_t)p->M;
+  sp.ticket = static_cast<unsigned long long*>(workspace);
+  return sp;
+}
+
+int reset_ticket(void* workspace, cudaStream_t st) {
+  if (!workspace) return QSIM_OK;
+  cudaError_t ce = cudaMemsetAsync(workspace, 0, sizeof(unsigned long long), st);
+  return ce == cudaSuccess ? QSIM_OK : cuda_fail(ce, "ticket reset");
+}
+
+int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan) {
+  std::memset(plan, 0, sizeof *plan);
+  plan->M = M;
+  plan->dtype = dtype;
+  plan->chunk_log2 = M < 16 ? (uint32_t)M : 16u;
+  plan->blocks_per_sm = 2;
+  for (int k = 0; k < 32; ++k) plan->sigma[k] = (uint8_t)k;
+  if (M < 10) {
+    plan->flags = 1;
+    return QSIM_OK;
+  }
+  std::unique_ptr<uint32_t[]> cm(new uint32_t[n > 0 ? n : 1]), tm(new uint32_t[n > 0 ? n : 1]);
+  for (int k = 0; k < n; ++k) {
+    const qsim_gate& g = gates[k];
+    cm[k] = (g.kind >= 1 ? 1u << g.c0 : 0u) | (g.kind == 2 ? 1u << g.c1 : 0u);
+    tm[k] = 1u << g.target;
+  }
+  const int line_bits = dtype == QSIM_C64 ? 4 : 3;  // one 128-byte line of k1
+  const int lines = 2048;
+  uint32_t count[32] = {0};
+  const uint64_t nlines = 1ull << (M - line_bits);
+  for (int s = 0; s < lines; ++s) {
+    const uint32_t base = (uint32_t)((plan_mix(0x51a3ull + s) % nlines) << line_bits);
+    const uint32_t r0 = plan_inverse_walk(cm.get(), tm.get(), n, base);
+    uint32_t diff = 0;
+    for (uint32_t e = 1; e < (1u << line_bits); ++e)
+      diff |= plan_inverse_walk(cm.get(), tm.get(), n, base | e) ^ r0;
+    for (int b = 0; b < M; ++b) count[b] += (diff >> b) & 1u;
+  }
+  for (int b = 0; b < M; ++b) plan->change_freq[b] = (float)count[b] / lines;
+  // sigma: bits 0..4 fixed; then output bits by descending change frequency
+  int order[32], m = 0;
+  for (int b = 5; b < M; ++b) order[m++] = b;
+  for (int i = 1; i < m; ++i)  // stable insertion sort
+    for (int j = i; j > 0 && count[order[j]] > count[order[j - 1]]; --j) {
+      int t = order[j];
+      order[j] = order[j - 1];
+      order[j - 1] = t;
+    }
+  for (int k = 0; k < m; ++k) plan->sigma[5 + k] = (uint8_t)order[k];
+  return QSIM_OK;
+}
+
+int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* k1, void* k2,
+                       void* workspace, cudaStream_t st) {
+  int rc = plan_validate(plan);
+  if (rc) return rc;
+  const int M = plan->M;
+  if (plan_natural(plan)) return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
+  const int e = elem_bytes(plan->dtype);
+  if (!perm || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2))
+    return QSIM_EINVAL;
+  if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
+  const uint64_t N = 1ull << M;
+  if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e)) return QSIM_EALIAS;
+  const qsim::SigmaParams sp = plan_params(plan, workspace);
+  if ((rc = reset_ticket(workspace, st))) return rc;
+  const uint64_t nchunks = N >> sp.chunk_log2;
+  uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
+  if (blocks > nchunks) blocks = nchunks;
+  if (plan->dtype == QSIM_C64)
+    qsim::k_apply_sigma<uint2, 8><<<(unsigned)blocks, 256, 0, st>>>(
+        sp, perm, N, static_cast<const uint2*>(k1), static_cast<uint2*>(k2));
+  else
+    qsim::k_apply_sigma<uint4, 8><<<(unsigned)blocks, 256, 0, st>>>(
+        sp, perm, N, static_cast<const uint4*>(k1), static_cast<uint4*>(k2));
+  QSIM_CHECK_LAUNCH("k_apply_sigma");
+  return QSIM_OK;
+}
+
+template <int CAP, typename T>
+int launch_fused_sigma(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const T* k1, T* k2,
+                       void* workspace, cudaStream_t st) {
+  std::unique_ptr<qsim::GateList<CAP>> gl(new qsim::GateList<CAP>);
+  pack_gates<CAP>(gates, n, true, *gl);
+  const qsim::SigmaParams sp = plan_params(plan, workspace);
+  int rc = reset_ticket(workspace, st);
+  if (rc) return rc;
+  const uint64_t N = 1ull << plan->M;
+  const uint64_t nchunks = N >> sp.chunk_log2;
+  uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
+  if (blocks > nchunks) blocks = nchunks;
+  const size_t smem = qsim::bs_smem_bytes((uint32_t)n);
+  cudaFuncSetAttribute(qsim::k_fused_sigma<CAP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  qsim::k_fused_sigma<CAP, T><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(*gl, sp, N, k1, k2);
+  QSIM_CHECK_LAUNCH("k_fused_sigma");
+  return QSIM_OK;
+}
+
+template <typename T>
+int fused_planned_t(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const T* k1, T* k2,
+                    void* workspace, cudaStream_t st) {
+  if (n <= 64) return launch_fused_sigma<64, T>(plan, gates, n, k1, k2, workspace, st);
+  if (n <= 256) return launch_fused_sigma<256, T>(plan, gates, n, k1, k2, workspace, st);
+  if (n <= 1024) return launch_fused_sigma<1024, T>(plan, gates, n, k1, k2, workspace, st);
+  return launch_fused_sigma<qsim::kMaxGates, T>(plan, gates, n, k1, k2, workspace, st);
+}
+
+int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
+                       void* k2, void* workspace, cudaStream_t st) {
+  int rc = plan_validate(plan);
+  if (rc) return rc;
+  const int M = plan->M;
+  if ((rc = check_gates(gates, n, M))) return rc;
+  if (plan_natural(plan))
+    return fused_impl(gates, n, M, plan->dtype, 0, 1ull << M, k1, k2, QSIM_WALK_AUTO, st);
+  const int e = elem_bytes(plan->dtype);
+  if (!k1 || !k2 || !aligned16(k1) || !aligned16(k2)) return QSIM_EINVAL;
+  if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
+  const uint64_t N = 1ull << M;
+  if (overlap(k1, N * e, k2, N * e)) return QSIM_EALIAS;
+  if (plan->dtype == QSIM_C64)
+    return fused_planned_t<uint2>(plan, gates, n, static_cast<const uint2*>(k1),
+                                  static_cast<uint2*>(k2), workspace, st);
+  return fused_planned_t<uint4>(plan, gates, n, static_cast<const uint4*>(k1),
+                                static_cast<uint4*>(k2), workspace, st);
 }
 
 }  // namespace
@@ -245,11 +450,33 @@ int qsim_run_fused_ex(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_
                     static_cast<cudaStream_t>(stream));
 }
 
+int qsim_plan_create(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype,
+                     qsim_plan* plan) {
+  g_launches = 0;
+  int rc = check_gates(gates, n, M);
+  if (rc) return rc;
+  if (!plan || elem_bytes(dtype) == 0) return QSIM_EINVAL;
+  return plan_fill(gates, n, M, dtype, plan);
+}
+
+int qsim_apply_map_planned(const qsim_plan* plan, const uint32_t* perm, const void* k1, void* k2,
+                           void* workspace, void* stream) {
+  g_launches = 0;
+  return apply_planned_impl(plan, perm, k1, k2, workspace, static_cast<cudaStream_t>(stream));
+}
+
+int qsim_run_fused_planned(const qsim_plan* plan, const qsim_gate* gates, int32_t n_gates,
+                           const void* k1, void* k2, void* workspace, void* stream) {
+  g_launches = 0;
+  return fused_planned_impl(plan, gates, n_gates, k1, k2, workspace,
+                            static_cast<cudaStream_t>(stream));
+}
+
 int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype, int32_t mode,
                   const void* k1_host, void* k2_host, void* k1_dev, void* k2_dev,
-                  uint32_t* perm_dev, void* stream) {
+                  uint32_t* perm_dev, void* workspace, void* stream) {
   g_launches = 0;
-  int rc = check_gates_args(gates, n_gates, M);
+  int rc = check_gates(gates, n_gates, M);
   if (rc) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0 || (mode != 0 && mode != 1)) return QSIM_EINVAL;
@@ -258,18 +485,15 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
   const uint64_t N = 1ull << M, bytes = N * e;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // validate the compute step before enqueuing anything
-  if (!aligned16(k1_dev) || !aligned16(k2_dev) || (mode == 0 && !aligned16(perm_dev)))
+  if (!aligned16(k1_dev) || !aligned16(k2_dev) || (mode == 0 && !aligned16(perm_dev)) ||
+      (workspace && !aligned16(workspace)))
     return QSIM_EINVAL;
   if (overlap(k1_dev, bytes, k2_dev, bytes) ||
       (mode == 0 && (overlap(perm_dev, N * 4, k2_dev, bytes) ||
                      overlap(perm_dev, N * 4, k1_dev, bytes))))
     return QSIM_EALIAS;
-  {
-    qsim::GateList<qsim::kMaxGates>* probe = new qsim::GateList<qsim::kMaxGates>;
-    rc = pack_gates(gates, n_gates, M, *probe);
-    delete probe;
-    if (rc) return rc;
-  }
+  qsim_plan plan;
+  if ((rc = plan_fill(gates, n_gates, M, dtype, &plan))) return rc;
   cudaError_t ce = cudaMemcpyAsync(k1_dev, k1_host, bytes, cudaMemcpyHostToDevice, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "H2D k1");
   int launches = 0;
@@ -278,9 +502,9 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
     launches += g_launches;
     g_launches = 0;
     if (rc) return rc;
-    rc = apply_impl(perm_dev, N, M, dtype, k1_dev, k2_dev, st);
+    rc = apply_planned_impl(&plan, perm_dev, k1_dev, k2_dev, workspace, st);
   } else {
-    rc = fused_impl(gates, n_gates, M, dtype, 0, N, k1_dev, k2_dev, QSIM_WALK_AUTO, st);
+    rc = fused_planned_impl(&plan, gates, n_gates, k1_dev, k2_dev, workspace, st);
   }
   launches += g_launches;
   if (rc) return rc;
@@ -297,7 +521,7 @@ int32_t qsim_last_launch_count(void) { return g_launches; }
 const char* qsim_strerror(int32_t code) {
   switch (code) {
     case QSIM_OK: return "ok";
-    case QSIM_EINVAL: return "invalid argument (null/misaligned pointer, bad dtype/mode/kind)";
+    case QSIM_EINVAL: return "invalid argument (null/misaligned pointer, bad dtype/mode/kind/plan)";
     case QSIM_ERANGE: return "M outside [1, 32] or range outside [0, 2^M)";
     case QSIM_EBIT: return "gate bit out of range, target among controls, or duplicate control";
     case QSIM_ECAP: return "gate count outside [0, QSIM_MAX_GATES]";

@@ -13,6 +13,11 @@
 //     A step is plane[t] ^= plane[c0] & plane[c1] (one logic op for 32
 //     addresses); a 32x32 bit transpose turns planes back into addresses.
 // Gathers move entries as raw 8/16-byte integers (bit-exact, R15).
+//
+// Traversal order: "counter" c runs over [0, 2^M); the output it handles is
+// sigma(c), a permutation of the address bits (identity = natural order).
+// sigma fixes bits 0..4, so the 32 lanes of a warp always cover 32
+// consecutive outputs.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -20,10 +25,12 @@
 namespace qsim {
 
 constexpr int kMaxGates = 4096;
+constexpr uint32_t kOnesPlane = 32;  // bit-sliced: an all-ones plane (absent control)
 
-// Gate list in the launch's kernel-parameter bank (constant bank 0): one
-// 32-bit word per gate, kind | target << 8 | c0 << 16 | c1 << 24, with the
-// unused control slots of NOT / CNOT normalised to 0 by the host.
+// Gate list in the launch's kernel-parameter bank (constant bank 0), one
+// 32-bit word per gate.  Per-lane format: kind | target << 8 | c0 << 16 |
+// c1 << 24 (unused controls 0).  Bit-sliced format: target | c0 << 8 |
+// c1 << 16 with absent controls = kOnesPlane.
 template <int CAP>
 struct GateList {
   uint32_t n;
@@ -50,8 +57,8 @@ __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) { __stcs(
 
 // ------------------------------------------------------------------ per-lane
 // One address per lane: walk the gates last -> first, x ^= tmask when all
-// control bits of x are set.  ADDR_PER_THREAD independent walks interleave
-// to fill the ALU pipe.
+// control bits of x are set.  APT independent walks interleave to fill the
+// ALU pipe.
 template <int CAP, int MODE, typename T, int APT>
 __global__ void __launch_bounds__(256)
 k_walk_per_lane(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_t count,
@@ -84,16 +91,52 @@ k_walk_per_lane(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_
   }
 }
 
+// ------------------------------------------------------------ sigma tables
+struct SigmaParams {
+  uint8_t sigma[32];            // counter bit k -> output bit sigma[k]; sigma[k] = k for k < 5
+  uint32_t chunk_log2;          // counters per CTA chunk
+  uint32_t nbits;               // M
+  unsigned long long* ticket;   // in-order chunk dispenser (zeroed), or null: grid-stride
+};
+
+// deposit tables: T[b][v] = OR over bits j of byte v of (1 << sigma[8b + j])
+__device__ __forceinline__ void sigma_tables(const SigmaParams& sp, uint32_t (*T)[256]) {
+  for (int x = threadIdx.x; x < 4 * 256; x += blockDim.x) {
+    const int b = x >> 8, v = x & 255;
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (((v >> j) & 1) && 8 * b + j < (int)sp.nbits) r |= 1u << sp.sigma[8 * b + j];
+    T[b][v] = r;
+  }
+}
+
+__device__ __forceinline__ uint32_t sigma_apply(uint32_t (*T)[256], uint64_t c) {
+  return T[0][c & 255] | T[1][(c >> 8) & 255] | T[2][(c >> 16) & 255] | T[3][(c >> 24) & 255];
+}
+
+// Next chunk for this CTA: in counter order from the ticket, else grid-stride.
+__device__ __forceinline__ uint64_t next_chunk(const SigmaParams& sp, uint64_t cur,
+                                               uint64_t* s_chunk, bool first) {
+  if (sp.ticket) {
+    __syncthreads();
+    if (threadIdx.x == 0) *s_chunk = atomicAdd(sp.ticket, 1ull);
+    __syncthreads();
+    return *s_chunk;
+  }
+  return first ? (uint64_t)blockIdx.x : cur + gridDim.x;
+}
+
 // ---------------------------------------------------------------- bit-sliced
-// Tile = 1024 consecutive output addresses per warp.  Lane L, word bit l
-// holds address tile*1024 + 32*l + L: address bits 0..4 are the lane
-// (constant within a thread), bits 5..9 are the word bit l (the classic
-// 0xAAAAAAAA.. patterns), bits >= 10 are the tile (constant per warp).
+// A warp tile = 1024 counters: counter bits 0..4 are the lane, bits 5..9 the
+// word bit l, bits >= 10 the tile.  Lane L, word bit l handles output
+// out_base | Ltab[l] | L, where out_base = sigma(tile << 10) and Ltab[l] =
+// sigma(l << 5).  Initial plane b of a thread: lane bit b (b < 5), the
+// standard 0xAAAAAAAA.. pattern if b is the image of an l-bit, else the
+// (warp-uniform) bit b of out_base.
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
 
-// In-register 32x32 bit transpose: on return bit b of a[l] = bit l of the
-// input a[b].  Five block-swap stages (16, 8, 4, 2, 1).
 template <int J, uint32_t MASK>
 __device__ __forceinline__ void transpose_stage(uint32_t (&a)[32]) {
 #pragma unroll
@@ -106,6 +149,8 @@ __device__ __forceinline__ void transpose_stage(uint32_t (&a)[32]) {
   }
 }
 
+// In-register 32x32 bit transpose: on return bit b of a[l] = bit l of the
+// input a[b].  Five block-swap stages (16, 8, 4, 2, 1).
 __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
   transpose_stage<16, 0x0000ffffu>(a);
   transpose_stage<8, 0x00ff00ffu>(a);
@@ -114,70 +159,161 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
   transpose_stage<1, 0x55555555u>(a);
 }
 
-__device__ __forceinline__ uint32_t bs_init_plane(int b, uint32_t lane, uint64_t base) {
-  if (b < 5) return ((lane >> b) & 1u) ? 0xffffffffu : 0u;
-  if (b < 10) {
-    const uint32_t pat[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u, 0xffff0000u};
-    return pat[b - 5];
-  }
-  return ((base >> b) & 1u) ? 0xffffffffu : 0u;
+struct BsShared {
+  uint32_t S[33][kBsThreads];  // S[plane][thread] (private columns); plane 32 = ones
+  uint32_t tab[4][256];        // sigma deposit tables
+  uint32_t patw[32];           // l-bit pattern of each output plane (0 if none)
+  uint32_t ltab[32];           // sigma(l << 5)
+  uint64_t chunk;
+  uint2 gate[1];               // [n]: byte offsets of (target | c0 << 16, c1) planes
+};
+
+__host__ __device__ constexpr size_t bs_smem_bytes(uint32_t n) {
+  return sizeof(BsShared) + (n > 0 ? n - 1 : 0) * sizeof(uint2);
 }
 
-template <int CAP, int MODE, typename T>
+template <int CAP>
+__device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaParams& sp,
+                                         BsShared& sh) {
+  sigma_tables(sp, sh.tab);
+  const uint32_t pat[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u, 0xffff0000u};
+  if (threadIdx.x < 32) sh.patw[threadIdx.x] = 0;
+  sh.S[kOnesPlane][threadIdx.x] = 0xffffffffu;
+  // gate list, last gate first (the walk order), as plane byte offsets
+  for (uint32_t k = threadIdx.x; k < g.n; k += blockDim.x) {
+    const uint32_t w = g.w[g.n - 1 - k];
+    const uint32_t row = kBsThreads * 4u;
+    sh.gate[k] = make_uint2((w & 0xffu) * row | (((w >> 8) & 0xffu) * row) << 16,
+                            ((w >> 16) & 0xffu) * row);
+  }
+  __syncthreads();
+  if (threadIdx.x < 5 && 5 + threadIdx.x < sp.nbits) sh.patw[sp.sigma[5 + threadIdx.x]] = pat[threadIdx.x];
+  if (threadIdx.x < 32) {
+    uint32_t o = 0;
+    for (int j = 0; j < 5; ++j)
+      if (((threadIdx.x >> j) & 1) && 5 + j < (int)sp.nbits) o |= 1u << sp.sigma[5 + j];
+    sh.ltab[threadIdx.x] = o;
+  }
+  __syncthreads();
+}
+
+// Walk one warp tile; on return a[l] = perm(out_base | ltab[l] | lane).
+__device__ __forceinline__ void bs_walk_tile(uint32_t n, BsShared& sh, uint32_t out_base,
+                                             uint32_t (&a)[32]) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31u;
+#pragma unroll
+  for (int b = 0; b < 32; ++b) {
+    const uint32_t lanew = (b < 5) ? (((lane >> b) & 1u) ? 0xffffffffu : 0u) : 0u;
+    const uint32_t basew = ((out_base >> b) & 1u) ? 0xffffffffu : 0u;
+    sh.S[b][tid] = lanew | sh.patw[b] | basew;
+  }
+  // walk last -> first (R1, R2): plane[t] ^= plane[c0] & plane[c1]
+  char* col = reinterpret_cast<char*>(&sh.S[0][tid]);
+#pragma unroll 4
+  for (uint32_t k = 0; k < n; ++k) {
+    const uint2 gk = sh.gate[k];
+    uint32_t* pt = reinterpret_cast<uint32_t*>(col + (gk.x & 0xffffu));
+    const uint32_t x0 = *reinterpret_cast<const uint32_t*>(col + (gk.x >> 16));
+    const uint32_t x1 = *reinterpret_cast<const uint32_t*>(col + gk.y);
+    *pt ^= x0 & x1;
+  }
+#pragma unroll
+  for (int b = 0; b < 32; ++b) a[b] = sh.S[b][tid];
+  transpose32(a);
+}
+
+// MODE 0: perm_out[out - start] = perm(out) for out in [start, end), natural
+// order (identity sigma), tiles [tile_begin, tile_end) grid-stride.
+template <int CAP>
 __global__ void __launch_bounds__(kBsThreads, 2)
-k_walk_bitsliced(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_t end,
-                 uint64_t tile_begin, uint64_t tile_end, uint32_t* __restrict__ perm_out,
-                 const T* __restrict__ k1, T* __restrict__ k2_out) {
-  __shared__ uint32_t S[32][kBsThreads];  // S[plane][thread]: private columns
-  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+k_build_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant__ SigmaParams sp,
+                  uint64_t start, uint64_t end, uint64_t tile_begin, uint64_t tile_end,
+                  uint32_t* __restrict__ perm_out) {
+  extern __shared__ __align__(16) uint8_t bs_smem[];
+  BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
+  bs_setup(g, sp, sh);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
        tile += (uint64_t)gridDim.x * kBsWarps) {
     const uint64_t base = tile << 10;
-#pragma unroll
-    for (int b = 0; b < 32; ++b) S[b][tid] = bs_init_plane(b, lane, base);
-    // walk last -> first (R1, R2): one logic op per gate for 32 addresses
-    for (int k = (int)g.n - 1; k >= 0; --k) {
-      const uint32_t w = g.w[k];
-      const uint32_t kind = gate_kind(w), t = gate_t(w);
-      uint32_t x = S[t][tid];
-      if (kind == 0) x = ~x;
-      else if (kind == 1) x ^= S[gate_c0(w)][tid];
-      else x ^= S[gate_c0(w)][tid] & S[gate_c1(w)][tid];
-      S[t][tid] = x;
-    }
     uint32_t a[32];
+    bs_walk_tile(g.n, sh, (uint32_t)base, a);
 #pragma unroll
-    for (int b = 0; b < 32; ++b) a[b] = S[b][tid];
-    transpose32(a);  // a[l] = perm(base + 32 l + lane)
-    if (MODE == 0) {
+    for (int l = 0; l < 32; ++l) {
+      const uint64_t addr = base + 32u * l + lane;
+      if (addr >= start && addr < end) st_stream_u32(perm_out + (addr - start), a[l]);
+    }
+  }
+}
+
+// Fused, natural order with an output range: k2_out[out - start] = k1[perm(out)].
+template <int CAP, typename T>
+__global__ void __launch_bounds__(kBsThreads, 2)
+k_fused_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant__ SigmaParams sp,
+                  uint64_t start, uint64_t end, uint64_t tile_begin, uint64_t tile_end,
+                  const T* __restrict__ k1, T* __restrict__ k2_out) {
+  extern __shared__ __align__(16) uint8_t bs_smem[];
+  BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
+  bs_setup(g, sp, sh);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
+       tile += (uint64_t)gridDim.x * kBsWarps) {
+    const uint64_t base = tile << 10;
+    uint32_t a[32];
+    bs_walk_tile(g.n, sh, (uint32_t)base, a);
+    constexpr int B = 16;  // gathers in flight per thread
 #pragma unroll
-      for (int l = 0; l < 32; ++l) {
-        const uint64_t addr = base + 32u * l + lane;
-        if (addr >= start && addr < end) st_stream_u32(perm_out + (addr - start), a[l]);
+    for (int h = 0; h < 32; h += B) {
+      T v[B];
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        const uint64_t addr = base + 32u * (h + l) + lane;
+        if (addr >= start && addr < end) v[l] = ld_gather(k1 + a[h + l]);
       }
-    } else {
-      constexpr int B = 16;  // gathers in flight per thread
+#pragma unroll
+      for (int l = 0; l < B; ++l) {
+        const uint64_t addr = base + 32u * (h + l) + lane;
+        if (addr >= start && addr < end) st_stream(k2_out + (addr - start), v[l]);
+      }
+    }
+  }
+}
+
+// Fused in sigma order over all 2^M outputs (M >= 10), chunks of
+// 2^chunk_log2 counters taken from the ticket.
+template <int CAP, typename T>
+__global__ void __launch_bounds__(kBsThreads, 2)
+k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ SigmaParams sp,
+              uint64_t N, const T* __restrict__ k1, T* __restrict__ k2) {
+  extern __shared__ __align__(16) uint8_t bs_smem[];
+  BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
+  bs_setup(g, sp, sh);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t nchunks = N >> sp.chunk_log2;
+  const uint32_t tiles_per_chunk = 1u << (sp.chunk_log2 - 10);
+  for (uint64_t ch = next_chunk(sp, 0, &sh.chunk, true); ch < nchunks;
+       ch = next_chunk(sp, ch, &sh.chunk, false)) {
+    for (uint32_t tt = warp; tt < tiles_per_chunk; tt += kBsWarps) {
+      const uint64_t c = (ch << sp.chunk_log2) + ((uint64_t)tt << 10);
+      const uint32_t out_base = sigma_apply(sh.tab, c);
+      uint32_t a[32];
+      bs_walk_tile(g.n, sh, out_base, a);
+      constexpr int B = 16;
 #pragma unroll
       for (int h = 0; h < 32; h += B) {
         T v[B];
 #pragma unroll
-        for (int l = 0; l < B; ++l) {
-          const uint64_t addr = base + 32u * (h + l) + lane;
-          if (addr >= start && addr < end) v[l] = ld_gather(k1 + a[h + l]);
-        }
+        for (int l = 0; l < B; ++l) v[l] = ld_gather(k1 + a[h + l]);
 #pragma unroll
-        for (int l = 0; l < B; ++l) {
-          const uint64_t addr = base + 32u * (h + l) + lane;
-          if (addr >= start && addr < end) st_stream(k2_out + (addr - start), v[l]);
-        }
+        for (int l = 0; l < B; ++l) st_stream(k2 + (out_base | sh.ltab[h + l] | lane), v[l]);
       }
     }
   }
 }
 
 // --------------------------------------------------------------------- apply
-// k2[r] = k1[perm[r]]: perm streamed with 128-bit loads (4 indices), the
-// gathers issued back to back (8 in flight per thread), k2 streamed out.
+// Natural order: k2[r] = k1[perm[r]]: perm streamed with 128-bit loads (4
+// indices), the gathers issued back to back (8 in flight per thread).
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_apply(const uint32_t* __restrict__ perm, uint64_t count, const T* __restrict__ k1,
@@ -207,6 +343,40 @@ k_apply(const uint32_t* __restrict__ perm, uint64_t count, const T* __restrict__
   if (blockIdx.x == 0 && threadIdx.x < (count & 3u)) {
     const uint64_t r = (ngroups << 2) + threadIdx.x;
     k2[r] = ld_gather(k1 + perm[r]);
+  }
+}
+
+// Sigma order (M >= 10): each warp takes U groups of 32 consecutive
+// counters per iteration (perm: one 128-B line per group, k2: 256 B), chunks
+// of 2^chunk_log2 counters from the ticket.
+template <typename T, int U>
+__global__ void __launch_bounds__(256)
+k_apply_sigma(const __grid_constant__ SigmaParams sp, const uint32_t* __restrict__ perm,
+              uint64_t N, const T* __restrict__ k1, T* __restrict__ k2) {
+  __shared__ uint32_t tab[4][256];
+  __shared__ uint64_t s_chunk;
+  sigma_tables(sp, tab);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint64_t chunk = 1ull << sp.chunk_log2;
+  const uint64_t nchunks = N >> sp.chunk_log2;
+  for (uint64_t ch = next_chunk(sp, 0, &s_chunk, true); ch < nchunks;
+       ch = next_chunk(sp, ch, &s_chunk, false)) {
+    const uint64_t c0 = ch << sp.chunk_log2;
+    for (uint64_t c = c0 + (uint64_t)warp * 32u * U; c < c0 + chunk;
+         c += (uint64_t)nwarps * 32u * U) {
+      uint32_t idx[U];
+      uint32_t src[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        idx[u] = sigma_apply(tab, c + 32u * u) | lane;
+        src[u] = __ldcs(perm + idx[u]);
+      }
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = ld_gather(k1 + src[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_stream(k2 + idx[u], v[u]);
+    }
   }
 }
 

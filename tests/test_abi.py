@@ -81,8 +81,12 @@ def test_validation_errors_without_gpu(q):
     assert L.qsim_apply_map(FAKE, 4, q.C64, FAKE * 4, FAKE + 32, None) == q.EALIAS
     assert L.qsim_apply_map(FAKE, 4, q.C128, FAKE * 4, FAKE * 4 + 128, None) == q.EALIAS
     # run_host: bad mode, missing perm workspace
-    assert L.qsim_run_host(gp, 1, 4, q.C64, 5, FAKE, FAKE, FAKE, FAKE * 4, FAKE * 8, None) == q.EINVAL
-    assert L.qsim_run_host(gp, 1, 4, q.C64, 0, FAKE, FAKE, FAKE, FAKE * 4, None, None) == q.EINVAL
+    assert L.qsim_run_host(gp, 1, 4, q.C64, 5, FAKE, FAKE, FAKE, FAKE * 4, FAKE * 8, None,
+                           None) == q.EINVAL
+    assert L.qsim_run_host(gp, 1, 4, q.C64, 0, FAKE, FAKE, FAKE, FAKE * 4, None, None,
+                           None) == q.EINVAL
+    assert L.qsim_run_host(gp, 1, 4, q.C64, 0, FAKE, FAKE, FAKE, FAKE * 4, FAKE * 8, FAKE + 8,
+                           None) == q.EINVAL
 
 
 @pytest.mark.parametrize("bad,code", [
@@ -99,6 +103,37 @@ def test_gate_validation(q, bad, code):
     assert rc == getattr(q, code)
     rc = q.lib().qsim_run_fused(g.ctypes.data, 2, 4, q.C64, FAKE, FAKE * 4, None)
     assert rc == getattr(q, code)
+
+
+def test_plan_create_and_validation(q):
+    """Plans are host-only: create them and check the validator (no launch)."""
+    g = wl.CONFIGS["cfg2"].gates()
+    plan = q.plan_create(g, 20, "c64")
+    sig = list(plan.sigma)[:20]
+    assert sorted(sig) == list(range(20)) and sig[:5] == [0, 1, 2, 3, 4]
+    assert plan.chunk_log2 == 16 and plan.blocks_per_sm == 2
+    # deterministic
+    assert list(q.plan_create(g, 20, "c64").sigma) == list(plan.sigma)
+    L = q.lib()
+    import ctypes
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.sigma[3], bad.sigma[7] = bad.sigma[7], bad.sigma[3]          # moves a lane bit
+    assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.sigma[9] = bad.sigma[10]                                      # not a permutation
+    assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.chunk_log2 = 9
+    assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.blocks_per_sm = 0
+    assert L.qsim_run_fused_planned(ctypes.byref(bad), g.ctypes.data, 64, FAKE * 4, FAKE * 64,
+                                    None, None) == q.EINVAL
+    # gates must validate against the plan's M
+    assert L.qsim_run_fused_planned(ctypes.byref(plan), g.ctypes.data, 64, FAKE * 4, FAKE * 64,
+                                    FAKE + 8, None) in (q.EINVAL,)
+    with pytest.raises(q.QsimError):
+        q.plan_create(g, 19, "c64")                                    # bit 19 >= M
 
 
 def test_unused_control_slots_are_ignored(q):

@@ -121,6 +121,65 @@ def test_apply_ragged_counts(q):
         assert k2.cpu().numpy()[:count * 16].tobytes() == oracle.apply_map(perm[:count], k1).tobytes()
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("M", [10, 11, 14, 17])
+def test_planned_apply_and_fused(q, M, dtype):
+    """sigma-ordered traversal (plans): same bytes as the oracle for every
+    chunk size / occupancy / scheduling variant."""
+    gates = wl.random_gates(80, M, 70 + M)
+    k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 7 + M))
+    ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+    k1_d = _to_dev(k1)
+    perm = _new_perm(1 << M)
+    q.build_map(gates, M, perm)
+    plan = q.plan_create(gates, M, dtype)
+    assert sorted(list(plan.sigma)[:M]) == list(range(M))
+    ws = q.workspace()
+    for cl in sorted({10, min(M, 12), M}):
+        for bps in (1, 2, 8):
+            for w in (ws, None):
+                plan.chunk_log2, plan.blocks_per_sm = cl, bps
+                out = torch.empty_like(k1_d)
+                q.apply_map_planned(plan, perm, k1_d, out, w)
+                outf = torch.empty_like(k1_d)
+                q.run_fused_planned(plan, gates, k1_d, outf, w)
+                torch.cuda.synchronize()
+                assert out.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
+                assert outf.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
+
+
+def test_planned_small_M_falls_back_to_natural(q):
+    for M in (1, 3, 9):
+        gates = wl.random_gates(20, M, M) if M >= 3 else wl.gates_array([wl.gate(wl.NOT, 0)])
+        k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 1))
+        ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+        plan = q.plan_create(gates, M, "c64")
+        k1_d = _to_dev(k1)
+        perm = _new_perm(1 << M)
+        q.build_map(gates, M, perm)
+        out, outf = torch.empty_like(k1_d), torch.empty_like(k1_d)
+        q.apply_map_planned(plan, perm, k1_d, out, q.workspace())
+        q.run_fused_planned(plan, gates, k1_d, outf, q.workspace())
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == ref.tobytes()
+        assert outf.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_run_host_end_to_end(q):
+    M = 16
+    gates = wl.random_gates(64, M, 33)
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 33))
+    ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+    for mode in (q.MATERIALISED, q.FUSED):
+        k1_h = torch.from_numpy(k1.view(np.uint8).copy()).pin_memory()
+        k2_h = torch.empty_like(k1_h).pin_memory()
+        k1_d = torch.empty(k1_h.numel(), dtype=torch.uint8, device=DEV)
+        k2_d = torch.empty_like(k1_d)
+        perm = _new_perm(1 << M)
+        q.run_host(gates, M, mode, k1_h, k2_h, k1_d, k2_d, perm, q.workspace(), dtype="c64")
+        assert k2_h.numpy().tobytes() == ref.tobytes(), mode
+
+
 def test_special_values_survive(q):
     """-0.0, NaN payloads, denormals, inf: moved as bits (R15)."""
     M = 11
@@ -241,6 +300,17 @@ def _full_config(q, name, fused):
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d)
     if fused:
         assert torch.equal(k2_d, k2f_d)          # materialised == fused, every byte
+    # the planned (sigma-ordered) calls bench.py times: same bytes
+    plan = q.plan_create(gates, cfg.M, cfg.dtype)
+    ws = q.workspace()
+    k2p = torch.empty_like(k2_d)
+    q.apply_map_planned(plan, perm_d, k1_d, k2p, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(k2_d, k2p)
+    q.run_fused_planned(plan, gates, k1_d, k2p, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(k2_d, k2p)
+    del k2p
     # perm(reverse G) o perm(G) == identity over all 2^M outputs (group identity)
     rev_d = torch.empty_like(perm_d)
     q.build_map(gates[::-1].copy(), cfg.M, rev_d)
@@ -277,17 +347,23 @@ def test_cfg5_full_size_sampled(q):
         k1_d[s * 8:(s + chunk) * 8].copy_(torch.from_numpy(k1_host[s:s + chunk].view(np.uint8)))
     perm_d = torch.empty(N, dtype=torch.int32, device=DEV)
     k2_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
+    plan = q.plan_create(gates, cfg.M, "c64")
+    ws = q.workspace()
     q.build_map(gates, cfg.M, perm_d)
-    q.apply_map(perm_d, cfg.M, k1_d, k2_d, dtype="c64")
+    q.apply_map_planned(plan, perm_d, k1_d, k2_d, ws)       # the bench's launch config
     torch.cuda.synchronize()
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, None)
-    # fused == materialised over all 2^32 entries, compared chunk-wise on device
+    # every other path == the planned apply over all 2^32 entries (on device)
     k2f_d = torch.empty_like(k2_d)
-    q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype="c64")
-    torch.cuda.synchronize()
+    for run in (lambda: q.run_fused_planned(plan, gates, k1_d, k2f_d, ws),
+                lambda: q.apply_map(perm_d, cfg.M, k1_d, k2f_d, dtype="c64"),
+                lambda: q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype="c64")):
+        k2f_d.zero_()
+        run()
+        torch.cuda.synchronize()
+        for s in range(0, N * 8, 1 << 32):
+            assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2f_d, None)
-    for s in range(0, N * 8, 1 << 32):
-        assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
     del k2f_d, k2_d, k1_d
     # group identity at full size: perm(rev G)[perm(G)[i]] == i for all 2^32 i
     rev_d = torch.empty_like(perm_d)
