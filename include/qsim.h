@@ -155,9 +155,11 @@ typedef struct qsim_plan {
     int32_t M;
     int32_t dtype;          /* QSIM_C64 / QSIM_C128: a 128-B line holds 16 / 8 entries */
     uint32_t chunk_log2;    /* counters per CTA chunk (default 16), within [10, M] */
-    int32_t blocks_per_sm;  /* resident CTAs per SM (default 2), 1..8          */
+    int32_t blocks_per_sm;  /* resident CTAs per SM (default 1), 1..8          */
     uint32_t flags;         /* bit 0: natural order (no sigma)                 */
-    uint32_t reserved;
+    uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
+    uint16_t cta_threads;   /* apply kernel CTA size: 256, 512 or 1024 (0 = 256)    */
+    uint32_t fused_chunk_log2; /* counters per CTA chunk of the fused kernel (default 19) */
     uint8_t sigma[32];      /* counter bit k -> output bit sigma[k]            */
     float change_freq[32];  /* per output bit: fraction of sampled k1 lines whose
                                readers differ in that bit                     */

@@ -50,7 +50,8 @@ class Plan(ctypes.Structure):
     """qsim_plan (include/qsim.h): traversal order of the gather."""
     _fields_ = [("M", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("chunk_log2", ctypes.c_uint32), ("blocks_per_sm", ctypes.c_int32),
-                ("flags", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("flags", ctypes.c_uint32), ("ilp", ctypes.c_uint16),
+                ("cta_threads", ctypes.c_uint16), ("fused_chunk_log2", ctypes.c_uint32),
                 ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32)]
 
 

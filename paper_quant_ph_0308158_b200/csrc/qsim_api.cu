@@ -247,16 +247,23 @@ int plan_validate(const qsim_plan* p) {
   }
   if (seen != ((1ull << p->M) - 1)) return QSIM_EINVAL;
   if (p->M >= 10 && (p->chunk_log2 < 10 || (int)p->chunk_log2 > p->M)) return QSIM_EINVAL;
+  if (p->M >= 10 && (p->fused_chunk_log2 < 10 || (int)p->fused_chunk_log2 > p->M))
+    return QSIM_EINVAL;
   if (p->blocks_per_sm < 1 || p->blocks_per_sm > 8) return QSIM_EINVAL;
+  if (p->ilp != 0 && p->ilp != 8 && p->ilp != 16 && p->ilp != 32) return QSIM_EINVAL;
+  if (p->cta_threads != 0 && p->cta_threads != 256 && p->cta_threads != 512 &&
+      p->cta_threads != 1024)
+    return QSIM_EINVAL;
+  if (p->ilp == 32 && p->cta_threads == 1024) return QSIM_EINVAL;  // register file
   return QSIM_OK;
 }
 
 bool plan_natural(const qsim_plan* p) { return (p->flags & 1u) || p->M < 10; }
 
-qsim::SigmaParams plan_params(const qsim_plan* p, void* workspace) {
+qsim::SigmaParams plan_params(const qsim_plan* p, void* workspace, bool fused = false) {
   qsim::SigmaParams sp;
   std::memcpy(sp.sigma, p->sigma, 32);
-  sp.chunk_log2 = p->chunk_log2;
+  sp.chunk_log2 = fused ? p->fused_chunk_log2 : p->chunk_log2;
   sp.nbits = (uint32_t)p->M;
   sp.ticket = static_cast<unsigned long long*>(workspace);
   return sp;
@@ -273,7 +280,10 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   plan->M = M;
   plan->dtype = dtype;
   plan->chunk_log2 = M < 16 ? (uint32_t)M : 16u;
-  plan->blocks_per_sm = 2;
+  plan->fused_chunk_log2 = M < 19 ? (uint32_t)M : 19u;
+  plan->blocks_per_sm = 1;
+  plan->ilp = 16;
+  plan->cta_threads = 256;
   for (int k = 0; k < 32; ++k) plan->sigma[k] = (uint8_t)k;
   if (M < 10) {
     plan->flags = 1;
@@ -311,6 +321,35 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   return QSIM_OK;
 }
 
+// The gather wants most of the unified L1/shared array as L1 (the reuse
+// cache of k1 lines): ask for the smallest carveout that still fits
+// blocks_per_sm CTAs (4 KB sigma tables + 1 KB driver reserve each).
+template <typename T, int U, int THREADS>
+void launch_apply_sigma_u(int bps, unsigned blocks, const qsim::SigmaParams& sp,
+                          const uint32_t* perm, uint64_t N, const T* k1, T* k2, cudaStream_t st) {
+  const int pct = (bps * 5200 * 100 + 228 * 1024 - 1) / (228 * 1024);
+  cudaFuncSetAttribute(qsim::k_apply_sigma<T, U, THREADS>,
+                       cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+  qsim::k_apply_sigma<T, U, THREADS><<<blocks, THREADS, 0, st>>>(sp, perm, N, k1, k2);
+}
+
+template <typename T, int U>
+void launch_apply_sigma_t(uint32_t threads, int bps, unsigned blocks, const qsim::SigmaParams& sp,
+                          const uint32_t* perm, uint64_t N, const T* k1, T* k2, cudaStream_t st) {
+  if (threads == 512) launch_apply_sigma_u<T, U, 512>(bps, blocks, sp, perm, N, k1, k2, st);
+  else if (threads == 1024) launch_apply_sigma_u<T, (U > 16 ? 16 : U), 1024>(bps, blocks, sp, perm, N, k1, k2, st);
+  else launch_apply_sigma_u<T, U, 256>(bps, blocks, sp, perm, N, k1, k2, st);
+}
+
+template <typename T>
+void launch_apply_sigma(uint32_t ilp, uint32_t threads, int bps, unsigned blocks,
+                        const qsim::SigmaParams& sp, const uint32_t* perm, uint64_t N, const T* k1,
+                        T* k2, cudaStream_t st) {
+  if (ilp == 8) launch_apply_sigma_t<T, 8>(threads, bps, blocks, sp, perm, N, k1, k2, st);
+  else if (ilp == 32) launch_apply_sigma_t<T, 32>(threads, bps, blocks, sp, perm, N, k1, k2, st);
+  else launch_apply_sigma_t<T, 16>(threads, bps, blocks, sp, perm, N, k1, k2, st);
+}
+
 int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* k1, void* k2,
                        void* workspace, cudaStream_t st) {
   int rc = plan_validate(plan);
@@ -328,12 +367,14 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
   const uint64_t nchunks = N >> sp.chunk_log2;
   uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
   if (blocks > nchunks) blocks = nchunks;
+  const uint32_t ilp = plan->ilp ? plan->ilp : 16u;
+  const uint32_t thr = plan->cta_threads ? plan->cta_threads : 256u;
   if (plan->dtype == QSIM_C64)
-    qsim::k_apply_sigma<uint2, 8><<<(unsigned)blocks, 256, 0, st>>>(
-        sp, perm, N, static_cast<const uint2*>(k1), static_cast<uint2*>(k2));
+    launch_apply_sigma<uint2>(ilp, thr, plan->blocks_per_sm, (unsigned)blocks, sp, perm, N,
+                              static_cast<const uint2*>(k1), static_cast<uint2*>(k2), st);
   else
-    qsim::k_apply_sigma<uint4, 8><<<(unsigned)blocks, 256, 0, st>>>(
-        sp, perm, N, static_cast<const uint4*>(k1), static_cast<uint4*>(k2));
+    launch_apply_sigma<uint4>(ilp, thr, plan->blocks_per_sm, (unsigned)blocks, sp, perm, N,
+                              static_cast<const uint4*>(k1), static_cast<uint4*>(k2), st);
   QSIM_CHECK_LAUNCH("k_apply_sigma");
   return QSIM_OK;
 }
@@ -343,7 +384,7 @@ int launch_fused_sigma(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
                        void* workspace, cudaStream_t st) {
   std::unique_ptr<qsim::GateList<CAP>> gl(new qsim::GateList<CAP>);
   pack_gates<CAP>(gates, n, true, *gl);
-  const qsim::SigmaParams sp = plan_params(plan, workspace);
+  const qsim::SigmaParams sp = plan_params(plan, workspace, true);
   int rc = reset_ticket(workspace, st);
   if (rc) return rc;
   const uint64_t N = 1ull << plan->M;
@@ -353,6 +394,10 @@ int launch_fused_sigma(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
   const size_t smem = qsim::bs_smem_bytes((uint32_t)n);
   cudaFuncSetAttribute(qsim::k_fused_sigma<CAP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
+  // leave the rest of the unified array to L1 (reuse cache of k1 lines)
+  const int pct = (int)(((smem + 1024) * plan->blocks_per_sm * 100 + 228 * 1024 - 1) / (228 * 1024));
+  cudaFuncSetAttribute(qsim::k_fused_sigma<CAP, T>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       pct > 100 ? 100 : pct);
   qsim::k_fused_sigma<CAP, T><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(*gl, sp, N, k1, k2);
   QSIM_CHECK_LAUNCH("k_fused_sigma");
   return QSIM_OK;

@@ -349,8 +349,8 @@ k_apply(const uint32_t* __restrict__ perm, uint64_t count, const T* __restrict__
 // Sigma order (M >= 10): each warp takes U groups of 32 consecutive
 // counters per iteration (perm: one 128-B line per group, k2: 256 B), chunks
 // of 2^chunk_log2 counters from the ticket.
-template <typename T, int U>
-__global__ void __launch_bounds__(256)
+template <typename T, int U, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 k_apply_sigma(const __grid_constant__ SigmaParams sp, const uint32_t* __restrict__ perm,
               uint64_t N, const T* __restrict__ k1, T* __restrict__ k2) {
   __shared__ uint32_t tab[4][256];

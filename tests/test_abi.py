@@ -111,7 +111,7 @@ def test_plan_create_and_validation(q):
     plan = q.plan_create(g, 20, "c64")
     sig = list(plan.sigma)[:20]
     assert sorted(sig) == list(range(20)) and sig[:5] == [0, 1, 2, 3, 4]
-    assert plan.chunk_log2 == 16 and plan.blocks_per_sm == 2
+    assert plan.chunk_log2 == 16 and plan.blocks_per_sm == 1
     # deterministic
     assert list(q.plan_create(g, 20, "c64").sigma) == list(plan.sigma)
     L = q.lib()
@@ -124,6 +124,13 @@ def test_plan_create_and_validation(q):
     assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
     bad = q.Plan.from_buffer_copy(plan)
     bad.chunk_log2 = 9
+    assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.fused_chunk_log2 = 21
+    assert L.qsim_run_fused_planned(ctypes.byref(bad), g.ctypes.data, 64, FAKE * 4, FAKE * 64,
+                                    None, None) == q.EINVAL
+    bad = q.Plan.from_buffer_copy(plan)
+    bad.ilp = 12
     assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
     bad = q.Plan.from_buffer_copy(plan)
     bad.blocks_per_sm = 0

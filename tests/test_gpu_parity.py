@@ -138,7 +138,7 @@ def test_planned_apply_and_fused(q, M, dtype):
     for cl in sorted({10, min(M, 12), M}):
         for bps in (1, 2, 8):
             for w in (ws, None):
-                plan.chunk_log2, plan.blocks_per_sm = cl, bps
+                plan.chunk_log2, plan.blocks_per_sm, plan.fused_chunk_log2 = cl, bps, cl
                 out = torch.empty_like(k1_d)
                 q.apply_map_planned(plan, perm, k1_d, out, w)
                 outf = torch.empty_like(k1_d)

@@ -21,6 +21,9 @@ def main():
     ap.add_argument("--config", default="cfg5")
     ap.add_argument("--chunks", default="11,12,14,16")
     ap.add_argument("--bps", default="2,4,8")
+    ap.add_argument("--ilp", default="16")
+    ap.add_argument("--threads", default="256")
+    ap.add_argument("--modes", default="apply,fused")
     args = ap.parse_args()
     cfg = wl.CONFIGS[args.config]
     gates, M, N = cfg.gates(), cfg.M, cfg.N
@@ -35,11 +38,15 @@ def main():
     useful = N * (4 + 2 * e)
     plan = q.plan_create(gates, M, cfg.dtype)
     ws = q.workspace()
-    for mode, cl, bps in itertools.product(("apply", "fused"), map(int, args.chunks.split(",")),
-                                           map(int, args.bps.split(","))):
-        if cl > M:
+    for mode, cl, bps, ilp, thr in itertools.product(args.modes.split(","),
+                                                     map(int, args.chunks.split(",")),
+                                                     map(int, args.bps.split(",")),
+                                                     map(int, args.ilp.split(",")),
+                                                     map(int, args.threads.split(","))):
+        if cl > M or (ilp == 32 and thr == 1024):
             continue
-        plan.chunk_log2, plan.blocks_per_sm = cl, bps
+        plan.chunk_log2, plan.blocks_per_sm, plan.ilp, plan.cta_threads = cl, bps, ilp, thr
+        plan.fused_chunk_log2 = cl
         out.zero_()
         if mode == "apply":
             ms = timeit(lambda: q.apply_map_planned(plan, perm, k1, out, ws))
@@ -47,7 +54,7 @@ def main():
             ms = timeit(lambda: q.run_fused_planned(plan, gates, k1, out, ws))
         ok = bool(torch.equal(out, ref))
         print(json.dumps({"config": args.config, "mode": mode, "chunk_log2": cl,
-                          "bps": bps, "ms": round(ms, 3), "GBps": round((useful if mode == "apply" else N * 2 * e) / ms / 1e6, 1),
+                          "bps": bps, "ilp": ilp, "threads": thr, "ms": round(ms, 3), "GBps": round((useful if mode == "apply" else N * 2 * e) / ms / 1e6, 1),
                           "equal": ok}), flush=True)
 
 
