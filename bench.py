@@ -347,6 +347,9 @@ def run_qsim(args):
         "gpu_launches_fused_loop": launches_fused,
         "clocks": clocks,
         "setup_s": t_setup,
+        "jit": {"status": q.jit_status(), "compile_ms": q.jit_last_compile_ms(),
+                "note": "build_map uses a kernel NVRTC-compiled for the circuit on first use "
+                        "(warm-up); timed steps reuse it"},
         "plan": {"seconds": t_plan, "sigma": list(plan.sigma)[:M], "chunk_log2": plan.chunk_log2,
                  "blocks_per_sm": plan.blocks_per_sm,
                  "note": "qsim_plan_create (host sampling of the circuit) runs once per circuit, "

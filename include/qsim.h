@@ -117,14 +117,19 @@ int qsim_run_fused_range(const qsim_gate *gates, int32_t n_gates, int32_t M,
                          const void *k1, void *k2_out, void *stream);
 
 /* Walk algorithm selection for build / fused (ablation and tests).
- *   QSIM_WALK_AUTO       library choice (bit-sliced)
+ *   QSIM_WALK_AUTO       library choice: build with >= 2^22 outputs uses the
+ *                        circuit-specialised JIT kernel when NVRTC loads
+ *                        (compiled once per circuit per process, then
+ *                        cached), else the bit-sliced interpreter
  *   QSIM_WALK_PER_LANE   one address per lane, 2 integer ops per gate
  *   QSIM_WALK_BITSLICED  32 addresses per thread, one bit-plane word per
  *                        address bit in shared memory, one logic op per gate */
 typedef enum qsim_walk {
     QSIM_WALK_AUTO = 0,
     QSIM_WALK_PER_LANE = 1,
-    QSIM_WALK_BITSLICED = 2
+    QSIM_WALK_BITSLICED = 2,
+    QSIM_WALK_JIT = 3       /* build only: kernel compiled for this circuit (NVRTC);
+                               QSIM_ECUDA if NVRTC is unavailable                */
 } qsim_walk;
 
 int qsim_build_map_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
@@ -204,6 +209,14 @@ int32_t qsim_last_launch_count(void);
 
 const char *qsim_strerror(int32_t code);
 const char *qsim_last_error(void);
+/* JIT diagnostics: "ready", or why the JIT path is unavailable; duration of
+ * the most recent NVRTC compile (0 if none).                               */
+const char *qsim_jit_status(void);
+double qsim_jit_last_compile_ms(void);
+/* NVRTC-compiles (does not load or launch) the circuit-specialised build
+ * kernel for this gate list; works without a GPU.  QSIM_ECUDA with the
+ * NVRTC log in qsim_last_error() on failure.                               */
+int qsim_jit_check_compile(const qsim_gate *gates, int32_t n_gates, int32_t M);
 int32_t qsim_abi_version(void);
 
 #ifdef __cplusplus

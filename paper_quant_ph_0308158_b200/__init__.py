@@ -28,7 +28,7 @@ LIB_PATH = os.path.join(_PKG, "libqsim.so")
 
 OK, EINVAL, ERANGE, EBIT, ECAP, EALIAS, ECUDA = 0, -1, -2, -3, -4, -5, -6
 C64, C128 = 0, 1
-WALK_AUTO, WALK_PER_LANE, WALK_BITSLICED = 0, 1, 2
+WALK_AUTO, WALK_PER_LANE, WALK_BITSLICED, WALK_JIT = 0, 1, 2, 3
 MAX_GATES = 4096
 MATERIALISED, FUSED = 0, 1
 
@@ -85,6 +85,8 @@ def _load() -> ctypes.CDLL:
     lib.qsim_last_error.argtypes = []
     lib.qsim_last_error.restype = ctypes.c_char_p
     lib.qsim_abi_version.restype = i32
+    lib.qsim_jit_status.restype = ctypes.c_char_p
+    lib.qsim_jit_last_compile_ms.restype = ctypes.c_double
     lib.qsim_last_launch_count.restype = i32
     return lib
 
@@ -216,6 +218,14 @@ def workspace(device=None):
     import torch
     return torch.zeros(WORKSPACE_BYTES, dtype=torch.uint8,
                        device=device if device is not None else "cuda")
+
+
+def jit_status() -> str:
+    return _lib.qsim_jit_status().decode()
+
+
+def jit_last_compile_ms() -> float:
+    return float(_lib.qsim_jit_last_compile_ms())
 
 
 def last_launch_count() -> int:

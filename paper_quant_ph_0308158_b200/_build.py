@@ -17,7 +17,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 
 TARGETS = {
-    LIB: (os.path.join(CSRC, "*.cu"), os.path.join(CSRC, "*.cuh"), "qsim.h"),
+    LIB: (os.path.join(CSRC, "*.cu"), os.path.join(CSRC, "*.h*"), "qsim.h"),
     MB_LIB: ([os.path.join(CSRC, "mb", "*.cu"), os.path.join(CSRC, "qsim_tma_host.cu")],
              os.path.join(CSRC, "*.cuh"), "qsim_mb.h"),
 }
@@ -43,7 +43,7 @@ def build_one(lib, force=False, verbose=False) -> str:
         return lib
     cus, _, _ = sources(lib)
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp, *cus]
+    cmd = [NVCC, *FLAGS, "-o", tmp, *cus, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
@@ -62,4 +62,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    import sys
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)

@@ -9,8 +9,10 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <string>
 
 #include "qsim.h"
+#include "qsim_jit.h"
 #include "qsim_kernels.cuh"
 
 namespace {
@@ -166,13 +168,32 @@ int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, ui
                                                    walk, st);
 }
 
+// Large builds use the circuit-specialised kernel (qsim_jit.cu) when NVRTC
+// is present; everything else (and any JIT failure under AUTO) uses the
+// shared-memory bit-sliced interpreter.
+constexpr uint64_t kJitMinCount = 1ull << 22;
+
 int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                uint32_t* perm_out, int32_t walk, cudaStream_t st) {
   int rc = check_gates(gates, n, M);
   if (rc) return rc;
   if ((rc = check_range(M, start, count))) return rc;
-  if (walk < 0 || walk > 2) return QSIM_EINVAL;
+  if (walk < 0 || walk > 3) return QSIM_EINVAL;
   if (perm_out == nullptr || !aligned16(perm_out)) return QSIM_EINVAL;
+  if (walk == QSIM_WALK_JIT || (walk == QSIM_WALK_AUTO && count >= kJitMinCount)) {
+    std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+    pack_gates(gates, n, false, *gl);
+    std::string err;
+    if (qsim::jit_build(gl->w, n, M, start, count, perm_out, sm_count(), st, err) == 0) {
+      if (count) ++g_launches;
+      return QSIM_OK;
+    }
+    if (walk == QSIM_WALK_JIT) {
+      std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+      return QSIM_ECUDA;
+    }
+    walk = QSIM_WALK_BITSLICED;
+  }
   return launch_walk<0, uint2>(gates, n, M, start, count, perm_out, nullptr, nullptr, walk, st);
 }
 
@@ -577,6 +598,24 @@ const char* qsim_strerror(int32_t code) {
 }
 
 const char* qsim_last_error(void) { return g_err; }
+
+const char* qsim_jit_status(void) { return qsim::jit_status(); }
+
+double qsim_jit_last_compile_ms(void) { return qsim::jit_last_compile_ms(); }
+
+int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
+  g_launches = 0;
+  int rc = check_gates(gates, n_gates, M);
+  if (rc) return rc;
+  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+  pack_gates(gates, n_gates, false, *gl);
+  std::string err;
+  if (qsim::jit_check_compile(gl->w, n_gates, M, err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+    return QSIM_ECUDA;
+  }
+  return QSIM_OK;
+}
 
 int32_t qsim_abi_version(void) { return 1; }
 

@@ -1,0 +1,344 @@
+// qsim_jit.cu -- circuit-specialised walk kernels compiled at run time.
+//
+// The bit-sliced walk keeps 32 addresses per thread as 32 bit-plane words
+// (qsim_kernels.cuh).  With a run-time gate list the planes must live in
+// shared memory (dynamic indices); compiled for one circuit they live in
+// registers and a step of the wiring diagram (toggle the target bit
+// when all control bits are 1) is one LOP3 for 32 addresses:
+//     p_t ^= p_c0 & p_c1        (CCNOT)      p_t ^= p_c (CNOT)
+// and a NOT costs nothing: the generator tracks each plane's polarity and
+// folds the inversion into the logic ops that read it (one final NOT per
+// inverted plane).  Gates are emitted last -> first (readings R1, R2).
+//
+// NVRTC is loaded with dlopen (no link-time dependency); the compiled
+// module is cached per circuit for the life of the process.  If NVRTC or
+// the driver entry points are unavailable the caller falls back to the
+// shared-memory interpreter kernel (still this library's own CUDA code).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <chrono>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "qsim_jit.h"
+
+namespace qsim {
+namespace {
+
+// ---- NVRTC through dlopen -------------------------------------------------
+typedef int nvrtcResult_t;
+typedef struct _nvrtcProgram* nvrtcProgram_t;
+struct Nvrtc {
+  void* h = nullptr;
+  nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int, const char* const*,
+                          const char* const*) = nullptr;
+  nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*) = nullptr;
+  nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*cubin)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*log)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*destroy)(nvrtcProgram_t*) = nullptr;
+  bool ok = false;
+};
+
+struct Driver {
+  PFN_cuModuleLoadData_v2000 load = nullptr;
+  PFN_cuModuleGetFunction_v2000 getfn = nullptr;
+  PFN_cuLaunchKernel_v4000 launch = nullptr;
+  bool ok = false;
+};
+
+std::mutex g_mu;
+Nvrtc g_nvrtc;
+Driver g_drv;
+bool g_init = false;
+std::string g_status = "not initialised";
+
+template <typename F>
+bool sym(void* h, const char* name, F& f) {
+  f = reinterpret_cast<F>(dlsym(h, name));
+  return f != nullptr;
+}
+
+void init_locked() {
+  if (g_init) return;
+  g_init = true;
+  if (const char* off = std::getenv("QSIM_NO_JIT")) {
+    if (off[0] && off[0] != '0') {
+      g_status = "disabled by QSIM_NO_JIT";
+      return;
+    }
+  }
+  const char* cands[] = {std::getenv("QSIM_NVRTC"), "libnvrtc.so.12",
+                         "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    g_nvrtc.h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+    if (g_nvrtc.h) break;
+  }
+  if (!g_nvrtc.h) {
+    g_status = "libnvrtc not found";
+    return;
+  }
+  Nvrtc& n = g_nvrtc;
+  n.ok = sym(n.h, "nvrtcCreateProgram", n.create) && sym(n.h, "nvrtcCompileProgram", n.compile) &&
+         sym(n.h, "nvrtcGetCUBINSize", n.cubin_size) && sym(n.h, "nvrtcGetCUBIN", n.cubin) &&
+         sym(n.h, "nvrtcGetProgramLogSize", n.log_size) &&
+         sym(n.h, "nvrtcGetProgramLog", n.log) && sym(n.h, "nvrtcDestroyProgram", n.destroy);
+  if (!n.ok) {
+    g_status = "libnvrtc symbols missing";
+    return;
+  }
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  bool ok = true;
+  ok = ok && cudaGetDriverEntryPoint("cuModuleLoadData", &p, cudaEnableDefault, &q) == cudaSuccess &&
+       q == cudaDriverEntryPointSuccess;
+  g_drv.load = reinterpret_cast<PFN_cuModuleLoadData_v2000>(p);
+  ok = ok && cudaGetDriverEntryPoint("cuModuleGetFunction", &p, cudaEnableDefault, &q) ==
+                 cudaSuccess && q == cudaDriverEntryPointSuccess;
+  g_drv.getfn = reinterpret_cast<PFN_cuModuleGetFunction_v2000>(p);
+  ok = ok && cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess &&
+       q == cudaDriverEntryPointSuccess;
+  g_drv.launch = reinterpret_cast<PFN_cuLaunchKernel_v4000>(p);
+  g_drv.ok = ok;
+  g_status = ok ? "ready" : "driver entry points unavailable";
+}
+
+// ---- code generation --------------------------------------------------------
+const char* kPrelude = R"(
+typedef unsigned int u32;
+typedef unsigned long long u64;
+#define QSIM_TS(J, MASK, a)                                                     \
+  _Pragma("unroll") for (int k = 0; k < 32; ++k)                                \
+    if ((k & J) == 0) { u32 t = ((a[k] >> J) ^ a[k + J]) & MASK;                \
+                        a[k + J] ^= t; a[k] ^= t << J; }
+)";
+
+// Straight-line walk for one tile: planes p0..p31 in registers.
+std::string walk_code(const uint32_t* w, int n, int M) {
+  std::string s;
+  bool inv[33] = {false};
+  char buf[160];
+  auto ref = [&](uint32_t b) -> std::string {
+    return std::string(inv[b] ? "~p" : "p") + std::to_string(b);
+  };
+  for (int k = n - 1; k >= 0; --k) {
+    const uint32_t kind = w[k] & 0xffu, t = (w[k] >> 8) & 0xffu, c0 = (w[k] >> 16) & 0xffu,
+                   c1 = w[k] >> 24;
+    if (kind == 0) {
+      inv[t] = !inv[t];
+      continue;
+    }
+    if (kind == 1)
+      std::snprintf(buf, sizeof buf, "  p%u ^= %s;\n", t, ref(c0).c_str());
+    else
+      std::snprintf(buf, sizeof buf, "  p%u ^= %s & %s;\n", t, ref(c0).c_str(), ref(c1).c_str());
+    s += buf;
+  }
+  for (int b = 0; b < 32; ++b)
+    if (inv[b]) {
+      std::snprintf(buf, sizeof buf, "  p%d = ~p%d;\n", b, b);
+      s += buf;
+    }
+  (void)M;
+  return s;
+}
+
+std::string build_source(const uint32_t* w, int n, int M) {
+  std::string s = kPrelude;
+  s += R"(
+extern "C" __global__ void __launch_bounds__(256)
+qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
+    const u64 base = tile << 10;
+    const u32 b32 = (u32)base;
+)";
+  char buf[160];
+  for (int b = 0; b < 32; ++b) {
+    if (b < 5)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (b < 10) {
+      const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u",
+                            "0xffff0000u"};
+      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
+    } else
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += walk_code(w, n, M);
+  s += "    u32 a[32] = {";
+  for (int b = 0; b < 32; ++b) {
+    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += R"(
+    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
+    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
+    if (base >= start && base + 1024u <= end) {
+      _Pragma("unroll") for (int l = 0; l < 32; ++l)
+        __stcs(perm_out + (base - start + 32u * l + lane), a[l]);
+    } else {
+      _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+        const u64 addr = base + 32u * l + lane;
+        if (addr >= start && addr < end) __stcs(perm_out + (addr - start), a[l]);
+      }
+    }
+  }
+}
+)";
+  return s;
+}
+
+struct Entry {
+  std::vector<uint32_t> words;
+  int M;
+  CUfunction fn;
+  double compile_ms;
+};
+std::unordered_map<uint64_t, std::vector<Entry>> g_cache;
+double g_last_compile_ms = 0.0;
+
+uint64_t fnv(const uint32_t* w, int n, uint64_t salt) {
+  uint64_t h = 1469598103934665603ull ^ salt;
+  for (int k = 0; k < n; ++k) {
+    h ^= w[k];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+bool compile_cubin_locked(const std::string& src, std::vector<char>& cubin, std::string& err) {
+  Nvrtc& nv = g_nvrtc;
+  nvrtcProgram_t prog = nullptr;
+  if (nv.create(&prog, src.c_str(), "qsim_jit.cu", 0, nullptr, nullptr) != 0) {
+    err = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-default-device", "--std=c++17",
+                        "-lineinfo"};
+  const int rc = nv.compile(prog, 4, opts);
+  if (rc != 0) {
+    size_t ls = 0;
+    nv.log_size(prog, &ls);
+    std::string log(ls, '\0');
+    if (ls) nv.log(prog, &log[0]);
+    err = "nvrtc compile failed: " + log.substr(0, 400);
+    nv.destroy(&prog);
+    return false;
+  }
+  size_t cs = 0;
+  nv.cubin_size(prog, &cs);
+  cubin.resize(cs);
+  nv.cubin(prog, cubin.data());
+  nv.destroy(&prog);
+  if (const char* dir = std::getenv("QSIM_JIT_DUMP")) {  // debugging aid
+    const std::string base = std::string(dir) + "/qsim_jit_" + std::to_string(src.size());
+    if (FILE* f = std::fopen((base + ".cu").c_str(), "w")) {
+      std::fwrite(src.data(), 1, src.size(), f);
+      std::fclose(f);
+    }
+    if (FILE* f = std::fopen((base + ".cubin").c_str(), "wb")) {
+      std::fwrite(cubin.data(), 1, cubin.size(), f);
+      std::fclose(f);
+    }
+  }
+  return true;
+}
+
+CUfunction compile_locked(const std::string& src, const char* name, std::string& err) {
+  std::vector<char> cubin;
+  if (!compile_cubin_locked(src, cubin, err)) return nullptr;
+  CUmodule mod = nullptr;
+  if (g_drv.load(&mod, cubin.data()) != CUDA_SUCCESS) {
+    err = "cuModuleLoadData failed";
+    return nullptr;
+  }
+  CUfunction fn = nullptr;
+  if (g_drv.getfn(&fn, mod, name) != CUDA_SUCCESS) {
+    err = "cuModuleGetFunction failed";
+    return nullptr;
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool jit_available() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  return g_nvrtc.ok && g_drv.ok;
+}
+
+const char* jit_status() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  return g_status.c_str();
+}
+
+double jit_last_compile_ms() { return g_last_compile_ms; }
+
+int jit_check_compile(const uint32_t* words, int n, int M, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(build_source(words, n, M), cubin, err) ? 0 : -1;
+}
+
+// words: per-lane gate format (kind | t << 8 | c0 << 16 | c1 << 24).
+int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t count,
+              uint32_t* perm_out, int sms, cudaStream_t st, std::string& err) {
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    const uint64_t key = fnv(words, n, 0x6275696c64ull);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && (int)e.words.size() == n &&
+          std::memcmp(e.words.data(), words, n * sizeof(uint32_t)) == 0)
+        fn = e.fn;
+    if (!fn) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const std::string src = build_source(words, n, M);
+      fn = compile_locked(src, "qsim_jit_build", err);
+      if (!fn) return -1;
+      g_last_compile_ms =
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      g_cache[key].push_back(
+          Entry{std::vector<uint32_t>(words, words + n), M, fn, g_last_compile_ms});
+    }
+  }
+  if (count == 0) return 0;
+  uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  uint64_t blocks = (te - tb + 7) / 8;
+  const uint64_t cap = (uint64_t)sms * 8;
+  if (blocks > cap) blocks = cap;
+  uint64_t end = start + count;
+  void* args[] = {&start, &end, &tb, &te, &perm_out};
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+}  // namespace qsim

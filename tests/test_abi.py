@@ -149,3 +149,17 @@ def test_unused_control_slots_are_ignored(q):
     range of count 0 (nothing is launched)."""
     g = np.ascontiguousarray(np.array([[0, 1, 200, 17], [1, 2, 0, 99]], dtype=np.uint8))
     assert q.lib().qsim_build_map_range(g.ctypes.data, 2, 3, 0, 0, FAKE, None) == q.OK
+
+
+def test_jit_source_compiles_without_gpu(q):
+    """The circuit-specialised build kernel is generated and NVRTC-compiled
+    for sm_100a on the host (load/launch needs the GPU)."""
+    L = q.lib()
+    L.qsim_jit_check_compile.restype = ctypes.c_int
+    for gates, M in ((wl.CONFIGS["cfg5"].gates(), 32), (wl.CONFIGS["cfg4"].gates(), 30),
+                     (np.zeros((0, 4), np.uint8), 5), (wl.CONFIGS["cfg1"].gates(), 3)):
+        g = np.ascontiguousarray(gates)
+        rc = L.qsim_jit_check_compile(g.ctypes.data if len(g) else None, len(g), M)
+        if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+            pytest.skip("NVRTC not available here")
+        assert rc == q.OK, L.qsim_last_error().decode()

@@ -68,6 +68,32 @@ def test_build_full_small(q, M, walk):
         assert np.array_equal(_perm_np(perm)[:N], oracle.build_map(gates, M)), (M, n, walk)
 
 
+@pytest.mark.parametrize("M", [3, 10, 16, 23])
+def test_build_jit(q, M):
+    """Circuit-specialised (NVRTC) build kernel: full compare, ragged ranges."""
+    if q.jit_status() != "ready":
+        pytest.skip(f"JIT unavailable: {q.jit_status()}")
+    N = 1 << M
+    for seed, n in ((M, 0), (M + 1, 1), (M + 2, 64), (M + 3, 257)):
+        gates = wl.random_gates(n, M, seed)
+        want = oracle.build_map(gates, M)
+        perm = _new_perm(N)
+        q.build_map_range(gates, M, 0, N, perm, walk=q.WALK_JIT)
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(perm)[:N], want), (M, n)
+        for start, count in ((5, min(N - 5, 3000)), (N - 3, 3), (N // 2, N // 2)):
+            pr = _new_perm(count)
+            q.build_map_range(gates, M, start, count, pr, walk=q.WALK_JIT)
+            torch.cuda.synchronize()
+            assert np.array_equal(_perm_np(pr)[:count], want[start:start + count])
+    rg = wl.ripple_gates(M, 200) if M >= 3 else None
+    if rg is not None:
+        perm = _new_perm(N)
+        q.build_map_range(rg, M, 0, N, perm, walk=q.WALK_JIT)
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(perm)[:N], oracle.build_map(rg, M))
+
+
 @pytest.mark.parametrize("dtype", ["c64", "c128"])
 @pytest.mark.parametrize("M", [4, 12, 17])
 def test_apply_and_fused_full(q, M, dtype):
