@@ -20,6 +20,15 @@ extern "C" {
 #endif
 int qsim_mb_gather_c64(const uint32_t *idx, uint64_t count, const void *k1, void *k2,
                        int32_t variant, int32_t unroll, int32_t blocks, void *stream);
+/* qsim_mb_tma_gather_c64: the same gather with the TMA engine
+ * (cp.async.bulk.tensor tile::gather4, 16-byte rows) into shared memory;
+ * stages = producers * 100 + pipeline depth.
+ * qsim_mb_scatter_c64: k2[idx[r]] = k1[r] (divergent stores).            */
+int qsim_mb_tma_gather_c64(const uint32_t *idx, uint64_t count, const void *k1,
+                           uint64_t k1_entries, void *k2, int32_t stages, int32_t blocks,
+                           void *stream);
+int qsim_mb_scatter_c64(const uint32_t *idx, uint64_t count, const void *k1, void *k2,
+                        int32_t unroll, int32_t blocks, void *stream);
 #ifdef __cplusplus
 }
 #endif

@@ -193,3 +193,45 @@ extern "C" int qsim_mb_tma_gather_c64(const uint32_t* idx, uint64_t count, const
   }
   return cudaGetLastError() == cudaSuccess ? 0 : -6;
 }
+
+// ---------------------------------------------------------------------------
+// Scatter: k2[idx[r]] = k1[r] (complex64), k1 streamed, k2 written at
+// random positions -- the mirror image of the gather, to compare the cost of
+// divergent stores with divergent loads.
+namespace {
+template <int U>
+__global__ void __launch_bounds__(256)
+k_mb_scatter(const uint32_t* __restrict__ idx, uint64_t count, const uint2* __restrict__ k1,
+             uint2* __restrict__ k2) {
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += nthreads * U) {
+    uint32_t d[U];
+    uint2 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t rr = r + u * nthreads;
+      if (rr < count) { d[u] = __ldcs(idx + rr); v[u] = __ldcs(k1 + rr); }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t rr = r + u * nthreads;
+      if (rr < count) k2[d[u]] = v[u];
+    }
+  }
+}
+}  // namespace
+
+extern "C" int qsim_mb_scatter_c64(const uint32_t* idx, uint64_t count, const void* k1, void* k2,
+                                   int32_t unroll, int32_t blocks, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (blocks <= 0) blocks = 148 * 8;
+  const uint2* a = static_cast<const uint2*>(k1);
+  uint2* b = static_cast<uint2*>(k2);
+  switch (unroll) {
+    case 4: k_mb_scatter<4><<<blocks, 256, 0, st>>>(idx, count, a, b); break;
+    case 8: k_mb_scatter<8><<<blocks, 256, 0, st>>>(idx, count, a, b); break;
+    case 16: k_mb_scatter<16><<<blocks, 256, 0, st>>>(idx, count, a, b); break;
+    default: return -1;
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -6;
+}
