@@ -5,10 +5,13 @@ Metric (BASELINE.json): "state entries/sec and achieved HBM GB/s (fraction of
 8 TB/s) for map+gather at M=32".  Workload: config 5 (M = 32, 64 random
 NOT/CNOT/CCNOT gates, seed 4, complex64 Gaussian normalised state).
 
-One step = the whole hot path over the 2^32-entry state: qsim_build_map
-(materialise perm, uint32) then qsim_apply_map (k2[i] = k1[perm[i]]).  The
-fused mode (qsim_run_fused: the map recomputed in registers, no perm) is
-timed in its own loop and reported under "modes".  Inputs are larger than L2
+One step = the whole hot path over the 2^32-entry state, materialised:
+qsim_map_gather_planned computes the composite map perm (uint32, stored:
+"save information about the unitary matrix") and the state transform
+k2[i] = k1[perm[i]] in one kernel compiled for the circuit.  The
+two-call form (qsim_build_map then qsim_apply_map_planned) and the fused
+mode (qsim_run_fused_planned: the map recomputed, no perm) are timed in
+their own loops and reported under "modes".  Inputs are larger than L2
 (80 GiB working set vs 126 MB L2), so no flush is needed between steps.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg5]
@@ -241,6 +244,16 @@ def run_qsim(args):
                 marks.append(("apply_map", b, c))
         return n
 
+    def step_map_gather(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.map_gather_planned(plan, gates, perm, k1, k2, ws, stream=stream)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("map_gather", a, b))
+        return n
+
     def step_fused(marks):
         with torch.cuda.stream(stream):
             a = ev() if marks is not None else None
@@ -253,6 +266,8 @@ def run_qsim(args):
 
     sampler = ClockSampler(local)
     with sampler:
+        ms_mg, launches_mg, kern_mg = timed_loop(step_map_gather, args.steps, args.warmup,
+                                                 per_kernel=True)
         ms_mat, launches_mat, kern_mat = timed_loop(step_materialised, args.steps, args.warmup,
                                                     per_kernel=True)
         ms_fused, launches_fused, kern_fused = timed_loop(step_fused, args.steps, args.warmup,
@@ -280,7 +295,7 @@ def run_qsim(args):
         e2e = {"value": world * N * args.e2e_steps / dt, "unit": "entries/s",
                "h2d_bytes_per_step": N * e, "d2h_bytes_per_step": N * e,
                "ms_per_step": 1e3 * dt / args.e2e_steps,
-               "path": "qsim_run_host: H2D k1 (pinned), build_map, apply_map, D2H k2, sync"}
+               "path": "qsim_run_host: H2D k1 (pinned), map_gather (perm + k2), D2H k2, sync"}
         del k2_host
 
     # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
@@ -301,13 +316,21 @@ def run_qsim(args):
         return
     hbm, hbm_src = peaks()
     bytes_apply = N * (4 + 2 * e)          # read perm, gather k1, write k2
-    bytes_build = N * 4
-    bytes_fused = N * 2 * e
+    bytes_build = N * 4                    # write perm
+    bytes_fused = N * 2 * e                # gather k1, write k2
+    bytes_mg = N * (4 + 2 * e)             # write perm, gather k1, write k2
+    mg_ms = statistics.mean(kern_mg["map_gather"])
     apply_ms = statistics.mean(kern_mat["apply_map"])
     build_ms = statistics.mean(kern_mat["build_map"])
     fused_ms = statistics.mean(kern_fused["run_fused"])
-    ms_step = ms_mat / args.steps
-    achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
+    ms_step = ms_mg / args.steps
+    achieved = bytes_mg / (mg_ms * 1e-3) / 1e9
+    mg_kernel = ("qsim_jit_fused (NVRTC, circuit-specialised, perm + gather)"
+                 if launches_mg == args.steps else "k_build/k_apply_sigma (no JIT)")
+
+    def gbps(b, ms):
+        return b / (ms * 1e-3) / 1e9
+
     line = {
         "metric": METRIC,
         "value": world * N / (ms_step * 1e-3),
@@ -323,35 +346,46 @@ def run_qsim(args):
         "data": "synthetic (seeded counter-based Gaussian state, numpy PCG64 gate list)",
         "config": {"workload": f"{args.config}: {cfg.description}", "M": M,
                    "n_gates": int(gates.shape[0]), "state_dtype": "complex64" if e == 8 else
-                   "complex128", "step": "build_map + apply_map (materialised map+gather)",
+                   "complex128",
+                   "step": "qsim_map_gather_planned: materialised map (perm, uint32) + gather "
+                           "k2 = k1[perm], one kernel",
                    "l2": "inputs larger than L2 (k1, k2 %d GiB each; perm %d GiB)"
                    % (N * e >> 30, N * 4 >> 30), "parallelism": f"replicas x{world}"},
-        "achieved_GBps": (bytes_build + bytes_apply) / (ms_step * 1e-3) / 1e9,
-        "frac_of_8TBps": (bytes_build + bytes_apply) / (ms_step * 1e-3) / 8e12,
-        "roofline": {"bound": "hbm", "kernel": "qsim_apply_map_planned (k_apply_sigma)", "achieved": achieved,
+        "achieved_GBps": gbps(bytes_mg, ms_step),
+        "frac_of_8TBps": gbps(bytes_mg, ms_step) * 1e9 / 8e12,
+        "roofline": {"bound": "hbm", "kernel": mg_kernel, "achieved": achieved,
                      "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
                      "frac": achieved / hbm, "frac_of_8TBps": achieved * 1e9 / 8e12,
-                     "traffic": ncu_traffic(args.config, "apply_map"),
-                     "algorithmic_bytes_per_launch": bytes_apply},
+                     "traffic": ncu_traffic(args.config, "map_gather"),
+                     "algorithmic_bytes_per_launch": bytes_mg,
+                     "algorithmic_bytes_per_entry": 4 + 2 * e},
         "modes": {
-            "build_map": {"ms": build_ms, "GBps": bytes_build / (build_ms * 1e-3) / 1e9,
-                          "entries_per_s": N / (build_ms * 1e-3), "bound": "alu/hbm"},
-            "apply_map": {"ms": apply_ms, "GBps": achieved, "entries_per_s": N / (apply_ms * 1e-3)},
-            "run_fused": {"ms": fused_ms, "GBps": bytes_fused / (fused_ms * 1e-3) / 1e9,
-                          "entries_per_s": N / (fused_ms * 1e-3),
-                          "frac_of_peak": bytes_fused / (fused_ms * 1e-3) / 1e9 / hbm},
+            "map_gather_1pass": {"ms": mg_ms, "GBps": achieved, "entries_per_s": N / (mg_ms * 1e-3),
+                                 "launches_per_step": launches_mg / args.steps},
+            "two_call": {"ms": ms_mat / args.steps, "entries_per_s": N / (ms_mat / args.steps * 1e-3),
+                         "calls": "qsim_build_map + qsim_apply_map_planned"},
+            "build_map": {"ms": build_ms, "GBps": gbps(bytes_build, build_ms),
+                          "entries_per_s": N / (build_ms * 1e-3), "bytes_per_entry": 4,
+                          "frac_of_peak": gbps(bytes_build, build_ms) / hbm},
+            "apply_map": {"ms": apply_ms, "GBps": gbps(bytes_apply, apply_ms),
+                          "entries_per_s": N / (apply_ms * 1e-3), "bytes_per_entry": 4 + 2 * e,
+                          "frac_of_peak": gbps(bytes_apply, apply_ms) / hbm},
+            "run_fused": {"ms": fused_ms, "GBps": gbps(bytes_fused, fused_ms),
+                          "entries_per_s": N / (fused_ms * 1e-3), "bytes_per_entry": 2 * e,
+                          "frac_of_peak": gbps(bytes_fused, fused_ms) / hbm},
         },
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": launches_mat,
-        "gpu_launches_fused_loop": launches_fused,
+        "gpu_launches": launches_mg,
+        "gpu_launches_other_loops": {"two_call": launches_mat, "fused": launches_fused},
         "clocks": clocks,
         "setup_s": t_setup,
-        "jit": {"status": q.jit_status(), "compile_ms": q.jit_last_compile_ms(),
-                "note": "build_map uses a kernel NVRTC-compiled for the circuit on first use "
-                        "(warm-up); timed steps reuse it"},
+        "jit": {"status": q.jit_status(), "last_compile_ms": q.jit_last_compile_ms(),
+                "note": "kernels NVRTC-compiled for the circuit on first use (warm-up steps); "
+                        "timed steps reuse them"},
         "plan": {"seconds": t_plan, "sigma": list(plan.sigma)[:M], "chunk_log2": plan.chunk_log2,
-                 "blocks_per_sm": plan.blocks_per_sm,
+                 "fused_chunk_log2": plan.fused_chunk_log2, "blocks_per_sm": plan.blocks_per_sm,
+                 "natural_order": bool(plan.flags & 1),
                  "note": "qsim_plan_create (host sampling of the circuit) runs once per circuit, "
                          "outside the timed region, like an FFT plan"},
     }

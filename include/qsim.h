@@ -161,10 +161,15 @@ typedef struct qsim_plan {
     int32_t dtype;          /* QSIM_C64 / QSIM_C128: a 128-B line holds 16 / 8 entries */
     uint32_t chunk_log2;    /* counters per CTA chunk (default 16), within [10, M] */
     int32_t blocks_per_sm;  /* resident CTAs per SM (default 1), 1..8          */
-    uint32_t flags;         /* bit 0: natural order (no sigma)                 */
+    uint32_t flags;         /* bit 0: natural order (no sigma): set when the state is
+                               L2-resident (<= 64 MB), when natural order already keeps
+                               a line's readers within 2^20 outputs, or when sigma does
+                               not bring them under 2^24                         */
     uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
     uint16_t cta_threads;   /* apply kernel CTA size: 256, 512 or 1024 (0 = 256)    */
-    uint32_t fused_chunk_log2; /* counters per CTA chunk of the fused kernel (default 19) */
+    uint16_t fused_chunk_log2; /* counters per CTA chunk of the fused kernel (default 16) */
+    uint16_t reserved_spread;  /* diagnostics: log2 of the 0.9-quantile spread of a line's
+                                  readers, natural order (low byte) and sigma order (high) */
     uint8_t sigma[32];      /* counter bit k -> output bit sigma[k]            */
     float change_freq[32];  /* per output bit: fraction of sampled k1 lines whose
                                readers differ in that bit                     */
@@ -185,15 +190,28 @@ int qsim_apply_map_planned(const qsim_plan *plan, const uint32_t *perm, const vo
 
 /* qsim_run_fused_planned -- qsim_run_fused (the same k2) with the walk done
  * for the outputs in the plan's order; `gates` must be the circuit the plan
- * was created from (same n_gates; the plan is not re-derived).              */
+ * was created from (same n_gates; the plan is not re-derived).  With a
+ * workspace and NVRTC the kernel is compiled for (circuit, sigma, dtype) on
+ * first use and cached for the process.                                      */
 int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_t n_gates,
                            const void *k1, void *k2, void *workspace, void *stream);
 
+/* qsim_map_gather_planned -- materialised map AND gather in one call:
+ * perm[i] = f_1(...f_n(i)) for all i (natural layout, as qsim_build_map) and
+ * k2[i] = k1[perm[i]] (as qsim_apply_map).  With a sigma plan, a workspace
+ * and NVRTC available this is ONE kernel compiled for the circuit that
+ * walks each output once, stores its map entry and gathers (no re-read of
+ * perm); otherwise it is qsim_build_map followed by the planned gather.    */
+int qsim_map_gather_planned(const qsim_plan *plan, const qsim_gate *gates, int32_t n_gates,
+                            uint32_t *perm, const void *k1, void *k2, void *workspace,
+                            void *stream);
+
 /* qsim_run_host -- the whole path from HOST buffers (end-to-end use):
- * copies k1_host -> k1_dev, computes k2 (mode 0: qsim_build_map into
- * perm_dev, then the planned gather; mode 1: planned fused, perm_dev unused
+ * copies k1_host -> k1_dev, computes k2 (mode 0: qsim_map_gather_planned,
+ * the map materialised in perm_dev; mode 1: planned fused, perm_dev unused
  * and may be NULL), copies k2_dev -> k2_host, and SYNCHRONISES `stream`
- * before returning.  The plan is created inside the call.
+ * before returning.  The plan is created inside the call (host sampling,
+ * ~1-3 ms); the first call for a circuit also JIT-compiles its kernel.
  *   k1_host, k2_host  host, 2^M entries each (pinned memory recommended)
  *   k1_dev, k2_dev    device workspaces, 2^M entries each
  *   perm_dev          device workspace, 2^M uint32 (mode 0)
@@ -217,6 +235,9 @@ double qsim_jit_last_compile_ms(void);
  * kernel for this gate list; works without a GPU.  QSIM_ECUDA with the
  * NVRTC log in qsim_last_error() on failure.                               */
 int qsim_jit_check_compile(const qsim_gate *gates, int32_t n_gates, int32_t M);
+/* Same for the sigma-ordered fused / map+gather kernel of a plan.          */
+int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
+                                   int32_t n_gates);
 int32_t qsim_abi_version(void);
 
 #ifdef __cplusplus

@@ -51,7 +51,8 @@ class Plan(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("dtype", ctypes.c_int32),
                 ("chunk_log2", ctypes.c_uint32), ("blocks_per_sm", ctypes.c_int32),
                 ("flags", ctypes.c_uint32), ("ilp", ctypes.c_uint16),
-                ("cta_threads", ctypes.c_uint16), ("fused_chunk_log2", ctypes.c_uint32),
+                ("cta_threads", ctypes.c_uint16), ("fused_chunk_log2", ctypes.c_uint16),
+                ("reserved_spread", ctypes.c_uint16),
                 ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32)]
 
 
@@ -76,6 +77,9 @@ def _load() -> ctypes.CDLL:
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
     sig["qsim_apply_map_planned"] = [ctypes.POINTER(Plan), vp, vp, vp, vp, vp]
     sig["qsim_run_fused_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp]
+    sig["qsim_map_gather_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp, vp]
+    sig["qsim_jit_check_compile"] = [vp, i32, i32]
+    sig["qsim_jit_check_compile_planned"] = [ctypes.POINTER(Plan), vp, i32]
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -211,6 +215,14 @@ def run_fused_planned(plan: Plan, gates, k1, k2, workspace=None, stream=None) ->
     _check(_lib.qsim_run_fused_planned(ctypes.byref(plan), gp, n, _ptr(k1), _ptr(k2),
                                        _ptr(workspace), _stream(stream)),
            "qsim_run_fused_planned")
+
+
+def map_gather_planned(plan: Plan, gates, perm, k1, k2, workspace=None, stream=None) -> None:
+    """perm (materialised map) and k2 = k1[perm] in one call (one kernel when JIT)."""
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_map_gather_planned(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
+                                        _ptr(workspace), _stream(stream)),
+           "qsim_map_gather_planned")
 
 
 def workspace(device=None):

@@ -9,7 +9,9 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <algorithm>
 #include <string>
+#include <vector>
 
 #include "qsim.h"
 #include "qsim_jit.h"
@@ -296,16 +298,30 @@ int reset_ticket(void* workspace, cudaStream_t st) {
   return ce == cudaSuccess ? QSIM_OK : cuda_fail(ce, "ticket reset");
 }
 
+// A line's readers spread (max - min position of its 8 or 16 readers in a
+// traversal order), as log2, 0.9-quantile over the sampled lines.
+int spread_q90_log2(std::vector<uint64_t>& spreads) {
+  std::sort(spreads.begin(), spreads.end());
+  const uint64_t v = spreads[(spreads.size() * 9) / 10];
+  int l = 0;
+  while (l < 40 && (1ull << l) <= v) ++l;
+  return l;
+}
+
 int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan) {
   std::memset(plan, 0, sizeof *plan);
   plan->M = M;
   plan->dtype = dtype;
-  plan->chunk_log2 = M < 16 ? (uint32_t)M : 16u;
-  plan->fused_chunk_log2 = M < 19 ? (uint32_t)M : 19u;
+  // chunks: 2^16 counters (apply) / 2^19 (fused), but at least 8 chunks per SM
+  int cap = M - 10 - 3;  // 2^(M-13) counters per chunk leaves >= 8 * 1024 chunks
+  if (cap < 10) cap = 10;
+  plan->chunk_log2 = (uint32_t)std::min(std::min(16, cap), (int)M);
+  plan->fused_chunk_log2 = (uint32_t)std::min(std::min(16, cap), (int)M);
   plan->blocks_per_sm = 1;
   plan->ilp = 16;
   plan->cta_threads = 256;
   for (int k = 0; k < 32; ++k) plan->sigma[k] = (uint8_t)k;
+  const int e = elem_bytes(dtype);
   if (M < 10) {
     plan->flags = 1;
     return QSIM_OK;
@@ -320,12 +336,19 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   const int lines = 2048;
   uint32_t count[32] = {0};
   const uint64_t nlines = 1ull << (M - line_bits);
+  std::vector<uint32_t> readers((size_t)lines << line_bits);
+  std::vector<uint64_t> spread_nat(lines);
   for (int s = 0; s < lines; ++s) {
     const uint32_t base = (uint32_t)((plan_mix(0x51a3ull + s) % nlines) << line_bits);
-    const uint32_t r0 = plan_inverse_walk(cm.get(), tm.get(), n, base);
-    uint32_t diff = 0;
-    for (uint32_t e = 1; e < (1u << line_bits); ++e)
-      diff |= plan_inverse_walk(cm.get(), tm.get(), n, base | e) ^ r0;
+    uint32_t* r = &readers[(size_t)s << line_bits];
+    uint32_t diff = 0, lo = 0xffffffffu, hi = 0;
+    for (uint32_t d = 0; d < (1u << line_bits); ++d) {
+      r[d] = plan_inverse_walk(cm.get(), tm.get(), n, base | d);
+      diff |= r[d] ^ r[0];
+      lo = std::min(lo, r[d]);
+      hi = std::max(hi, r[d]);
+    }
+    spread_nat[s] = hi - lo;
     for (int b = 0; b < M; ++b) count[b] += (diff >> b) & 1u;
   }
   for (int b = 0; b < M; ++b) plan->change_freq[b] = (float)count[b] / lines;
@@ -339,6 +362,29 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
       order[j - 1] = t;
     }
   for (int k = 0; k < m; ++k) plan->sigma[5 + k] = (uint8_t)order[k];
+  // spread of the readers in sigma order (counter positions)
+  uint8_t inv[32];
+  for (int k = 0; k < M; ++k) inv[plan->sigma[k]] = (uint8_t)k;
+  std::vector<uint64_t> spread_sig(lines);
+  for (int s = 0; s < lines; ++s) {
+    uint64_t lo = ~0ull, hi = 0;
+    for (uint32_t d = 0; d < (1u << line_bits); ++d) {
+      const uint32_t r = readers[((size_t)s << line_bits) + d];
+      uint64_t c = 0;
+      for (int b = 0; b < M; ++b) c |= (uint64_t)((r >> b) & 1u) << inv[b];
+      lo = std::min(lo, c);
+      hi = std::max(hi, c);
+    }
+    spread_sig[s] = hi - lo;
+  }
+  const int nat = spread_q90_log2(spread_nat), sig = spread_q90_log2(spread_sig);
+  // Natural order when it already keeps a line's readers within ~2^20
+  // outputs (e.g. ripple cascades) or when sigma cannot bring them under
+  // ~2^24 either (an effectively random permutation: no order helps).
+  if (nat <= 20 || sig > 24 || sig >= nat) plan->flags = 1;
+  // small states are L2-resident: natural order, full parallelism
+  if ((1ull << M) * (uint64_t)e <= (64ull << 20)) plan->flags = 1;
+  plan->reserved_spread = (uint16_t)(nat | (sig << 8));
   return QSIM_OK;
 }
 
@@ -433,6 +479,36 @@ int fused_planned_t(const qsim_plan* plan, const qsim_gate* gates, int32_t n, co
   return launch_fused_sigma<qsim::kMaxGates, T>(plan, gates, n, k1, k2, workspace, st);
 }
 
+// Sigma-ordered fused kernel compiled for the circuit (qsim_jit.cu), or the
+// shared-memory interpreter if NVRTC is unavailable.  perm_out != null also
+// stores the map (one-pass map + gather).
+int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
+                         void* k2, uint32_t* perm_out, void* workspace, cudaStream_t st,
+                         bool* used_jit) {
+  *used_jit = false;
+  const int e = elem_bytes(plan->dtype);
+  if (workspace) {
+    std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+    pack_gates(gates, n, false, *gl);
+    std::string err;
+    const uint64_t nchunks = (1ull << plan->M) >> plan->fused_chunk_log2;
+    uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
+    if (blocks > nchunks) blocks = nchunks;
+    if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2,
+                        perm_out, workspace, (int)blocks, st, err) == 0) {
+      ++g_launches;
+      *used_jit = true;
+      return QSIM_OK;
+    }
+  }
+  if (perm_out) return QSIM_EINVAL;  // caller handles the two-kernel fallback
+  if (plan->dtype == QSIM_C64)
+    return fused_planned_t<uint2>(plan, gates, n, static_cast<const uint2*>(k1),
+                                  static_cast<uint2*>(k2), workspace, st);
+  return fused_planned_t<uint4>(plan, gates, n, static_cast<const uint4*>(k1),
+                                static_cast<uint4*>(k2), workspace, st);
+}
+
 int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
                        void* k2, void* workspace, cudaStream_t st) {
   int rc = plan_validate(plan);
@@ -446,11 +522,38 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
   if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
   const uint64_t N = 1ull << M;
   if (overlap(k1, N * e, k2, N * e)) return QSIM_EALIAS;
-  if (plan->dtype == QSIM_C64)
-    return fused_planned_t<uint2>(plan, gates, n, static_cast<const uint2*>(k1),
-                                  static_cast<uint2*>(k2), workspace, st);
-  return fused_planned_t<uint4>(plan, gates, n, static_cast<const uint4*>(k1),
-                                static_cast<uint4*>(k2), workspace, st);
+  bool jit = false;
+  return fused_sigma_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st, &jit);
+}
+
+int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, uint32_t* perm,
+                    const void* k1, void* k2, void* workspace, cudaStream_t st) {
+  int rc = plan_validate(plan);
+  if (rc) return rc;
+  const int M = plan->M;
+  if ((rc = check_gates(gates, n, M))) return rc;
+  const int e = elem_bytes(plan->dtype);
+  if (!perm || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2))
+    return QSIM_EINVAL;
+  if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
+  const uint64_t N = 1ull << M;
+  if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e) ||
+      overlap(perm, N * 4, k1, N * e))
+    return QSIM_EALIAS;
+  if (!plan_natural(plan) && workspace) {
+    bool jit = false;
+    int launches = g_launches;
+    rc = fused_sigma_dispatch(plan, gates, n, k1, k2, perm, workspace, st, &jit);
+    if (rc == QSIM_OK && jit) return QSIM_OK;
+    g_launches = launches;
+  }
+  // two kernels: build (natural order, coalesced) then the planned gather
+  rc = build_impl(gates, n, M, 0, N, perm, QSIM_WALK_AUTO, st);
+  if (rc) return rc;
+  const int32_t launches = g_launches;
+  rc = apply_planned_impl(plan, perm, k1, k2, workspace, st);
+  g_launches += launches;
+  return rc;
 }
 
 }  // namespace
@@ -538,6 +641,14 @@ int qsim_run_fused_planned(const qsim_plan* plan, const qsim_gate* gates, int32_
                             static_cast<cudaStream_t>(stream));
 }
 
+int qsim_map_gather_planned(const qsim_plan* plan, const qsim_gate* gates, int32_t n_gates,
+                            uint32_t* perm, const void* k1, void* k2, void* workspace,
+                            void* stream) {
+  g_launches = 0;
+  return map_gather_impl(plan, gates, n_gates, perm, k1, k2, workspace,
+                         static_cast<cudaStream_t>(stream));
+}
+
 int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype, int32_t mode,
                   const void* k1_host, void* k2_host, void* k1_dev, void* k2_dev,
                   uint32_t* perm_dev, void* workspace, void* stream) {
@@ -564,11 +675,7 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
   if (ce != cudaSuccess) return cuda_fail(ce, "H2D k1");
   int launches = 0;
   if (mode == 0) {
-    rc = build_impl(gates, n_gates, M, 0, N, perm_dev, QSIM_WALK_AUTO, st);
-    launches += g_launches;
-    g_launches = 0;
-    if (rc) return rc;
-    rc = apply_planned_impl(&plan, perm_dev, k1_dev, k2_dev, workspace, st);
+    rc = map_gather_impl(&plan, gates, n_gates, perm_dev, k1_dev, k2_dev, workspace, st);
   } else {
     rc = fused_planned_impl(&plan, gates, n_gates, k1_dev, k2_dev, workspace, st);
   }
@@ -602,6 +709,23 @@ const char* qsim_last_error(void) { return g_err; }
 const char* qsim_jit_status(void) { return qsim::jit_status(); }
 
 double qsim_jit_last_compile_ms(void) { return qsim::jit_last_compile_ms(); }
+
+int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates,
+                                   int32_t n_gates) {
+  g_launches = 0;
+  int rc = plan_validate(plan);
+  if (rc) return rc;
+  if ((rc = check_gates(gates, n_gates, plan->M))) return rc;
+  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+  pack_gates(gates, n_gates, false, *gl);
+  std::string err;
+  if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma,
+                                    elem_bytes(plan->dtype), err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+    return QSIM_ECUDA;
+  }
+  return QSIM_OK;
+}
 
 int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   g_launches = 0;

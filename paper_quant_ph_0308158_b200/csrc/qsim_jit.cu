@@ -54,6 +54,7 @@ struct Driver {
   PFN_cuModuleLoadData_v2000 load = nullptr;
   PFN_cuModuleGetFunction_v2000 getfn = nullptr;
   PFN_cuLaunchKernel_v4000 launch = nullptr;
+  PFN_cuFuncSetAttribute_v9000 setattr = nullptr;
   bool ok = false;
 };
 
@@ -110,6 +111,9 @@ void init_locked() {
   ok = ok && cudaGetDriverEntryPoint("cuLaunchKernel", &p, cudaEnableDefault, &q) == cudaSuccess &&
        q == cudaDriverEntryPointSuccess;
   g_drv.launch = reinterpret_cast<PFN_cuLaunchKernel_v4000>(p);
+  ok = ok && cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) ==
+                 cudaSuccess && q == cudaDriverEntryPointSuccess;
+  g_drv.setattr = reinterpret_cast<PFN_cuFuncSetAttribute_v9000>(p);
   g_drv.ok = ok;
   g_status = ok ? "ready" : "driver entry points unavailable";
 }
@@ -118,6 +122,24 @@ void init_locked() {
 const char* kPrelude = R"(
 typedef unsigned int u32;
 typedef unsigned long long u64;
+// Coherent loads with a memory clobber keep the 16 gathers of a batch
+// issued back to back: ptxas may not sink a store below a later load that
+// could alias it, so program order (16 loads, then 16 stores) survives
+// (with .nc loads ptxas interleaves them with the stores to save registers,
+// which throws away the memory-level parallelism).
+__device__ __forceinline__ uint2 ldg(const uint2* p) {
+  uint2 r; asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p)
+                        : "memory");
+  return r; }
+__device__ __forceinline__ uint4 ldg(const uint4* p) {
+  uint4 r; asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                        : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r; }
+__device__ __forceinline__ void stcs(uint2* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" :: "l"(p), "r"(v.x), "r"(v.y) : "memory"); }
+__device__ __forceinline__ void stcs(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory"); }
 #define QSIM_TS(J, MASK, a)                                                     \
   _Pragma("unroll") for (int k = 0; k < 32; ++k)                                \
     if ((k & J) == 0) { u32 t = ((a[k] >> J) ^ a[k + J]) & MASK;                \
@@ -200,6 +222,95 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
   return s;
 }
 
+// Sigma-ordered fused walk + gather (qsim_kernels.cuh k_fused_sigma, with the
+// circuit and the traversal order compiled in).  If perm_out is non-null the
+// kernel also stores the map (one-pass materialised map + gather).
+std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem) {
+  std::string s = kPrelude;
+  char buf[256];
+  const char* T = elem == 8 ? "uint2" : "uint4";
+  s += "__constant__ unsigned char kSigma[32] = {";
+  for (int k = 0; k < 32; ++k) {
+    std::snprintf(buf, sizeof buf, "%u%s", (unsigned)sigma[k], k < 31 ? "," : "};\n");
+    s += buf;
+  }
+  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n", T, M,
+                elem == 8 ? 32 : 16);
+  s += buf;
+  s += R"(
+extern "C" __global__ void __launch_bounds__(256)
+qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
+               QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
+  __shared__ u32 tab[4][256];
+  __shared__ u64 s_chunk;
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
+    const int b = x >> 8, v = x & 255;
+    u32 r = 0;
+    for (int j = 0; j < 8; ++j)
+      if (((v >> j) & 1) && 8 * b + j < QSIM_M) r |= 1u << kSigma[8 * b + j];
+    tab[b][v] = r;
+  }
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const u64 nchunks = N >> chunk_log2;
+  const u32 tiles = 1u << (chunk_log2 - 10);
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const u64 ch = s_chunk;
+    if (ch >= nchunks) break;
+    for (u32 tt = warp; tt < tiles; tt += 8u) {
+      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
+      const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
+                     tab[3][(c >> 24) & 255];
+)";
+  // plane initialisation: lane bits, l-bit patterns (compile-time), base bits
+  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+  int lpat[32];
+  for (int b = 0; b < 32; ++b) lpat[b] = -1;
+  for (int j = 0; j < 5 && 5 + j < M; ++j) lpat[sigma[5 + j]] = j;
+  for (int b = 0; b < 32; ++b) {
+    if (b < 5)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (lpat[b] >= 0)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[lpat[b]]);
+    else
+      std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += walk_code(w, n, M);
+  s += "      u32 a[32] = {";
+  for (int b = 0; b < 32; ++b) {
+    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+  s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+  // output offsets of the 32 word bits: sigma(l << 5), compile-time
+  s += "      const u32 lt[32] = {";
+  for (int l = 0; l < 32; ++l) {
+    uint32_t o = 0;
+    for (int j = 0; j < 5 && 5 + j < M; ++j)
+      if ((l >> j) & 1) o |= 1u << sigma[5 + j];
+    std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += R"(
+      if (perm_out) {
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob | lt[l] | lane), a[l]);
+      }
+      _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
+        QSIM_T v[QSIM_B];
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob | lt[h + l] | lane), v[l]);
+      }
+    }
+  }
+}
+)";
+  return s;
+}
+
 struct Entry {
   std::vector<uint32_t> words;
   int M;
@@ -269,6 +380,9 @@ CUfunction compile_locked(const std::string& src, const char* name, std::string&
     err = "cuModuleGetFunction failed";
     return nullptr;
   }
+  // the walk kernels use <= 5 KB of static shared memory: give the rest of
+  // the unified array to L1 (the gather's reuse cache)
+  g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 3);
   return fn;
 }
 
@@ -287,6 +401,22 @@ const char* jit_status() {
 }
 
 double jit_last_compile_ms() { return g_last_compile_ms; }
+
+// Find or compile the kernel for (kind, words, M, extra); extra is folded
+// into the key words (sigma, element size).
+CUfunction get_kernel_locked(uint64_t kind, const std::vector<uint32_t>& keyw, int M,
+                             const std::string& src, const char* name, std::string& err) {
+  const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+  for (const Entry& e : g_cache[key])
+    if (e.M == M && e.words == keyw) return e.fn;
+  const auto t0 = std::chrono::steady_clock::now();
+  CUfunction fn = compile_locked(src, name, err);
+  if (!fn) return nullptr;
+  g_last_compile_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  g_cache[key].push_back(Entry{keyw, M, fn, g_last_compile_ms});
+  return fn;
+}
 
 int jit_check_compile(const uint32_t* words, int n, int M, std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
@@ -339,6 +469,55 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
     return -1;
   }
   return 0;
+}
+
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
+              int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
+              cudaStream_t st, std::string& err) {
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    std::vector<uint32_t> keyw(words, words + n);
+    for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
+    keyw.push_back((uint32_t)elem);
+    // the source is only generated on a cache miss
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), 0x66757365ull);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && e.words == keyw) fn = e.fn;
+    if (!fn) fn = get_kernel_locked(0x66757365ull, keyw, M, fused_source(words, n, M, sigma, elem),
+                                    "qsim_jit_fused", err);
+    if (!fn) return -1;
+  }
+  uint64_t N = 1ull << M;
+  uint32_t cl = chunk_log2;
+  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &perm_out};
+  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
+    err = "ticket reset failed";
+    return -1;
+  }
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
+                            std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(fused_source(words, n, M, sigma, elem), cubin, err) ? 0 : -1;
 }
 
 }  // namespace qsim

@@ -17,4 +17,13 @@ int jit_check_compile(const uint32_t* words, int n, int M, std::string& err);
 // caller then uses the interpreter kernel).
 int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t count,
               uint32_t* perm_out, int sms, cudaStream_t st, std::string& err);
+// Sigma-ordered fused walk + gather over all 2^M outputs with a kernel
+// compiled for (circuit, sigma, element size); if perm_out != null the map is
+// stored as well (one-pass map + gather).  ticket: device scratch (reset on
+// st).  Returns 0 or -1 with err.
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
+              int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
+              cudaStream_t st, std::string& err);
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
+                            std::string& err);
 }  // namespace qsim

@@ -49,10 +49,30 @@ __device__ __forceinline__ uint4 ld_stream_u4(const uint32_t* p) {
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-__device__ __forceinline__ uint2 ld_gather(const uint2* p) { return __ldg(p); }
-__device__ __forceinline__ uint4 ld_gather(const uint4* p) { return __ldg(p); }
-__device__ __forceinline__ void st_stream(uint2* p, uint2 v) { __stcs(p, v); }
-__device__ __forceinline__ void st_stream(uint4* p, uint4 v) { __stcs(p, v); }
+// Gathers as coherent loads with a memory clobber, streaming stores with a
+// memory clobber: ptxas may not sink a store below a later load that could
+// alias it, so a batch of gathers stays issued back to back (memory-level
+// parallelism) instead of being interleaved with the stores to save
+// registers (which it does with .nc loads).
+__device__ __forceinline__ uint2 ld_gather(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ uint4 ld_gather(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_stream(uint2* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
 __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) { __stcs(p, v); }
 
 // ------------------------------------------------------------------ per-lane
@@ -298,7 +318,7 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
       const uint32_t out_base = sigma_apply(sh.tab, c);
       uint32_t a[32];
       bs_walk_tile(g.n, sh, out_base, a);
-      constexpr int B = 16;
+      constexpr int B = sizeof(T) == 8 ? 32 : 16;  // gathers in flight per thread
 #pragma unroll
       for (int h = 0; h < 32; h += B) {
         T v[B];

@@ -107,13 +107,18 @@ def test_gate_validation(q, bad, code):
 
 def test_plan_create_and_validation(q):
     """Plans are host-only: create them and check the validator (no launch)."""
-    g = wl.CONFIGS["cfg2"].gates()
-    plan = q.plan_create(g, 20, "c64")
-    sig = list(plan.sigma)[:20]
-    assert sorted(sig) == list(range(20)) and sig[:5] == [0, 1, 2, 3, 4]
-    assert plan.chunk_log2 == 16 and plan.blocks_per_sm == 1
+    g = wl.CONFIGS["cfg5"].gates()
+    plan = q.plan_create(g, 32, "c64")
+    sig = list(plan.sigma)[:32]
+    assert sorted(sig) == list(range(32)) and sig[:5] == [0, 1, 2, 3, 4]
+    assert plan.chunk_log2 == 16 and plan.fused_chunk_log2 == 16 and plan.blocks_per_sm == 1
+    assert plan.flags == 0                       # cfg5: sigma order pays (SURVEY 8d)
     # deterministic
-    assert list(q.plan_create(g, 20, "c64").sigma) == list(plan.sigma)
+    assert list(q.plan_create(g, 32, "c64").sigma) == list(plan.sigma)
+    # L2-resident, ripple and fully random circuits keep natural order
+    for name in ("cfg2", "cfg3", "cfg4"):
+        cfg = wl.CONFIGS[name]
+        assert q.plan_create(cfg.gates(), cfg.M, cfg.dtype).flags & 1, name
     L = q.lib()
     import ctypes
     bad = q.Plan.from_buffer_copy(plan)
@@ -126,7 +131,7 @@ def test_plan_create_and_validation(q):
     bad.chunk_log2 = 9
     assert L.qsim_apply_map_planned(ctypes.byref(bad), FAKE, FAKE * 4, FAKE * 64, None, None) == q.EINVAL
     bad = q.Plan.from_buffer_copy(plan)
-    bad.fused_chunk_log2 = 21
+    bad.fused_chunk_log2 = 9
     assert L.qsim_run_fused_planned(ctypes.byref(bad), g.ctypes.data, 64, FAKE * 4, FAKE * 64,
                                     None, None) == q.EINVAL
     bad = q.Plan.from_buffer_copy(plan)
@@ -140,7 +145,7 @@ def test_plan_create_and_validation(q):
     assert L.qsim_run_fused_planned(ctypes.byref(plan), g.ctypes.data, 64, FAKE * 4, FAKE * 64,
                                     FAKE + 8, None) in (q.EINVAL,)
     with pytest.raises(q.QsimError):
-        q.plan_create(g, 19, "c64")                                    # bit 19 >= M
+        q.plan_create(g, 30, "c64")                                    # bit 31 >= M
 
 
 def test_unused_control_slots_are_ignored(q):
@@ -160,6 +165,18 @@ def test_jit_source_compiles_without_gpu(q):
                      (np.zeros((0, 4), np.uint8), 5), (wl.CONFIGS["cfg1"].gates(), 3)):
         g = np.ascontiguousarray(gates)
         rc = L.qsim_jit_check_compile(g.ctypes.data if len(g) else None, len(g), M)
+        if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+            pytest.skip("NVRTC not available here")
+        assert rc == q.OK, L.qsim_last_error().decode()
+
+
+def test_jit_fused_source_compiles_without_gpu(q):
+    L = q.lib()
+    for name in ("cfg5", "cfg3"):
+        cfg = wl.CONFIGS[name]
+        g = np.ascontiguousarray(cfg.gates())
+        plan = q.plan_create(g, cfg.M, cfg.dtype)
+        rc = L.qsim_jit_check_compile_planned(ctypes.byref(plan), g.ctypes.data, len(g))
         if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
             pytest.skip("NVRTC not available here")
         assert rc == q.OK, L.qsim_last_error().decode()

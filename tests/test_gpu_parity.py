@@ -160,6 +160,9 @@ def test_planned_apply_and_fused(q, M, dtype):
     q.build_map(gates, M, perm)
     plan = q.plan_create(gates, M, dtype)
     assert sorted(list(plan.sigma)[:M]) == list(range(M))
+    if M > 10:
+        assert list(plan.sigma)[:M] != list(range(M))   # a real reordering
+    plan.flags = 0                                       # force the sigma kernels
     ws = q.workspace()
     for cl in sorted({10, min(M, 12), M}):
         for bps in (1, 2, 8):
@@ -169,9 +172,14 @@ def test_planned_apply_and_fused(q, M, dtype):
                 q.apply_map_planned(plan, perm, k1_d, out, w)
                 outf = torch.empty_like(k1_d)
                 q.run_fused_planned(plan, gates, k1_d, outf, w)
+                outm = torch.empty_like(k1_d)
+                pm = _new_perm(1 << M)
+                q.map_gather_planned(plan, gates, pm, k1_d, outm, w)
                 torch.cuda.synchronize()
                 assert out.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
                 assert outf.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
+                assert outm.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
+                assert np.array_equal(_perm_np(pm), _perm_np(perm)), (cl, bps)
 
 
 def test_planned_small_M_falls_back_to_natural(q):
@@ -336,7 +344,11 @@ def _full_config(q, name, fused):
     q.run_fused_planned(plan, gates, k1_d, k2p, ws)
     torch.cuda.synchronize()
     assert torch.equal(k2_d, k2p)
-    del k2p
+    pm = torch.empty_like(perm_d)
+    q.map_gather_planned(plan, gates, pm, k1_d, k2p, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(k2_d, k2p) and torch.equal(perm_d, pm)
+    del k2p, pm
     # perm(reverse G) o perm(G) == identity over all 2^M outputs (group identity)
     rev_d = torch.empty_like(perm_d)
     q.build_map(gates[::-1].copy(), cfg.M, rev_d)
@@ -381,6 +393,13 @@ def test_cfg5_full_size_sampled(q):
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, None)
     # every other path == the planned apply over all 2^32 entries (on device)
     k2f_d = torch.empty_like(k2_d)
+    pm = torch.empty_like(perm_d)
+    q.map_gather_planned(plan, gates, pm, k1_d, k2f_d, ws)       # one-pass map + gather
+    torch.cuda.synchronize()
+    assert torch.equal(pm, perm_d)
+    for s in range(0, N * 8, 1 << 32):
+        assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
+    del pm
     for run in (lambda: q.run_fused_planned(plan, gates, k1_d, k2f_d, ws),
                 lambda: q.apply_map(perm_d, cfg.M, k1_d, k2f_d, dtype="c64"),
                 lambda: q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype="c64")):

@@ -41,6 +41,11 @@ elif args.variant.startswith("fsigma"):
     plan.chunk_log2, plan.blocks_per_sm = f[0], f[1]
     ws = q.workspace()
     fn = lambda: q.run_fused_planned(plan, gates, k1, k2, ws)  # noqa: E731
+elif args.variant.startswith("mapgather"):
+    plan = q.plan_create(gates, M, cfg.dtype)
+    ws = q.workspace()
+    p2 = torch.empty_like(perm)
+    fn = lambda: q.map_gather_planned(plan, gates, p2, k1, k2, ws)  # noqa: E731
 elif args.variant == "build":
     fn = lambda: q.build_map(gates, M, perm)  # noqa: E731
 for _ in range(args.reps):

@@ -50,6 +50,11 @@ def main():
         out.zero_()
         if mode == "apply":
             ms = timeit(lambda: q.apply_map_planned(plan, perm, k1, out, ws))
+        elif mode == "mapgather":
+            pm = torch.empty_like(perm)
+            ms = timeit(lambda: q.map_gather_planned(plan, gates, pm, k1, out, ws))
+            assert torch.equal(pm, perm)
+            del pm
         else:
             ms = timeit(lambda: q.run_fused_planned(plan, gates, k1, out, ws))
         ok = bool(torch.equal(out, ref))
