@@ -126,10 +126,10 @@ class ClockSampler:
 
 
 def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return world, rank, local
+    """(world, rank, local_rank) from the torchrun environment (no package
+    import: the reference arm must not load libqsim.so)."""
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
 
 
 # ------------------------------------------------------------ cpu baseline
@@ -190,10 +190,7 @@ def run_qsim(args):
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
 
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
+    from paper_quant_ph_0308158_b200.dist import barrier, max_over_ranks
 
     def timed_loop(step_fn, steps, warmup, per_kernel=None):
         for _ in range(warmup):
@@ -213,12 +210,7 @@ def run_qsim(args):
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
-        ms = t0.elapsed_time(t1)
-        if world > 1:
-            import torch.distributed as dist
-            tt = torch.tensor([ms], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms = float(tt.item())
+        ms = max_over_ranks(t0.elapsed_time(t1), device=dev)
         kern = {}
         if marks:
             for name, a, b in marks:
@@ -286,12 +278,7 @@ def run_qsim(args):
         for _ in range(args.e2e_steps):
             q.run_host(gates, M, q.MATERIALISED, k1_host, k2_host, k1, k2, perm, ws,
                        stream=stream, dtype=cfg.dtype)
-        dt = time.perf_counter() - t0
-        if world > 1:
-            import torch.distributed as dist
-            tt = torch.tensor([dt], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            dt = float(tt.item())
+        dt = max_over_ranks(time.perf_counter() - t0, device=dev)
         e2e = {"value": world * N * args.e2e_steps / dt, "unit": "entries/s",
                "h2d_bytes_per_step": N * e, "d2h_bytes_per_step": N * e,
                "ms_per_step": 1e3 * dt / args.e2e_steps,
