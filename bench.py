@@ -246,6 +246,18 @@ def run_qsim(args):
                 marks.append(("map_gather", a, b))
         return n
 
+    qubits = wl.random_qubits(M, 2024, cfg.dtype)
+
+    def step_kron(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.run_fused_kron(gates, M, qubits, k2, dtype=cfg.dtype, stream=stream)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("fused_kron", a, b))
+        return n
+
     def step_fused(marks):
         with torch.cuda.stream(stream):
             a = ev() if marks is not None else None
@@ -264,6 +276,8 @@ def run_qsim(args):
                                                     per_kernel=True)
         ms_fused, launches_fused, kern_fused = timed_loop(step_fused, args.steps, args.warmup,
                                                           per_kernel=True)
+        ms_kron, launches_kron, kern_kron = timed_loop(step_kron, args.steps, args.warmup,
+                                                       per_kernel=True)
     clocks = sampler.summary()
 
     # ---- end to end through the C ABI from pinned host buffers
@@ -310,6 +324,7 @@ def run_qsim(args):
     apply_ms = statistics.mean(kern_mat["apply_map"])
     build_ms = statistics.mean(kern_mat["build_map"])
     fused_ms = statistics.mean(kern_fused["run_fused"])
+    kron_ms = statistics.mean(kern_kron["fused_kron"])
     ms_step = ms_mg / args.steps
     achieved = bytes_mg / (mg_ms * 1e-3) / 1e9
     mg_kernel = ("qsim_jit_fused (NVRTC, circuit-specialised, perm + gather)"
@@ -360,11 +375,17 @@ def run_qsim(args):
             "run_fused": {"ms": fused_ms, "GBps": gbps(bytes_fused, fused_ms),
                           "entries_per_s": N / (fused_ms * 1e-3), "bytes_per_entry": 2 * e,
                           "frac_of_peak": gbps(bytes_fused, fused_ms) / hbm},
+            "fused_kron": {"ms": kron_ms, "GBps": gbps(N * e, kron_ms),
+                           "entries_per_s": N / (kron_ms * 1e-3), "bytes_per_entry": e,
+                           "frac_of_peak": gbps(N * e, kron_ms) / hbm,
+                           "note": "qsim_run_fused_kron: Appendix-1 input generated on the fly "
+                                   "(k1 never read), write-only"},
         },
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mg,
-        "gpu_launches_other_loops": {"two_call": launches_mat, "fused": launches_fused},
+        "gpu_launches_other_loops": {"two_call": launches_mat, "fused": launches_fused,
+                                     "fused_kron": launches_kron},
         "clocks": clocks,
         "setup_s": t_setup,
         "jit": {"status": q.jit_status(), "last_compile_ms": q.jit_last_compile_ms(),

@@ -196,6 +196,27 @@ int qsim_apply_map_planned(const qsim_plan *plan, const uint32_t *perm, const vo
 int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_t n_gates,
                            const void *k1, void *k2, void *workspace, void *stream);
 
+/* qsim_run_fused_kron -- the state transform with the INPUT GENERATED ON THE
+ * FLY (Appendix 1): k1 is never stored; it is the Kronecker
+ * product k1 = q_M (x) ... (x) q_1 of M qubits [q_j(0) q_j(1)] (P:L81,
+ * P:L83), so k1(s) = q_M(b_M) ... q_1(b_1) for s = b_M...b_1 ("use i = 101
+ * to obtain q_3(1)q_2(0)q_1(1)"), and
+ *     k2_out[r] = k1(perm[start + r]),   r < count.
+ *   qubits  host, 4*M doubles: qubit j (1-based) at [4(j-1)]: re q_j(0),
+ *           im q_j(0), re q_j(1), im q_j(1); rounded to the state precision
+ *           (float for QSIM_C64) before use
+ *   k2_out  device, count entries of dtype (written)
+ *   walk    QSIM_WALK_AUTO / QSIM_WALK_BITSLICED / QSIM_WALK_JIT
+ * Arithmetic: the factors are grouped by bytes of s into 256-entry tables
+ * of products (8 qubits, descending j), combined as ((T3 T2) T1) T0; every
+ * complex product is rounded as written (re = ar*br - ai*bi, im = ar*bi +
+ * ai*br), no FMA.  Not bit-exact against a sequential double product: the
+ * normwise relative error is at most (M-1)*sqrt(5)*u (u = 2^-24 for
+ * complex64, 2^-53 for complex128), the tolerance the tests use.          */
+int qsim_run_fused_kron(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
+                        const double *qubits, uint64_t start, uint64_t count, void *k2_out,
+                        int32_t walk, void *stream);
+
 /* qsim_map_gather_planned -- materialised map AND gather in one call:
  * perm[i] = f_1(...f_n(i)) for all i (natural layout, as qsim_build_map) and
  * k2[i] = k1[perm[i]] (as qsim_apply_map).  With a sigma plan, a workspace
@@ -235,7 +256,10 @@ double qsim_jit_last_compile_ms(void);
  * kernel for this gate list; works without a GPU.  QSIM_ECUDA with the
  * NVRTC log in qsim_last_error() on failure.                               */
 int qsim_jit_check_compile(const qsim_gate *gates, int32_t n_gates, int32_t M);
-/* Same for the sigma-ordered fused / map+gather kernel of a plan.          */
+/* Same for the sigma-ordered fused / map+gather kernel of a plan, and for the
+ * Appendix-1 (input on the fly) kernel.                                     */
+int qsim_jit_check_compile_kron(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                                int32_t dtype);
 int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
                                    int32_t n_gates);
 int32_t qsim_abi_version(void);

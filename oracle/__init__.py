@@ -63,6 +63,12 @@ def _load():
         lib.oracle_walk_many.restype = None
         lib.oracle_walk_many.argtypes = [u8p, ctypes.c_int32, ctypes.c_void_p,
                                          ctypes.c_uint64, ctypes.c_void_p]
+        lib.oracle_kron_element.restype = None
+        lib.oracle_kron_element.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
+                                            ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_fused_kron.restype = None
+        lib.oracle_fused_kron.argtypes = [u8p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p,
+                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
         lib.oracle_accumulate.restype = None
         lib.oracle_accumulate.argtypes = [u8p, ctypes.c_int32, ctypes.c_int32,
                                           ctypes.c_int32, ctypes.c_void_p]
@@ -146,3 +152,30 @@ def accumulate(gates, k1: np.ndarray) -> np.ndarray:
     g, ptr, n = _gates_arg(gates)
     _load().oracle_accumulate(ptr, n, M, _elem_bytes(k), k.ctypes.data)
     return k
+
+
+def _qubits_arg(qubits) -> np.ndarray:
+    """(M, 2) complex array -> 4M doubles: re/im of q_j(0), q_j(1), j = 1..M."""
+    q = np.asarray(qubits, dtype=np.complex128).reshape(-1, 2)
+    return np.ascontiguousarray(q.view(np.float64).reshape(-1))
+
+
+def kron_element(qubits, i: int) -> complex:
+    """k_1(i) = q_M(b_M) ... q_1(b_1) (Appendix 1), double precision."""
+    q = _qubits_arg(qubits)
+    M = q.shape[0] // 4
+    re, im = ctypes.c_double(), ctypes.c_double()
+    _load().oracle_kron_element(q.ctypes.data, M, i, ctypes.byref(re), ctypes.byref(im))
+    return complex(re.value, im.value)
+
+
+def fused_kron(gates, qubits, start: int = 0, count: int | None = None) -> np.ndarray:
+    """k2[i] = k_1(perm[i]) with k_1 generated on the fly (complex128)."""
+    q = _qubits_arg(qubits)
+    M = q.shape[0] // 4
+    if count is None:
+        count = (1 << M) - start
+    g, ptr, n = _gates_arg(gates)
+    out = np.empty(count, dtype=np.complex128)
+    _load().oracle_fused_kron(ptr, n, M, q.ctypes.data, start, count, out.ctypes.data)
+    return out

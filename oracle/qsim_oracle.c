@@ -142,4 +142,41 @@ void oracle_accumulate(const uint8_t *gates, int32_t n_gates, int32_t M,
     }
 }
 
+/* ---- Appendix 1: "CALCULATING THE INPUT STATE ON THE FLY" ----
+ * "The input can be stored in the form of M qubits labeled q_i, 1 <= i <= M,
+ * each represented as a pair of complex numbers [q_i(0) q_i(1)]";
+ * k_1 = q_M (x) q_{M-1} (x) ... (x) q_1; "if a particular element
+ * ... is wanted, simply use the binary form of i to identify the appropriate
+ * components of each qubit to be multiplied. For example, if k_1(5) is
+ * wanted, use i = 101 to obtain q_3(1)q_2(0)q_1(1)" ("k_i" read as
+ * k_1, reading R12).
+ * qubits: 4*M doubles, qubit j (1-based) at [4(j-1)]: re q_j(0), im q_j(0),
+ * re q_j(1), im q_j(1).  The product is formed left to right in the order
+ * the Kronecker product is written, q_M first, in double precision.        */
+void oracle_kron_element(const double *qubits, int32_t M, uint64_t i, double *out_re,
+                         double *out_im)
+{
+    double re = 1.0, im = 0.0;
+    for (int32_t j = M; j >= 1; --j) {
+        const double *q = qubits + 4 * (size_t)(j - 1) + 2 * (size_t)oracle_bit(i, (unsigned)(j - 1));
+        const double r = re * q[0] - im * q[1];
+        const double m = re * q[1] + im * q[0];
+        re = r;
+        im = m;
+    }
+    *out_re = re;
+    *out_im = im;
+}
+
+/* Fused with the map: k2[i] = k_1(perm[i]) for the
+ * portion [start, start+count); out holds 2*count doubles (re, im).       */
+void oracle_fused_kron(const uint8_t *gates, int32_t n_gates, int32_t M, const double *qubits,
+                       uint64_t start, uint64_t count, double *out)
+{
+    for (uint64_t r = 0; r < count; ++r) {
+        const uint64_t j = oracle_walk(gates, n_gates, start + r);
+        oracle_kron_element(qubits, M, j, out + 2 * r, out + 2 * r + 1);
+    }
+}
+
 int oracle_abi_version(void) { return 1; }

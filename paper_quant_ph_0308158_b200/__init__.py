@@ -79,6 +79,8 @@ def _load() -> ctypes.CDLL:
     sig["qsim_run_fused_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp]
     sig["qsim_map_gather_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp, vp]
     sig["qsim_jit_check_compile"] = [vp, i32, i32]
+    sig["qsim_jit_check_compile_kron"] = [vp, i32, i32, i32]
+    sig["qsim_run_fused_kron"] = [vp, i32, i32, i32, vp, u64, u64, vp, i32, vp]
     sig["qsim_jit_check_compile_planned"] = [ctypes.POINTER(Plan), vp, i32]
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -223,6 +225,21 @@ def map_gather_planned(plan: Plan, gates, perm, k1, k2, workspace=None, stream=N
     _check(_lib.qsim_map_gather_planned(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
                                         _ptr(workspace), _stream(stream)),
            "qsim_map_gather_planned")
+
+
+def run_fused_kron(gates, M: int, qubits, k2_out, start: int = 0, count: int | None = None,
+                   dtype="c64", walk: int = WALK_AUTO, stream=None) -> None:
+    """k2_out[r] = k1(perm[start + r]) with k1 = q_M (x) ... (x) q_1 generated on
+    the fly (Appendix 1).  qubits: (M, 2) complex, row j-1 = [q_j(0), q_j(1)]."""
+    q = np.ascontiguousarray(np.asarray(qubits, dtype=np.complex128).reshape(-1, 2))
+    if q.shape[0] != M:
+        raise ValueError(f"need {M} qubits, got {q.shape[0]}")
+    qd = np.ascontiguousarray(q.view(np.float64).reshape(-1))
+    if count is None:
+        count = (1 << M) - start
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_run_fused_kron(gp, n, M, _dtype_code(dtype), qd.ctypes.data, start, count,
+                                    _ptr(k2_out), walk, _stream(stream)), "qsim_run_fused_kron")
 
 
 def workspace(device=None):

@@ -20,6 +20,7 @@
 namespace {
 
 thread_local char g_err[512] = "";
+constexpr uint64_t kJitMinCount = 1ull << 22;  // outputs from which AUTO uses the JIT kernels
 thread_local int32_t g_launches = 0;
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -172,8 +173,7 @@ int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, ui
 
 // Large builds use the circuit-specialised kernel (qsim_jit.cu) when NVRTC
 // is present; everything else (and any JIT failure under AUTO) uses the
-// shared-memory bit-sliced interpreter.
-constexpr uint64_t kJitMinCount = 1ull << 22;
+// shared-memory bit-sliced interpreter (kJitMinCount, top of file).
 
 int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                uint32_t* perm_out, int32_t walk, cudaStream_t st) {
@@ -214,6 +214,69 @@ int fused_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, uint
                                  static_cast<const uint2*>(k1), static_cast<uint2*>(k2), walk, st);
   return launch_walk<1, uint4>(gates, n, M, start, count, nullptr, static_cast<const uint4*>(k1),
                                static_cast<uint4*>(k2), walk, st);
+}
+
+// ---- Appendix 1: input generated on the fly, fused with the map
+template <int CAP, typename C>
+int launch_kron_cap(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qubits& qb,
+                    uint64_t start, uint64_t count, C* k2, cudaStream_t st) {
+  std::unique_ptr<qsim::GateList<CAP>> gl(new qsim::GateList<CAP>);
+  pack_gates<CAP>(gates, n, true, *gl);
+  const qsim::SigmaParams sp = identity_sigma(M);
+  const uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  uint64_t blocks = (te - tb + qsim::kBsWarps - 1) / qsim::kBsWarps;
+  const uint64_t cap = (uint64_t)sm_count() * 2 * 16;
+  if (blocks > cap) blocks = cap;
+  const size_t smem = qsim::bs_smem_bytes((uint32_t)n);
+  cudaFuncSetAttribute(qsim::k_fused_kron_bitsliced<CAP, C>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  qsim::k_fused_kron_bitsliced<CAP, C><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(
+      *gl, sp, qb, start, start + count, tb, te, k2);
+  QSIM_CHECK_LAUNCH("k_fused_kron_bitsliced");
+  return QSIM_OK;
+}
+
+template <typename C>
+int launch_kron(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qubits& qb,
+                uint64_t start, uint64_t count, C* k2, cudaStream_t st) {
+  if (n <= 64) return launch_kron_cap<64, C>(gates, n, M, qb, start, count, k2, st);
+  if (n <= 256) return launch_kron_cap<256, C>(gates, n, M, qb, start, count, k2, st);
+  if (n <= 1024) return launch_kron_cap<1024, C>(gates, n, M, qb, start, count, k2, st);
+  return launch_kron_cap<qsim::kMaxGates, C>(gates, n, M, qb, start, count, k2, st);
+}
+
+int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const double* qubits,
+              uint64_t start, uint64_t count, void* k2, int32_t walk, cudaStream_t st) {
+  int rc = check_gates(gates, n, M);
+  if (rc) return rc;
+  if ((rc = check_range(M, start, count))) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0 || !qubits || !k2 || !aligned16(k2)) return QSIM_EINVAL;
+  if (walk != QSIM_WALK_AUTO && walk != QSIM_WALK_BITSLICED && walk != QSIM_WALK_JIT)
+    return QSIM_EINVAL;
+  qsim::Qubits qb;
+  std::memset(&qb, 0, sizeof qb);
+  qb.M = (uint32_t)M;
+  for (int j = 0; j < M; ++j)
+    for (int c = 0; c < 4; ++c) qb.v[j][c] = qubits[4 * j + c];
+  if (count == 0) return QSIM_OK;
+  if (walk == QSIM_WALK_JIT || (walk == QSIM_WALK_AUTO && count >= kJitMinCount)) {
+    std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+    pack_gates(gates, n, false, *gl);
+    std::string err;
+    if (qsim::jit_kron(gl->w, n, M, &qb, sizeof qb, e, start, count, k2, sm_count(), st, err) ==
+        0) {
+      ++g_launches;
+      return QSIM_OK;
+    }
+    if (walk == QSIM_WALK_JIT) {
+      std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+      return QSIM_ECUDA;
+    }
+  }
+  if (dtype == QSIM_C64)
+    return launch_kron<float2>(gates, n, M, qb, start, count, static_cast<float2*>(k2), st);
+  return launch_kron<double2>(gates, n, M, qb, start, count, static_cast<double2*>(k2), st);
 }
 
 int apply_impl(const uint32_t* perm, uint64_t count, int32_t M, int32_t dtype, const void* k1,
@@ -619,6 +682,14 @@ int qsim_run_fused_ex(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_
                     static_cast<cudaStream_t>(stream));
 }
 
+int qsim_run_fused_kron(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype,
+                        const double* qubits, uint64_t start, uint64_t count, void* k2_out,
+                        int32_t walk, void* stream) {
+  g_launches = 0;
+  return kron_impl(gates, n_gates, M, dtype, qubits, start, count, k2_out, walk,
+                   static_cast<cudaStream_t>(stream));
+}
+
 int qsim_plan_create(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype,
                      qsim_plan* plan) {
   g_launches = 0;
@@ -721,6 +792,22 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
   std::string err;
   if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma,
                                     elem_bytes(plan->dtype), err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+    return QSIM_ECUDA;
+  }
+  return QSIM_OK;
+}
+
+int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t M,
+                                int32_t dtype) {
+  g_launches = 0;
+  int rc = check_gates(gates, n_gates, M);
+  if (rc) return rc;
+  if (elem_bytes(dtype) == 0) return QSIM_EINVAL;
+  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+  pack_gates(gates, n_gates, false, *gl);
+  std::string err;
+  if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }

@@ -311,6 +311,87 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   return s;
 }
 
+// Natural-order fused walk with the input generated on the fly (Appendix 1,
+// P:L81-L89): k2_out[out - start] = k1(perm(out)) from byte tables of
+// qubit products (same arithmetic as qsim_kernels.cuh kron_tables /
+// kron_element: products rounded as written, no FMA contraction).
+std::string kron_source(const uint32_t* w, int n, int M, int elem) {
+  std::string s = kPrelude;
+  char buf[256];
+  const bool f32 = elem == 8;
+  s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n", M);
+  s += buf;
+  s += f32 ? R"(
+__device__ __forceinline__ C cmul(C a, C b) {
+  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
+                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x))); }
+)" : R"(
+__device__ __forceinline__ C cmul(C a, C b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))); }
+)";
+  s += R"(
+struct Qubits { double v[32][4]; u32 M; };
+extern "C" __global__ void __launch_bounds__(256)
+qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) {
+  __shared__ C T[4][256];
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
+    const int g = x >> 8, v = x & 255;
+    C acc; bool first = true;
+    for (int j = 7; j >= 0; --j) {
+      const int b = 8 * g + j;
+      if (b >= QSIM_M) continue;
+      const int bit = (v >> j) & 1;
+      C f; f.x = (R)q.v[b][2 * bit]; f.y = (R)q.v[b][2 * bit + 1];
+      acc = first ? f : cmul(acc, f);
+      first = false;
+    }
+    if (first) { acc.x = (R)1; acc.y = (R)0; }
+    T[g][v] = acc;
+  }
+  __syncthreads();
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
+    const u64 base = tile << 10;
+    const u32 b32 = (u32)base;
+)";
+  for (int b = 0; b < 32; ++b) {
+    if (b < 5)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (b < 10) {
+      const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u",
+                            "0xffff0000u"};
+      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
+    } else
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += walk_code(w, n, M);
+  s += "    u32 a[32] = {";
+  for (int b = 0; b < 32; ++b) {
+    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += R"(
+    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
+    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
+    const bool full = base >= start && base + 1024u <= end;
+    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+      const u32 sv = a[l];
+      C r = T[3][sv >> 24];
+      r = cmul(r, T[2][(sv >> 16) & 255]);
+      r = cmul(r, T[1][(sv >> 8) & 255]);
+      r = cmul(r, T[0][sv & 255]);
+      const u64 addr = base + 32u * l + lane;
+      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), r);
+    }
+  }
+}
+)";
+  return s;
+}
+
 struct Entry {
   std::vector<uint32_t> words;
   int M;
@@ -506,6 +587,54 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     return -1;
   }
   return 0;
+}
+
+int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
+             int elem, uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
+             std::string& err) {
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    std::vector<uint32_t> keyw(words, words + n);
+    keyw.push_back((uint32_t)elem);
+    const uint64_t kind = 0x6b726f6eull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && e.words == keyw) fn = e.fn;
+    if (!fn) fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem), "qsim_jit_kron",
+                                    err);
+    if (!fn) return -1;
+  }
+  if (count == 0) return 0;
+  uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  uint64_t blocks = (te - tb + 7) / 8;
+  const uint64_t cap = (uint64_t)sms * 8;
+  if (blocks > cap) blocks = cap;
+  uint64_t end = start + count;
+  (void)qbytes;
+  void* args[] = {&start, &end, &tb, &te, const_cast<void*>(qubits_struct), &k2_out};
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(kron_source(words, n, M, elem), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,

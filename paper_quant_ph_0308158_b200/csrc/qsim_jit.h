@@ -24,6 +24,13 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
 int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err);
+// Natural-order fused walk with the input generated on the fly (Appendix 1):
+// k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
+// qsim::Qubits (passed by value as a kernel parameter).
+int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
+             int elem, uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
+             std::string& err);
+int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::string& err);
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
                             std::string& err);
 }  // namespace qsim

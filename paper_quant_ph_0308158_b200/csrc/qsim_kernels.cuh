@@ -331,6 +331,87 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
   }
 }
 
+// ------------------------------------------------ input generated on the fly
+// Appendix 1: k1(s) = q_M(b_M) ... q_1(b_1).  The M factors are
+// grouped in bytes of s: T_g[v] = product of q_j(bit) over the 8 qubits of
+// byte g (j descending, the Kronecker order), and k1(s) = ((T_3 T_2) T_1) T_0
+// evaluated in the state precision without FMA contraction (each complex
+// product rounded as written: re = ar*br - ai*bi, im = ar*bi + ai*br).
+struct Qubits {
+  double v[32][4];  // qubit j (1-based) at v[j-1]: re q(0), im q(0), re q(1), im q(1)
+  uint32_t M;
+};
+
+__device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
+  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
+                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x)));
+}
+__device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+}
+template <typename C> __device__ __forceinline__ C cmake(double re, double im);
+template <> __device__ __forceinline__ float2 cmake<float2>(double re, double im) {
+  return make_float2((float)re, (float)im);
+}
+template <> __device__ __forceinline__ double2 cmake<double2>(double re, double im) {
+  return make_double2(re, im);
+}
+
+// Every thread of the CTA helps fill T[4][256] (call, then __syncthreads()).
+template <typename C>
+__device__ __forceinline__ void kron_tables(const Qubits& q, C (*T)[256]) {
+  for (int x = threadIdx.x; x < 4 * 256; x += blockDim.x) {
+    const int g = x >> 8, v = x & 255;
+    C acc = cmake<C>(1.0, 0.0);
+    bool first = true;
+    for (int j = 7; j >= 0; --j) {  // qubit index 8g + j (0-based), descending
+      const int b = 8 * g + j;
+      if (b >= (int)q.M) continue;
+      const int bit = (v >> j) & 1;
+      const C f = cmake<C>(q.v[b][2 * bit], q.v[b][2 * bit + 1]);
+      acc = first ? f : cmul_rn(acc, f);
+      first = false;
+    }
+    T[g][v] = acc;
+  }
+}
+
+template <typename C>
+__device__ __forceinline__ C kron_element(C (*T)[256], uint32_t s) {
+  C r = T[3][s >> 24];
+  r = cmul_rn(r, T[2][(s >> 16) & 255]);
+  r = cmul_rn(r, T[1][(s >> 8) & 255]);
+  return cmul_rn(r, T[0][s & 255]);
+}
+
+// Fused with the map, natural order, output range [start, end):
+// k2_out[out - start] = k1(perm(out)), k1 never stored.
+template <int CAP, typename C>
+__global__ void __launch_bounds__(kBsThreads, 2)
+k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
+                       const __grid_constant__ SigmaParams sp, const __grid_constant__ Qubits q,
+                       uint64_t start, uint64_t end, uint64_t tile_begin, uint64_t tile_end,
+                       C* __restrict__ k2_out) {
+  extern __shared__ __align__(16) uint8_t bs_smem[];
+  BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
+  __shared__ C T[4][256];
+  kron_tables<C>(q, T);
+  bs_setup(g, sp, sh);  // ends with __syncthreads()
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
+       tile += (uint64_t)gridDim.x * kBsWarps) {
+    const uint64_t base = tile << 10;
+    uint32_t a[32];
+    bs_walk_tile(g.n, sh, (uint32_t)base, a);
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const uint64_t addr = base + 32u * l + lane;
+      if (addr >= start && addr < end) k2_out[addr - start] = kron_element<C>(T, a[l]);
+    }
+  }
+}
+
 // --------------------------------------------------------------------- apply
 // Natural order: k2[r] = k1[perm[r]]: perm streamed with 128-bit loads (4
 // indices), the gathers issued back to back (8 in flight per thread).

@@ -180,3 +180,29 @@ def test_jit_fused_source_compiles_without_gpu(q):
         if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
             pytest.skip("NVRTC not available here")
         assert rc == q.OK, L.qsim_last_error().decode()
+
+
+def test_jit_kron_source_compiles_without_gpu(q):
+    L = q.lib()
+    for gates, M, dt in ((wl.CONFIGS["cfg5"].gates(), 32, q.C64), (wl.CONFIGS["cfg4"].gates(), 30, q.C128),
+                         (wl.random_gates(10, 9, 1), 9, q.C64)):
+        g = np.ascontiguousarray(gates)
+        rc = L.qsim_jit_check_compile_kron(g.ctypes.data, len(g), M, dt)
+        if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+            pytest.skip("NVRTC not available here")
+        assert rc == q.OK, L.qsim_last_error().decode()
+
+
+def test_kron_validation(q):
+    L = q.lib()
+    g = np.ascontiguousarray(wl.random_gates(5, 8, 1))
+    qd = np.zeros(4 * 8)
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, None, 0, 256, FAKE, 0, None) == q.EINVAL
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 257, FAKE, 0,
+                                 None) == q.ERANGE
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, 9, qd.ctypes.data, 0, 256, FAKE, 0,
+                                 None) == q.EINVAL
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 256, FAKE, 1,
+                                 None) == q.EINVAL      # per-lane walk not offered here
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 0, FAKE, 0,
+                                 None) == q.OK

@@ -1,0 +1,116 @@
+"""GPU parity of the Appendix-1 path (input generated on the fly, fused
+with the map) against the oracle.
+
+The GPU forms the Kronecker product with byte tables in the state precision
+(header qsim.h, qsim_run_fused_kron), the oracle sequentially in double
+precision, so the bar is the rounding bound of the arithmetic: the normwise
+relative error of a product of M complex factors, each complex product
+rounded as written (no FMA), is at most (M-1)*sqrt(5)*u (Brent, Percival &
+Zimmermann 2007), u = 2^-24 (complex64) or 2^-53 (complex128).  Exact
+special cases (basis qubits) are compared bit for bit.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def q():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_native()
+    import paper_quant_ph_0308158_b200 as q
+    return q
+
+
+def tol(M, dtype):
+    u = 2.0 ** -24 if dtype == "c64" else 2.0 ** -53
+    return 1.01 * max(M - 1, 1) * math.sqrt(5.0) * u
+
+
+def _check(got, ref, M, dtype):
+    err = np.abs(got.astype(np.complex128) - ref)
+    bound = tol(M, dtype) * np.abs(ref)
+    bad = np.nonzero(err > bound)[0]
+    assert bad.size == 0, (bad[:5], err[bad[:5]], bound[bad[:5]])
+
+
+def _out(count, dtype):
+    return torch.empty(max(count, 1), dtype=torch.complex64 if dtype == "c64" else torch.complex128,
+                       device=DEV)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("M", [1, 5, 10, 13, 18])
+def test_kron_full(q, M, dtype):
+    gates = wl.random_gates(48, M, 3 + M) if M >= 3 else wl.gates_array([wl.gate(wl.NOT, 0)])
+    qb = wl.random_qubits(M, 30 + M, dtype)
+    ref = oracle.fused_kron(gates, qb)
+    walks = [q.WALK_BITSLICED] + ([q.WALK_JIT] if q.jit_status() == "ready" else [])
+    for walk in walks:
+        out = _out(1 << M, dtype)
+        q.run_fused_kron(gates, M, qb, out, dtype=dtype, walk=walk)
+        torch.cuda.synchronize()
+        _check(out.cpu().numpy()[: 1 << M], ref, M, dtype)
+
+
+@pytest.mark.parametrize("walk", ["bitsliced", "jit"])
+def test_kron_ranges(q, walk):
+    w = q.WALK_BITSLICED if walk == "bitsliced" else q.WALK_JIT
+    if w == q.WALK_JIT and q.jit_status() != "ready":
+        pytest.skip("JIT unavailable")
+    M = 15
+    gates = wl.random_gates(70, M, 4)
+    qb = wl.random_qubits(M, 4, "c64")
+    for start, count in ((0, 1), (7, 1000), (1023, 3), (5000, 12000), ((1 << M) - 9, 9), (11, 0)):
+        out = _out(count, "c64")
+        q.run_fused_kron(gates, M, qb, out, start=start, count=count, dtype="c64", walk=w)
+        torch.cuda.synchronize()
+        if count:
+            _check(out.cpu().numpy()[:count], oracle.fused_kron(gates, qb, start, count), M, "c64")
+
+
+def test_kron_basis_input_is_exact(q):
+    """All qubits |1>: k1 is the basis vector of 2^M - 1, so k2 has
+    exactly one 1, at the output whose source is 2^M - 1, zeros elsewhere."""
+    M = 16
+    gates = wl.random_gates(64, M, 9)
+    qb = wl.basis_qubits(M, 1, "c64")
+    perm = oracle.build_map(gates, M)
+    for walk in (q.WALK_BITSLICED, q.WALK_AUTO):
+        out = _out(1 << M, "c64")
+        q.run_fused_kron(gates, M, qb, out, dtype="c64", walk=walk)
+        torch.cuda.synchronize()
+        got = out.cpu().numpy()
+        want = np.zeros(1 << M, dtype=np.complex64)
+        want[int(np.nonzero(perm == (1 << M) - 1)[0][0])] = 1
+        assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.slow
+def test_kron_cfg5_full_size_sampled(q):
+    """M = 32, the cfg5 circuit, write-only (no k1 in memory): sampled outputs."""
+    cfg = wl.CONFIGS["cfg5"]
+    gates, M, N = cfg.gates(), 32, 1 << 32
+    qb = wl.random_qubits(M, 2024, "c64")
+    out = torch.empty(N, dtype=torch.complex64, device=DEV)
+    q.run_fused_kron(gates, M, qb, out, dtype="c64")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    idx = np.concatenate([[0, 1, 1023, 1024, N - 1], rng.integers(0, N, 4096, dtype=np.uint64)])
+    idx = idx.astype(np.uint64)
+    src = oracle.walk_many(gates, idx)
+    ref = np.array([oracle.kron_element(qb, int(s)) for s in src])
+    got = out.index_select(0, torch.from_numpy(idx.astype(np.int64)).to(DEV)).cpu().numpy()
+    _check(got, ref, M, "c64")
+    del out
+    torch.cuda.empty_cache()

@@ -262,3 +262,54 @@ def test_high_bits_untouched_by_low_circuit():
     gates = wl.random_gates(50, 8, 5)
     perm = oracle.build_map(gates, M).astype(np.int64)
     assert np.array_equal(perm >> 8, np.arange(1 << M) >> 8)
+
+
+# ------------------------------------------------ Appendix 1 (input on the fly)
+def test_appendix1_worked_example_P89():
+    """P:L89: k_1(5) with i = 101 is q_3(1) q_2(0) q_1(1)."""
+    (tag, M, ibits, *factors), = _rows("appendix1_P87_P89.txt")
+    M, i = int(M), int(ibits, 2)
+    q = wl.random_qubits(M, 11, "c128")
+    want = 1.0 + 0j
+    for f in factors:
+        j, c = map(int, f.split(":"))
+        want *= q[j - 1, c]
+    assert abs(oracle.kron_element(q, i) - want) <= 1e-15 * abs(want)
+
+
+@pytest.mark.parametrize("M", [1, 3, 7])
+def test_appendix1_all_ones_P87(M):
+    """Every qubit |1> = [0 1]: the Kronecker product is the basis vector of
+    the all-ones address 2^M - 1 (reading R12)."""
+    q = wl.basis_qubits(M, 1, "c128")
+    vals = [oracle.kron_element(q, i) for i in range(1 << M)]
+    assert vals[(1 << M) - 1] == 1
+    assert all(v == 0 for v in vals[:-1])
+
+
+@pytest.mark.parametrize("M", [1, 2, 5, 10])
+def test_appendix1_equals_numpy_kron(M):
+    """Element-wise generation equals the full Kronecker product built with
+    numpy.kron in the written order q_M (x) ... (x) q_1."""
+    q = wl.random_qubits(M, 100 + M, "c128")
+    full = np.ones(1, dtype=np.complex128)
+    for j in range(M, 0, -1):
+        full = np.kron(full, q[j - 1])
+    got = np.array([oracle.kron_element(q, i) for i in range(1 << M)])
+    np.testing.assert_allclose(got, full, rtol=1e-14, atol=0)
+    # the product state is normalised when every qubit is (norm is multiplicative)
+    assert abs(np.linalg.norm(full) - 1) < 1e-13
+
+
+def test_fused_kron_equals_apply_of_kron_vector():
+    M = 11
+    gates = wl.random_gates(40, M, 8)
+    q = wl.random_qubits(M, 8, "c128")
+    full = np.ones(1, dtype=np.complex128)
+    for j in range(M, 0, -1):
+        full = np.kron(full, q[j - 1])
+    ref = oracle.apply_map(oracle.build_map(gates, M), full)
+    got = oracle.fused_kron(gates, q)
+    np.testing.assert_allclose(got, ref, rtol=1e-14, atol=0)
+    part = oracle.fused_kron(gates, q, 300, 77)
+    np.testing.assert_array_equal(part, got[300:377])

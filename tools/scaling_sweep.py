@@ -1,0 +1,56 @@
+"""Per-bit scaling sweep on one B200 (Figure 4 analogue).
+
+The paper reports run time growing "roughly x3.4 per bit ... from M = 30 to
+31" on NCSA modi4 with up to 64 threads.  This times the hot path
+for M = 20..32 on 64 random NOT/CNOT/CCNOT gates (seed 4, the cfg5 recipe
+over M bits) and complex64 Gaussian states, and prints a CSV with the
+growth factor per added bit.
+
+    python tools/scaling_sweep.py [--mmin 20] [--mmax 32] > profiles/rNN_scaling.csv
+"""
+import argparse
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_quant_ph_0308158_b200 as q  # noqa: E402
+import workloads as wl  # noqa: E402
+from tools.sweep_apply import timeit  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--mmin", type=int, default=20)
+    ap.add_argument("--mmax", type=int, default=32)
+    args = ap.parse_args()
+    print("M,entries,map_gather_ms,build_ms,apply_ms,fused_ms,entries_per_s,growth_per_bit,"
+          "plan_natural")
+    prev = None
+    for M in range(args.mmin, args.mmax + 1):
+        N = 1 << M
+        gates = wl.random_gates(64, M, 4)
+        spec = wl.StateSpec(M, "c64", wl.GAUSS, 1004)
+        host = torch.empty(N * 8, dtype=torch.uint8, pin_memory=True)
+        wl.fill_state(spec, host.data_ptr())
+        k1 = host.to("cuda")
+        del host
+        k2 = torch.empty_like(k1)
+        perm = torch.empty(N, dtype=torch.int32, device="cuda")
+        ws = q.workspace()
+        plan = q.plan_create(gates, M, "c64")
+        t_mg = timeit(lambda: q.map_gather_planned(plan, gates, perm, k1, k2, ws))
+        t_b = timeit(lambda: q.build_map(gates, M, perm))
+        t_a = timeit(lambda: q.apply_map_planned(plan, perm, k1, k2, ws))
+        t_f = timeit(lambda: q.run_fused_planned(plan, gates, k1, k2, ws))
+        growth = "" if prev is None else f"{t_mg / prev:.3f}"
+        print(f"{M},{N},{t_mg:.4f},{t_b:.4f},{t_a:.4f},{t_f:.4f},{N / t_mg * 1e3:.4e},{growth},"
+              f"{int(plan.flags & 1)}", flush=True)
+        prev = t_mg
+        del k1, k2, perm
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

@@ -160,6 +160,23 @@ def fill_tagged(dtype: str, out_ptr: int, start: int, count: int) -> None:
     _load().gen_tagged(_ELEM[dtype], start, count, out_ptr)
 
 
+def random_qubits(M: int, seed: int, dtype: str = "c64") -> np.ndarray:
+    """M normalised qubits [q_j(0), q_j(1)] (Appendix 1), row j-1 = q_j:
+    i.i.d. Gaussian complex pairs scaled to |q(0)|^2 + |q(1)|^2 = 1, rounded
+    to the state dtype (the rounded values are the input both sides use)."""
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((M, 2)) + 1j * rng.standard_normal((M, 2))
+    z /= np.sqrt((np.abs(z) ** 2).sum(axis=1, keepdims=True))
+    return z.astype(NP_DTYPE[dtype])
+
+
+def basis_qubits(M: int, bit: int, dtype: str = "c64") -> np.ndarray:
+    """Every qubit |bit>: [1, 0] for |0>, [0, 1] for |1> (P:L87 uses all |1>)."""
+    q = np.zeros((M, 2), dtype=NP_DTYPE[dtype])
+    q[:, bit] = 1
+    return q
+
+
 # --------------------------------------------------------------------------
 # the five BASELINE.json configs (cfg1..cfg5 = configs[0..4])
 # --------------------------------------------------------------------------
