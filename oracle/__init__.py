@@ -63,6 +63,15 @@ def _load():
         lib.oracle_walk_many.restype = None
         lib.oracle_walk_many.argtypes = [u8p, ctypes.c_int32, ctypes.c_void_p,
                                          ctypes.c_uint64, ctypes.c_void_p]
+        lib.oracle_build_signed.restype = None
+        lib.oracle_build_signed.argtypes = [u8p, ctypes.c_int32, ctypes.c_uint64,
+                                            ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_apply_signed.restype = None
+        lib.oracle_apply_signed.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64,
+                                            ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p]
+        lib.oracle_walk_signed.restype = ctypes.c_uint64
+        lib.oracle_walk_signed.argtypes = [u8p, ctypes.c_int32, ctypes.c_uint64,
+                                           ctypes.POINTER(ctypes.c_int)]
         lib.oracle_kron_element.restype = None
         lib.oracle_kron_element.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64,
                                             ctypes.c_void_p, ctypes.c_void_p]
@@ -111,6 +120,37 @@ def build_map(gates, M: int, start: int = 0, count: int | None = None) -> np.nda
     perm = np.empty(count, dtype=np.uint32)
     _load().oracle_build(ptr, n, start, count, perm.ctypes.data)
     return perm
+
+
+def build_map_signed(gates, M: int, start: int = 0, count: int | None = None):
+    """(perm, signs): phased permutation (reading R17); bit r % 32 of
+    signs[r // 32] is 1 when row start + r holds -1."""
+    N = 1 << M
+    if count is None:
+        count = N - start
+    g, ptr, n = _gates_arg(gates)
+    perm = np.empty(count, dtype=np.uint32)
+    signs = np.empty(max((count + 31) // 32, 1), dtype=np.uint32)
+    _load().oracle_build_signed(ptr, n, start, count, perm.ctypes.data, signs.ctypes.data)
+    return perm, signs
+
+
+def walk_signed(gates, i: int):
+    g, ptr, n = _gates_arg(gates)
+    s = ctypes.c_int()
+    x = _load().oracle_walk_signed(ptr, n, i, ctypes.byref(s))
+    return int(x), int(s.value)
+
+
+def apply_map_signed(perm: np.ndarray, signs: np.ndarray, k1: np.ndarray) -> np.ndarray:
+    """k2[i] = sign[i] * k1[perm[i]] (IEEE negation for -1)."""
+    perm = np.ascontiguousarray(perm, dtype=np.uint32)
+    signs = np.ascontiguousarray(signs, dtype=np.uint32)
+    k1 = np.ascontiguousarray(k1)
+    k2 = np.empty(perm.shape[0], dtype=k1.dtype)
+    _load().oracle_apply_signed(perm.ctypes.data, signs.ctypes.data, perm.shape[0],
+                                _elem_bytes(k1), k1.ctypes.data, k2.ctypes.data)
+    return k2
 
 
 def apply_map(perm: np.ndarray, k1: np.ndarray) -> np.ndarray:

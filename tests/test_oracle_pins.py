@@ -313,3 +313,107 @@ def test_fused_kron_equals_apply_of_kron_vector():
     np.testing.assert_allclose(got, ref, rtol=1e-14, atol=0)
     part = oracle.fused_kron(gates, q, 300, 77)
     np.testing.assert_array_equal(part, got[300:377])
+
+
+# ------------------------------------- phased permutations (NEXT(3), R17)
+def _all_ext_gates(M):
+    gs = list(_all_gates(M))
+    for t in range(M):
+        gs.append(wl.gate(wl.Z, t))
+        for c in range(M):
+            if c != t:
+                gs.append(wl.gate(wl.CZ, t, c))
+                gs.append(wl.gate(wl.SWAP, t, c))
+        for c0 in range(M):
+            for c1 in range(c0 + 1, M):
+                if t not in (c0, c1):
+                    gs.append(wl.gate(wl.CCZ, t, c0, c1))
+    return gs
+
+
+def test_paper_matrix_P37_exact_with_phase():
+    """Dropping P:L39's "phase gates are not used" admits the P:L37 matrix
+    itself, -1 included: the 4-gate circuit of the direction pin followed by
+    CZ(a(1), a(2)) reproduces it entry for entry."""
+    rows = _rows("example_matrix_P37.txt")
+    P = np.zeros((4, 4))
+    for r, c, v in rows:
+        P[int(r), int(c)] = float(v)
+    gates = wl.gates_array([wl.gate(wl.CNOT, 1, 0), wl.gate(wl.NOT, 1),
+                            wl.gate(wl.CNOT, 0, 1), wl.gate(wl.NOT, 1), wl.gate(wl.CZ, 0, 1)])
+    np.testing.assert_array_equal(dense.composite_matrix(gates, 2), P)
+    perm, signs = oracle.build_map_signed(gates, 2)
+    assert perm.tolist() == [3, 0, 2, 1]
+    assert int(signs[0]) == 0b1000                     # row 3 holds -1
+    k1 = wl.make_state(wl.StateSpec(2, "c128", wl.GAUSS, 3))
+    np.testing.assert_array_equal(oracle.apply_map_signed(perm, signs, k1), P @ k1)
+
+
+@pytest.mark.parametrize("M", [2, 3, 4])
+def test_ext_step_equals_kronecker_matrix_exhaustive(M):
+    for g in _all_ext_gates(M):
+        S = dense.step_matrix(g, M)
+        assert np.array_equal(S, S.T)                    # symmetric (P:L39)
+        cols, vals = dense.signed_perm_of(S)
+        assert [oracle.step(g, x) for x in range(1 << M)] == cols.tolist()
+        assert [oracle.walk_signed(g, x)[1] for x in range(1 << M)] == vals.astype(int).tolist()
+        assert np.array_equal(S @ S, np.eye(1 << M))    # every step is an involution
+
+
+@pytest.mark.parametrize("M", [2, 3, 4])
+def test_ext_composite_equals_dense_product(M):
+    for seed in range(30):
+        gates = wl.random_gates_ext([0, 1, 3, 8, 15][seed % 5], M, seed,
+                                    kinds=(0, 1, 3, 4, 6) if M == 2 else
+                                    (0, 1, 2, 3, 4, 5, 6))
+        U = dense.composite_matrix(gates, M)
+        cols, vals = dense.signed_perm_of(U)
+        perm, signs = oracle.build_map_signed(gates, M)
+        assert np.array_equal(perm, cols)
+        got = np.array([-1.0 if (int(signs[i // 32]) >> (i % 32)) & 1 else 1.0
+                        for i in range(1 << M)])
+        assert np.array_equal(got, vals)
+        k1 = wl.make_state(wl.StateSpec(M, "c128", wl.GAUSS, seed))
+        np.testing.assert_array_equal(U @ k1, oracle.apply_map_signed(perm, signs, k1))
+
+
+@pytest.mark.parametrize("M", [5, 10, 12])
+def test_ext_accumulation_equals_composite(M):
+    gates = wl.random_gates_ext(60, M, 50 + M)
+    for dtype in ("c64", "c128"):
+        k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, M))
+        perm, signs = oracle.build_map_signed(gates, M)
+        want = oracle.apply_map_signed(perm, signs, k1)
+        assert oracle.accumulate(gates, k1).tobytes() == want.tobytes()
+        assert oracle.run_fused(gates, k1).tobytes() == want.tobytes()
+
+
+def test_swap_only_is_a_bit_permutation_and_z_only_a_parity():
+    M = 10
+    rng = np.random.default_rng(2)
+    pairs = [tuple(map(int, rng.choice(M, 2, replace=False))) for _ in range(25)]
+    gates = wl.gates_array([wl.gate(wl.SWAP, a, b) for a, b in pairs])
+    # the composite moves whole bits: bit b of perm[i] is bit src[b] of i,
+    # src obtained by applying the swaps in walk order (last gate first)
+    src = list(range(M))
+    for a, b in reversed(pairs):
+        src[a], src[b] = src[b], src[a]
+    perm = oracle.build_map(gates, M)
+    for i in range(1 << M):
+        assert int(perm[i]) == sum(((i >> src[b]) & 1) << b for b in range(M))
+    ts = rng.integers(0, M, size=9)
+    zg = wl.gates_array([wl.gate(wl.Z, int(t)) for t in ts])
+    p2, s2 = oracle.build_map_signed(zg, M)
+    assert np.array_equal(p2, np.arange(1 << M, dtype=np.uint32))
+    mask = 0
+    for t in ts:
+        mask ^= 1 << int(t)
+    for i in range(1 << M):
+        assert ((int(s2[i // 32]) >> (i % 32)) & 1) == bin(i & mask).count("1") % 2
+
+
+def test_ext_group_identity():
+    M = 12
+    gates = wl.random_gates_ext(80, M, 9)
+    p, s = oracle.build_map_signed(np.concatenate([gates, gates[::-1]]), M)
+    assert np.array_equal(p, np.arange(1 << M, dtype=np.uint32)) and not s.any()

@@ -20,7 +20,9 @@ from dataclasses import dataclass
 import numpy as np
 
 NOT, CNOT, CCNOT = 0, 1, 2
+Z, CZ, CCZ, SWAP = 3, 4, 5, 6      # phased permutations
 UNUSED = 255
+_NCTRL = {NOT: 0, CNOT: 1, CCNOT: 2, Z: 0, CZ: 1, CCZ: 2, SWAP: 1}
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "stategen.c")
@@ -32,7 +34,8 @@ _lib = None
 # gates
 # --------------------------------------------------------------------------
 def gate(kind: int, target: int, *controls: int) -> np.ndarray:
-    assert len(controls) == kind, (kind, controls)
+    """(kind, target, c0, c1); SWAP(a, b) is gate(SWAP, a, b)."""
+    assert len(controls) == _NCTRL[kind], (kind, controls)
     c = list(controls) + [UNUSED] * (2 - len(controls))
     return np.array([kind, target, c[0], c[1]], dtype=np.uint8)
 
@@ -53,6 +56,19 @@ def random_gates(n: int, nbits: int, seed: int) -> np.ndarray:
     for _ in range(n):
         kind = int(rng.integers(3))
         bits = rng.choice(nbits, size=1 + kind, replace=False)
+        rows.append(gate(kind, int(bits[0]), *[int(b) for b in bits[1:]]))
+    return gates_array(rows)
+
+
+def random_gates_ext(n: int, nbits: int, seed: int,
+                     kinds=(NOT, CNOT, CCNOT, Z, CZ, CCZ, SWAP)) -> np.ndarray:
+    """Test circuits over the extended gate set: kind uniform over `kinds`,
+    then 1 + (#controls) distinct bits, the first being the target."""
+    rng = np.random.default_rng(seed)
+    rows = []
+    for _ in range(n):
+        kind = int(kinds[int(rng.integers(len(kinds)))])
+        bits = rng.choice(nbits, size=1 + _NCTRL[kind], replace=False)
         rows.append(gate(kind, int(bits[0]), *[int(b) for b in bits[1:]]))
     return gates_array(rows)
 
