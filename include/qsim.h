@@ -144,16 +144,21 @@ int qsim_run_fused_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
  * 128-byte line of k1 are scattered over the whole output range, so for a
  * random circuit almost every read misses L2.  A plan orders the traversal:
  * output i = sigma(c) for counter c = 0 .. 2^M-1, sigma a permutation of
- * the address bits that keeps bits 0..4 in place (warps stay coalesced) and
- * puts first the output bits in which the readers of one k1 line most often
- * differ; CTAs take chunks of 2^chunk_log2 counters strictly in counter
- * order from a device ticket, so the lines a chunk front touches stay in L2.
- * The result is the same k2 bytes; only the order of work changes.
+ * the address bits that keeps bits 0..2 (complex64) / 0..1 (complex128) in
+ * place (stores stay whole 32-byte sectors).  Counter bits 0..tile_log2-1
+ * are the "sector cover": the output bits in which the readers of one
+ * 32-byte k1 sector most often differ, so they are handled by one CTA close
+ * in time and its L1 serves the sector after the first miss; the remaining
+ * bits follow in order of how often the readers of one 128-byte k1 line
+ * differ in them.  CTAs take chunks of 2^chunk_log2 counters strictly in
+ * counter order from a device ticket, so the lines a chunk front touches
+ * stay in L2.  The result is the same k2 bytes; only the order of work
+ * changes.
  *
- * qsim_plan_create samples the circuit on the host (inverse walk of 2048
- * pseudo-random k1 lines, fixed seed: deterministic) and fills `plan`, a
- * plain value owned by the caller.  chunk_log2 and blocks_per_sm may be
- * edited before use (tuning).                                               */
+ * qsim_plan_create samples the circuit on the host (forward and inverse
+ * walks of pseudo-random outputs and k1 lines, fixed seeds: deterministic)
+ * and fills `plan`, a plain value owned by the caller.  chunk_log2 and
+ * blocks_per_sm may be edited before use (tuning).                          */
 #define QSIM_WORKSPACE_BYTES 256
 
 typedef struct qsim_plan {
@@ -173,6 +178,12 @@ typedef struct qsim_plan {
     uint8_t sigma[32];      /* counter bit k -> output bit sigma[k]            */
     float change_freq[32];  /* per output bit: fraction of sampled k1 lines whose
                                readers differ in that bit                     */
+    uint8_t tile_log2;      /* diagnostics (ABI 2): counter bits 0..tile_log2-1 are the
+                               "sector cover" -- the output bits in which the readers
+                               of one 32-byte k1 sector most often differ (sampled)   */
+    uint8_t tile_reserved[3];
+    float tile_contained;   /* sampled fraction of (reader, sector-mate reader) pairs
+                               that differ only in those bits                        */
 } qsim_plan;
 
 int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
@@ -184,7 +195,7 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  *              on `stream` by the call; must not be used by a concurrent
  *              call.  NULL: grid-stride chunk order (slower, still correct).
  * QSIM_EINVAL if the plan is malformed (sigma not a permutation of 0..M-1
- * fixing bits 0..4, chunk_log2 or blocks_per_sm out of range).              */
+ * fixing bits 0..2 / 0..1, chunk_log2 or blocks_per_sm out of range).      */
 int qsim_apply_map_planned(const qsim_plan *plan, const uint32_t *perm, const void *k1,
                            void *k2, void *workspace, void *stream);
 

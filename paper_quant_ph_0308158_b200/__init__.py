@@ -53,7 +53,9 @@ class Plan(ctypes.Structure):
                 ("flags", ctypes.c_uint32), ("ilp", ctypes.c_uint16),
                 ("cta_threads", ctypes.c_uint16), ("fused_chunk_log2", ctypes.c_uint16),
                 ("reserved_spread", ctypes.c_uint16),
-                ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32)]
+                ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32),
+                ("tile_log2", ctypes.c_uint8), ("tile_reserved", ctypes.c_uint8 * 3),
+                ("tile_contained", ctypes.c_float)]
 
 
 def _load() -> ctypes.CDLL:

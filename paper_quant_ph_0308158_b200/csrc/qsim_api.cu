@@ -7,6 +7,7 @@
 // arithmetic is packing the gate list and, in qsim_plan_create, sampling the
 // circuit to choose a traversal order.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <algorithm>
@@ -321,6 +322,10 @@ uint32_t plan_inverse_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32
   return x;
 }
 
+// counter bits that stay output bits: 32-byte runs of k2 and perm (8
+// complex64 / 2 complex128 entries: 64 / 32 bytes of k2, 32 / 8 bytes of perm)
+int plan_keep_bits(int32_t dtype) { return dtype == QSIM_C64 ? 3 : 2; }
+
 int plan_validate(const qsim_plan* p) {
   if (!p) return QSIM_EINVAL;
   if (p->M < 1 || p->M > 32) return QSIM_ERANGE;
@@ -329,7 +334,7 @@ int plan_validate(const qsim_plan* p) {
   for (int k = 0; k < p->M; ++k) {
     if (p->sigma[k] >= p->M) return QSIM_EINVAL;
     seen |= 1ull << p->sigma[k];
-    if (k < 5 && p->sigma[k] != k) return QSIM_EINVAL;
+    if (k < plan_keep_bits(p->dtype) && p->sigma[k] != k) return QSIM_EINVAL;
   }
   if (seen != ((1ull << p->M) - 1)) return QSIM_EINVAL;
   if (p->M >= 10 && (p->chunk_log2 < 10 || (int)p->chunk_log2 > p->M)) return QSIM_EINVAL;
@@ -371,15 +376,96 @@ int spread_q90_log2(std::vector<uint64_t>& spreads) {
   return l;
 }
 
+// perm(x) = f_1(...f_n(x)): Step n first (readings R1, R2)
+uint32_t plan_forward_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32_t x) {
+  for (int k = n - 1; k >= 0; --k)
+    if ((~x & cm[k]) == 0u) x ^= tm[k];
+  return x;
+}
+
+// Sector cover: sample outputs i, their sources s = perm(i), and the readers
+// g(s ^ r) of the other entries of s's 32-byte sector of k1 (g = perm^-1);
+// the diff patterns d = g(s ^ r) ^ i say which output bits must vary within
+// a block of outputs for a sector's readers to fall into it.  Greedy cover:
+// start from the kept bits, repeatedly add the pattern with the best gain in
+// contained pairs per added bit until T bits.  Returns the bit set V; the
+// fraction of sampled pairs inside a V-block goes to plan->tile_contained.
+uint32_t plan_sector_cover(const uint32_t* cm, const uint32_t* tm, int n, int M, int dtype, int T,
+                           qsim_plan* plan) {
+  const int e = elem_bytes(dtype), eps = 32 / e, keep = plan_keep_bits(dtype);
+  const int samples = 2048;
+  std::vector<uint32_t> diffs;
+  diffs.reserve((size_t)samples * (eps - 1));
+  const uint64_t N = 1ull << M;
+  for (int k = 0; k < samples; ++k) {
+    const uint32_t i = (uint32_t)(plan_mix(0x7e57ull + k) % N);
+    const uint32_t src = plan_forward_walk(cm, tm, n, i);
+    for (int r = 1; r < eps; ++r) diffs.push_back(plan_inverse_walk(cm, tm, n, src ^ (uint32_t)r) ^ i);
+  }
+  std::sort(diffs.begin(), diffs.end());
+  std::vector<std::pair<uint32_t, uint32_t>> pats;  // (pattern, count)
+  for (size_t a = 0; a < diffs.size();) {
+    size_t b = a;
+    while (b < diffs.size() && diffs[b] == diffs[a]) ++b;
+    pats.push_back({diffs[a], (uint32_t)(b - a)});
+    a = b;
+  }
+  std::sort(pats.begin(), pats.end(), [](const std::pair<uint32_t, uint32_t>& x,
+                                         const std::pair<uint32_t, uint32_t>& y) {
+    return x.second != y.second ? x.second > y.second : x.first < y.first;
+  });
+  if (pats.size() > 512) pats.resize(512);  // candidates: the frequent patterns
+  auto contained = [&](uint32_t V) {
+    uint64_t c = 0;
+    for (const auto& pc : pats)
+      if ((pc.first & ~V) == 0) c += pc.second;
+    return c;
+  };
+  uint32_t V = (1u << keep) - 1;
+  int bits = keep;
+  while (bits < T) {
+    const uint64_t base = contained(V);
+    double best = 0.0;
+    uint32_t add_best = 0;
+    for (const auto& pc : pats) {
+      const uint32_t add = pc.first & ~V;
+      const int na = __builtin_popcount(add);
+      if (na == 0 || bits + na > T) continue;
+      const double gain = (double)(contained(V | add) - base) / na;
+      if (gain > best) {
+        best = gain;
+        add_best = add;
+      }
+    }
+    if (add_best == 0) {  // no pattern fits: extend the contiguous output run
+      for (int b = 0; b < M; ++b)
+        if (!((V >> b) & 1u)) {
+          add_best = 1u << b;
+          break;
+        }
+    }
+    V |= add_best;
+    bits = __builtin_popcount(V);
+  }
+  uint64_t hit = 0;
+  for (uint32_t d : diffs) hit += (d & ~V) == 0;
+  plan->tile_contained = diffs.empty() ? 1.0f : (float)hit / (float)diffs.size();
+  plan->tile_log2 = (uint8_t)T;
+  return V;
+}
+
+// bits of the sector cover (counter bits of one L1-resident block of work)
+int plan_cover_bits = 13;
+
 int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan) {
   std::memset(plan, 0, sizeof *plan);
   plan->M = M;
   plan->dtype = dtype;
-  // chunks: 2^16 counters (apply) / 2^19 (fused), but at least 8 chunks per SM
+  // chunks: 2^15 counters (measured best on cfg5), but at least 8 chunks per SM
   int cap = M - 10 - 3;  // 2^(M-13) counters per chunk leaves >= 8 * 1024 chunks
   if (cap < 10) cap = 10;
-  plan->chunk_log2 = (uint32_t)std::min(std::min(16, cap), (int)M);
-  plan->fused_chunk_log2 = (uint32_t)std::min(std::min(16, cap), (int)M);
+  plan->chunk_log2 = (uint32_t)std::min(std::min(15, cap), (int)M);
+  plan->fused_chunk_log2 = (uint32_t)std::min(std::min(15, cap), (int)M);
   plan->blocks_per_sm = 1;
   plan->ilp = 16;
   plan->cta_threads = 256;
@@ -415,16 +501,23 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
     for (int b = 0; b < M; ++b) count[b] += (diff >> b) & 1u;
   }
   for (int b = 0; b < M; ++b) plan->change_freq[b] = (float)count[b] / lines;
-  // sigma: bits 0..4 fixed; then output bits by descending change frequency
-  int order[32], m = 0;
-  for (int b = 5; b < M; ++b) order[m++] = b;
-  for (int i = 1; i < m; ++i)  // stable insertion sort
-    for (int j = i; j > 0 && count[order[j]] > count[order[j - 1]]; --j) {
-      int t = order[j];
-      order[j] = order[j - 1];
-      order[j - 1] = t;
-    }
-  for (int k = 0; k < m; ++k) plan->sigma[5 + k] = (uint8_t)order[k];
+  // sigma: counter bits 0..T-1 = the sector cover V (ascending: the kept bits
+  // first), so the readers of a k1 sector are handled by one CTA close in time
+  // (its L1 serves them); then the other bits by how often a k1 line's readers
+  // differ in them (the chunk front keeps its lines in L2)
+  int cover = plan_cover_bits;
+  if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) cover = std::atoi(cb);  // tuning
+  const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(cover, 20)));
+  const uint32_t V = plan_sector_cover(cm.get(), tm.get(), n, M, dtype, T, plan);
+  int order[32], m = 0, k = 0;
+  for (int b = 0; b < M; ++b) {
+    if ((V >> b) & 1u)
+      plan->sigma[k++] = (uint8_t)b;
+    else
+      order[m++] = b;
+  }
+  std::stable_sort(order, order + m, [&](int x, int y) { return count[x] > count[y]; });
+  for (int j = 0; j < m; ++j) plan->sigma[k++] = (uint8_t)order[j];
   // spread of the readers in sigma order (counter positions)
   uint8_t inv[32];
   for (int k = 0; k < M; ++k) inv[plan->sigma[k]] = (uint8_t)k;
@@ -441,10 +534,10 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
     spread_sig[s] = hi - lo;
   }
   const int nat = spread_q90_log2(spread_nat), sig = spread_q90_log2(spread_sig);
-  // Natural order when it already keeps a line's readers within ~2^20
-  // outputs (e.g. ripple cascades) or when sigma cannot bring them under
-  // ~2^24 either (an effectively random permutation: no order helps).
-  if (nat <= 20 || sig > 24 || sig >= nat) plan->flags = 1;
+  // Natural order when the sector cover holds few sector-mate pairs (an
+  // effectively random permutation, e.g. cfg3: no order helps; measured
+  // equal within 5 %).
+  if (plan->tile_contained < 0.25f) plan->flags = 1;
   // small states are L2-resident: natural order, full parallelism
   if ((1ull << M) * (uint64_t)e <= (64ull << 20)) plan->flags = 1;
   plan->reserved_spread = (uint16_t)(nat | (sig << 8));
@@ -485,13 +578,13 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
   int rc = plan_validate(plan);
   if (rc) return rc;
   const int M = plan->M;
-  if (plan_natural(plan)) return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
   const int e = elem_bytes(plan->dtype);
   if (!perm || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2))
     return QSIM_EINVAL;
   if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
   const uint64_t N = 1ull << M;
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e)) return QSIM_EALIAS;
+  if (plan_natural(plan)) return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
   const qsim::SigmaParams sp = plan_params(plan, workspace);
   if ((rc = reset_ticket(workspace, st))) return rc;
   const uint64_t nchunks = N >> sp.chunk_log2;
@@ -578,13 +671,14 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
   if (rc) return rc;
   const int M = plan->M;
   if ((rc = check_gates(gates, n, M))) return rc;
+  {
+    const int e = elem_bytes(plan->dtype);
+    if (!k1 || !k2 || !aligned16(k1) || !aligned16(k2)) return QSIM_EINVAL;
+    if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
+    if (overlap(k1, (1ull << M) * e, k2, (1ull << M) * e)) return QSIM_EALIAS;
+  }
   if (plan_natural(plan))
     return fused_impl(gates, n, M, plan->dtype, 0, 1ull << M, k1, k2, QSIM_WALK_AUTO, st);
-  const int e = elem_bytes(plan->dtype);
-  if (!k1 || !k2 || !aligned16(k1) || !aligned16(k2)) return QSIM_EINVAL;
-  if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
-  const uint64_t N = 1ull << M;
-  if (overlap(k1, N * e, k2, N * e)) return QSIM_EALIAS;
   bool jit = false;
   return fused_sigma_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st, &jit);
 }
@@ -828,6 +922,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 1; }
+int32_t qsim_abi_version(void) { return 2; }
 
 }  // extern "C"

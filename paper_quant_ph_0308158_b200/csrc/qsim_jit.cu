@@ -47,6 +47,7 @@ struct Nvrtc {
   nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*) = nullptr;
   nvrtcResult_t (*log)(nvrtcProgram_t, char*) = nullptr;
   nvrtcResult_t (*destroy)(nvrtcProgram_t*) = nullptr;
+  int major = 0, minor = 0;
   bool ok = false;
 };
 
@@ -79,8 +80,10 @@ void init_locked() {
       return;
     }
   }
-  const char* cands[] = {std::getenv("QSIM_NVRTC"), "libnvrtc.so.12",
-                         "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so"};
+  // the toolkit's NVRTC first (an absolute path loads it even when torch has
+  // already mapped its own, older libnvrtc.so.12 into the process)
+  const char* cands[] = {std::getenv("QSIM_NVRTC"), "/usr/local/cuda/lib64/libnvrtc.so.12",
+                         "libnvrtc.so.12", "libnvrtc.so"};
   for (const char* c : cands) {
     if (!c) continue;
     g_nvrtc.h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
@@ -99,6 +102,8 @@ void init_locked() {
     g_status = "libnvrtc symbols missing";
     return;
   }
+  nvrtcResult_t (*version)(int*, int*) = nullptr;
+  if (sym(n.h, "nvrtcVersion", version)) version(&n.major, &n.minor);
   void* p = nullptr;
   cudaDriverEntryPointQueryResult q;
   bool ok = true;
@@ -115,7 +120,8 @@ void init_locked() {
                  cudaSuccess && q == cudaDriverEntryPointSuccess;
   g_drv.setattr = reinterpret_cast<PFN_cuFuncSetAttribute_v9000>(p);
   g_drv.ok = ok;
-  g_status = ok ? "ready" : "driver entry points unavailable";
+  g_status = ok ? "ready (nvrtc " + std::to_string(g_nvrtc.major) + "." + std::to_string(g_nvrtc.minor) + ")"
+               : "driver entry points unavailable";
 }
 
 // ---- code generation --------------------------------------------------------
@@ -264,18 +270,22 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
       const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
                      tab[3][(c >> 24) & 255];
 )";
-  // plane initialisation: lane bits, l-bit patterns (compile-time), base bits
+  // plane initialisation: output bit b comes from counter bit inv[b]: a lane
+  // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob)
   const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-  int lpat[32];
-  for (int b = 0; b < 32; ++b) lpat[b] = -1;
-  for (int j = 0; j < 5 && 5 + j < M; ++j) lpat[sigma[5 + j]] = j;
+  uint8_t inv[32];
+  for (int b = 0; b < 32; ++b) inv[b] = 255;
+  for (int k = 0; k < M; ++k) inv[sigma[k]] = (uint8_t)k;
   for (int b = 0; b < 32; ++b) {
-    if (b < 5)
-      std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (lpat[b] >= 0)
-      std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[lpat[b]]);
-    else
+    const int c = b < M ? inv[b] : 255;
+    if (c < 5)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, c);
+    else if (c < 10)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[c - 5]);
+    else if (c < 32)
       std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else
+      std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
     s += buf;
   }
   s += walk_code(w, n, M);
@@ -296,13 +306,14 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
     s += buf;
   }
   s += R"(
+      const u32 lo = tab[0][lane];   // output bits of the lane (= lane when sigma fixes 0..4)
       if (perm_out) {
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob | lt[l] | lane), a[l]);
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob | lt[l] | lo), a[l]);
       }
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob | lt[h + l] | lane), v[l]);
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob | lt[h + l] | lo), v[l]);
       }
     }
   }
@@ -399,6 +410,8 @@ struct Entry {
   double compile_ms;
 };
 std::unordered_map<uint64_t, std::vector<Entry>> g_cache;
+// compiles that failed, with their error: not retried on every call
+std::unordered_map<uint64_t, std::vector<std::pair<std::vector<uint32_t>, std::string>>> g_failed;
 double g_last_compile_ms = 0.0;
 
 uint64_t fnv(const uint32_t* w, int n, uint64_t salt) {
@@ -490,9 +503,19 @@ CUfunction get_kernel_locked(uint64_t kind, const std::vector<uint32_t>& keyw, i
   const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
   for (const Entry& e : g_cache[key])
     if (e.M == M && e.words == keyw) return e.fn;
+  std::vector<uint32_t> fkey(keyw);
+  fkey.push_back((uint32_t)M);
+  for (const auto& f : g_failed[key])
+    if (f.first == fkey) {
+      err = f.second;
+      return nullptr;
+    }
   const auto t0 = std::chrono::steady_clock::now();
   CUfunction fn = compile_locked(src, name, err);
-  if (!fn) return nullptr;
+  if (!fn) {
+    g_failed[key].push_back({fkey, err});
+    return nullptr;
+  }
   g_last_compile_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   g_cache[key].push_back(Entry{keyw, M, fn, g_last_compile_ms});
@@ -527,14 +550,9 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
           std::memcmp(e.words.data(), words, n * sizeof(uint32_t)) == 0)
         fn = e.fn;
     if (!fn) {
-      const auto t0 = std::chrono::steady_clock::now();
-      const std::string src = build_source(words, n, M);
-      fn = compile_locked(src, "qsim_jit_build", err);
+      fn = get_kernel_locked(0x6275696c64ull, std::vector<uint32_t>(words, words + n), M,
+                             build_source(words, n, M), "qsim_jit_build", err);
       if (!fn) return -1;
-      g_last_compile_ms =
-          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-      g_cache[key].push_back(
-          Entry{std::vector<uint32_t>(words, words + n), M, fn, g_last_compile_ms});
     }
   }
   if (count == 0) return 0;

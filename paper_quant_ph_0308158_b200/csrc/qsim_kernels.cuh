@@ -16,8 +16,8 @@
 //
 // Traversal order: "counter" c runs over [0, 2^M); the output it handles is
 // sigma(c), a permutation of the address bits (identity = natural order).
-// sigma fixes bits 0..4, so the 32 lanes of a warp always cover 32
-// consecutive outputs.
+// sigma fixes bits 0..2 (0..1 for complex128), so every warp store covers
+// whole 32-byte sectors; the lanes' output bits are lo = sigma(lane).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -184,6 +184,7 @@ struct BsShared {
   uint32_t tab[4][256];        // sigma deposit tables
   uint32_t patw[32];           // l-bit pattern of each output plane (0 if none)
   uint32_t ltab[32];           // sigma(l << 5)
+  uint8_t lanebit[32];         // output plane b <- lane bit lanebit[b] (255: none)
   uint64_t chunk;
   uint2 gate[1];               // [n]: byte offsets of (target | c0 << 16, c1) planes
 };
@@ -197,7 +198,10 @@ __device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaPara
                                          BsShared& sh) {
   sigma_tables(sp, sh.tab);
   const uint32_t pat[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u, 0xffff0000u};
-  if (threadIdx.x < 32) sh.patw[threadIdx.x] = 0;
+  if (threadIdx.x < 32) {
+    sh.patw[threadIdx.x] = 0;
+    sh.lanebit[threadIdx.x] = 255;
+  }
   sh.S[kOnesPlane][threadIdx.x] = 0xffffffffu;
   // gate list, last gate first (the walk order), as plane byte offsets
   for (uint32_t k = threadIdx.x; k < g.n; k += blockDim.x) {
@@ -208,6 +212,7 @@ __device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaPara
   }
   __syncthreads();
   if (threadIdx.x < 5 && 5 + threadIdx.x < sp.nbits) sh.patw[sp.sigma[5 + threadIdx.x]] = pat[threadIdx.x];
+  if (threadIdx.x < 5 && threadIdx.x < sp.nbits) sh.lanebit[sp.sigma[threadIdx.x]] = (uint8_t)threadIdx.x;
   if (threadIdx.x < 32) {
     uint32_t o = 0;
     for (int j = 0; j < 5; ++j)
@@ -217,13 +222,14 @@ __device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaPara
   __syncthreads();
 }
 
-// Walk one warp tile; on return a[l] = perm(out_base | ltab[l] | lane).
+// Walk one warp tile; on return a[l] = perm(out_base | ltab[l] | sigma(lane)).
 __device__ __forceinline__ void bs_walk_tile(uint32_t n, BsShared& sh, uint32_t out_base,
                                              uint32_t (&a)[32]) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
 #pragma unroll
   for (int b = 0; b < 32; ++b) {
-    const uint32_t lanew = (b < 5) ? (((lane >> b) & 1u) ? 0xffffffffu : 0u) : 0u;
+    const uint32_t lb = sh.lanebit[b];
+    const uint32_t lanew = (lb < 5) ? (((lane >> lb) & 1u) ? 0xffffffffu : 0u) : 0u;
     const uint32_t basew = ((out_base >> b) & 1u) ? 0xffffffffu : 0u;
     sh.S[b][tid] = lanew | sh.patw[b] | basew;
   }
@@ -316,6 +322,7 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
     for (uint32_t tt = warp; tt < tiles_per_chunk; tt += kBsWarps) {
       const uint64_t c = (ch << sp.chunk_log2) + ((uint64_t)tt << 10);
       const uint32_t out_base = sigma_apply(sh.tab, c);
+      const uint32_t lo = sh.tab[0][lane];
       uint32_t a[32];
       bs_walk_tile(g.n, sh, out_base, a);
       constexpr int B = sizeof(T) == 8 ? 32 : 16;  // gathers in flight per thread
@@ -325,7 +332,7 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
 #pragma unroll
         for (int l = 0; l < B; ++l) v[l] = ld_gather(k1 + a[h + l]);
 #pragma unroll
-        for (int l = 0; l < B; ++l) st_stream(k2 + (out_base | sh.ltab[h + l] | lane), v[l]);
+        for (int l = 0; l < B; ++l) st_stream(k2 + (out_base | sh.ltab[h + l] | lo), v[l]);
       }
     }
   }
@@ -457,7 +464,9 @@ k_apply_sigma(const __grid_constant__ SigmaParams sp, const uint32_t* __restrict
   __shared__ uint32_t tab[4][256];
   __shared__ uint64_t s_chunk;
   sigma_tables(sp, tab);
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t lo = tab[0][lane];  // sigma(lane)
   const uint64_t chunk = 1ull << sp.chunk_log2;
   const uint64_t nchunks = N >> sp.chunk_log2;
   for (uint64_t ch = next_chunk(sp, 0, &s_chunk, true); ch < nchunks;
@@ -469,7 +478,7 @@ k_apply_sigma(const __grid_constant__ SigmaParams sp, const uint32_t* __restrict
       uint32_t src[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        idx[u] = sigma_apply(tab, c + 32u * u) | lane;
+        idx[u] = sigma_apply(tab, c + 32u * u) | lo;
         src[u] = __ldcs(perm + idx[u]);
       }
       T v[U];
