@@ -421,8 +421,10 @@ uint32_t plan_sector_cover(const uint32_t* cm, const uint32_t* tm, int n, int M,
       if ((pc.first & ~V) == 0) c += pc.second;
     return c;
   };
-  uint32_t V = (1u << keep) - 1;
-  int bits = keep;
+  int run = keep;  // low output bits in the cover: contiguous output runs of 2^run entries
+  if (const char* rb = std::getenv("QSIM_PLAN_RUN_BITS")) run = std::max(keep, std::min(T, std::atoi(rb)));  // tuning
+  uint32_t V = (1u << run) - 1;
+  int bits = run;
   while (bits < T) {
     const uint64_t base = contained(V);
     double best = 0.0;

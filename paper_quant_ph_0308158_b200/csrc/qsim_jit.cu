@@ -231,6 +231,12 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // Sigma-ordered fused walk + gather (qsim_kernels.cuh k_fused_sigma, with the
 // circuit and the traversal order compiled in).  If perm_out is non-null the
 // kernel also stores the map (one-pass materialised map + gather).
+// QSIM_JIT_PIPE=0 disables the software pipeline of the fused kernel (A/B)
+bool pipelined() {
+  const char* v = std::getenv("QSIM_JIT_PIPE");
+  return !(v && v[0] == '0');
+}
+
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem) {
   std::string s = kPrelude;
   char buf[256];
@@ -240,9 +246,17 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
     std::snprintf(buf, sizeof buf, "%u%s", (unsigned)sigma[k], k < 31 ? "," : "};\n");
     s += buf;
   }
-  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n", T, M,
-                elem == 8 ? 32 : 16);
+  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n"
+                "#define QSIM_PIPE %d\n", T, M, elem == 8 ? 32 : 16, elem == 8 && pipelined() ? 1 : 0);
   s += buf;
+  s += "__constant__ unsigned int lt_g[32] = {";
+  for (int l = 0; l < 32; ++l) {
+    uint32_t o = 0;
+    for (int j = 0; j < 5 && 5 + j < M; ++j)
+      if ((l >> j) & 1) o |= 1u << sigma[5 + j];
+    std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
+    s += buf;
+  }
   s += R"(
 extern "C" __global__ void __launch_bounds__(256)
 qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
@@ -259,6 +273,13 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const u64 nchunks = N >> chunk_log2;
   const u32 tiles = 1u << (chunk_log2 - 10);
+#if QSIM_PIPE
+  // software pipeline: a warp tile's 32 gathers stay in flight while the
+  // warp walks its next tile; they are stored after that walk
+  QSIM_T v[32];
+  u32 pob = 0u;
+  bool pend = false;
+#endif
   for (;;) {
     __syncthreads();
     if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
@@ -310,13 +331,28 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
       if (perm_out) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob | lt[l] | lo), a[l]);
       }
+#if QSIM_PIPE
+      if (pend) {
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) stcs(k2 + (pob | lt[l] | lo), v[l]);
+      }
+      _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
+      pob = ob;
+      pend = true;
+#else
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob | lt[h + l] | lo), v[l]);
       }
+#endif
     }
   }
+#if QSIM_PIPE
+  if (pend) {
+    const u32 lo = tab[0][lane];
+    _Pragma("unroll") for (int l = 0; l < 32; ++l) stcs(k2 + (pob | lt_g[l] | lo), v[l]);
+  }
+#endif
 }
 )";
   return s;
