@@ -49,7 +49,19 @@ extern "C" {
  * target: 0-based bit b, i.e. address bit a(b+1).  c0 (CNOT, CCNOT) and
  * c1 (CCNOT) are the control bits; slots a kind does not use are ignored.
  * Valid: target < M, used controls < M, distinct from the target and from
- * each other.                                                              */
+ * each other.
+ *
+ * Phased permutations (reading R17: "Assuming that phase gates are
+ * not used, each matrix element ... will be non-negative"; the P:L37 matrix
+ * has a -1): kind 3 Z, 4 CZ (control c0), 5 CCZ (c0, c1) -- a diagonal step
+ * whose row x holds -1 when the target bit and every control bit of x are
+ * 1; kind 6 SWAP -- row x has its unity in the column with bits `target` and
+ * c0 exchanged.  SWAP is a plain permutation and is accepted everywhere.
+ * A circuit with phase steps is a permutation with row values +-1: the calls
+ * that produce k2 (run_fused*, run_fused_kron, and build_map_signed +
+ * apply_map_signed) apply the -1 as an IEEE negation of both parts (sign
+ * bits flipped: bit-exact); the calls whose only output is a uint32 map
+ * (build_map*, map_gather_planned, run_host mode 0) return QSIM_EINVAL.      */
 typedef struct qsim_gate {
     uint8_t kind;
     uint8_t target;
@@ -89,6 +101,21 @@ int qsim_build_map(const qsim_gate *gates, int32_t n_gates, int32_t M,
 int qsim_build_map_range(const qsim_gate *gates, int32_t n_gates, int32_t M,
                          uint64_t start, uint64_t count, uint32_t *perm_out,
                          void *stream);
+
+/* qsim_build_map_signed -- a phased permutation materialised: perm_out[r]
+ * as above and its row values, bit r % 32 of signs[r / 32] = 1 when row
+ * start + r holds -1 (words of the range fully written; bits past count 0).
+ *   start   multiple of 32 (QSIM_EINVAL otherwise); count may be 0
+ *   signs   device, (count + 31) / 32 uint32 words, 4-byte aligned       */
+int qsim_build_map_signed(const qsim_gate *gates, int32_t n_gates, int32_t M,
+                          uint64_t start, uint64_t count, uint32_t *perm_out,
+                          uint32_t *signs, void *stream);
+
+/* qsim_apply_map_signed -- k2_out[r] = sign[r] k1[perm_in[r]], r < count,
+ * with the bitmap of qsim_build_map_signed (bit r % 32 of signs[r / 32]).  */
+int qsim_apply_map_signed(const uint32_t *perm_in, const uint32_t *signs, uint64_t count,
+                          int32_t M, int32_t dtype, const void *k1, void *k2_out,
+                          void *stream);
 
 /* qsim_apply_map -- the state transform k2 = U k1 given the
  * materialised map: k2[i] = k1[perm[i]] for all i < 2^M.  Entries are

@@ -29,6 +29,8 @@ LIB_PATH = os.path.join(_PKG, "libqsim.so")
 OK, EINVAL, ERANGE, EBIT, ECAP, EALIAS, ECUDA = 0, -1, -2, -3, -4, -5, -6
 C64, C128 = 0, 1
 WALK_AUTO, WALK_PER_LANE, WALK_BITSLICED, WALK_JIT = 0, 1, 2, 3
+# gate kinds (include/qsim.h): toggles, phase steps (reading R17), SWAP
+NOT, CNOT, CCNOT, Z, CZ, CCZ, SWAP = 0, 1, 2, 3, 4, 5, 6
 MAX_GATES = 4096
 MATERIALISED, FUSED = 0, 1
 
@@ -76,6 +78,8 @@ def _load() -> ctypes.CDLL:
         "qsim_run_fused_ex": [vp, i32, i32, i32, u64, u64, vp, vp, i32, vp],
         "qsim_run_host": [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp],
     }
+    sig["qsim_build_map_signed"] = [vp, i32, i32, u64, u64, vp, vp, vp]
+    sig["qsim_apply_map_signed"] = [vp, vp, u64, i32, i32, vp, vp, vp]
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
     sig["qsim_apply_map_planned"] = [ctypes.POINTER(Plan), vp, vp, vp, vp, vp]
     sig["qsim_run_fused_planned"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp]
@@ -159,6 +163,21 @@ def build_map_range(gates, M: int, start: int, count: int, perm_out, stream=None
     g, gp, n = _gates(gates)
     _check(_lib.qsim_build_map_ex(gp, n, M, start, count, _ptr(perm_out), walk,
                                   _stream(stream)), "qsim_build_map_ex")
+
+
+def build_map_signed(gates, M: int, start: int, count: int, perm_out, signs, stream=None) -> None:
+    """Phased permutation (Z / CZ / CCZ / SWAP steps allowed): perm_out and the
+    row values as a bitmap, bit r % 32 of signs[r // 32] = 1 for -1."""
+    g, gp, n = _gates(gates)
+    _check(_lib.qsim_build_map_signed(gp, n, M, start, count, _ptr(perm_out), _ptr(signs),
+                                      _stream(stream)), "qsim_build_map_signed")
+
+
+def apply_map_signed(perm_in, signs, count: int, M: int, k1, k2_out, stream=None,
+                     dtype=None) -> None:
+    code = _dtype_code(k1 if dtype is None else dtype)
+    _check(_lib.qsim_apply_map_signed(_ptr(perm_in), _ptr(signs), count, M, code, _ptr(k1),
+                                      _ptr(k2_out), _stream(stream)), "qsim_apply_map_signed")
 
 
 def apply_map(perm, M: int, k1, k2, stream=None, dtype=None) -> None:

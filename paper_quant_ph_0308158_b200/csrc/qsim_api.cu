@@ -67,13 +67,25 @@ int check_gates_args(const qsim_gate* gates, int32_t n, int32_t M) {
   return QSIM_OK;
 }
 
-// Validate one gate (P:L43 step semantics; readings R3-R5).
+// Controls a kind uses (the "other bit" for SWAP counts as one).
+int gate_nctrl(uint8_t kind) { return kind == 6 ? 1 : kind % 3; }
+
+// Validate one gate (P:L43 step semantics; readings R3-R5, R17).
 int check_gate(const qsim_gate& g, int32_t M) {
-  if (g.kind > 2) return QSIM_EINVAL;
+  if (g.kind > 6) return QSIM_EINVAL;
+  const int nc = gate_nctrl(g.kind);
   if (g.target >= M) return QSIM_EBIT;
-  if (g.kind >= 1 && (g.c0 >= M || g.c0 == g.target)) return QSIM_EBIT;
-  if (g.kind == 2 && (g.c1 >= M || g.c1 == g.target || g.c1 == g.c0)) return QSIM_EBIT;
+  if (nc >= 1 && (g.c0 >= M || g.c0 == g.target)) return QSIM_EBIT;
+  if (nc == 2 && (g.c1 >= M || g.c1 == g.target || g.c1 == g.c0)) return QSIM_EBIT;
   return QSIM_OK;
+}
+
+// Any phase step (Z, CZ, CCZ): rows take values -1, a uint32 map alone does
+// not hold the operator (qsim_build_map_signed does).
+bool has_phase(const qsim_gate* gates, int32_t n) {
+  for (int32_t k = 0; k < n; ++k)
+    if (gates[k].kind >= 3 && gates[k].kind <= 5) return true;
+  return false;
 }
 
 int check_gates(const qsim_gate* gates, int32_t n, int32_t M) {
@@ -83,19 +95,22 @@ int check_gates(const qsim_gate* gates, int32_t n, int32_t M) {
 }
 
 // Pack for the kernels (gates already validated).  bitsliced: target |
-// c0 << 8 | c1 << 16 with absent controls = the all-ones plane; per-lane:
-// kind | target << 8 | c0 << 16 | c1 << 24 with absent controls = 0.
+// c0 << 8 | c1 << 16 | op << 24 with absent controls = the all-ones plane
+// (op: toggle / swap / phase); per-lane (and NVRTC): kind | target << 8 |
+// c0 << 16 | c1 << 24 with absent controls = 0.
 template <int CAP>
 void pack_gates(const qsim_gate* gates, int32_t n, bool bitsliced, qsim::GateList<CAP>& out) {
   out.n = (uint32_t)n;
   for (int32_t k = 0; k < n; ++k) {
     const qsim_gate& g = gates[k];
+    const int nc = gate_nctrl(g.kind);
     if (bitsliced) {
-      const uint32_t c0 = g.kind >= 1 ? g.c0 : qsim::kOnesPlane;
-      const uint32_t c1 = g.kind == 2 ? g.c1 : qsim::kOnesPlane;
-      out.w[k] = (uint32_t)g.target | (c0 << 8) | (c1 << 16);
+      const uint32_t c0 = nc >= 1 ? g.c0 : qsim::kOnesPlane;
+      const uint32_t c1 = nc == 2 ? g.c1 : qsim::kOnesPlane;
+      const uint32_t op = g.kind == 6 ? qsim::kOpSwap : g.kind >= 3 ? qsim::kOpPhase : qsim::kOpToggle;
+      out.w[k] = (uint32_t)g.target | (c0 << 8) | (c1 << 16) | (op << 24);
     } else {
-      const uint32_t c0 = g.kind >= 1 ? g.c0 : 0u, c1 = g.kind == 2 ? g.c1 : 0u;
+      const uint32_t c0 = nc >= 1 ? g.c0 : 0u, c1 = nc == 2 ? g.c1 : 0u;
       out.w[k] = (uint32_t)g.kind | ((uint32_t)g.target << 8) | (c0 << 16) | (c1 << 24);
     }
   }
@@ -120,7 +135,8 @@ qsim::SigmaParams identity_sigma(int32_t M) {
 // MODE 1 gathers k1 into k2_out (fused).
 template <int CAP, int MODE, typename T>
 int launch_walk_cap(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
-                    uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st) {
+                    uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st,
+                    uint32_t* signs_out) {
   if (count == 0) return QSIM_OK;
   const int sms = sm_count();
   std::unique_ptr<qsim::GateList<CAP>> gl(new qsim::GateList<CAP>);
@@ -147,7 +163,7 @@ int launch_walk_cap(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start
     cudaFuncSetAttribute(qsim::k_build_bitsliced<CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     qsim::k_build_bitsliced<CAP><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(
-        *gl, sp, start, start + count, tb, te, perm_out);
+        *gl, sp, start, start + count, tb, te, perm_out, signs_out);
     QSIM_CHECK_LAUNCH("k_build_bitsliced");
   } else {
     cudaFuncSetAttribute(qsim::k_fused_bitsliced<CAP, T>,
@@ -161,15 +177,19 @@ int launch_walk_cap(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start
 
 template <int MODE, typename T>
 int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
-                uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st) {
+                uint32_t* perm_out, const T* k1, T* k2_out, int32_t walk, cudaStream_t st,
+                uint32_t* signs_out = nullptr) {
   if (n <= 64)
-    return launch_walk_cap<64, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st);
+    return launch_walk_cap<64, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st,
+                                        signs_out);
   if (n <= 256)
-    return launch_walk_cap<256, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st);
+    return launch_walk_cap<256, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st,
+                                         signs_out);
   if (n <= 1024)
-    return launch_walk_cap<1024, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk, st);
+    return launch_walk_cap<1024, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out, walk,
+                                          st, signs_out);
   return launch_walk_cap<qsim::kMaxGates, MODE, T>(gates, n, M, start, count, perm_out, k1, k2_out,
-                                                   walk, st);
+                                                   walk, st, signs_out);
 }
 
 // Large builds use the circuit-specialised kernel (qsim_jit.cu) when NVRTC
@@ -180,6 +200,10 @@ int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uin
                uint32_t* perm_out, int32_t walk, cudaStream_t st) {
   int rc = check_gates(gates, n, M);
   if (rc) return rc;
+  if (has_phase(gates, n)) {  // the map alone would drop the -1 rows
+    std::snprintf(g_err, sizeof g_err, "phase gates: use qsim_build_map_signed");
+    return QSIM_EINVAL;
+  }
   if ((rc = check_range(M, start, count))) return rc;
   if (walk < 0 || walk > 3) return QSIM_EINVAL;
   if (perm_out == nullptr || !aligned16(perm_out)) return QSIM_EINVAL;
@@ -198,6 +222,49 @@ int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uin
     walk = QSIM_WALK_BITSLICED;
   }
   return launch_walk<0, uint2>(gates, n, M, start, count, perm_out, nullptr, nullptr, walk, st);
+}
+
+// Phased permutation, materialised: perm and the row values (signs bitmap),
+// natural order, bit-sliced walk (the sign plane rides along).
+int build_signed_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
+                      uint32_t* perm_out, uint32_t* signs_out, cudaStream_t st) {
+  int rc = check_gates(gates, n, M);
+  if (rc) return rc;
+  if ((rc = check_range(M, start, count))) return rc;
+  if (start % 32) return QSIM_EINVAL;
+  if (!perm_out || !signs_out || !aligned16(perm_out) || (reinterpret_cast<uintptr_t>(signs_out) & 3u))
+    return QSIM_EINVAL;
+  if (overlap(perm_out, count * 4, signs_out, (count + 31) / 32 * 4)) return QSIM_EALIAS;
+  return launch_walk<0, uint2>(gates, n, M, start, count, perm_out, nullptr, nullptr,
+                               QSIM_WALK_BITSLICED, st, signs_out);
+}
+
+int apply_signed_impl(const uint32_t* perm, const uint32_t* signs, uint64_t count, int32_t M,
+                      int32_t dtype, const void* k1, void* k2, cudaStream_t st) {
+  if (M < 1 || M > 32) return QSIM_ERANGE;
+  if (count > (1ull << M)) return QSIM_ERANGE;
+  const int e = elem_bytes(dtype);
+  if (e == 0) return QSIM_EINVAL;
+  if (!perm || !signs || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2) ||
+      (reinterpret_cast<uintptr_t>(signs) & 3u))
+    return QSIM_EINVAL;
+  const uint64_t N = 1ull << M;
+  if (overlap(k1, N * e, k2, count * e) || overlap(perm, count * 4, k2, count * e) ||
+      overlap(signs, (count + 31) / 32 * 4, k2, count * e))
+    return QSIM_EALIAS;
+  if (count == 0) return QSIM_OK;
+  uint64_t blocks = (count / 4 + 255) / 256;
+  const uint64_t cap = (uint64_t)sm_count() * 8 * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  if (dtype == QSIM_C64)
+    qsim::k_apply_signed<uint2><<<(unsigned)blocks, 256, 0, st>>>(
+        perm, signs, count, static_cast<const uint2*>(k1), static_cast<uint2*>(k2));
+  else
+    qsim::k_apply_signed<uint4><<<(unsigned)blocks, 256, 0, st>>>(
+        perm, signs, count, static_cast<const uint4*>(k1), static_cast<uint4*>(k2));
+  QSIM_CHECK_LAUNCH("k_apply_signed");
+  return QSIM_OK;
 }
 
 int fused_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, uint64_t start,
@@ -316,9 +383,24 @@ uint64_t plan_mix(uint64_t z) {
 }
 
 // inverse map perm^-1(j) = f_n(...f_1(j)): Step 1 first
-uint32_t plan_inverse_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32_t x) {
-  for (int k = 0; k < n; ++k)
-    if ((~x & cm[k]) == 0u) x ^= tm[k];
+// A step's action on addresses (host plans): toggle tm when the controls cm
+// are set; a SWAP (swap = true) toggles both bits of tm when they differ;
+// phase steps leave addresses unchanged (tm = 0).
+struct PlanGate {
+  uint32_t cm, tm;
+  bool swap;
+};
+
+uint32_t plan_step(const PlanGate& g, uint32_t x) {
+  if (g.swap) {
+    const uint32_t b = x & g.tm;
+    return (b != 0u && b != g.tm) ? x ^ g.tm : x;
+  }
+  return (~x & g.cm) == 0u ? x ^ g.tm : x;
+}
+
+uint32_t plan_inverse_walk(const PlanGate* g, int n, uint32_t x) {
+  for (int k = 0; k < n; ++k) x = plan_step(g[k], x);
   return x;
 }
 
@@ -377,9 +459,8 @@ int spread_q90_log2(std::vector<uint64_t>& spreads) {
 }
 
 // perm(x) = f_1(...f_n(x)): Step n first (readings R1, R2)
-uint32_t plan_forward_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32_t x) {
-  for (int k = n - 1; k >= 0; --k)
-    if ((~x & cm[k]) == 0u) x ^= tm[k];
+uint32_t plan_forward_walk(const PlanGate* g, int n, uint32_t x) {
+  for (int k = n - 1; k >= 0; --k) x = plan_step(g[k], x);
   return x;
 }
 
@@ -390,8 +471,7 @@ uint32_t plan_forward_walk(const uint32_t* cm, const uint32_t* tm, int n, uint32
 // start from the kept bits, repeatedly add the pattern with the best gain in
 // contained pairs per added bit until T bits.  Returns the bit set V; the
 // fraction of sampled pairs inside a V-block goes to plan->tile_contained.
-uint32_t plan_sector_cover(const uint32_t* cm, const uint32_t* tm, int n, int M, int dtype, int T,
-                           qsim_plan* plan) {
+uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan) {
   const int e = elem_bytes(dtype), eps = 32 / e, keep = plan_keep_bits(dtype);
   const int samples = 2048;
   std::vector<uint32_t> diffs;
@@ -399,8 +479,8 @@ uint32_t plan_sector_cover(const uint32_t* cm, const uint32_t* tm, int n, int M,
   const uint64_t N = 1ull << M;
   for (int k = 0; k < samples; ++k) {
     const uint32_t i = (uint32_t)(plan_mix(0x7e57ull + k) % N);
-    const uint32_t src = plan_forward_walk(cm, tm, n, i);
-    for (int r = 1; r < eps; ++r) diffs.push_back(plan_inverse_walk(cm, tm, n, src ^ (uint32_t)r) ^ i);
+    const uint32_t src = plan_forward_walk(pg, n, i);
+    for (int r = 1; r < eps; ++r) diffs.push_back(plan_inverse_walk(pg, n, src ^ (uint32_t)r) ^ i);
   }
   std::sort(diffs.begin(), diffs.end());
   std::vector<std::pair<uint32_t, uint32_t>> pats;  // (pattern, count)
@@ -477,11 +557,13 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
     plan->flags = 1;
     return QSIM_OK;
   }
-  std::unique_ptr<uint32_t[]> cm(new uint32_t[n > 0 ? n : 1]), tm(new uint32_t[n > 0 ? n : 1]);
+  std::unique_ptr<PlanGate[]> pg(new PlanGate[n > 0 ? n : 1]);
   for (int k = 0; k < n; ++k) {
     const qsim_gate& g = gates[k];
-    cm[k] = (g.kind >= 1 ? 1u << g.c0 : 0u) | (g.kind == 2 ? 1u << g.c1 : 0u);
-    tm[k] = 1u << g.target;
+    const int nc = g.kind == 6 ? 0 : g.kind % 3;
+    pg[k].swap = g.kind == 6;
+    pg[k].cm = (nc >= 1 ? 1u << g.c0 : 0u) | (nc == 2 ? 1u << g.c1 : 0u);
+    pg[k].tm = g.kind == 6 ? (1u << g.target) | (1u << g.c0) : g.kind >= 3 ? 0u : 1u << g.target;
   }
   const int line_bits = dtype == QSIM_C64 ? 4 : 3;  // one 128-byte line of k1
   const int lines = 2048;
@@ -494,7 +576,7 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
     uint32_t* r = &readers[(size_t)s << line_bits];
     uint32_t diff = 0, lo = 0xffffffffu, hi = 0;
     for (uint32_t d = 0; d < (1u << line_bits); ++d) {
-      r[d] = plan_inverse_walk(cm.get(), tm.get(), n, base | d);
+      r[d] = plan_inverse_walk(pg.get(), n, base | d);
       diff |= r[d] ^ r[0];
       lo = std::min(lo, r[d]);
       hi = std::max(hi, r[d]);
@@ -510,7 +592,7 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   int cover = plan_cover_bits;
   if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) cover = std::atoi(cb);  // tuning
   const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(cover, 20)));
-  const uint32_t V = plan_sector_cover(cm.get(), tm.get(), n, M, dtype, T, plan);
+  const uint32_t V = plan_sector_cover(pg.get(), n, M, dtype, T, plan);
   int order[32], m = 0, k = 0;
   for (int b = 0; b < M; ++b) {
     if ((V >> b) & 1u)
@@ -691,6 +773,10 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
   if (rc) return rc;
   const int M = plan->M;
   if ((rc = check_gates(gates, n, M))) return rc;
+  if (has_phase(gates, n)) {  // the stored map would drop the -1 rows
+    std::snprintf(g_err, sizeof g_err, "phase gates: use qsim_build_map_signed");
+    return QSIM_EINVAL;
+  }
   const int e = elem_bytes(plan->dtype);
   if (!perm || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2))
     return QSIM_EINVAL;
@@ -808,6 +894,20 @@ int qsim_run_fused_planned(const qsim_plan* plan, const qsim_gate* gates, int32_
                             static_cast<cudaStream_t>(stream));
 }
 
+int qsim_build_map_signed(const qsim_gate* gates, int32_t n_gates, int32_t M, uint64_t start,
+                          uint64_t count, uint32_t* perm, uint32_t* signs, void* stream) {
+  g_launches = 0;
+  if (M < 1 || M > 32) return QSIM_ERANGE;
+  return build_signed_impl(gates, n_gates, M, start, count, perm, signs,
+                           static_cast<cudaStream_t>(stream));
+}
+
+int qsim_apply_map_signed(const uint32_t* perm, const uint32_t* signs, uint64_t count, int32_t M,
+                          int32_t dtype, const void* k1, void* k2, void* stream) {
+  g_launches = 0;
+  return apply_signed_impl(perm, signs, count, M, dtype, k1, k2, static_cast<cudaStream_t>(stream));
+}
+
 int qsim_map_gather_planned(const qsim_plan* plan, const qsim_gate* gates, int32_t n_gates,
                             uint32_t* perm, const void* k1, void* k2, void* workspace,
                             void* stream) {
@@ -826,6 +926,7 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
   if (e == 0 || (mode != 0 && mode != 1)) return QSIM_EINVAL;
   if (!k1_host || !k2_host || !k1_dev || !k2_dev) return QSIM_EINVAL;
   if (mode == 0 && !perm_dev) return QSIM_EINVAL;
+  if (mode == 0 && has_phase(gates, n_gates)) return QSIM_EINVAL;  // map + gather stores the map
   const uint64_t N = 1ull << M, bytes = N * e;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // validate the compute step before enqueuing anything
@@ -924,6 +1025,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 2; }
+int32_t qsim_abi_version(void) { return 3; }
 
 }  // extern "C"

@@ -146,38 +146,89 @@ __device__ __forceinline__ void stcs(uint2* p, uint2 v) {
 __device__ __forceinline__ void stcs(uint4* p, uint4 v) {
   asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory"); }
+// row value -1 (phase gates): IEEE negation of both parts on the sign bits
+__device__ __forceinline__ uint2 negate_if(uint2 v, u32 neg) {
+  const u32 m = neg << 31; v.x ^= m; v.y ^= m; return v; }
+__device__ __forceinline__ uint4 negate_if(uint4 v, u32 neg) {
+  const u32 m = neg << 31; v.y ^= m; v.w ^= m; return v; }
+__device__ __forceinline__ float2 negate_if(float2 v, u32 neg) {
+  const u32 m = neg << 31;
+  return make_float2(__uint_as_float(__float_as_uint(v.x) ^ m), __uint_as_float(__float_as_uint(v.y) ^ m)); }
+__device__ __forceinline__ double2 negate_if(double2 v, u32 neg) {
+  const u64 m = (u64)neg << 63;
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ m)); }
 #define QSIM_TS(J, MASK, a)                                                     \
   _Pragma("unroll") for (int k = 0; k < 32; ++k)                                \
     if ((k & J) == 0) { u32 t = ((a[k] >> J) ^ a[k + J]) & MASK;                \
                         a[k + J] ^= t; a[k] ^= t << J; }
 )";
 
-// Straight-line walk for one tile: planes p0..p31 in registers.
+// Straight-line walk for one tile: planes p0..p31 in registers, gates last
+// -> first (readings R1, R2).  A NOT costs nothing (the plane's polarity is
+// tracked and folded into the ops that read it); a SWAP costs nothing (the
+// two logical bits exchange variables); a phase step (Z / CZ / CCZ, R17) adds
+// the AND of its planes to `sg` (bit l = row value -1), which the caller
+// declares.  An epilogue moves logical bit b back into p<b>.
 std::string walk_code(const uint32_t* w, int n, int M) {
   std::string s;
-  bool inv[33] = {false};
-  char buf[160];
+  int phys[32];
+  bool inv[32];
+  for (int b = 0; b < 32; ++b) {
+    phys[b] = b;
+    inv[b] = false;
+  }
+  char buf[200];
   auto ref = [&](uint32_t b) -> std::string {
-    return std::string(inv[b] ? "~p" : "p") + std::to_string(b);
+    return std::string(inv[b] ? "~p" : "p") + std::to_string(phys[b]);
   };
   for (int k = n - 1; k >= 0; --k) {
     const uint32_t kind = w[k] & 0xffu, t = (w[k] >> 8) & 0xffu, c0 = (w[k] >> 16) & 0xffu,
                    c1 = w[k] >> 24;
-    if (kind == 0) {
-      inv[t] = !inv[t];
-      continue;
+    buf[0] = 0;
+    switch (kind) {
+      case 0: inv[t] = !inv[t]; break;
+      case 1: std::snprintf(buf, sizeof buf, "  p%d ^= %s;\n", phys[t], ref(c0).c_str()); break;
+      case 2:
+        std::snprintf(buf, sizeof buf, "  p%d ^= %s & %s;\n", phys[t], ref(c0).c_str(),
+                      ref(c1).c_str());
+        break;
+      case 3: std::snprintf(buf, sizeof buf, "  sg ^= %s;\n", ref(t).c_str()); break;
+      case 4:
+        std::snprintf(buf, sizeof buf, "  sg ^= %s & %s;\n", ref(t).c_str(), ref(c0).c_str());
+        break;
+      case 5:
+        std::snprintf(buf, sizeof buf, "  sg ^= %s & %s & %s;\n", ref(t).c_str(), ref(c0).c_str(),
+                      ref(c1).c_str());
+        break;
+      case 6:
+        std::swap(phys[t], phys[c0]);
+        std::swap(inv[t], inv[c0]);
+        break;
+      default: break;
     }
-    if (kind == 1)
-      std::snprintf(buf, sizeof buf, "  p%u ^= %s;\n", t, ref(c0).c_str());
-    else
-      std::snprintf(buf, sizeof buf, "  p%u ^= %s & %s;\n", t, ref(c0).c_str(), ref(c1).c_str());
     s += buf;
   }
-  for (int b = 0; b < 32; ++b)
-    if (inv[b]) {
-      std::snprintf(buf, sizeof buf, "  p%d = ~p%d;\n", b, b);
+  bool moved = false;
+  for (int b = 0; b < 32; ++b) moved = moved || phys[b] != b;
+  if (moved) {  // parallel copy back to p<b>
+    s += "  {\n";
+    for (int b = 0; b < 32; ++b) {
+      std::snprintf(buf, sizeof buf, "    const u32 q%d = %s;\n", b, ref(b).c_str());
       s += buf;
     }
+    for (int b = 0; b < 32; ++b) {
+      std::snprintf(buf, sizeof buf, "    p%d = q%d;\n", b, b);
+      s += buf;
+    }
+    s += "  }\n";
+  } else {
+    for (int b = 0; b < 32; ++b)
+      if (inv[b]) {
+        std::snprintf(buf, sizeof buf, "  p%d = ~p%d;\n", b, b);
+        s += buf;
+      }
+  }
   (void)M;
   return s;
 }
@@ -204,6 +255,7 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
       std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
     s += buf;
   }
+  s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   s += "    u32 a[32] = {";
   for (int b = 0; b < 32; ++b) {
@@ -231,10 +283,10 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // Sigma-ordered fused walk + gather (qsim_kernels.cuh k_fused_sigma, with the
 // circuit and the traversal order compiled in).  If perm_out is non-null the
 // kernel also stores the map (one-pass materialised map + gather).
-// QSIM_JIT_PIPE=0 disables the software pipeline of the fused kernel (A/B)
+// QSIM_JIT_PIPE=1 enables the software pipeline of the fused kernel (A/B)
 bool pipelined() {
   const char* v = std::getenv("QSIM_JIT_PIPE");
-  return !(v && v[0] == '0');
+  return v && v[0] == '1';  // default off: measured neutral (map+gather) to 4 % slower (fused)
 }
 
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem) {
@@ -277,7 +329,7 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   // software pipeline: a warp tile's 32 gathers stay in flight while the
   // warp walks its next tile; they are stored after that walk
   QSIM_T v[32];
-  u32 pob = 0u;
+  u32 pob = 0u, psg = 0u;
   bool pend = false;
 #endif
   for (;;) {
@@ -309,6 +361,7 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
       std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
     s += buf;
   }
+  s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   s += "      u32 a[32] = {";
   for (int b = 0; b < 32; ++b) {
@@ -333,16 +386,19 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
       }
 #if QSIM_PIPE
       if (pend) {
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) stcs(k2 + (pob | lt[l] | lo), v[l]);
+        _Pragma("unroll") for (int l = 0; l < 32; ++l)
+          stcs(k2 + (pob | lt[l] | lo), negate_if(v[l], (psg >> l) & 1u));
       }
       _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
       pob = ob;
+      psg = sg;
       pend = true;
 #else
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob | lt[h + l] | lo), v[l]);
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
+          stcs(k2 + (ob | lt[h + l] | lo), negate_if(v[l], (sg >> (h + l)) & 1u));
       }
 #endif
     }
@@ -350,7 +406,8 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
 #if QSIM_PIPE
   if (pend) {
     const u32 lo = tab[0][lane];
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) stcs(k2 + (pob | lt_g[l] | lo), v[l]);
+    _Pragma("unroll") for (int l = 0; l < 32; ++l)
+      stcs(k2 + (pob | lt_g[l] | lo), negate_if(v[l], (psg >> l) & 1u));
   }
 #endif
 }
@@ -414,6 +471,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
       std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
     s += buf;
   }
+  s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   s += "    u32 a[32] = {";
   for (int b = 0; b < 32; ++b) {
@@ -431,7 +489,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
       r = cmul(r, T[1][(sv >> 8) & 255]);
       r = cmul(r, T[0][sv & 255]);
       const u64 addr = base + 32u * l + lane;
-      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), r);
+      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), negate_if(r, (sg >> l) & 1u));
     }
   }
 }

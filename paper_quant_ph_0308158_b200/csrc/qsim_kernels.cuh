@@ -26,11 +26,19 @@ namespace qsim {
 
 constexpr int kMaxGates = 4096;
 constexpr uint32_t kOnesPlane = 32;  // bit-sliced: an all-ones plane (absent control)
+constexpr uint32_t kSignPlane = 33;  // bit-sliced: the row-value (sign) plane
+
+// Gate kinds (include/qsim.h): 0 NOT, 1 CNOT, 2 CCNOT toggle the target when
+// the controls are 1; 3 Z, 4 CZ, 5 CCZ put -1 on the rows whose
+// target and controls are 1 (phased permutations, reading R17); 6 SWAP
+// exchanges bits target and c0.
+// Bit-sliced ops: 0 toggle, 1 swap, 2 phase.
+constexpr uint32_t kOpToggle = 0, kOpSwap = 1, kOpPhase = 2;
 
 // Gate list in the launch's kernel-parameter bank (constant bank 0), one
 // 32-bit word per gate.  Per-lane format: kind | target << 8 | c0 << 16 |
 // c1 << 24 (unused controls 0).  Bit-sliced format: target | c0 << 8 |
-// c1 << 16 with absent controls = kOnesPlane.
+// c1 << 16 | op << 24 with absent controls = kOnesPlane.
 template <int CAP>
 struct GateList {
   uint32_t n;
@@ -75,6 +83,31 @@ __device__ __forceinline__ void st_stream(uint4* p, uint4 v) {
 }
 __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v) { __stcs(p, v); }
 
+// Row value -1 of a phased permutation: IEEE negation of both parts, done on
+// the sign bits (bit-exact, NaN payloads kept; the oracle's -x).
+__device__ __forceinline__ uint2 negate_if(uint2 v, uint32_t neg) {
+  const uint32_t m = neg << 31;
+  v.x ^= m;
+  v.y ^= m;
+  return v;
+}
+__device__ __forceinline__ uint4 negate_if(uint4 v, uint32_t neg) {  // two doubles
+  const uint32_t m = neg << 31;
+  v.y ^= m;
+  v.w ^= m;
+  return v;
+}
+__device__ __forceinline__ float2 negate_if(float2 v, uint32_t neg) {
+  const uint32_t m = neg << 31;
+  return make_float2(__uint_as_float(__float_as_uint(v.x) ^ m),
+                     __uint_as_float(__float_as_uint(v.y) ^ m));
+}
+__device__ __forceinline__ double2 negate_if(double2 v, uint32_t neg) {
+  const unsigned long long m = (unsigned long long)neg << 63;
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ m));
+}
+
 // ------------------------------------------------------------------ per-lane
 // One address per lane: walk the gates last -> first, x ^= tmask when all
 // control bits of x are set.  APT independent walks interleave to fill the
@@ -87,15 +120,30 @@ k_walk_per_lane(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * APT;
   for (uint64_t r0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * APT; r0 < count;
        r0 += stride) {
-    uint32_t x[APT];
+    uint32_t x[APT], sg[APT];
 #pragma unroll
-    for (int a = 0; a < APT; ++a) x[a] = (uint32_t)(start + r0 + a);
+    for (int a = 0; a < APT; ++a) {
+      x[a] = (uint32_t)(start + r0 + a);
+      sg[a] = 0u;
+    }
     for (int k = (int)g.n - 1; k >= 0; --k) {
       const uint32_t w = g.w[k];
-      const uint32_t kind = gate_kind(w);
-      const uint32_t cmask = (kind >= 1 ? (1u << gate_c0(w)) : 0u) |
-                             (kind == 2 ? (1u << gate_c1(w)) : 0u);
-      const uint32_t tmask = 1u << gate_t(w);
+      const uint32_t kind = gate_kind(w), t = gate_t(w);
+      const uint32_t tmask = 1u << t;
+      if (kind == 6) {  // SWAP: exchange bits t and c0 (toggle both when they differ)
+        const uint32_t c = gate_c0(w), both = tmask | (1u << c);
+#pragma unroll
+        for (int a = 0; a < APT; ++a) x[a] ^= (((x[a] >> t) ^ (x[a] >> c)) & 1u) ? both : 0u;
+        continue;
+      }
+      const uint32_t nc = kind % 3;  // controls: NOT/Z 0, CNOT/CZ 1, CCNOT/CCZ 2
+      const uint32_t cmask = (nc >= 1 ? (1u << gate_c0(w)) : 0u) | (nc == 2 ? (1u << gate_c1(w)) : 0u);
+      if (kind >= 3) {  // phase: -1 on the rows with target and controls all 1
+        const uint32_t pm = cmask | tmask;
+#pragma unroll
+        for (int a = 0; a < APT; ++a) sg[a] ^= (~x[a] & pm) == 0u ? 1u : 0u;
+        continue;
+      }
 #pragma unroll
       for (int a = 0; a < APT; ++a)
         if ((~x[a] & cmask) == 0u) x[a] ^= tmask;
@@ -105,7 +153,7 @@ k_walk_per_lane(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_
       const uint64_t r = r0 + a;
       if (r < count) {
         if (MODE == 0) perm_out[r] = x[a];
-        else k2_out[r] = ld_gather(k1 + x[a]);
+        else k2_out[r] = negate_if(ld_gather(k1 + x[a]), sg[a]);
       }
     }
   }
@@ -180,7 +228,7 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
 }
 
 struct BsShared {
-  uint32_t S[33][kBsThreads];  // S[plane][thread] (private columns); plane 32 = ones
+  uint32_t S[34][kBsThreads];  // S[plane][thread] (private columns); 32 = ones, 33 = sign
   uint32_t tab[4][256];        // sigma deposit tables
   uint32_t patw[32];           // l-bit pattern of each output plane (0 if none)
   uint32_t ltab[32];           // sigma(l << 5)
@@ -208,7 +256,7 @@ __device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaPara
     const uint32_t w = g.w[g.n - 1 - k];
     const uint32_t row = kBsThreads * 4u;
     sh.gate[k] = make_uint2((w & 0xffu) * row | (((w >> 8) & 0xffu) * row) << 16,
-                            ((w >> 16) & 0xffu) * row);
+                            ((w >> 16) & 0xffu) * row | (w >> 24) << 16);
   }
   __syncthreads();
   if (threadIdx.x < 5 && 5 + threadIdx.x < sp.nbits) sh.patw[sp.sigma[5 + threadIdx.x]] = pat[threadIdx.x];
@@ -222,9 +270,10 @@ __device__ __forceinline__ void bs_setup(const GateList<CAP>& g, const SigmaPara
   __syncthreads();
 }
 
-// Walk one warp tile; on return a[l] = perm(out_base | ltab[l] | sigma(lane)).
+// Walk one warp tile; on return a[l] = perm(out_base | ltab[l] | sigma(lane))
+// and bit l of sgn is 1 when that row's value is -1 (phase gates).
 __device__ __forceinline__ void bs_walk_tile(uint32_t n, BsShared& sh, uint32_t out_base,
-                                             uint32_t (&a)[32]) {
+                                             uint32_t (&a)[32], uint32_t& sgn) {
   const uint32_t tid = threadIdx.x, lane = tid & 31u;
 #pragma unroll
   for (int b = 0; b < 32; ++b) {
@@ -233,28 +282,43 @@ __device__ __forceinline__ void bs_walk_tile(uint32_t n, BsShared& sh, uint32_t 
     const uint32_t basew = ((out_base >> b) & 1u) ? 0xffffffffu : 0u;
     sh.S[b][tid] = lanew | sh.patw[b] | basew;
   }
-  // walk last -> first (R1, R2): plane[t] ^= plane[c0] & plane[c1]
+  sh.S[kSignPlane][tid] = 0u;
+  // walk last -> first (R1, R2): plane[t] ^= plane[c0] & plane[c1]; a SWAP
+  // exchanges two planes; a phase gate adds plane[t] & plane[c0] & plane[c1]
+  // to the sign plane (the op is warp-uniform)
   char* col = reinterpret_cast<char*>(&sh.S[0][tid]);
 #pragma unroll 4
   for (uint32_t k = 0; k < n; ++k) {
     const uint2 gk = sh.gate[k];
     uint32_t* pt = reinterpret_cast<uint32_t*>(col + (gk.x & 0xffffu));
-    const uint32_t x0 = *reinterpret_cast<const uint32_t*>(col + (gk.x >> 16));
-    const uint32_t x1 = *reinterpret_cast<const uint32_t*>(col + gk.y);
-    *pt ^= x0 & x1;
+    uint32_t* p0 = reinterpret_cast<uint32_t*>(col + (gk.x >> 16));
+    const uint32_t x1 = *reinterpret_cast<const uint32_t*>(col + (gk.y & 0xffffu));
+    const uint32_t op = gk.y >> 16;
+    if (op == kOpToggle) {
+      *pt ^= *p0 & x1;
+    } else if (op == kOpSwap) {
+      const uint32_t d = *pt ^ *p0;
+      *pt ^= d;
+      *p0 ^= d;
+    } else {
+      sh.S[kSignPlane][tid] ^= *pt & *p0 & x1;
+    }
   }
 #pragma unroll
   for (int b = 0; b < 32; ++b) a[b] = sh.S[b][tid];
+  sgn = sh.S[kSignPlane][tid];
   transpose32(a);
 }
 
 // MODE 0: perm_out[out - start] = perm(out) for out in [start, end), natural
-// order (identity sigma), tiles [tile_begin, tile_end) grid-stride.
+// order (identity sigma), tiles [tile_begin, tile_end) grid-stride.  With
+// signs_out (start % 32 == 0): bit r % 32 of signs_out[r / 32] = 1 when row
+// start + r has value -1 (words of the range fully written, 0 past end).
 template <int CAP>
 __global__ void __launch_bounds__(kBsThreads, 2)
 k_build_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant__ SigmaParams sp,
                   uint64_t start, uint64_t end, uint64_t tile_begin, uint64_t tile_end,
-                  uint32_t* __restrict__ perm_out) {
+                  uint32_t* __restrict__ perm_out, uint32_t* __restrict__ signs_out) {
   extern __shared__ __align__(16) uint8_t bs_smem[];
   BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
   bs_setup(g, sp, sh);
@@ -262,12 +326,23 @@ k_build_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant
   for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
        tile += (uint64_t)gridDim.x * kBsWarps) {
     const uint64_t base = tile << 10;
-    uint32_t a[32];
-    bs_walk_tile(g.n, sh, (uint32_t)base, a);
+    uint32_t a[32], sgn;
+    bs_walk_tile(g.n, sh, (uint32_t)base, a, sgn);
 #pragma unroll
     for (int l = 0; l < 32; ++l) {
       const uint64_t addr = base + 32u * l + lane;
       if (addr >= start && addr < end) st_stream_u32(perm_out + (addr - start), a[l]);
+    }
+    if (signs_out) {  // row base + 32 l + lane: word l of the tile = ballot over lanes
+      uint32_t mine = 0u;
+#pragma unroll
+      for (int l = 0; l < 32; ++l) {
+        const uint64_t addr = base + 32u * l + lane;
+        const uint32_t b = __ballot_sync(0xffffffffu, addr < end && ((sgn >> l) & 1u));
+        if ((uint32_t)l == lane) mine = b;
+      }
+      const uint64_t row = base + 32u * lane;  // first output of word `lane`
+      if (row >= start && row < end) signs_out[(row - start) >> 5] = mine;
     }
   }
 }
@@ -285,8 +360,8 @@ k_fused_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant
   for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
        tile += (uint64_t)gridDim.x * kBsWarps) {
     const uint64_t base = tile << 10;
-    uint32_t a[32];
-    bs_walk_tile(g.n, sh, (uint32_t)base, a);
+    uint32_t a[32], sgn;
+    bs_walk_tile(g.n, sh, (uint32_t)base, a, sgn);
     constexpr int B = 16;  // gathers in flight per thread
 #pragma unroll
     for (int h = 0; h < 32; h += B) {
@@ -299,7 +374,8 @@ k_fused_bitsliced(const __grid_constant__ GateList<CAP> g, const __grid_constant
 #pragma unroll
       for (int l = 0; l < B; ++l) {
         const uint64_t addr = base + 32u * (h + l) + lane;
-        if (addr >= start && addr < end) st_stream(k2_out + (addr - start), v[l]);
+        if (addr >= start && addr < end)
+          st_stream(k2_out + (addr - start), negate_if(v[l], (sgn >> (h + l)) & 1u));
       }
     }
   }
@@ -323,8 +399,8 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
       const uint64_t c = (ch << sp.chunk_log2) + ((uint64_t)tt << 10);
       const uint32_t out_base = sigma_apply(sh.tab, c);
       const uint32_t lo = sh.tab[0][lane];
-      uint32_t a[32];
-      bs_walk_tile(g.n, sh, out_base, a);
+      uint32_t a[32], sgn;
+      bs_walk_tile(g.n, sh, out_base, a, sgn);
       constexpr int B = sizeof(T) == 8 ? 32 : 16;  // gathers in flight per thread
 #pragma unroll
       for (int h = 0; h < 32; h += B) {
@@ -332,7 +408,8 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
 #pragma unroll
         for (int l = 0; l < B; ++l) v[l] = ld_gather(k1 + a[h + l]);
 #pragma unroll
-        for (int l = 0; l < B; ++l) st_stream(k2 + (out_base | sh.ltab[h + l] | lo), v[l]);
+        for (int l = 0; l < B; ++l)
+          st_stream(k2 + (out_base | sh.ltab[h + l] | lo), negate_if(v[l], (sgn >> (h + l)) & 1u));
       }
     }
   }
@@ -409,12 +486,13 @@ k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
   for (uint64_t tile = tile_begin + (uint64_t)blockIdx.x * kBsWarps + warp; tile < tile_end;
        tile += (uint64_t)gridDim.x * kBsWarps) {
     const uint64_t base = tile << 10;
-    uint32_t a[32];
-    bs_walk_tile(g.n, sh, (uint32_t)base, a);
+    uint32_t a[32], sgn;
+    bs_walk_tile(g.n, sh, (uint32_t)base, a, sgn);
 #pragma unroll
     for (int l = 0; l < 32; ++l) {
       const uint64_t addr = base + 32u * l + lane;
-      if (addr >= start && addr < end) k2_out[addr - start] = kron_element<C>(T, a[l]);
+      if (addr >= start && addr < end)
+        k2_out[addr - start] = negate_if(kron_element<C>(T, a[l]), (sgn >> l) & 1u);
     }
   }
 }
@@ -451,6 +529,32 @@ k_apply(const uint32_t* __restrict__ perm, uint64_t count, const T* __restrict__
   if (blockIdx.x == 0 && threadIdx.x < (count & 3u)) {
     const uint64_t r = (ngroups << 2) + threadIdx.x;
     k2[r] = ld_gather(k1 + perm[r]);
+  }
+}
+
+// Phased form: k2[r] = sign[r] k1[perm[r]], bit r % 32 of signs[r / 32] = 1
+// for -1 (qsim_apply_map_signed).  One thread per 4 entries.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_apply_signed(const uint32_t* __restrict__ perm, const uint32_t* __restrict__ signs,
+               uint64_t count, const T* __restrict__ k1, T* __restrict__ k2) {
+  const uint64_t ngroups = count >> 2;
+  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups;
+       gi += nthreads) {
+    const uint4 p = ld_stream_u4(perm + 4 * gi);
+    const uint32_t sw = signs[gi >> 3] >> (4u * (uint32_t)(gi & 7u));
+    const T v0 = ld_gather(k1 + p.x), v1 = ld_gather(k1 + p.y);
+    const T v2 = ld_gather(k1 + p.z), v3 = ld_gather(k1 + p.w);
+    T* o = k2 + 4 * gi;
+    st_stream(o + 0, negate_if(v0, sw & 1u));
+    st_stream(o + 1, negate_if(v1, (sw >> 1) & 1u));
+    st_stream(o + 2, negate_if(v2, (sw >> 2) & 1u));
+    st_stream(o + 3, negate_if(v3, (sw >> 3) & 1u));
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (count & 3u)) {
+    const uint64_t r = (ngroups << 2) + threadIdx.x;
+    k2[r] = negate_if(ld_gather(k1 + perm[r]), (signs[r >> 5] >> (r & 31u)) & 1u);
   }
 }
 

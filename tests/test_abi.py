@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(q):
     lib = ctypes.CDLL(q.LIB_PATH)
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.qsim_abi_version() == 2
+    assert lib.qsim_abi_version() == 3
 
 
 def test_strerror_covers_every_status(q):
@@ -90,7 +90,11 @@ def test_validation_errors_without_gpu(q):
 
 
 @pytest.mark.parametrize("bad,code", [
-    ([3, 0, 255, 255], "EINVAL"),      # unknown kind
+    ([7, 0, 255, 255], "EINVAL"),      # unknown kind
+    ([6, 1, 1, 255], "EBIT"),          # SWAP of a bit with itself
+    ([6, 1, 5, 255], "EBIT"),          # SWAP partner >= M
+    ([4, 0, 0, 255], "EBIT"),          # CZ control == target
+    ([5, 0, 1, 1], "EBIT"),            # CCZ duplicate control
     ([0, 4, 255, 255], "EBIT"),        # target >= M
     ([1, 0, 0, 255], "EBIT"),          # control == target
     ([1, 0, 9, 255], "EBIT"),          # control >= M
@@ -244,3 +248,41 @@ def test_sector_cover_plan_matches_an_independent_sample(q):
             hits += int(np.count_nonzero((d & ~np.uint64(V)) == 0))
             tot += d.size
         assert abs(hits / tot - plan.tile_contained) < 0.05, (name, hits / tot, plan.tile_contained)
+
+
+def test_phase_gates_rejected_where_only_a_map_is_produced(q):
+    """A circuit with Z / CZ / CCZ has rows of value -1: the calls whose only
+    output is a uint32 map refuse it (EINVAL) before any launch; SWAP passes
+    validation; the signed build checks its alignment rule."""
+    L = q.lib()
+    ph = np.ascontiguousarray(np.array([[1, 0, 1, 255], [4, 2, 0, 255]], dtype=np.uint8))
+    sw = np.ascontiguousarray(np.array([[6, 0, 3, 255]], dtype=np.uint8))
+    assert L.qsim_build_map(ph.ctypes.data, 2, 4, FAKE, None) == q.EINVAL
+    assert L.qsim_build_map_ex(ph.ctypes.data, 2, 4, 0, 16, FAKE, q.WALK_JIT, None) == q.EINVAL
+    plan = q.plan_create(ph, 4, "c64")                  # plans accept any valid circuit
+    assert L.qsim_map_gather_planned(ctypes.byref(plan), ph.ctypes.data, 2, FAKE, FAKE * 4,
+                                     FAKE * 64, None, None) == q.EINVAL
+    assert L.qsim_run_host(ph.ctypes.data, 2, 4, q.C64, 0, FAKE, FAKE, FAKE, FAKE * 4, FAKE * 8,
+                           None, None) == q.EINVAL
+    assert L.qsim_build_map_signed(ph.ctypes.data, 2, 6, 16, 16, FAKE, FAKE * 4, None) == q.EINVAL
+    assert L.qsim_build_map_signed(ph.ctypes.data, 2, 6, 0, 16, FAKE, None, None) == q.EINVAL
+    assert L.qsim_build_map_signed(ph.ctypes.data, 2, 4, 0, 17, FAKE, FAKE * 4, None) == q.ERANGE
+    assert L.qsim_apply_map_signed(FAKE, None, 16, 4, q.C64, FAKE * 4, FAKE * 8, None) == q.EINVAL
+    # SWAP is a plain permutation: it validates (the EALIAS proves validation passed)
+    rc = L.qsim_run_fused(sw.ctypes.data, 1, 4, q.C64, FAKE, FAKE, None)
+    assert rc == q.EALIAS
+
+
+def test_jit_sources_with_phase_and_swap_compile_without_gpu(q):
+    """NVRTC accepts the generated kernels for the extended gate set (swap =
+    variable renaming, phase = sign register) -- fused (planned) and kron."""
+    L = q.lib()
+    g = np.ascontiguousarray(wl.random_gates_ext(64, 20, 3))
+    plan = q.plan_create(g, 20, "c64")
+    rc = L.qsim_jit_check_compile_planned(ctypes.byref(plan), g.ctypes.data, len(g))
+    if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+        pytest.skip("NVRTC not available here")
+    assert rc == q.OK, L.qsim_last_error().decode()
+    for dt in (q.C64, q.C128):
+        assert L.qsim_jit_check_compile_kron(g.ctypes.data, len(g), 20, dt) == q.OK, \
+            L.qsim_last_error().decode()
