@@ -243,10 +243,18 @@ int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_
  *   qubits  host, 4*M doubles: qubit j (1-based) at [4(j-1)]: re q_j(0),
  *           im q_j(0), re q_j(1), im q_j(1); rounded to the state precision
  *           (float for QSIM_C64) before use
+ *   M       1..63: the only call that accepts M > 32 -- k1 is never stored,
+ *           so only the output portion [start, start+count) needs memory
+ *           ("output in convenient continuous portions"; "a quantum
+ *           computer of 64 qubits ... impossible to store").  For
+ *           M > 32 addresses are 64-bit (64 bit planes in the NVRTC kernel)
  *   k2_out  device, count entries of dtype (written)
- *   walk    QSIM_WALK_AUTO / QSIM_WALK_BITSLICED / QSIM_WALK_JIT
+ *   walk    QSIM_WALK_AUTO / QSIM_WALK_BITSLICED / QSIM_WALK_JIT, or
+ *           QSIM_WALK_PER_LANE (one 64-bit address per lane; the fallback
+ *           for M > 32 without NVRTC, where BITSLICED means PER_LANE)
  * Arithmetic: the factors are grouped by bytes of s into 256-entry tables
- * of products (8 qubits, descending j), combined as ((T3 T2) T1) T0; every
+ * of products (8 qubits, descending j), combined from the top byte down,
+ * ((T3 T2) T1) T0 for M <= 32 (T7 ... T0 for M > 32); every
  * complex product is rounded as written (re = ar*br - ai*bi, im = ar*bi +
  * ai*br), no FMA.  Not bit-exact against a sequential double product: the
  * normwise relative error is at most (M-1)*sqrt(5)*u (u = 2^-24 for

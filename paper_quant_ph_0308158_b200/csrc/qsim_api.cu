@@ -94,6 +94,16 @@ int check_gates(const qsim_gate* gates, int32_t n, int32_t M) {
   return rc;
 }
 
+// The input-on-the-fly path takes M up to 63 (64-bit addresses).
+int check_gates_kron(const qsim_gate* gates, int32_t n, int32_t M) {
+  if (M < 1 || M > 63) return QSIM_ERANGE;
+  if (n < 0 || n > QSIM_MAX_GATES) return QSIM_ECAP;
+  if (n > 0 && gates == nullptr) return QSIM_EINVAL;
+  int rc = QSIM_OK;
+  for (int32_t k = 0; rc == QSIM_OK && k < n; ++k) rc = check_gate(gates[k], M);
+  return rc;
+}
+
 // Pack for the kernels (gates already validated).  bitsliced: target |
 // c0 << 8 | c1 << 16 | op << 24 with absent controls = the all-ones plane
 // (op: toggle / swap / phase); per-lane (and NVRTC): kind | target << 8 |
@@ -313,15 +323,53 @@ int launch_kron(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qubits
   return launch_kron_cap<qsim::kMaxGates, C>(gates, n, M, qb, start, count, k2, st);
 }
 
+template <typename C>
+int launch_kron64(const qsim_gate* gates, int32_t n, const qsim::Qubits64& qb, uint64_t start,
+                  uint64_t count, C* k2, cudaStream_t st) {
+  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+  pack_gates(gates, n, false, *gl);
+  uint64_t blocks = (count + 255) / 256;
+  const uint64_t cap = (uint64_t)sm_count() * 8;
+  if (blocks > cap) blocks = cap;
+  qsim::k_fused_kron_perlane64<qsim::kMaxGates, C><<<(unsigned)blocks, 256, 0, st>>>(*gl, qb, start,
+                                                                                 count, k2);
+  QSIM_CHECK_LAUNCH("k_fused_kron_perlane64");
+  return QSIM_OK;
+}
+
 int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const double* qubits,
               uint64_t start, uint64_t count, void* k2, int32_t walk, cudaStream_t st) {
-  int rc = check_gates(gates, n, M);
+  // M up to 63 here (64-bit addresses): k1 is generated, never stored
+  int rc = check_gates_kron(gates, n, M);
   if (rc) return rc;
   if ((rc = check_range(M, start, count))) return rc;
   const int e = elem_bytes(dtype);
   if (e == 0 || !qubits || !k2 || !aligned16(k2)) return QSIM_EINVAL;
-  if (walk != QSIM_WALK_AUTO && walk != QSIM_WALK_BITSLICED && walk != QSIM_WALK_JIT)
-    return QSIM_EINVAL;
+  if (walk < QSIM_WALK_AUTO || walk > QSIM_WALK_JIT) return QSIM_EINVAL;
+  if (M > 32 || walk == QSIM_WALK_PER_LANE) {
+    qsim::Qubits64 q64;
+    std::memset(&q64, 0, sizeof q64);
+    q64.M = (uint32_t)M;
+    for (int j = 0; j < M; ++j)
+      for (int c = 0; c < 4; ++c) q64.v[j][c] = qubits[4 * j + c];
+    if (count == 0) return QSIM_OK;
+    if (M > 32 && (walk == QSIM_WALK_JIT || walk == QSIM_WALK_AUTO)) {
+      std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+      pack_gates(gates, n, false, *gl);
+      std::string err;
+      if (qsim::jit_kron(gl->w, n, M, &q64, sizeof q64, e, start, count, k2, sm_count(), st, err) ==
+          0) {
+        ++g_launches;
+        return QSIM_OK;
+      }
+      if (walk == QSIM_WALK_JIT) {
+        std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+        return QSIM_ECUDA;
+      }
+    }
+    if (dtype == QSIM_C64) return launch_kron64<float2>(gates, n, q64, start, count, static_cast<float2*>(k2), st);
+    return launch_kron64<double2>(gates, n, q64, start, count, static_cast<double2*>(k2), st);
+  }
   qsim::Qubits qb;
   std::memset(&qb, 0, sizeof qb);
   qb.M = (uint32_t)M;
@@ -998,7 +1046,7 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
 int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t M,
                                 int32_t dtype) {
   g_launches = 0;
-  int rc = check_gates(gates, n_gates, M);
+  int rc = check_gates_kron(gates, n_gates, M);
   if (rc) return rc;
   if (elem_bytes(dtype) == 0) return QSIM_EINVAL;
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);

@@ -172,9 +172,10 @@ __device__ __forceinline__ double2 negate_if(double2 v, u32 neg) {
 // declares.  An epilogue moves logical bit b back into p<b>.
 std::string walk_code(const uint32_t* w, int n, int M) {
   std::string s;
-  int phys[32];
-  bool inv[32];
-  for (int b = 0; b < 32; ++b) {
+  const int np = M > 32 ? 64 : 32;  // planes (64-bit addresses for M > 32)
+  int phys[64];
+  bool inv[64];
+  for (int b = 0; b < 64; ++b) {
     phys[b] = b;
     inv[b] = false;
   }
@@ -210,20 +211,20 @@ std::string walk_code(const uint32_t* w, int n, int M) {
     s += buf;
   }
   bool moved = false;
-  for (int b = 0; b < 32; ++b) moved = moved || phys[b] != b;
+  for (int b = 0; b < np; ++b) moved = moved || phys[b] != b;
   if (moved) {  // parallel copy back to p<b>
     s += "  {\n";
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < np; ++b) {
       std::snprintf(buf, sizeof buf, "    const u32 q%d = %s;\n", b, ref(b).c_str());
       s += buf;
     }
-    for (int b = 0; b < 32; ++b) {
+    for (int b = 0; b < np; ++b) {
       std::snprintf(buf, sizeof buf, "    p%d = q%d;\n", b, b);
       s += buf;
     }
     s += "  }\n";
   } else {
-    for (int b = 0; b < 32; ++b)
+    for (int b = 0; b < np; ++b)
       if (inv[b]) {
         std::snprintf(buf, sizeof buf, "  p%d = ~p%d;\n", b, b);
         s += buf;
@@ -497,6 +498,92 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   return s;
 }
 
+// Input on the fly for M > 32 (64-bit addresses, "continuous
+// portions"): 64 planes, two 32x32 transposes (low and high address
+// words), eight byte tables of qubit products combined from the top byte
+// down -- for M <= 32 the same products as kron_source.
+std::string kron64_source(const uint32_t* w, int n, int M, int elem) {
+  std::string s = kPrelude;
+  char buf[256];
+  const bool f32 = elem == 8;
+  s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_TOP %d\n", M, (M - 1) / 8);
+  s += buf;
+  s += f32 ? R"(
+__device__ __forceinline__ C cmul(C a, C b) {
+  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
+                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x))); }
+)" : R"(
+__device__ __forceinline__ C cmul(C a, C b) {
+  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
+                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))); }
+)";
+  s += R"(
+struct Qubits64 { double v[64][4]; u32 M; };
+extern "C" __global__ void __launch_bounds__(256)
+qsim_jit_kron64(u64 start, u64 end, u64 tb, u64 te, Qubits64 q, C* __restrict__ k2) {
+  __shared__ C T[8][256];
+  for (int x = threadIdx.x; x < 2048; x += blockDim.x) {
+    const int g = x >> 8, v = x & 255;
+    C acc; bool first = true;
+    for (int j = 7; j >= 0; --j) {
+      const int b = 8 * g + j;
+      if (b >= QSIM_M) continue;
+      const int bit = (v >> j) & 1;
+      C f; f.x = (R)q.v[b][2 * bit]; f.y = (R)q.v[b][2 * bit + 1];
+      acc = first ? f : cmul(acc, f);
+      first = false;
+    }
+    if (first) { acc.x = (R)1; acc.y = (R)0; }
+    T[g][v] = acc;
+  }
+  __syncthreads();
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
+    const u64 base = tile << 10;
+)";
+  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+  for (int b = 0; b < 64; ++b) {
+    if (b >= M)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
+    else if (b < 5)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (b < 10)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
+    else
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += "    u32 sg = 0u;\n";
+  s += walk_code(w, n, M);
+  for (int h = 0; h < 2; ++h) {
+    std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
+    s += buf;
+    for (int b = 0; b < 32; ++b) {
+      std::snprintf(buf, sizeof buf, "p%d%s", 32 * h + b, b < 31 ? ", " : "};\n");
+      s += buf;
+    }
+    std::snprintf(buf, sizeof buf,
+                  "    QSIM_TS(16, 0x0000ffffu, a%d) QSIM_TS(8, 0x00ff00ffu, a%d) "
+                  "QSIM_TS(4, 0x0f0f0f0fu, a%d)\n    QSIM_TS(2, 0x33333333u, a%d) "
+                  "QSIM_TS(1, 0x55555555u, a%d)\n", h, h, h, h, h);
+    s += buf;
+  }
+  s += R"(
+    const bool full = base >= start && base + 1024u <= end;
+    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+      const u64 sv = ((u64)a1[l] << 32) | a0[l];
+      C r = T[QSIM_TOP][(sv >> (8 * QSIM_TOP)) & 255];
+      _Pragma("unroll") for (int g = QSIM_TOP - 1; g >= 0; --g) r = cmul(r, T[g][(sv >> (8 * g)) & 255]);
+      const u64 addr = base + 32u * l + lane;
+      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), negate_if(r, (sg >> l) & 1u));
+    }
+  }
+}
+)";
+  return s;
+}
+
 struct Entry {
   std::vector<uint32_t> words;
   int M;
@@ -718,8 +805,11 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
-    if (!fn) fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem), "qsim_jit_kron",
-                                    err);
+    if (!fn)
+      fn = M > 32 ? get_kernel_locked(kind, keyw, M, kron64_source(words, n, M, elem),
+                                      "qsim_jit_kron64", err)
+                  : get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem),
+                                      "qsim_jit_kron", err);
     if (!fn) return -1;
   }
   if (count == 0) return 0;
@@ -746,7 +836,8 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::s
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(kron_source(words, n, M, elem), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(M > 32 ? kron64_source(words, n, M, elem) : kron_source(words, n, M, elem),
+                              cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,

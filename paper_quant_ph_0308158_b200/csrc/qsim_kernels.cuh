@@ -497,6 +497,62 @@ k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
   }
 }
 
+// M > 32 (64-bit addresses; output portions): one address per lane,
+// the gates walked with 64-bit masks, eight byte tables of qubit products
+// combined from the top byte down (the NVRTC kernel's order).  The fallback
+// of qsim_run_fused_kron when NVRTC is unavailable.
+struct Qubits64 {
+  double v[64][4];
+  uint32_t M;
+};
+
+template <int CAP, typename C>
+__global__ void __launch_bounds__(256)
+k_fused_kron_perlane64(const __grid_constant__ GateList<CAP> g, const __grid_constant__ Qubits64 q,
+                       uint64_t start, uint64_t count, C* __restrict__ k2_out) {
+  __shared__ C T[8][256];
+  for (int x = threadIdx.x; x < 8 * 256; x += blockDim.x) {
+    const int gi = x >> 8, v = x & 255;
+    C acc = cmake<C>(1.0, 0.0);
+    bool first = true;
+    for (int j = 7; j >= 0; --j) {
+      const int b = 8 * gi + j;
+      if (b >= (int)q.M) continue;
+      const int bit = (v >> j) & 1;
+      const C f = cmake<C>(q.v[b][2 * bit], q.v[b][2 * bit + 1]);
+      acc = first ? f : cmul_rn(acc, f);
+      first = false;
+    }
+    T[gi][v] = acc;
+  }
+  __syncthreads();
+  const int top = ((int)q.M - 1) / 8;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += stride) {
+    uint64_t x = start + r;
+    uint32_t sg = 0u;
+    for (int k = (int)g.n - 1; k >= 0; --k) {
+      const uint32_t w = g.w[k], kind = gate_kind(w), t = gate_t(w);
+      const uint64_t tm = 1ull << t;
+      if (kind == 6) {
+        const uint32_t c = gate_c0(w);
+        if (((x >> t) ^ (x >> c)) & 1ull) x ^= tm | (1ull << c);
+        continue;
+      }
+      const uint32_t nc = kind % 3;
+      const uint64_t cm = (nc >= 1 ? 1ull << gate_c0(w) : 0ull) | (nc == 2 ? 1ull << gate_c1(w) : 0ull);
+      if (kind >= 3) {
+        sg ^= (~x & (cm | tm)) == 0ull ? 1u : 0u;
+        continue;
+      }
+      if ((~x & cm) == 0ull) x ^= tm;
+    }
+    C v = T[top][(x >> (8 * top)) & 255u];
+    for (int gi = top - 1; gi >= 0; --gi) v = cmul_rn(v, T[gi][(x >> (8 * gi)) & 255u]);
+    k2_out[r] = negate_if(v, sg);
+  }
+}
+
 // --------------------------------------------------------------------- apply
 // Natural order: k2[r] = k1[perm[r]]: perm streamed with 128-bit loads (4
 // indices), the gathers issued back to back (8 in flight per thread).

@@ -209,10 +209,20 @@ def test_kron_validation(q):
                                  None) == q.ERANGE
     assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, 9, qd.ctypes.data, 0, 256, FAKE, 0,
                                  None) == q.EINVAL
-    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 256, FAKE, 1,
-                                 None) == q.EINVAL      # per-lane walk not offered here
+    assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 256, FAKE, 4,
+                                 None) == q.EINVAL      # no such walk
     assert L.qsim_run_fused_kron(g.ctypes.data, 5, 8, q.C64, qd.ctypes.data, 0, 0, FAKE, 0,
                                  None) == q.OK
+    # M > 32 only here (input on the fly, 64-bit addresses): up to 63
+    g40 = np.ascontiguousarray(wl.random_gates(5, 40, 1))
+    q40 = np.zeros(4 * 64)
+    for M, want in ((40, q.OK), (63, q.OK), (64, q.ERANGE), (0, q.ERANGE)):
+        gg = g40 if M >= 40 else g
+        assert L.qsim_run_fused_kron(gg.ctypes.data, 5, M, q.C64, q40.ctypes.data, 1 << 35, 0,
+                                     FAKE, 0, None) == (want if M != 0 else q.ERANGE), M
+    assert L.qsim_run_fused_kron(g40.ctypes.data, 5, 40, q.C64, q40.ctypes.data, (1 << 40) - 3, 4,
+                                 FAKE, 0, None) == q.ERANGE
+    assert L.qsim_build_map(g40.ctypes.data, 5, 40, FAKE, None) == q.ERANGE   # maps stay M <= 32
 
 
 def test_sector_cover_plan_matches_an_independent_sample(q):

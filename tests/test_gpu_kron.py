@@ -114,3 +114,50 @@ def test_kron_cfg5_full_size_sampled(q):
     _check(got, ref, M, "c64")
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("M", [33, 36, 40])
+def test_kron_beyond_32_qubits_in_portions(q, M):
+    """M > 32: k1 is never stored, so a portion
+    [start, start + count) of k2 needs only its own memory ("output in
+    convenient continuous portions").  64-bit addresses through the
+    NVRTC kernel (64 bit planes) and the per-lane kernel: both within the
+    rounding bound of the oracle, equal to each other bit for bit, and
+    portions glue (two halves = the whole, byte for byte)."""
+    N = 1 << M
+    for gates in (wl.random_gates(64, M, 40 + M), wl.random_gates_ext(64, M, 50 + M)):
+        qb = wl.random_qubits(M, 60 + M, "c64")
+        for start, count in ((0, 1 << 14), (N // 2 - 700, (1 << 15) + 333), (N - 5000, 5000),
+                             (0x5a5a5a5a5 % (N - 40000), 40000)):
+            ref = oracle.fused_kron(gates, qb, start, count)
+            outs = {}
+            for w in (q.WALK_JIT, q.WALK_PER_LANE):
+                out = _out(count, "c64")
+                q.run_fused_kron(gates, M, qb, out, start=start, count=count, dtype="c64", walk=w)
+                torch.cuda.synchronize()
+                outs[w] = out.cpu().numpy()[:count]
+                _check(outs[w], ref, M, "c64")
+            assert outs[q.WALK_JIT].tobytes() == outs[q.WALK_PER_LANE].tobytes()
+            half = count // 2 + 17
+            a, b = _out(half, "c64"), _out(count - half, "c64")
+            q.run_fused_kron(gates, M, qb, a, start=start, count=half, dtype="c64")
+            q.run_fused_kron(gates, M, qb, b, start=start + half, count=count - half, dtype="c64")
+            torch.cuda.synchronize()
+            glued = np.concatenate([a.cpu().numpy()[:half], b.cpu().numpy()[:count - half]])
+            assert glued.tobytes() == outs[q.WALK_JIT].tobytes()
+
+
+def test_kron_64bit_kernel_equals_32bit_kernel_below_33(q):
+    """For M <= 32 the per-lane 64-bit kernel forms the same products in the
+    same order as the 32-bit kernels: identical bytes (c64 and c128)."""
+    M = 20
+    gates = wl.random_gates_ext(64, M, 77)
+    for dtype in ("c64", "c128"):
+        qb = wl.random_qubits(M, 8, dtype)
+        outs = []
+        for w in (q.WALK_PER_LANE, q.WALK_BITSLICED, q.WALK_JIT):
+            out = _out(1 << M, dtype)
+            q.run_fused_kron(gates, M, qb, out, dtype=dtype, walk=w)
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy().tobytes())
+        assert outs[0] == outs[1] == outs[2]
