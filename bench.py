@@ -258,6 +258,24 @@ def run_qsim(args):
                 marks.append(("fused_kron", a, b))
         return n
 
+    # M = 40 (beyond a stored state): a 2^M-entry portion of a 40-qubit
+    # circuit's output with the input generated on the fly (64-bit walk)
+    M40 = 40
+    gates40 = wl.random_gates(64, M40, 4)
+    qubits40 = wl.random_qubits(M40, 2040, cfg.dtype)
+    start40 = (1 << (M40 - 1)) - N // 2          # straddles the middle of the 2^40 outputs
+
+    def step_kron40(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.run_fused_kron(gates40, M40, qubits40, k2, start=start40, count=N, dtype=cfg.dtype,
+                             stream=stream)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("fused_kron40", a, b))
+        return n
+
     def step_fused(marks):
         with torch.cuda.stream(stream):
             a = ev() if marks is not None else None
@@ -278,6 +296,8 @@ def run_qsim(args):
                                                           per_kernel=True)
         ms_kron, launches_kron, kern_kron = timed_loop(step_kron, args.steps, args.warmup,
                                                        per_kernel=True)
+        ms_k40, launches_k40, kern_k40 = timed_loop(step_kron40, max(2, args.steps // 4),
+                                                    args.warmup, per_kernel=True)
     clocks = sampler.summary()
 
     # ---- end to end through the C ABI from pinned host buffers
@@ -325,6 +345,7 @@ def run_qsim(args):
     build_ms = statistics.mean(kern_mat["build_map"])
     fused_ms = statistics.mean(kern_fused["run_fused"])
     kron_ms = statistics.mean(kern_kron["fused_kron"])
+    k40_ms = statistics.mean(kern_k40["fused_kron40"])
     ms_step = ms_mg / args.steps
     achieved = bytes_mg / (mg_ms * 1e-3) / 1e9
     mg_kernel = ("qsim_jit_fused (NVRTC, circuit-specialised, perm + gather)"
@@ -380,12 +401,17 @@ def run_qsim(args):
                            "frac_of_peak": gbps(N * e, kron_ms) / hbm,
                            "note": "qsim_run_fused_kron: Appendix-1 input generated on the fly "
                                    "(k1 never read), write-only"},
+            "fused_kron_M40_portion": {
+                "ms": k40_ms, "GBps": gbps(N * e, k40_ms), "entries_per_s": N / (k40_ms * 1e-3),
+                "bytes_per_entry": e, "frac_of_peak": gbps(N * e, k40_ms) / hbm,
+                "note": "M = 40 qubits (64 random gates, seed 4): output portion "
+                        "[2^39 - 2^31, 2^39 + 2^31) of 2^40, input on the fly, 64-bit walk"},
         },
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mg,
         "gpu_launches_other_loops": {"two_call": launches_mat, "fused": launches_fused,
-                                     "fused_kron": launches_kron},
+                                     "fused_kron": launches_kron, "fused_kron_M40": launches_k40},
         "clocks": clocks,
         "setup_s": t_setup,
         "jit": {"status": q.jit_status(), "last_compile_ms": q.jit_last_compile_ms(),
@@ -393,7 +419,8 @@ def run_qsim(args):
                         "timed steps reuse them"},
         "plan": {"seconds": t_plan, "sigma": list(plan.sigma)[:M], "chunk_log2": plan.chunk_log2,
                  "fused_chunk_log2": plan.fused_chunk_log2, "blocks_per_sm": plan.blocks_per_sm,
-                 "natural_order": bool(plan.flags & 1),
+                 "natural_order": bool(plan.flags & 1), "sector_cover_bits": plan.tile_log2,
+                 "sector_pairs_contained": plan.tile_contained,
                  "note": "qsim_plan_create (host sampling of the circuit) runs once per circuit, "
                          "outside the timed region, like an FFT plan"},
     }
