@@ -211,6 +211,18 @@ typedef struct qsim_plan {
     uint8_t tile_reserved[3];
     float tile_contained;   /* sampled fraction of (reader, sector-mate reader) pairs
                                that differ only in those bits                        */
+    /* Linear traversal (ABI 4, complex64, NVRTC kernels of the planned calls):
+     * when lin_flags bit 0 is set, output = XOR of lin[k] over the set counter
+     * bits k (an invertible GF(2) map instead of the bit permutation sigma).
+     * lin[0..4] (the lanes of a warp) are the commonest differences between the
+     * readers of one 32-byte k1 sector, so a warp load touches fewer sectors;
+     * lin[0..12] span the sector cover, lin[13..] = 1 << sigma[13..]; the span
+     * of lin[0..9] holds output bits 0..3, and k2 / perm are written through a
+     * per-warp shared-memory transpose in 128-byte runs.  lanes_sectors: sampled
+     * distinct k1 sectors per warp load with lin (32 = every lane its own).   */
+    uint32_t lin[32];
+    uint32_t lin_flags;
+    float lanes_sectors;
 } qsim_plan;
 
 int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
@@ -291,6 +303,9 @@ int qsim_run_host(const qsim_gate *gates, int32_t n_gates, int32_t M,
 /* Number of kernel launches the last successful call on this thread
  * enqueued (for launch accounting in bench.py).                            */
 int32_t qsim_last_launch_count(void);
+/* Name of the last kernel the last planned call on this thread launched
+ * ("qsim_jit_fused_lt", "qsim_jit_fused", "k_fused_sigma", ...; "" if none). */
+const char *qsim_last_kernel(void);
 
 const char *qsim_strerror(int32_t code);
 const char *qsim_last_error(void);

@@ -57,7 +57,9 @@ class Plan(ctypes.Structure):
                 ("reserved_spread", ctypes.c_uint16),
                 ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32),
                 ("tile_log2", ctypes.c_uint8), ("tile_reserved", ctypes.c_uint8 * 3),
-                ("tile_contained", ctypes.c_float)]
+                ("tile_contained", ctypes.c_float),
+                ("lin", ctypes.c_uint32 * 32), ("lin_flags", ctypes.c_uint32),
+                ("lanes_sectors", ctypes.c_float)]
 
 
 def _load() -> ctypes.CDLL:
@@ -100,6 +102,7 @@ def _load() -> ctypes.CDLL:
     lib.qsim_jit_status.restype = ctypes.c_char_p
     lib.qsim_jit_last_compile_ms.restype = ctypes.c_double
     lib.qsim_last_launch_count.restype = i32
+    lib.qsim_last_kernel.restype = ctypes.c_char_p
     return lib
 
 
@@ -268,6 +271,11 @@ def workspace(device=None):
     import torch
     return torch.zeros(WORKSPACE_BYTES, dtype=torch.uint8,
                        device=device if device is not None else "cuda")
+
+
+def last_kernel() -> str:
+    """Kernel the last planned call on this thread launched (diagnostics)."""
+    return _lib.qsim_last_kernel().decode()
 
 
 def jit_status() -> str:

@@ -23,6 +23,7 @@ namespace {
 thread_local char g_err[512] = "";
 constexpr uint64_t kJitMinCount = 1ull << 22;  // outputs from which AUTO uses the JIT kernels
 thread_local int32_t g_launches = 0;
+thread_local const char* g_last_kernel = "";
 
 int cuda_fail(cudaError_t e, const char* what) {
   std::snprintf(g_err, sizeof g_err, "%s: %s (%s)", what, cudaGetErrorString(e),
@@ -452,6 +453,22 @@ uint32_t plan_inverse_walk(const PlanGate* g, int n, uint32_t x) {
   return x;
 }
 
+// ---- GF(2) helpers for the linear traversal
+// Insert v into an echelon basis (pivot = highest bit); false if v is in the span.
+bool gf2_insert(std::vector<uint32_t>& ech, uint32_t v) {
+  for (uint32_t b : ech)
+    if ((v ^ b) < v) v ^= b;  // b's pivot bit is set in v
+  if (v == 0) return false;
+  ech.push_back(v);
+  std::sort(ech.begin(), ech.end(), [](uint32_t x, uint32_t y) { return x > y; });
+  return true;
+}
+bool gf2_in_span(const std::vector<uint32_t>& ech, uint32_t v) {
+  for (uint32_t b : ech)
+    if ((v ^ b) < v) v ^= b;
+  return v == 0;
+}
+
 // counter bits that stay output bits: 32-byte runs of k2 and perm (8
 // complex64 / 2 complex128 entries: 64 / 32 bytes of k2, 32 / 8 bytes of perm)
 int plan_keep_bits(int32_t dtype) { return dtype == QSIM_C64 ? 3 : 2; }
@@ -476,6 +493,17 @@ int plan_validate(const qsim_plan* p) {
       p->cta_threads != 1024)
     return QSIM_EINVAL;
   if (p->ilp == 32 && p->cta_threads == 1024) return QSIM_EINVAL;  // register file
+  if (p->lin_flags & 1u) {  // invertible on the M address bits, output bits 0..3 in the warp tile
+    if (p->dtype != QSIM_C64 || p->M < 14) return QSIM_EINVAL;
+    std::vector<uint32_t> ech, ten;
+    for (int k = 0; k < p->M; ++k) {
+      if ((uint64_t)p->lin[k] >> p->M) return QSIM_EINVAL;
+      if (!gf2_insert(ech, p->lin[k])) return QSIM_EINVAL;
+      if (k < 10) gf2_insert(ten, p->lin[k]);
+    }
+    for (int b = 0; b < 4; ++b)
+      if (!gf2_in_span(ten, 1u << b)) return QSIM_EINVAL;
+  }
   return QSIM_OK;
 }
 
@@ -519,7 +547,8 @@ uint32_t plan_forward_walk(const PlanGate* g, int n, uint32_t x) {
 // start from the kept bits, repeatedly add the pattern with the best gain in
 // contained pairs per added bit until T bits.  Returns the bit set V; the
 // fraction of sampled pairs inside a V-block goes to plan->tile_contained.
-uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan) {
+uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan,
+                           std::vector<uint32_t>* top_patterns = nullptr) {
   const int e = elem_bytes(dtype), eps = 32 / e, keep = plan_keep_bits(dtype);
   const int samples = 2048;
   std::vector<uint32_t> diffs;
@@ -543,6 +572,8 @@ uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, q
     return x.second != y.second ? x.second > y.second : x.first < y.first;
   });
   if (pats.size() > 512) pats.resize(512);  // candidates: the frequent patterns
+  if (top_patterns)
+    for (const auto& pc : pats) top_patterns->push_back(pc.first);
   auto contained = [&](uint32_t V) {
     uint64_t c = 0;
     for (const auto& pc : pats)
@@ -582,6 +613,83 @@ uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, q
   plan->tile_contained = diffs.empty() ? 1.0f : (float)hit / (float)diffs.size();
   plan->tile_log2 = (uint8_t)T;
   return V;
+}
+
+// Sampled distinct k1 sectors per warp load when the 32 lanes' outputs are
+// base ^ span(vecs) (averaged over fixed pseudo-random bases), per lane.
+double plan_lane_score(const PlanGate* pg, int n, int M, const std::vector<uint32_t>& vecs) {
+  const int k = (int)vecs.size(), nb = 48;
+  const uint64_t N = 1ull << M;
+  std::vector<uint32_t> sec(1u << k);
+  double tot = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t base = (uint32_t)(plan_mix(0xb45eull + b) % N);
+    for (uint32_t i = 0; i < (1u << k); ++i) {
+      uint32_t o = base;
+      for (int j = 0; j < k; ++j)
+        if ((i >> j) & 1u) o ^= vecs[j];
+      sec[i] = plan_forward_walk(pg, n, o) >> 2;
+    }
+    std::sort(sec.begin(), sec.end());
+    tot += (double)(std::unique(sec.begin(), sec.end()) - sec.begin());
+  }
+  return tot / nb / (double)(1u << k);
+}
+
+// Linear traversal for complex64 (qsim_plan.lin): lanes = the vectors in the
+// cover span that most reduce the sectors a warp load touches (greedy over
+// the frequent sector-mate difference patterns and their pairwise XORs),
+// words = output bits 0..3 (runs for the transposed stores) completed from
+// the cover, warp bits = the rest of the cover; higher counter bits keep sigma.
+void plan_linear(const PlanGate* pg, int n, int M, uint32_t V, const std::vector<uint32_t>& pats,
+                 qsim_plan* plan) {
+  plan->lin_flags = 0;
+  for (int k = 0; k < 32; ++k) plan->lin[k] = k < M ? 1u << plan->sigma[k] : 0u;
+  const int T = __builtin_popcount(V);
+  if (plan->dtype != QSIM_C64 || M < 14 || T < 13 || (V & 15u) != 15u) return;
+  std::vector<uint32_t> cand;
+  const size_t top = std::min<size_t>(pats.size(), 12);
+  for (size_t a = 0; a < top; ++a) {
+    if ((pats[a] & ~V) == 0) cand.push_back(pats[a]);
+    for (size_t b = a + 1; b < top; ++b)
+      if (((pats[a] ^ pats[b]) & ~V) == 0) cand.push_back(pats[a] ^ pats[b]);
+  }
+  for (int b = 0; b < M; ++b)
+    if ((V >> b) & 1u) cand.push_back(1u << b);
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  std::vector<uint32_t> lanes, ech;
+  for (int step = 0; step < 5; ++step) {
+    double best = 1e9;
+    uint32_t bv = 0;
+    for (uint32_t c : cand) {
+      if (c == 0 || gf2_in_span(ech, c)) continue;
+      std::vector<uint32_t> t(lanes);
+      t.push_back(c);
+      const double sc = plan_lane_score(pg, n, M, t);
+      if (sc < best - 1e-9) {
+        best = sc;
+        bv = c;
+      }
+    }
+    if (bv == 0) return;
+    lanes.push_back(bv);
+    gf2_insert(ech, bv);
+  }
+  std::vector<uint32_t> cols(lanes);
+  for (int b = 0; b < 4; ++b)  // words: output bits 0..3 first
+    if (gf2_insert(ech, 1u << b)) cols.push_back(1u << b);
+  for (int b = 0; b < M && (int)cols.size() < T; ++b)
+    if (((V >> b) & 1u) && gf2_insert(ech, 1u << b)) cols.push_back(1u << b);
+  if ((int)cols.size() != T || (int)cols.size() < 10) return;
+  const double sc = plan_lane_score(pg, n, M, lanes);
+  std::vector<uint32_t> unit;
+  for (int j = 0; j < 5; ++j) unit.push_back(1u << plan->sigma[j]);
+  const double sc_sigma = plan_lane_score(pg, n, M, unit);
+  plan->lanes_sectors = (float)(sc * 32.0);
+  if (sc >= 0.85 * sc_sigma) return;  // not worth the transposed stores
+  for (int k = 0; k < T; ++k) plan->lin[k] = cols[k];
+  plan->lin_flags = 1;
 }
 
 // bits of the sector cover (counter bits of one L1-resident block of work)
@@ -640,7 +748,8 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   int cover = plan_cover_bits;
   if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) cover = std::atoi(cb);  // tuning
   const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(cover, 20)));
-  const uint32_t V = plan_sector_cover(pg.get(), n, M, dtype, T, plan);
+  std::vector<uint32_t> pats;
+  const uint32_t V = plan_sector_cover(pg.get(), n, M, dtype, T, plan, &pats);
   int order[32], m = 0, k = 0;
   for (int b = 0; b < M; ++b) {
     if ((V >> b) & 1u)
@@ -673,6 +782,14 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   // small states are L2-resident: natural order, full parallelism
   if ((1ull << M) * (uint64_t)e <= (64ull << 20)) plan->flags = 1;
   plan->reserved_spread = (uint16_t)(nat | (sig << 8));
+  // Linear traversal: opt-in (QSIM_PLAN_LINEAR=1).  Measured on cfg5 it cuts the
+  // L1 sector lookups of the gather 2.6x (32 -> 12.5 per warp load) but loses
+  // the L1 hits (45 % -> 10 %) and 64 KB of L1 to the transposes: 23.8 ms vs
+  // 19.9 ms for the bit-permutation plan (profiles/r01_linear_traversal.txt).
+  if (!(plan->flags & 1u)) {
+    const char* lo = std::getenv("QSIM_PLAN_LINEAR");
+    if (lo && lo[0] == '1') plan_linear(pg.get(), n, M, V, pats, plan);
+  }
   return QSIM_OK;
 }
 
@@ -782,14 +899,25 @@ int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t 
     const uint64_t nchunks = (1ull << plan->M) >> plan->fused_chunk_log2;
     uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
+    const char* lt_off = std::getenv("QSIM_NO_LINEAR");  // A/B switch
+    if ((plan->lin_flags & 1u) && e == 8 && !(lt_off && lt_off[0] == '1') &&
+        qsim::jit_fused_lt(gl->w, n, plan->M, plan->lin, plan->fused_chunk_log2, k1, k2, perm_out,
+                           workspace, (int)blocks, st, err) == 0) {
+      ++g_launches;
+      *used_jit = true;
+      g_last_kernel = "qsim_jit_fused_lt";
+      return QSIM_OK;
+    }
     if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2,
                         perm_out, workspace, (int)blocks, st, err) == 0) {
       ++g_launches;
       *used_jit = true;
+      g_last_kernel = "qsim_jit_fused";
       return QSIM_OK;
     }
   }
   if (perm_out) return QSIM_EINVAL;  // caller handles the two-kernel fallback
+  g_last_kernel = "k_fused_sigma";
   if (plan->dtype == QSIM_C64)
     return fused_planned_t<uint2>(plan, gates, n, static_cast<const uint2*>(k1),
                                   static_cast<uint2*>(k2), workspace, st);
@@ -846,6 +974,7 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
   const int32_t launches = g_launches;
   rc = apply_planned_impl(plan, perm, k1, k2, workspace, st);
   g_launches += launches;
+  g_last_kernel = "build + apply";
   return rc;
 }
 
@@ -932,12 +1061,14 @@ int qsim_plan_create(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype
 int qsim_apply_map_planned(const qsim_plan* plan, const uint32_t* perm, const void* k1, void* k2,
                            void* workspace, void* stream) {
   g_launches = 0;
+  g_last_kernel = "";
   return apply_planned_impl(plan, perm, k1, k2, workspace, static_cast<cudaStream_t>(stream));
 }
 
 int qsim_run_fused_planned(const qsim_plan* plan, const qsim_gate* gates, int32_t n_gates,
                            const void* k1, void* k2, void* workspace, void* stream) {
   g_launches = 0;
+  g_last_kernel = "";
   return fused_planned_impl(plan, gates, n_gates, k1, k2, workspace,
                             static_cast<cudaStream_t>(stream));
 }
@@ -960,6 +1091,7 @@ int qsim_map_gather_planned(const qsim_plan* plan, const qsim_gate* gates, int32
                             uint32_t* perm, const void* k1, void* k2, void* workspace,
                             void* stream) {
   g_launches = 0;
+  g_last_kernel = "";
   return map_gather_impl(plan, gates, n_gates, perm, k1, k2, workspace,
                          static_cast<cudaStream_t>(stream));
 }
@@ -1007,6 +1139,8 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
 
 int32_t qsim_last_launch_count(void) { return g_launches; }
 
+const char* qsim_last_kernel(void) { return g_last_kernel; }
+
 const char* qsim_strerror(int32_t code) {
   switch (code) {
     case QSIM_OK: return "ok";
@@ -1038,6 +1172,11 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
   if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma,
                                     elem_bytes(plan->dtype), err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+    return QSIM_ECUDA;
+  }
+  if ((plan->lin_flags & 1u) &&
+      qsim::jit_check_compile_fused_lt(gl->w, n_gates, plan->M, plan->lin, err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit (linear traversal): %s", err.c_str());
     return QSIM_ECUDA;
   }
   return QSIM_OK;
@@ -1073,6 +1212,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 3; }
+int32_t qsim_abi_version(void) { return 4; }
 
 }  // extern "C"

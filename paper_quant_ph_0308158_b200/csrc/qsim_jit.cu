@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -416,6 +417,286 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   return s;
 }
 
+// Linear-traversal fused walk + gather (complex64): output = XOR of lin[k]
+// over the set bits k of the counter (qsim_plan.lin).  The lanes of a warp
+// differ by the commonest sector-mate differences, so one warp load touches
+// ~12 instead of 32 k1 sectors; the warp's 1024 outputs are a union of
+// 16-entry runs (lin[0..9] span output bits 0..3) and are written through a
+// per-warp shared-memory transpose: entry (lane, l) sits at l*32 + lane, the
+// write order u (bits 0..3 = output bits 0..3) reads it at B.u (B = the
+// coordinates of the write basis W in lin[0..9]).
+namespace {
+struct LtWrite {
+  uint32_t W[10], B[10];
+  uint32_t Sk[6], Sp[5];  // bank swizzles: k2 view (8-B entries), perm view (4-B entries)
+};
+// rank over GF(2) of a set of vectors
+int gf2_rank(std::vector<uint32_t> v) {
+  int r = 0;
+  for (int bit = 31; bit >= 0; --bit) {
+    int piv = -1;
+    for (size_t i = r; i < v.size(); ++i)
+      if ((v[i] >> bit) & 1u) {
+        piv = (int)i;
+        break;
+      }
+    if (piv < 0) continue;
+    std::swap(v[r], v[piv]);
+    for (size_t i = 0; i < v.size(); ++i)
+      if ((int)i != r && ((v[i] >> bit) & 1u)) v[i] ^= v[r];
+    ++r;
+  }
+  return r;
+}
+// position of counter offset q in a view whose banks are the low `lb` bits:
+// q ^ S(q >> lb), S linear (columns S[j] for bit j of q >> lb)
+uint32_t swz(uint32_t q, const uint32_t* S, int lb, int hb) {
+  uint32_t r = q;
+  for (int j = 0; j < hb; ++j)
+    if ((q >> (lb + j)) & 1u) r ^= S[j];
+  return r;
+}
+// choose S so that lanes reading q = sum lane_j L[j] hit distinct banks
+void pick_swizzle(const uint32_t* L, int lb, int hb, uint32_t* S) {
+  uint64_t z = 0x243f6a8885a308d3ull;
+  for (int tries = 0; tries < 4096; ++tries) {
+    for (int j = 0; j < hb; ++j) {
+      if (tries == 0) {
+        S[j] = 0;
+        continue;
+      }
+      z = z * 6364136223846793005ull + 1442695040888963407ull;
+      S[j] = (uint32_t)(z >> 40) & ((1u << lb) - 1u);
+    }
+    std::vector<uint32_t> low;
+    for (int j = 0; j < 5; ++j) low.push_back(swz(L[j], S, lb, hb) & ((1u << lb) - 1u));
+    if (gf2_rank(low) >= lb) return;
+  }
+}
+bool lt_write_basis(const uint32_t* lin, LtWrite& wb) {
+  // echelon of lin[0..9] with coordinates
+  std::vector<std::pair<uint32_t, uint32_t>> ech;  // (vector, coords)
+  auto reduce = [&](uint32_t v, uint32_t c, uint32_t& vo, uint32_t& co) {
+    for (const auto& e : ech)
+      if ((v ^ e.first) < v) {
+        v ^= e.first;
+        c ^= e.second;
+      }
+    vo = v;
+    co = c;
+  };
+  for (int j = 0; j < 10; ++j) {
+    uint32_t v, c;
+    reduce(lin[j], 1u << j, v, c);
+    if (v == 0) return false;
+    ech.push_back({v, c});
+    std::sort(ech.begin(), ech.end(),
+              [](const std::pair<uint32_t, uint32_t>& x, const std::pair<uint32_t, uint32_t>& y) {
+                return x.first > y.first;
+              });
+  }
+  auto coords = [&](uint32_t w, uint32_t& c) {
+    uint32_t v;
+    reduce(w, 0u, v, c);
+    return v == 0;
+  };
+  int k = 0;
+  std::vector<uint32_t> wech;
+  auto winsert = [&](uint32_t v) {
+    for (uint32_t b : wech)
+      if ((v ^ b) < v) v ^= b;
+    if (v == 0) return false;
+    wech.push_back(v);
+    std::sort(wech.begin(), wech.end(), [](uint32_t x, uint32_t y) { return x > y; });
+    return true;
+  };
+  for (int b = 0; b < 4; ++b) {
+    wb.W[k] = 1u << b;
+    if (!coords(wb.W[k], wb.B[k]) || !winsert(wb.W[k])) return false;
+    ++k;
+  }
+  for (int j = 0; j < 10 && k < 10; ++j) {
+    const uint32_t w = lin[j] & ~15u;  // output bits 0..3 come from u bits 0..3 only
+    if (!winsert(w)) continue;
+    wb.W[k] = w;
+    if (!coords(w, wb.B[k])) return false;
+    ++k;
+  }
+  if (k != 10) return false;
+  pick_swizzle(wb.B + 1, 4, 6, wb.Sk);  // k2 reads: lanes -> u bits 1..5
+  pick_swizzle(wb.B + 2, 5, 5, wb.Sp);  // perm reads: lanes -> u bits 2..6
+  return true;
+}
+}  // namespace
+
+std::string fused_lt_source(const uint32_t* w, int n, int M, const uint32_t* lin) {
+  std::string s = kPrelude;
+  char buf[256];
+  LtWrite wb;
+  if (!lt_write_basis(lin, wb)) return std::string();
+  s += "__constant__ unsigned int kLin[32] = {";
+  for (int k = 0; k < 32; ++k) {
+    std::snprintf(buf, sizeof buf, "%uu%s", k < M ? lin[k] : 0u, k < 31 ? "," : "};\n");
+    s += buf;
+  }
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n", M);
+  s += buf;
+  s += R"(
+extern "C" __global__ void __launch_bounds__(256)
+qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ k1,
+                  uint2* __restrict__ k2, u32* __restrict__ perm_out) {
+  extern __shared__ __align__(16) uint2 stage_all[];   // [8 warps][1024]
+  __shared__ u32 tab[4][256];
+  __shared__ u64 s_chunk;
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
+    const int b = x >> 8, v = x & 255;
+    u32 r = 0;
+    for (int j = 0; j < 8; ++j)
+      if (((v >> j) & 1) && 8 * b + j < QSIM_M) r ^= kLin[8 * b + j];
+    tab[b][v] = r;
+  }
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint2* sv = stage_all + warp * 1024u;
+  u32* sp = reinterpret_cast<u32*>(sv);
+  const u64 nchunks = N >> chunk_log2;
+  const u32 tiles = 1u << (chunk_log2 - 10);
+)";
+  // per-thread lane words and write-back offsets
+  for (int j = 0; j < 5; ++j) {
+    std::snprintf(buf, sizeof buf, "  const u32 lw%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", j, j);
+    s += buf;
+  }
+  auto lanexor = [&](const char* name, const uint32_t* vec, int off) {
+    std::string t = std::string("  const u32 ") + name + " = 0u";
+    for (int j = 0; j < 5; ++j) {
+      std::snprintf(buf, sizeof buf, " ^ (lw%d & %uu)", j, vec[off + j]);
+      t += buf;
+    }
+    return t + ";\n";
+  };
+  // shared-memory positions are bank-swizzled (linear): k2 view q ^ Sk(q >> 4),
+  // perm view q ^ Sp(q >> 5); everything below is already swizzled
+  uint32_t Bk[10], Bp[10];
+  for (int j = 0; j < 10; ++j) {
+    Bk[j] = swz(wb.B[j], wb.Sk, 4, 6);
+    Bp[j] = swz(wb.B[j], wb.Sp, 5, 5);
+  }
+  s += lanexor("qkl", Bk, 1);     // k2: u = it*64 + lane*2  (lane -> u bits 1..5)
+  s += lanexor("okl", wb.W, 1);
+  s += lanexor("qpl", Bp, 2);     // perm: u = it*128 + lane*4 (lane -> u bits 2..6)
+  s += lanexor("opl", wb.W, 2);
+  // writes: entry (lane, l) at q = 32 l + lane -> swizzled lane part + per-l constant
+  {
+    uint32_t lk[5], lp[5];
+    for (int j = 0; j < 5; ++j) {
+      lk[j] = swz(1u << j, wb.Sk, 4, 6);
+      lp[j] = swz(1u << j, wb.Sp, 5, 5);
+    }
+    s += lanexor("wkl", lk, 0);
+    s += lanexor("wpl", lp, 0);
+  }
+  std::snprintf(buf, sizeof buf, "#define QB0 %uu\n#define QB1 %uu\n#define PB0 %uu\n#define PB1 %uu\n",
+                Bk[0], Bk[1], Bp[0], Bp[1]);
+  s += buf;
+  s += "  const u32 wkc[32] = {";
+  for (int l = 0; l < 32; ++l) {
+    std::snprintf(buf, sizeof buf, "%uu%s", swz(32u * l, wb.Sk, 4, 6), l < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += "  const u32 wpc[32] = {";
+  for (int l = 0; l < 32; ++l) {
+    std::snprintf(buf, sizeof buf, "%uu%s", swz(32u * l, wb.Sp, 5, 5), l < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += R"(
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const u64 ch = s_chunk;
+    if (ch >= nchunks) break;
+    for (u32 tt = warp; tt < tiles; tt += 8u) {
+      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
+      const u32 ob = tab[1][(c >> 8) & 255] ^ tab[2][(c >> 16) & 255] ^ tab[3][(c >> 24) & 255];
+)";
+  // planes: XOR of the lane words, word patterns and ob bits
+  const uint32_t pat[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u, 0xffff0000u};
+  for (int b = 0; b < 32; ++b) {
+    if (b >= M) {
+      std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
+      s += buf;
+      continue;
+    }
+    std::string e = "      u32 p" + std::to_string(b) + " = ((ob >> " + std::to_string(b) +
+                    ") & 1u ? 0xffffffffu : 0u)";
+    uint32_t wordc = 0;
+    for (int j = 0; j < 10 && j < M; ++j)
+      if ((lin[j] >> b) & 1u) {
+        if (j < 5) e += " ^ lw" + std::to_string(j);
+        else wordc ^= pat[j - 5];
+      }
+    std::snprintf(buf, sizeof buf, " ^ %uu;\n", wordc);
+    s += e + buf;
+  }
+  s += "      u32 sg = 0u;\n";
+  s += walk_code(w, n, M);
+  s += "      u32 a[32] = {";
+  for (int b = 0; b < 32; ++b) {
+    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+  s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+  s += R"(
+      uint2 v[32];
+      _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
+      if (perm_out) {
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) sp[wpc[l] ^ wpl] = a[l];
+        __syncwarp();
+)";
+  for (int it = 0; it < 8; ++it) {
+    uint32_t qc = 0, oc = 0;
+    for (int j = 0; j < 3; ++j)
+      if ((it >> j) & 1) {
+        qc ^= Bp[7 + j];
+        oc ^= wb.W[7 + j];
+      }
+    std::snprintf(buf, sizeof buf,
+                  "        { const u32 q0 = qpl ^ %uu; const u32 o = ob ^ opl ^ %uu;\n"
+                  "          __stcs(reinterpret_cast<uint4*>(perm_out + o), make_uint4(sp[q0], "
+                  "sp[q0 ^ PB0], sp[q0 ^ PB1], sp[q0 ^ PB0 ^ PB1])); }\n",
+                  qc, oc);
+    s += buf;
+  }
+  s += R"(
+        __syncwarp();
+      }
+      _Pragma("unroll") for (int l = 0; l < 32; ++l) sv[wkc[l] ^ wkl] = negate_if(v[l], (sg >> l) & 1u);
+      __syncwarp();
+)";
+  for (int it = 0; it < 16; ++it) {
+    uint32_t qc = 0, oc = 0;
+    for (int j = 0; j < 4; ++j)
+      if ((it >> j) & 1) {
+        qc ^= Bk[6 + j];
+        oc ^= wb.W[6 + j];
+      }
+    std::snprintf(buf, sizeof buf,
+                  "      { const u32 q0 = qkl ^ %uu; const uint2 y0 = sv[q0], y1 = sv[q0 ^ QB0];\n"
+                  "        stcs(reinterpret_cast<uint4*>(k2 + (ob ^ okl ^ %uu)), "
+                  "make_uint4(y0.x, y0.y, y1.x, y1.y)); }\n",
+                  qc, oc);
+    s += buf;
+  }
+  s += R"(
+      __syncwarp();
+    }
+  }
+}
+)";
+  return s;
+}
+
 // Natural-order fused walk with the input generated on the fly (Appendix 1,
 // P:L81-L89): k2_out[out - start] = k1(perm(out)) from byte tables of
 // qubit products (same arithmetic as qsim_kernels.cuh kron_tables /
@@ -786,6 +1067,72 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     return -1;
   }
   return 0;
+}
+
+int jit_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin, uint32_t chunk_log2,
+                 const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
+                 cudaStream_t st, std::string& err) {
+  const int smem = 8 * 1024 * 8;  // per-warp transposes
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    std::vector<uint32_t> keyw(words, words + n);
+    for (int k = 0; k < 32; ++k) keyw.push_back(lin[k]);
+    const uint64_t kind = 0x6c696e6561ull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && e.words == keyw) fn = e.fn;
+    if (!fn) {
+      const std::string src = fused_lt_source(words, n, M, lin);
+      if (src.empty()) {
+        err = "linear traversal: no write basis";
+        return -1;
+      }
+      fn = get_kernel_locked(kind, keyw, M, src, "qsim_jit_fused_lt", err);
+      if (!fn) return -1;
+      if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
+        err = "cuFuncSetAttribute(max dynamic smem) failed";
+        return -1;
+      }
+      // shared memory for the transposes, the rest of the array stays L1
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 31);
+    }
+  }
+  uint64_t N = 1ull << M;
+  uint32_t cl = chunk_log2;
+  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &perm_out};
+  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
+    err = "ticket reset failed";
+    return -1;
+  }
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args,
+                   nullptr) != CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin,
+                               std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  const std::string src = fused_lt_source(words, n, M, lin);
+  if (src.empty()) {
+    err = "linear traversal: no write basis";
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(src, cubin, err) ? 0 : -1;
 }
 
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,

@@ -33,4 +33,11 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::string& err);
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
                             std::string& err);
+// Linear-traversal variant (complex64, qsim_plan.lin): one pass of walk,
+// gather and (optionally) map store, writes through per-warp transposes.
+int jit_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin, uint32_t chunk_log2,
+                 const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
+                 cudaStream_t st, std::string& err);
+int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin,
+                               std::string& err);
 }  // namespace qsim

@@ -481,3 +481,41 @@ def test_tagged_gather_m32(q):
     assert np.array_equal(words[:, 0].index_select(0, it).cpu().numpy().view(np.uint32)
                           .astype(np.uint64), src)
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("M", [14, 17, 20])
+def test_linear_traversal(q, M):
+    """Plans with a linear (GF(2)) traversal, complex64: lanes of a warp differ
+    by sector-mate differences, stores go through per-warp shared-memory
+    transposes -- the map, the fused result and the one-pass map + gather
+    equal the oracle byte for byte (the plan's own basis when it takes one,
+    and a hand-made basis with mixed lane vectors)."""
+    gates = wl.random_gates_ext(80, M, 1200 + M, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP))
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 3 + M))
+    perm_ref = oracle.build_map(gates, M)
+    ref = oracle.apply_map(perm_ref, k1)
+    k1_d = _to_dev(k1)
+    plan = q.plan_create(gates, M, "c64")
+    plan.flags = 0
+    bases = []
+    if plan.lin_flags & 1:
+        bases.append(list(plan.lin))
+    cols = [1 | 1 << 5, 2 | 1 << 7, 1 << 6, 1 << 8 | 1 << 9, 1 << 10, 1, 2, 4, 8, 1 << 4, 1 << 9]
+    cols += [1 << b for b in range(11, M)] + [0] * (32 - M)
+    bases.append(cols)
+    for basis in bases:
+        for k, v in enumerate(basis):
+            plan.lin[k] = v
+        plan.lin_flags = 1
+        for cl in (12, min(M, 15)):
+            plan.chunk_log2 = plan.fused_chunk_log2 = cl
+            pm = _new_perm(1 << M)
+            out, outf = torch.empty_like(k1_d), torch.empty_like(k1_d)
+            q.map_gather_planned(plan, gates, pm, k1_d, out, q.workspace())
+            assert q.last_kernel() == "qsim_jit_fused_lt"
+            q.run_fused_planned(plan, gates, k1_d, outf, q.workspace())
+            assert q.last_kernel() == "qsim_jit_fused_lt"
+            torch.cuda.synchronize()
+            assert np.array_equal(_perm_np(pm), perm_ref), (basis[:5], cl)
+            assert out.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)
+            assert outf.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)

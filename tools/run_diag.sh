@@ -1,3 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "linear or planned" > gpurun_out/pytest_lt.log 2>&1
 {
-for r in 4 5 6 8; do for T in 13 15; do for m in map_gather fused; do QSIM_PLAN_RUN_BITS=$r QSIM_PLAN_COVER_BITS=$T python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/run=$r T=$T /"; done; done; done
-} > gpurun_out/diag7.log 2>&1
+for m in map_gather fused; do python tools/diag_planned.py cfg5 $m | tail -1; QSIM_NO_LINEAR=1 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/nolin /"; done
+} > gpurun_out/diag8.log 2>&1
