@@ -159,10 +159,18 @@ __device__ __forceinline__ double2 negate_if(double2 v, u32 neg) {
   const u64 m = (u64)neg << 63;
   return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ m),
                       __longlong_as_double(__double_as_longlong(v.y) ^ m)); }
+// 32x32 bit transpose, one block-swap stage: afterwards bit b of a[l] = bit l
+// of the input a[b].  Stages 16 and 8 move whole bytes: two PRMT per pair;
+// stages 4, 2, 1: a shift and a bit-select (LOP3) per output word.
 #define QSIM_TS(J, MASK, a)                                                     \
   _Pragma("unroll") for (int k = 0; k < 32; ++k)                                \
-    if ((k & J) == 0) { u32 t = ((a[k] >> J) ^ a[k + J]) & MASK;                \
-                        a[k + J] ^= t; a[k] ^= t << J; }
+    if ((k & J) == 0) {                                                         \
+      const u32 x_ = a[k], y_ = a[k + J];                                       \
+      if (J == 16) { a[k] = __byte_perm(x_, y_, 0x5410); a[k + J] = __byte_perm(x_, y_, 0x7632); } \
+      else if (J == 8) { a[k] = __byte_perm(x_, y_, 0x6240); a[k + J] = __byte_perm(x_, y_, 0x7351); } \
+      else { a[k] = (x_ & ~((MASK) << J)) | ((y_ << J) & ((MASK) << J));        \
+             a[k + J] = (y_ & ~(MASK)) | ((x_ >> J) & (MASK)); }                \
+    }
 )";
 
 // Straight-line walk for one tile: planes p0..p31 in registers, gates last

@@ -205,14 +205,25 @@ __device__ __forceinline__ uint64_t next_chunk(const SigmaParams& sp, uint64_t c
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
 
+// One block-swap stage: a[k] takes the low J-bit blocks of a[k] and a[k+J]
+// shifted up, a[k+J] the high ones shifted down.  Stages 16 and 8 move whole
+// bytes (two PRMT per pair); stages 4, 2, 1 a shift and a bit-select each.
 template <int J, uint32_t MASK>
 __device__ __forceinline__ void transpose_stage(uint32_t (&a)[32]) {
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
     if ((k & J) == 0) {
-      const uint32_t t = ((a[k] >> J) ^ a[k + J]) & MASK;
-      a[k + J] ^= t;
-      a[k] ^= t << J;
+      const uint32_t x = a[k], y = a[k + J];
+      if (J == 16) {
+        a[k] = __byte_perm(x, y, 0x5410);
+        a[k + J] = __byte_perm(x, y, 0x7632);
+      } else if (J == 8) {
+        a[k] = __byte_perm(x, y, 0x6240);
+        a[k + J] = __byte_perm(x, y, 0x7351);
+      } else {
+        a[k] = (x & ~(MASK << J)) | ((y << J) & (MASK << J));
+        a[k + J] = (y & ~MASK) | ((x >> J) & MASK);
+      }
     }
   }
 }
