@@ -264,9 +264,10 @@ int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_
  *   walk    QSIM_WALK_AUTO / QSIM_WALK_BITSLICED / QSIM_WALK_JIT, or
  *           QSIM_WALK_PER_LANE (one 64-bit address per lane; the fallback
  *           for M > 32 without NVRTC, where BITSLICED means PER_LANE)
- * Arithmetic: the factors are grouped by bytes of s into 256-entry tables
- * of products (8 qubits, descending j), combined from the top byte down,
- * ((T3 T2) T1) T0 for M <= 32 (T7 ... T0 for M > 32); every
+ * Arithmetic: the factors are grouped by bits of s into ng tables of
+ * products of gb qubits each (descending j; complex64: gb <= 10, e.g. 4
+ * groups of 8 bits at M = 32, 4 of 10 at M = 40; complex128: gb <= 8), combined from the top
+ * group down, ((T_{ng-1} T_{ng-2}) ...) T_0 -- the same in every walk; every
  * complex product is rounded as written (re = ar*br - ai*bi, im = ar*bi +
  * ai*br), no FMA.  Not bit-exact against a sequential double product: the
  * normwise relative error is at most (M-1)*sqrt(5)*u (u = 2^-24 for

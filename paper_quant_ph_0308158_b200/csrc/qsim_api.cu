@@ -296,6 +296,19 @@ int fused_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, uint
 }
 
 // ---- Appendix 1: input generated on the fly, fused with the map
+// Product-table groups: as few groups (complex products per entry + 1) as fit
+// tables of <= 2^10 complex64 / 2^8 complex128 entries.  Measured
+// (profiles/r01_kron_group_bits.txt): M = 40 complex64 4 groups of 10 bits
+// 11.96 ms vs 5 bytes 14.6 ms; M = 32 4 bytes 9.22 ms vs 3 groups of 11 bits
+// 11.7 ms (larger tables cost more than the product they save).
+void kron_groups(int32_t M, int e, uint32_t* gbits, uint32_t* ngroups) {
+  int maxb = e == 8 ? 10 : 8;
+  if (const char* gb = std::getenv("QSIM_KRON_GROUP_BITS")) maxb = std::max(1, std::min(12, std::atoi(gb)));  // tuning
+  const int ng = (M + maxb - 1) / maxb;
+  *ngroups = (uint32_t)ng;
+  *gbits = (uint32_t)((M + ng - 1) / ng);
+}
+
 template <int CAP, typename C>
 int launch_kron_cap(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qubits& qb,
                     uint64_t start, uint64_t count, C* k2, cudaStream_t st) {
@@ -306,7 +319,8 @@ int launch_kron_cap(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qu
   uint64_t blocks = (te - tb + qsim::kBsWarps - 1) / qsim::kBsWarps;
   const uint64_t cap = (uint64_t)sm_count() * 2 * 16;
   if (blocks > cap) blocks = cap;
-  const size_t smem = qsim::bs_smem_bytes((uint32_t)n);
+  const size_t smem = ((qsim::bs_smem_bytes((uint32_t)n) + 15) & ~(size_t)15) +
+                      qsim::kron_table_bytes(qb.gbits, qb.ngroups, sizeof(C));
   cudaFuncSetAttribute(qsim::k_fused_kron_bitsliced<CAP, C>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   qsim::k_fused_kron_bitsliced<CAP, C><<<(unsigned)blocks, qsim::kBsThreads, smem, st>>>(
@@ -325,15 +339,18 @@ int launch_kron(const qsim_gate* gates, int32_t n, int32_t M, const qsim::Qubits
 }
 
 template <typename C>
-int launch_kron64(const qsim_gate* gates, int32_t n, const qsim::Qubits64& qb, uint64_t start,
+int launch_kron64(const qsim_gate* gates, int32_t n, const qsim::Qubits& qb, uint64_t start,
                   uint64_t count, C* k2, cudaStream_t st) {
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n, false, *gl);
   uint64_t blocks = (count + 255) / 256;
   const uint64_t cap = (uint64_t)sm_count() * 8;
   if (blocks > cap) blocks = cap;
-  qsim::k_fused_kron_perlane64<qsim::kMaxGates, C><<<(unsigned)blocks, 256, 0, st>>>(*gl, qb, start,
-                                                                                 count, k2);
+  const size_t smem = qsim::kron_table_bytes(qb.gbits, qb.ngroups, sizeof(C));
+  cudaFuncSetAttribute(qsim::k_fused_kron_perlane64<qsim::kMaxGates, C>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  qsim::k_fused_kron_perlane64<qsim::kMaxGates, C><<<(unsigned)blocks, 256, smem, st>>>(
+      *gl, qb, start, count, k2);
   QSIM_CHECK_LAUNCH("k_fused_kron_perlane64");
   return QSIM_OK;
 }
@@ -347,42 +364,21 @@ int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const
   const int e = elem_bytes(dtype);
   if (e == 0 || !qubits || !k2 || !aligned16(k2)) return QSIM_EINVAL;
   if (walk < QSIM_WALK_AUTO || walk > QSIM_WALK_JIT) return QSIM_EINVAL;
-  if (M > 32 || walk == QSIM_WALK_PER_LANE) {
-    qsim::Qubits64 q64;
-    std::memset(&q64, 0, sizeof q64);
-    q64.M = (uint32_t)M;
-    for (int j = 0; j < M; ++j)
-      for (int c = 0; c < 4; ++c) q64.v[j][c] = qubits[4 * j + c];
-    if (count == 0) return QSIM_OK;
-    if (M > 32 && (walk == QSIM_WALK_JIT || walk == QSIM_WALK_AUTO)) {
-      std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
-      pack_gates(gates, n, false, *gl);
-      std::string err;
-      if (qsim::jit_kron(gl->w, n, M, &q64, sizeof q64, e, start, count, k2, sm_count(), st, err) ==
-          0) {
-        ++g_launches;
-        return QSIM_OK;
-      }
-      if (walk == QSIM_WALK_JIT) {
-        std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
-        return QSIM_ECUDA;
-      }
-    }
-    if (dtype == QSIM_C64) return launch_kron64<float2>(gates, n, q64, start, count, static_cast<float2*>(k2), st);
-    return launch_kron64<double2>(gates, n, q64, start, count, static_cast<double2*>(k2), st);
-  }
   qsim::Qubits qb;
   std::memset(&qb, 0, sizeof qb);
   qb.M = (uint32_t)M;
+  kron_groups(M, e, &qb.gbits, &qb.ngroups);
   for (int j = 0; j < M; ++j)
     for (int c = 0; c < 4; ++c) qb.v[j][c] = qubits[4 * j + c];
   if (count == 0) return QSIM_OK;
-  if (walk == QSIM_WALK_JIT || (walk == QSIM_WALK_AUTO && count >= kJitMinCount)) {
+  const bool jit_try = walk == QSIM_WALK_JIT ||
+                       (walk == QSIM_WALK_AUTO && (M > 32 || count >= kJitMinCount));
+  if (jit_try) {
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n, false, *gl);
     std::string err;
-    if (qsim::jit_kron(gl->w, n, M, &qb, sizeof qb, e, start, count, k2, sm_count(), st, err) ==
-        0) {
+    if (qsim::jit_kron(gl->w, n, M, &qb, sizeof qb, e, (int)qb.gbits, (int)qb.ngroups, start, count,
+                       k2, sm_count(), st, err) == 0) {
       ++g_launches;
       return QSIM_OK;
     }
@@ -390,6 +386,11 @@ int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const
       std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
       return QSIM_ECUDA;
     }
+  }
+  if (M > 32 || walk == QSIM_WALK_PER_LANE) {
+    if (dtype == QSIM_C64)
+      return launch_kron64<float2>(gates, n, qb, start, count, static_cast<float2*>(k2), st);
+    return launch_kron64<double2>(gates, n, qb, start, count, static_cast<double2*>(k2), st);
   }
   if (dtype == QSIM_C64)
     return launch_kron<float2>(gates, n, M, qb, start, count, static_cast<float2*>(k2), st);
@@ -1191,7 +1192,9 @@ int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
-  if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), err) != 0) {
+  uint32_t gb = 0, ng = 0;
+  kron_groups(M, elem_bytes(dtype), &gb, &ng);
+  if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), (int)gb, (int)ng, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }

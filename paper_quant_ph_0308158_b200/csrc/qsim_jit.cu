@@ -706,15 +706,19 @@ qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ 
 }
 
 // Natural-order fused walk with the input generated on the fly (Appendix 1,
-// P:L81-L89): k2_out[out - start] = k1(perm(out)) from byte tables of
-// qubit products (same arithmetic as qsim_kernels.cuh kron_tables /
-// kron_element: products rounded as written, no FMA contraction).
-std::string kron_source(const uint32_t* w, int n, int M, int elem) {
+// P:L81-L89): k2_out[out - start] = k1(perm(out)) from tables of qubit
+// products, ng groups of gb address bits (same arithmetic and order as
+// qsim_kernels.cuh kron_tables / kron_element: products rounded as written,
+// no FMA contraction).  M > 32 (64-bit addresses; SURVEY 8f NEXT(2),
+// "continuous portions"): 64 planes and two 32x32 transposes (low and
+// high address words).
+std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int ng) {
   std::string s = kPrelude;
   char buf[256];
-  const bool f32 = elem == 8;
+  const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n", M);
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M,
+                gb, ng);
   s += buf;
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
@@ -726,15 +730,16 @@ __device__ __forceinline__ C cmul(C a, C b) {
                       __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))); }
 )";
   s += R"(
-struct Qubits { double v[32][4]; u32 M; };
+struct Qubits { double v[64][4]; u32 M, gbits, ngroups; };
 extern "C" __global__ void __launch_bounds__(256)
 qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) {
-  __shared__ C T[4][256];
-  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
-    const int g = x >> 8, v = x & 255;
+  extern __shared__ __align__(16) unsigned char kt_smem[];
+  C* T = reinterpret_cast<C*>(kt_smem);   // [QSIM_NG << QSIM_GB]
+  for (int x = threadIdx.x; x < (QSIM_NG << QSIM_GB); x += blockDim.x) {
+    const int g = x >> QSIM_GB, v = x & ((1 << QSIM_GB) - 1);
     C acc; bool first = true;
-    for (int j = 7; j >= 0; --j) {
-      const int b = 8 * g + j;
+    for (int j = QSIM_GB - 1; j >= 0; --j) {
+      const int b = QSIM_GB * g + j;
       if (b >= QSIM_M) continue;
       const int bit = (v >> j) & 1;
       C f; f.x = (R)q.v[b][2 * bit]; f.y = (R)q.v[b][2 * bit + 1];
@@ -742,89 +747,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
       first = false;
     }
     if (first) { acc.x = (R)1; acc.y = (R)0; }
-    T[g][v] = acc;
-  }
-  __syncthreads();
-  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
-    const u64 base = tile << 10;
-    const u32 b32 = (u32)base;
-)";
-  for (int b = 0; b < 32; ++b) {
-    if (b < 5)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (b < 10) {
-      const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u",
-                            "0xffff0000u"};
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
-    } else
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    s += buf;
-  }
-  s += "    u32 sg = 0u;\n";
-  s += walk_code(w, n, M);
-  s += "    u32 a[32] = {";
-  for (int b = 0; b < 32; ++b) {
-    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += R"(
-    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
-    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
-    const bool full = base >= start && base + 1024u <= end;
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u32 sv = a[l];
-      C r = T[3][sv >> 24];
-      r = cmul(r, T[2][(sv >> 16) & 255]);
-      r = cmul(r, T[1][(sv >> 8) & 255]);
-      r = cmul(r, T[0][sv & 255]);
-      const u64 addr = base + 32u * l + lane;
-      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), negate_if(r, (sg >> l) & 1u));
-    }
-  }
-}
-)";
-  return s;
-}
-
-// Input on the fly for M > 32 (64-bit addresses, "continuous
-// portions"): 64 planes, two 32x32 transposes (low and high address
-// words), eight byte tables of qubit products combined from the top byte
-// down -- for M <= 32 the same products as kron_source.
-std::string kron64_source(const uint32_t* w, int n, int M, int elem) {
-  std::string s = kPrelude;
-  char buf[256];
-  const bool f32 = elem == 8;
-  s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_TOP %d\n", M, (M - 1) / 8);
-  s += buf;
-  s += f32 ? R"(
-__device__ __forceinline__ C cmul(C a, C b) {
-  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
-                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x))); }
-)" : R"(
-__device__ __forceinline__ C cmul(C a, C b) {
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))); }
-)";
-  s += R"(
-struct Qubits64 { double v[64][4]; u32 M; };
-extern "C" __global__ void __launch_bounds__(256)
-qsim_jit_kron64(u64 start, u64 end, u64 tb, u64 te, Qubits64 q, C* __restrict__ k2) {
-  __shared__ C T[8][256];
-  for (int x = threadIdx.x; x < 2048; x += blockDim.x) {
-    const int g = x >> 8, v = x & 255;
-    C acc; bool first = true;
-    for (int j = 7; j >= 0; --j) {
-      const int b = 8 * g + j;
-      if (b >= QSIM_M) continue;
-      const int bit = (v >> j) & 1;
-      C f; f.x = (R)q.v[b][2 * bit]; f.y = (R)q.v[b][2 * bit + 1];
-      acc = first ? f : cmul(acc, f);
-      first = false;
-    }
-    if (first) { acc.x = (R)1; acc.y = (R)0; }
-    T[g][v] = acc;
+    T[x] = acc;
   }
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -832,7 +755,8 @@ qsim_jit_kron64(u64 start, u64 end, u64 tb, u64 te, Qubits64 q, C* __restrict__ 
     const u64 base = tile << 10;
 )";
   const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-  for (int b = 0; b < 64; ++b) {
+  const int np = wide ? 64 : 32;
+  for (int b = 0; b < np; ++b) {
     if (b >= M)
       std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
     else if (b < 5)
@@ -845,7 +769,7 @@ qsim_jit_kron64(u64 start, u64 end, u64 tb, u64 te, Qubits64 q, C* __restrict__ 
   }
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
-  for (int h = 0; h < 2; ++h) {
+  for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
     s += buf;
     for (int b = 0; b < 32; ++b) {
@@ -858,12 +782,16 @@ qsim_jit_kron64(u64 start, u64 end, u64 tb, u64 te, Qubits64 q, C* __restrict__ 
                   "QSIM_TS(1, 0x55555555u, a%d)\n", h, h, h, h, h);
     s += buf;
   }
+  s += wide ? "#define QSIM_SRC(l) (((u64)a1[l] << 32) | a0[l])\n"
+            : "#define QSIM_SRC(l) ((u64)a0[l])\n";
   s += R"(
     const bool full = base >= start && base + 1024u <= end;
+    const u64 gm = (1ull << QSIM_GB) - 1;
     _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u64 sv = ((u64)a1[l] << 32) | a0[l];
-      C r = T[QSIM_TOP][(sv >> (8 * QSIM_TOP)) & 255];
-      _Pragma("unroll") for (int g = QSIM_TOP - 1; g >= 0; --g) r = cmul(r, T[g][(sv >> (8 * g)) & 255]);
+      const u64 sv = QSIM_SRC(l);
+      C r = T[((QSIM_NG - 1) << QSIM_GB) | ((sv >> (QSIM_GB * (QSIM_NG - 1))) & gm)];
+      _Pragma("unroll") for (int g = QSIM_NG - 2; g >= 0; --g)
+        r = cmul(r, T[(g << QSIM_GB) | ((sv >> (QSIM_GB * g)) & gm)]);
       const u64 addr = base + 32u * l + lane;
       if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), negate_if(r, (sg >> l) & 1u));
     }
@@ -1144,8 +1072,9 @@ int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32
 }
 
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
-             int elem, uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
-             std::string& err) {
+             int elem, int gbits, int ngroups, uint64_t start, uint64_t count, void* k2_out,
+             int sms, cudaStream_t st, std::string& err) {
+  const int smem = (ngroups << gbits) * (elem == 8 ? 8 : 16);
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1156,16 +1085,21 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     }
     std::vector<uint32_t> keyw(words, words + n);
     keyw.push_back((uint32_t)elem);
+    keyw.push_back((uint32_t)gbits);
+    keyw.push_back((uint32_t)ngroups);
     const uint64_t kind = 0x6b726f6eull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
-    if (!fn)
-      fn = M > 32 ? get_kernel_locked(kind, keyw, M, kron64_source(words, n, M, elem),
-                                      "qsim_jit_kron64", err)
-                  : get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem),
-                                      "qsim_jit_kron", err);
-    if (!fn) return -1;
+    if (!fn) {
+      fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem, gbits, ngroups),
+                             "qsim_jit_kron", err);
+      if (!fn) return -1;
+      if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
+        err = "cuFuncSetAttribute(max dynamic smem) failed";
+        return -1;
+      }
+    }
   }
   if (count == 0) return 0;
   uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
@@ -1175,15 +1109,16 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
   uint64_t end = start + count;
   (void)qbytes;
   void* args[] = {&start, &end, &tb, &te, const_cast<void*>(qubits_struct), &k2_out};
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
-      CUDA_SUCCESS) {
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args,
+                   nullptr) != CUDA_SUCCESS) {
     err = "cuLaunchKernel failed";
     return -1;
   }
   return 0;
 }
 
-int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::string& err) {
+int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
+                           std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nvrtc.ok) {
@@ -1191,8 +1126,7 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::s
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(M > 32 ? kron64_source(words, n, M, elem) : kron_source(words, n, M, elem),
-                              cubin, err) ? 0 : -1;
+  return compile_cubin_locked(kron_source(words, n, M, elem, gbits, ngroups), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,

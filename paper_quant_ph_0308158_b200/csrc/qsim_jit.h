@@ -28,9 +28,10 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
 // k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
 // qsim::Qubits (passed by value as a kernel parameter).
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
-             int elem, uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
-             std::string& err);
-int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, std::string& err);
+             int elem, int gbits, int ngroups, uint64_t start, uint64_t count, void* k2_out,
+             int sms, cudaStream_t st, std::string& err);
+int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
+                           std::string& err);
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
                             std::string& err);
 // Linear-traversal variant (complex64, qsim_plan.lin): one pass of walk,

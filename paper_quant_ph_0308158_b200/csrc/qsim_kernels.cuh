@@ -428,13 +428,18 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
 
 // ------------------------------------------------ input generated on the fly
 // Appendix 1: k1(s) = q_M(b_M) ... q_1(b_1).  The M factors are
-// grouped in bytes of s: T_g[v] = product of q_j(bit) over the 8 qubits of
-// byte g (j descending, the Kronecker order), and k1(s) = ((T_3 T_2) T_1) T_0
-// evaluated in the state precision without FMA contraction (each complex
-// product rounded as written: re = ar*br - ai*bi, im = ar*bi + ai*br).
+// grouped by bits of s into ng groups of gb bits (gb <= 11 for complex64,
+// <= 8 for complex128; chosen on the host, kron_groups in qsim_api.cu):
+// T_g[v] = product of q_j(bit) over the qubits of group g (j descending, the
+// Kronecker order), and k1(s) = ((T_{ng-1} T_{ng-2}) ...) T_0, evaluated in
+// the state precision without FMA contraction (each complex product rounded
+// as written: re = ar*br - ai*bi, im = ar*bi + ai*br).  M - 1 roundings in
+// all, the bound the tests use.
 struct Qubits {
-  double v[32][4];  // qubit j (1-based) at v[j-1]: re q(0), im q(0), re q(1), im q(1)
+  double v[64][4];  // qubit j (1-based) at v[j-1]: re q(0), im q(0), re q(1), im q(1)
   uint32_t M;
+  uint32_t gbits;   // bits per group
+  uint32_t ngroups;
 };
 
 __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
@@ -453,35 +458,42 @@ template <> __device__ __forceinline__ double2 cmake<double2>(double re, double 
   return make_double2(re, im);
 }
 
-// Every thread of the CTA helps fill T[4][256] (call, then __syncthreads()).
+// Every thread of the CTA helps fill T[g << gbits | v] (call, then sync).
 template <typename C>
-__device__ __forceinline__ void kron_tables(const Qubits& q, C (*T)[256]) {
-  for (int x = threadIdx.x; x < 4 * 256; x += blockDim.x) {
-    const int g = x >> 8, v = x & 255;
+__device__ __forceinline__ void kron_tables(const Qubits& q, C* T) {
+  const int gb = (int)q.gbits;
+  for (int x = threadIdx.x; x < ((int)q.ngroups << gb); x += blockDim.x) {
+    const int g = x >> gb, v = x & ((1 << gb) - 1);
     C acc = cmake<C>(1.0, 0.0);
     bool first = true;
-    for (int j = 7; j >= 0; --j) {  // qubit index 8g + j (0-based), descending
-      const int b = 8 * g + j;
+    for (int j = gb - 1; j >= 0; --j) {  // qubit index gb*g + j (0-based), descending
+      const int b = gb * g + j;
       if (b >= (int)q.M) continue;
       const int bit = (v >> j) & 1;
       const C f = cmake<C>(q.v[b][2 * bit], q.v[b][2 * bit + 1]);
       acc = first ? f : cmul_rn(acc, f);
       first = false;
     }
-    T[g][v] = acc;
+    T[x] = acc;
   }
 }
 
 template <typename C>
-__device__ __forceinline__ C kron_element(C (*T)[256], uint32_t s) {
-  C r = T[3][s >> 24];
-  r = cmul_rn(r, T[2][(s >> 16) & 255]);
-  r = cmul_rn(r, T[1][(s >> 8) & 255]);
-  return cmul_rn(r, T[0][s & 255]);
+__device__ __forceinline__ C kron_element(const C* T, uint64_t s, uint32_t gb, uint32_t ng) {
+  const uint64_t mask = (1ull << gb) - 1;
+  C r = T[((ng - 1) << gb) | ((s >> (gb * (ng - 1))) & mask)];
+  for (int g = (int)ng - 2; g >= 0; --g) r = cmul_rn(r, T[((uint32_t)g << gb) | ((s >> (gb * g)) & mask)]);
+  return r;
+}
+
+__host__ __device__ constexpr size_t kron_table_bytes(uint32_t gbits, uint32_t ngroups,
+                                                      size_t elem) {
+  return ((size_t)ngroups << gbits) * elem;
 }
 
 // Fused with the map, natural order, output range [start, end):
-// k2_out[out - start] = k1(perm(out)), k1 never stored.
+// k2_out[out - start] = k1(perm(out)), k1 never stored (M <= 32).  Dynamic
+// shared memory: BsShared (+ gates), then the product tables.
 template <int CAP, typename C>
 __global__ void __launch_bounds__(kBsThreads, 2)
 k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
@@ -490,7 +502,7 @@ k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
                        C* __restrict__ k2_out) {
   extern __shared__ __align__(16) uint8_t bs_smem[];
   BsShared& sh = *reinterpret_cast<BsShared*>(bs_smem);
-  __shared__ C T[4][256];
+  C* T = reinterpret_cast<C*>(bs_smem + ((bs_smem_bytes(g.n) + 15) & ~(size_t)15));
   kron_tables<C>(q, T);
   bs_setup(g, sp, sh);  // ends with __syncthreads()
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -503,41 +515,24 @@ k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
     for (int l = 0; l < 32; ++l) {
       const uint64_t addr = base + 32u * l + lane;
       if (addr >= start && addr < end)
-        k2_out[addr - start] = negate_if(kron_element<C>(T, a[l]), (sgn >> l) & 1u);
+        k2_out[addr - start] =
+            negate_if(kron_element<C>(T, a[l], q.gbits, q.ngroups), (sgn >> l) & 1u);
     }
   }
 }
 
-// M > 32 (64-bit addresses; output portions): one address per lane,
-// the gates walked with 64-bit masks, eight byte tables of qubit products
-// combined from the top byte down (the NVRTC kernel's order).  The fallback
-// of qsim_run_fused_kron when NVRTC is unavailable.
-struct Qubits64 {
-  double v[64][4];
-  uint32_t M;
-};
-
+// Any M <= 63 (64-bit addresses; output portions): one address per
+// lane, the gates walked with 64-bit masks, the same product tables and
+// order as the NVRTC kernels.  The fallback of qsim_run_fused_kron for
+// M > 32 without NVRTC, and QSIM_WALK_PER_LANE.
 template <int CAP, typename C>
 __global__ void __launch_bounds__(256)
-k_fused_kron_perlane64(const __grid_constant__ GateList<CAP> g, const __grid_constant__ Qubits64 q,
+k_fused_kron_perlane64(const __grid_constant__ GateList<CAP> g, const __grid_constant__ Qubits q,
                        uint64_t start, uint64_t count, C* __restrict__ k2_out) {
-  __shared__ C T[8][256];
-  for (int x = threadIdx.x; x < 8 * 256; x += blockDim.x) {
-    const int gi = x >> 8, v = x & 255;
-    C acc = cmake<C>(1.0, 0.0);
-    bool first = true;
-    for (int j = 7; j >= 0; --j) {
-      const int b = 8 * gi + j;
-      if (b >= (int)q.M) continue;
-      const int bit = (v >> j) & 1;
-      const C f = cmake<C>(q.v[b][2 * bit], q.v[b][2 * bit + 1]);
-      acc = first ? f : cmul_rn(acc, f);
-      first = false;
-    }
-    T[gi][v] = acc;
-  }
+  extern __shared__ __align__(16) uint8_t kt_smem[];
+  C* T = reinterpret_cast<C*>(kt_smem);
+  kron_tables<C>(q, T);
   __syncthreads();
-  const int top = ((int)q.M - 1) / 8;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += stride) {
     uint64_t x = start + r;
@@ -558,9 +553,7 @@ k_fused_kron_perlane64(const __grid_constant__ GateList<CAP> g, const __grid_con
       }
       if ((~x & cm) == 0ull) x ^= tm;
     }
-    C v = T[top][(x >> (8 * top)) & 255u];
-    for (int gi = top - 1; gi >= 0; --gi) v = cmul_rn(v, T[gi][(x >> (8 * gi)) & 255u]);
-    k2_out[r] = negate_if(v, sg);
+    k2_out[r] = negate_if(kron_element<C>(T, x, q.gbits, q.ngroups), sg);
   }
 }
 
