@@ -223,6 +223,15 @@ typedef struct qsim_plan {
     uint32_t lin[32];
     uint32_t lin_flags;
     float lanes_sectors;
+    /* Lane pairs (ABI 5, complex64, NVRTC kernels): when pair_xor != 0 the
+     * traversal XORs pair_xor into the output when counter bit 5 (word bit 0)
+     * is set, so lane L's word l and lane L^1's word l^1 hold outputs o and
+     * o ^ d, d = the commonest difference between the readers of k1 entries
+     * 2m and 2m+1 (pair_frac of them, sampled).  Such a pair is read with ONE
+     * 16-byte load and split with a lane shuffle.  sigma still defines the
+     * order for the ahead-of-time kernels (another bijection, same k2).      */
+    uint32_t pair_xor;
+    float pair_frac;
 } qsim_plan;
 
 int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,

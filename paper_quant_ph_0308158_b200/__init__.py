@@ -59,7 +59,8 @@ class Plan(ctypes.Structure):
                 ("tile_log2", ctypes.c_uint8), ("tile_reserved", ctypes.c_uint8 * 3),
                 ("tile_contained", ctypes.c_float),
                 ("lin", ctypes.c_uint32 * 32), ("lin_flags", ctypes.c_uint32),
-                ("lanes_sectors", ctypes.c_float)]
+                ("lanes_sectors", ctypes.c_float),
+                ("pair_xor", ctypes.c_uint32), ("pair_frac", ctypes.c_float)]
 
 
 def _load() -> ctypes.CDLL:

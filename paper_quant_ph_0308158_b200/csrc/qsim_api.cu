@@ -494,6 +494,11 @@ int plan_validate(const qsim_plan* p) {
       p->cta_threads != 1024)
     return QSIM_EINVAL;
   if (p->ilp == 32 && p->cta_threads == 1024) return QSIM_EINVAL;  // register file
+  if (p->pair_xor) {  // counter bit 5 -> sigma[5] ^ pair_xor stays invertible
+    if (p->dtype != QSIM_C64 || p->M < 12 || ((uint64_t)p->pair_xor >> p->M) ||
+        ((p->pair_xor >> p->sigma[5]) & 1u))
+      return QSIM_EINVAL;
+  }
   if (p->lin_flags & 1u) {  // invertible on the M address bits, output bits 0..3 in the warp tile
     if (p->dtype != QSIM_C64 || p->M < 14) return QSIM_EINVAL;
     std::vector<uint32_t> ech, ten;
@@ -693,6 +698,47 @@ void plan_linear(const PlanGate* pg, int n, int M, uint32_t V, const std::vector
   plan->lin_flags = 1;
 }
 
+// Lane pairs: d = the commonest difference g(s ^ 1) ^ i between the readers
+// of the two entries of an aligned 16-byte pair (bit 0 of d is always set);
+// put one other bit b of d at counter bit 5 (swapping within the cover) and
+// XOR the rest of d into the output with counter bit 5, so lane L / word l and
+// lane L^1 / word l^1 are o and o ^ d.  Enabled when the sampled share of
+// such pairs is at least 1/4.
+void plan_pairs(const PlanGate* pg, int n, int M, uint32_t V, qsim_plan* plan) {
+  plan->pair_xor = 0;
+  plan->pair_frac = 0.0f;
+  if (plan->dtype != QSIM_C64 || M < 12) return;
+  const int samples = 2048;
+  const uint64_t N = 1ull << M;
+  std::vector<uint32_t> d(samples);
+  for (int k = 0; k < samples; ++k) {
+    const uint32_t i = (uint32_t)(plan_mix(0x9a17ull + k) % N);
+    d[k] = plan_inverse_walk(pg, n, plan_forward_walk(pg, n, i) ^ 1u) ^ i;
+  }
+  std::vector<uint32_t> srt(d);
+  std::sort(srt.begin(), srt.end());
+  uint32_t best = 0;
+  size_t bc = 0;
+  for (size_t a = 0; a < srt.size();) {
+    size_t b = a;
+    while (b < srt.size() && srt[b] == srt[a]) ++b;
+    if (b - a > bc) {
+      bc = b - a;
+      best = srt[a];
+    }
+    a = b;
+  }
+  plan->pair_frac = (float)bc / samples;
+  if (plan->pair_frac < 0.25f || !(best & 1u) || best == 1u) return;
+  // a bit of d (not bit 0, not a lane bit) to sit at counter bit 5
+  int pos = -1;
+  for (int k = 5; k < M && pos < 0; ++k)
+    if (((best >> plan->sigma[k]) & 1u) && ((V >> plan->sigma[k]) & 1u)) pos = k;
+  if (pos < 0) return;
+  std::swap(plan->sigma[5], plan->sigma[pos]);
+  plan->pair_xor = best & ~1u & ~(1u << plan->sigma[5]);
+}
+
 // bits of the sector cover (counter bits of one L1-resident block of work)
 int plan_cover_bits = 13;
 
@@ -783,6 +829,13 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   // small states are L2-resident: natural order, full parallelism
   if ((1ull << M) * (uint64_t)e <= (64ull << 20)) plan->flags = 1;
   plan->reserved_spread = (uint16_t)(nat | (sig << 8));
+  // Lane pairs: opt-in (QSIM_PLAN_PAIRS=1).  On cfg5 half the 16-byte pairs
+  // match, yet the step is slower: 22.0 vs 20.0 ms map+gather, 19.2 vs
+  // 16.0 ms fused (profiles/r01_lane_pairs.txt).
+  if (!(plan->flags & 1u)) {
+    const char* po = std::getenv("QSIM_PLAN_PAIRS");
+    if (po && po[0] == '1') plan_pairs(pg.get(), n, M, V, plan);
+  }
   // Linear traversal: opt-in (QSIM_PLAN_LINEAR=1).  Measured on cfg5 it cuts the
   // L1 sector lookups of the gather 2.6x (32 -> 12.5 per warp load) but loses
   // the L1 hits (45 % -> 10 %) and 64 KB of L1 to the transposes: 23.8 ms vs
@@ -909,8 +962,9 @@ int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t 
       g_last_kernel = "qsim_jit_fused_lt";
       return QSIM_OK;
     }
-    if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2,
-                        perm_out, workspace, (int)blocks, st, err) == 0) {
+    if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, e == 8 ? plan->pair_xor : 0u,
+                        plan->fused_chunk_log2, e, k1, k2, perm_out, workspace, (int)blocks, st,
+                        err) == 0) {
       ++g_launches;
       *used_jit = true;
       g_last_kernel = "qsim_jit_fused";
@@ -1171,6 +1225,7 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
   if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma,
+                                    elem_bytes(plan->dtype) == 8 ? plan->pair_xor : 0u,
                                     elem_bytes(plan->dtype), err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
@@ -1215,6 +1270,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 4; }
+int32_t qsim_abi_version(void) { return 5; }
 
 }  // extern "C"

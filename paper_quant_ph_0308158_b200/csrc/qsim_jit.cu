@@ -299,23 +299,26 @@ bool pipelined() {
   return v && v[0] == '1';  // default off: measured neutral (map+gather) to 4 % slower (fused)
 }
 
-std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem) {
+std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
+                         int elem) {
   std::string s = kPrelude;
   char buf[256];
   const char* T = elem == 8 ? "uint2" : "uint4";
+  const bool pair = elem == 8 && pair_xor != 0;
   s += "__constant__ unsigned char kSigma[32] = {";
   for (int k = 0; k < 32; ++k) {
     std::snprintf(buf, sizeof buf, "%u%s", (unsigned)sigma[k], k < 31 ? "," : "};\n");
     s += buf;
   }
   std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n"
-                "#define QSIM_PIPE %d\n", T, M, elem == 8 ? 32 : 16, elem == 8 && pipelined() ? 1 : 0);
+                "#define QSIM_PIPE %d\n#define QSIM_PAIR %d\n", T, M, elem == 8 ? 32 : 16,
+                elem == 8 && !pair && pipelined() ? 1 : 0, pair ? 1 : 0);
   s += buf;
   s += "__constant__ unsigned int lt_g[32] = {";
   for (int l = 0; l < 32; ++l) {
-    uint32_t o = 0;
+    uint32_t o = (l & 1) ? pair_xor : 0u;
     for (int j = 0; j < 5 && 5 + j < M; ++j)
-      if ((l >> j) & 1) o |= 1u << sigma[5 + j];
+      if ((l >> j) & 1) o ^= 1u << sigma[5 + j];
     std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
     s += buf;
   }
@@ -370,6 +373,10 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
     else
       std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
     s += buf;
+    if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
+      std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
+      s += buf;
+    }
   }
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
@@ -383,21 +390,52 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   // output offsets of the 32 word bits: sigma(l << 5), compile-time
   s += "      const u32 lt[32] = {";
   for (int l = 0; l < 32; ++l) {
-    uint32_t o = 0;
+    uint32_t o = (l & 1) ? pair_xor : 0u;
     for (int j = 0; j < 5 && 5 + j < M; ++j)
-      if ((l >> j) & 1) o |= 1u << sigma[5 + j];
+      if ((l >> j) & 1) o ^= 1u << sigma[5 + j];
     std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
     s += buf;
   }
   s += R"(
       const u32 lo = tab[0][lane];   // output bits of the lane (= lane when sigma fixes 0..4)
       if (perm_out) {
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob | lt[l] | lo), a[l]);
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob ^ lt[l] ^ lo), a[l]);
       }
-#if QSIM_PIPE
+#if QSIM_PAIR
+      // lane L word l and lane L^1 word l^1 hold outputs o and o ^ d: when their
+      // sources are the two entries of one aligned 16-byte pair, the lane with
+      // the even source loads both and hands the odd one over
+      _Pragma("unroll") for (int h = 0; h < 32; h += 16) {
+        uint4 w4[16];
+        bool take[16];
+        _Pragma("unroll") for (int j = 0; j < 16; j += 2) {
+          const u32 x0 = a[h + j], x1 = a[h + j + 1];
+          const u32 p0 = __shfl_xor_sync(0xffffffffu, x1, 1);  // partner's word l+1: pairs with my l
+          const u32 p1 = __shfl_xor_sync(0xffffffffu, x0, 1);  // partner's word l: pairs with my l+1
+          take[j] = ((x0 ^ p0) == 1u) && (x0 & 1u);
+          take[j + 1] = ((x1 ^ p1) == 1u) && (x1 & 1u);
+          w4[j] = make_uint4(0u, 0u, 0u, 0u);
+          w4[j + 1] = make_uint4(0u, 0u, 0u, 0u);
+          if (!take[j]) w4[j] = ldg(reinterpret_cast<const uint4*>(k1) + (x0 >> 1));
+          if (!take[j + 1]) w4[j + 1] = ldg(reinterpret_cast<const uint4*>(k1) + (x1 >> 1));
+        }
+        _Pragma("unroll") for (int j = 0; j < 16; j += 2) {
+          const int l = h + j;
+          const uint4 q0 = w4[j], q1 = w4[j + 1];
+          const u32 s0x = __shfl_xor_sync(0xffffffffu, q1.z, 1), s0y = __shfl_xor_sync(0xffffffffu, q1.w, 1);
+          const u32 s1x = __shfl_xor_sync(0xffffffffu, q0.z, 1), s1y = __shfl_xor_sync(0xffffffffu, q0.w, 1);
+          const uint2 v0 = take[j] ? make_uint2(s0x, s0y)
+                                   : ((a[l] & 1u) ? make_uint2(q0.z, q0.w) : make_uint2(q0.x, q0.y));
+          const uint2 v1 = take[j + 1] ? make_uint2(s1x, s1y)
+                                       : ((a[l + 1] & 1u) ? make_uint2(q1.z, q1.w) : make_uint2(q1.x, q1.y));
+          stcs(k2 + (ob ^ lt[l] ^ lo), negate_if(v0, (sg >> l) & 1u));
+          stcs(k2 + (ob ^ lt[l + 1] ^ lo), negate_if(v1, (sg >> (l + 1)) & 1u));
+        }
+      }
+#elif QSIM_PIPE
       if (pend) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l)
-          stcs(k2 + (pob | lt[l] | lo), negate_if(v[l], (psg >> l) & 1u));
+          stcs(k2 + (pob ^ lt[l] ^ lo), negate_if(v[l], (psg >> l) & 1u));
       }
       _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
       pob = ob;
@@ -408,7 +446,7 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
-          stcs(k2 + (ob | lt[h + l] | lo), negate_if(v[l], (sg >> (h + l)) & 1u));
+          stcs(k2 + (ob ^ lt[h + l] ^ lo), negate_if(v[l], (sg >> (h + l)) & 1u));
       }
 #endif
     }
@@ -417,7 +455,7 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   if (pend) {
     const u32 lo = tab[0][lane];
     _Pragma("unroll") for (int l = 0; l < 32; ++l)
-      stcs(k2 + (pob | lt_g[l] | lo), negate_if(v[l], (psg >> l) & 1u));
+      stcs(k2 + (pob ^ lt_g[l] ^ lo), negate_if(v[l], (psg >> l) & 1u));
   }
 #endif
 }
@@ -968,7 +1006,8 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
   return 0;
 }
 
-int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
+              uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err) {
   CUfunction fn = nullptr;
@@ -982,12 +1021,14 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     std::vector<uint32_t> keyw(words, words + n);
     for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
     keyw.push_back((uint32_t)elem);
+    keyw.push_back(pair_xor);
     // the source is only generated on a cache miss
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), 0x66757365ull);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
-    if (!fn) fn = get_kernel_locked(0x66757365ull, keyw, M, fused_source(words, n, M, sigma, elem),
-                                    "qsim_jit_fused", err);
+    if (!fn)
+      fn = get_kernel_locked(0x66757365ull, keyw, M, fused_source(words, n, M, sigma, pair_xor, elem),
+                             "qsim_jit_fused", err);
     if (!fn) return -1;
   }
   uint64_t N = 1ull << M;
@@ -1129,7 +1170,8 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gb
   return compile_cubin_locked(kron_source(words, n, M, elem, gbits, ngroups), cubin, err) ? 0 : -1;
 }
 
-int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,
+                            uint32_t pair_xor, int elem,
                             std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
@@ -1138,7 +1180,7 @@ int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(words, n, M, sigma, elem), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(words, n, M, sigma, pair_xor, elem), cubin, err) ? 0 : -1;
 }
 
 }  // namespace qsim

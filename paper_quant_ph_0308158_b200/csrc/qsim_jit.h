@@ -21,7 +21,8 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
 // compiled for (circuit, sigma, element size); if perm_out != null the map is
 // stored as well (one-pass map + gather).  ticket: device scratch (reset on
 // st).  Returns 0 or -1 with err.
-int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
+              uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err);
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
@@ -32,7 +33,8 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
              int sms, cudaStream_t st, std::string& err);
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
                            std::string& err);
-int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,
+                            uint32_t pair_xor, int elem,
                             std::string& err);
 // Linear-traversal variant (complex64, qsim_plan.lin): one pass of walk,
 // gather and (optionally) map store, writes through per-warp transposes.

@@ -519,3 +519,41 @@ def test_linear_traversal(q, M):
             assert np.array_equal(_perm_np(pm), perm_ref), (basis[:5], cl)
             assert out.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)
             assert outf.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)
+
+
+@pytest.mark.parametrize("M", [12, 15, 18])
+def test_lane_pairs(q, M):
+    """Plans with lane pairs (pair_xor): lane L word l and lane L^1 word l^1
+    read the two entries of one 16-byte pair with one load and a shuffle when
+    the circuit puts them there -- same map and k2 bytes as the oracle, for
+    the plan's own pair difference and for forced ones (pairs rarely
+    matching: every load still correct)."""
+    gates = wl.random_gates_ext(70, M, 1500 + M, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP, wl.Z))
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 9 + M))
+    perm_ref, signs_ref = oracle.build_map_signed(gates, M)
+    ref = oracle.apply_map_signed(perm_ref, signs_ref, k1)
+    plain = np.ascontiguousarray(gates[gates[:, 0] != wl.Z])
+    perm_plain = oracle.build_map(plain, M)
+    ref_plain = oracle.apply_map(perm_plain, k1)
+    k1_d = _to_dev(k1)
+    base = q.plan_create(plain, M, "c64")
+    base.flags = 0
+    cases = []
+    if base.pair_xor:
+        cases.append((list(base.sigma), base.pair_xor))
+    sig = list(range(M))
+    cases.append((sig, (1 << 7) | (1 << (M - 1))))          # counter bit 5 -> bit 5 ^ {7, M-1}
+    cases.append((sig, 1 << 6))
+    for sg, px in cases:
+        plan = q.Plan.from_buffer_copy(base)
+        for k, b in enumerate(sg):
+            plan.sigma[k] = b
+        plan.pair_xor = px
+        out, outf, pm = torch.empty_like(k1_d), torch.empty_like(k1_d), _new_perm(1 << M)
+        q.map_gather_planned(plan, plain, pm, k1_d, out, q.workspace())
+        assert q.last_kernel() == "qsim_jit_fused"
+        q.run_fused_planned(plan, gates, k1_d, outf, q.workspace())    # with a phase step
+        torch.cuda.synchronize()
+        assert np.array_equal(_perm_np(pm), perm_plain), px
+        assert out.cpu().numpy().tobytes() == ref_plain.tobytes(), px
+        assert outf.cpu().numpy().tobytes() == ref.tobytes(), px

@@ -1,4 +1,4 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "pairs or linear or planned" > gpurun_out/pytest_pairs.log 2>&1
 {
-for gb in 8 9 10 11; do QSIM_KRON_GROUP_BITS=$gb python tools/bench_kron.py 32; QSIM_KRON_GROUP_BITS=$gb python tools/bench_kron.py 40 32; done
-python tools/bench_kron.py 32 32 c128; python tools/bench_kron.py 26 26 c128
-} > gpurun_out/diag9.log 2>&1
+for m in map_gather fused; do QSIM_PLAN_PAIRS=1 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/pairs /"; done
+} > gpurun_out/diag10.log 2>&1
