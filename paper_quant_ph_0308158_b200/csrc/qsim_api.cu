@@ -768,7 +768,9 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
     pg[k].cm = (nc >= 1 ? 1u << g.c0 : 0u) | (nc == 2 ? 1u << g.c1 : 0u);
     pg[k].tm = g.kind == 6 ? (1u << g.target) | (1u << g.c0) : g.kind >= 3 ? 0u : 1u << g.target;
   }
-  const int line_bits = dtype == QSIM_C64 ? 4 : 3;  // one 128-byte line of k1
+  // one 128-byte line of k1 (wider "lines" for DRAM row locality measured
+  // slower: 4/5/6/7/8 bits -> 20.0/20.1/20.6/24.1/24.0 ms on cfg5)
+  const int line_bits = dtype == QSIM_C64 ? 4 : 3;
   const int lines = 2048;
   uint32_t count[32] = {0};
   const uint64_t nlines = 1ull << (M - line_bits);
@@ -888,6 +890,19 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
   const uint64_t N = 1ull << M;
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e)) return QSIM_EALIAS;
   if (plan_natural(plan)) return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
+  if (workspace) {  // NVRTC: the step kernel's traversal and batching, sources from perm
+    const uint64_t nchunks = N >> plan->fused_chunk_log2;
+    uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
+    if (blocks > nchunks) blocks = nchunks;
+    std::string err;
+    if (qsim::jit_apply(M, plan->sigma, plan->fused_chunk_log2, e, perm, k1, k2, workspace,
+                        (int)blocks, st, err) == 0) {
+      ++g_launches;
+      g_last_kernel = "qsim_jit_apply";
+      return QSIM_OK;
+    }
+  }
+  g_last_kernel = "k_apply_sigma";
   const qsim::SigmaParams sp = plan_params(plan, workspace);
   if ((rc = reset_ticket(workspace, st))) return rc;
   const uint64_t nchunks = N >> sp.chunk_log2;

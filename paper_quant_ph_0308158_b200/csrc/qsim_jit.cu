@@ -300,7 +300,7 @@ bool pipelined() {
 }
 
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
-                         int elem) {
+                         int elem, bool from_perm = false) {
   std::string s = kPrelude;
   char buf[256];
   const char* T = elem == 8 ? "uint2" : "uint4";
@@ -314,6 +314,7 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
                 "#define QSIM_PIPE %d\n#define QSIM_PAIR %d\n", T, M, elem == 8 ? 32 : 16,
                 elem == 8 && !pair && pipelined() ? 1 : 0, pair ? 1 : 0);
   s += buf;
+  s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
   s += "__constant__ unsigned int lt_g[32] = {";
   for (int l = 0; l < 32; ++l) {
     uint32_t o = (l & 1) ? pair_xor : 0u;
@@ -324,8 +325,8 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
   }
   s += R"(
 extern "C" __global__ void __launch_bounds__(256)
-qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
-               QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
+QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
+           QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
   __shared__ u32 tab[4][256];
   __shared__ u64 s_chunk;
   for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
@@ -356,37 +357,39 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
       const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
                      tab[3][(c >> 24) & 255];
 )";
+  if (!from_perm) {
   // plane initialisation: output bit b comes from counter bit inv[b]: a lane
-  // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob)
-  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-  uint8_t inv[32];
-  for (int b = 0; b < 32; ++b) inv[b] = 255;
-  for (int k = 0; k < M; ++k) inv[sigma[k]] = (uint8_t)k;
-  for (int b = 0; b < 32; ++b) {
-    const int c = b < M ? inv[b] : 255;
-    if (c < 5)
-      std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, c);
-    else if (c < 10)
-      std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[c - 5]);
-    else if (c < 32)
-      std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else
-      std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
-    s += buf;
-    if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
-      std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
+    // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob)
+    const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+    uint8_t inv[32];
+    for (int b = 0; b < 32; ++b) inv[b] = 255;
+    for (int k = 0; k < M; ++k) inv[sigma[k]] = (uint8_t)k;
+    for (int b = 0; b < 32; ++b) {
+      const int c = b < M ? inv[b] : 255;
+      if (c < 5)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, c);
+      else if (c < 10)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[c - 5]);
+      else if (c < 32)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+      else
+        std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
+      s += buf;
+      if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
+        std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
+        s += buf;
+      }
+    }
+    s += "    u32 sg = 0u;\n";
+    s += walk_code(w, n, M);
+    s += "      u32 a[32] = {";
+    for (int b = 0; b < 32; ++b) {
+      std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
       s += buf;
     }
+    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
   }
-  s += "    u32 sg = 0u;\n";
-  s += walk_code(w, n, M);
-  s += "      u32 a[32] = {";
-  for (int b = 0; b < 32; ++b) {
-    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-  s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
   // output offsets of the 32 word bits: sigma(l << 5), compile-time
   s += "      const u32 lt[32] = {";
   for (int l = 0; l < 32; ++l) {
@@ -398,9 +401,20 @@ qsim_jit_fused(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1
   }
   s += R"(
       const u32 lo = tab[0][lane];   // output bits of the lane (= lane when sigma fixes 0..4)
+)";
+  if (from_perm)  // the apply: sources read from the materialised map (32-B runs)
+    s += R"(
+      u32 a[32];
+      const u32 sg = 0u;
+      _Pragma("unroll") for (int l = 0; l < 32; ++l) a[l] = __ldcs(perm_out + (ob ^ lt[l] ^ lo));
+)";
+  else
+    s += R"(
       if (perm_out) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob ^ lt[l] ^ lo), a[l]);
       }
+)";
+  s += R"(
 #if QSIM_PAIR
       // lane L word l and lane L^1 word l^1 hold outputs o and o ^ d: when their
       // sources are the two entries of one aligned 16-byte pair, the lane with
@@ -1168,6 +1182,47 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gb
   }
   std::vector<char> cubin;
   return compile_cubin_locked(kron_source(words, n, M, elem, gbits, ngroups), cubin, err) ? 0 : -1;
+}
+
+// The planned apply from a materialised map: the fused kernel's traversal and
+// batching with the sources read from perm (k2[o] = k1[perm[o]]).
+int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,
+              const void* k1, void* k2, void* ticket, int blocks, cudaStream_t st,
+              std::string& err) {
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    std::vector<uint32_t> keyw;
+    for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
+    keyw.push_back((uint32_t)elem);
+    const uint64_t kind = 0x6170706c79ull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && e.words == keyw) fn = e.fn;
+    if (!fn)
+      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, 0u, elem, true),
+                             "qsim_jit_apply", err);
+    if (!fn) return -1;
+  }
+  uint64_t N = 1ull << M;
+  uint32_t cl = chunk_log2;
+  uint32_t* pm = const_cast<uint32_t*>(perm);
+  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &pm};
+  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
+    err = "ticket reset failed";
+    return -1;
+  }
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,

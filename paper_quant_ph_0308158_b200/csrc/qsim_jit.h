@@ -43,4 +43,9 @@ int jit_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin, uint3
                  cudaStream_t st, std::string& err);
 int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin,
                                std::string& err);
+// Planned apply from a materialised map (NVRTC; sigma order, the fused
+// kernel's batching).  Returns 0 or -1 with err.
+int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,
+              const void* k1, void* k2, void* ticket, int blocks, cudaStream_t st,
+              std::string& err);
 }  // namespace qsim
