@@ -310,6 +310,20 @@ int qsim_run_host(const qsim_gate *gates, int32_t n_gates, int32_t M,
                   void *k2_host, void *k1_dev, void *k2_dev,
                   uint32_t *perm_dev, void *workspace, void *stream);
 
+/* qsim_run_host_batch -- nsteps independent states end to end, with the
+ * copies overlapped (serving): step i copies k1_hosts[i] in, computes k2 as
+ * qsim_run_host (mode 0 / 1), copies it to k2_hosts[i]; step i+1's copy in
+ * and step i-1's copy out run while step i computes (PCIe is full duplex).
+ * Double-buffered device state: step i uses k1_dev{i&1}, k2_dev{i&1} (2^M
+ * entries each, e.g. 4 x 32 GiB + a 16 GiB map at M = 32).  One plan for
+ * all steps; library-created streams; SYNCHRONISES before returning.
+ * k1_hosts / k2_hosts: nsteps host pointers each (may repeat; pinned
+ * memory recommended).                                                     */
+int qsim_run_host_batch(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
+                        int32_t mode, int32_t nsteps, const void *const *k1_hosts,
+                        void *const *k2_hosts, void *k1_dev0, void *k1_dev1, void *k2_dev0,
+                        void *k2_dev1, uint32_t *perm_dev, void *workspace);
+
 /* Number of kernel launches the last successful call on this thread
  * enqueued (for launch accounting in bench.py).                            */
 int32_t qsim_last_launch_count(void);

@@ -82,6 +82,7 @@ def _load() -> ctypes.CDLL:
         "qsim_run_host": [vp, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp],
     }
     sig["qsim_build_map_signed"] = [vp, i32, i32, u64, u64, vp, vp, vp]
+    sig["qsim_run_host_batch"] = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
     sig["qsim_apply_map_signed"] = [vp, vp, u64, i32, i32, vp, vp, vp]
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
     sig["qsim_apply_map_planned"] = [ctypes.POINTER(Plan), vp, vp, vp, vp, vp]
@@ -209,6 +210,23 @@ def run_fused_range(gates, M: int, start: int, count: int, k1, k2_out, stream=No
     code = _dtype_code(k1 if dtype is None else dtype)
     _check(_lib.qsim_run_fused_ex(gp, n, M, code, start, count, _ptr(k1), _ptr(k2_out), walk,
                                   _stream(stream)), "qsim_run_fused_ex")
+
+
+def run_host_batch(gates, M: int, mode: int, k1_hosts, k2_hosts, k1_devs, k2_devs, perm_dev=None,
+                   workspace=None, dtype=None) -> None:
+    """nsteps = len(k1_hosts) states end to end with overlapped copies (two device
+    buffers each for k1 and k2); returns after everything is synchronised."""
+    g, gp, n = _gates(gates)
+    code = _dtype_code(k1_hosts[0] if dtype is None else dtype)
+    ns = len(k1_hosts)
+    if len(k2_hosts) != ns or len(k1_devs) != 2 or len(k2_devs) != 2:
+        raise ValueError("need nsteps host buffers each and two device buffers each")
+    kh1 = (ctypes.c_void_p * max(ns, 1))(*[_ptr(x) for x in k1_hosts])
+    kh2 = (ctypes.c_void_p * max(ns, 1))(*[_ptr(x) for x in k2_hosts])
+    _check(_lib.qsim_run_host_batch(gp, n, M, code, mode, ns, ctypes.cast(kh1, ctypes.c_void_p),
+                                    ctypes.cast(kh2, ctypes.c_void_p), _ptr(k1_devs[0]),
+                                    _ptr(k1_devs[1]), _ptr(k2_devs[0]), _ptr(k2_devs[1]),
+                                    _ptr(perm_dev), _ptr(workspace)), "qsim_run_host_batch")
 
 
 def run_host(gates, M: int, mode: int, k1_host, k2_host, k1_dev, k2_dev, perm_dev=None,

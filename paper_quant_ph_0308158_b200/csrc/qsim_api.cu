@@ -1207,6 +1207,98 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
   return QSIM_OK;
 }
 
+int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype,
+                        int32_t mode, int32_t nsteps, const void* const* k1_hosts,
+                        void* const* k2_hosts, void* k1_dev0, void* k1_dev1, void* k2_dev0,
+                        void* k2_dev1, uint32_t* perm_dev, void* workspace) {
+  g_launches = 0;
+  int rc = check_gates(gates, n_gates, M);
+  if (rc) return rc;
+  const int e = elem_bytes(dtype);
+  if (e == 0 || (mode != 0 && mode != 1) || nsteps < 0) return QSIM_EINVAL;
+  if (nsteps > 0 && (!k1_hosts || !k2_hosts)) return QSIM_EINVAL;
+  for (int32_t i = 0; i < nsteps; ++i)
+    if (!k1_hosts[i] || !k2_hosts[i]) return QSIM_EINVAL;
+  void* k1d[2] = {k1_dev0, k1_dev1};
+  void* k2d[2] = {k2_dev0, k2_dev1};
+  const uint64_t N = 1ull << M, bytes = N * e;
+  for (int b = 0; b < 2; ++b)
+    if (!k1d[b] || !k2d[b] || !aligned16(k1d[b]) || !aligned16(k2d[b])) return QSIM_EINVAL;
+  if (mode == 0 && (!perm_dev || !aligned16(perm_dev))) return QSIM_EINVAL;
+  if (mode == 0 && has_phase(gates, n_gates)) return QSIM_EINVAL;
+  if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
+  const void* bufs[5] = {k1d[0], k1d[1], k2d[0], k2d[1], perm_dev};
+  const uint64_t sz[5] = {bytes, bytes, bytes, bytes, mode == 0 ? N * 4 : 0};
+  for (int a = 0; a < 5; ++a)
+    for (int b = a + 1; b < 5; ++b)
+      if (overlap(bufs[a], sz[a], bufs[b], sz[b])) return QSIM_EALIAS;
+  if (nsteps == 0) return QSIM_OK;
+  qsim_plan plan;
+  if ((rc = plan_fill(gates, n_gates, M, dtype, &plan))) return rc;
+  // three streams: copies in, compute, copies out; step i uses buffer i & 1
+  cudaStream_t sin = nullptr, scmp = nullptr, sout = nullptr;
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr},
+              ev_out[2] = {nullptr, nullptr};
+  cudaError_t ce = cudaSuccess;
+  auto cleanup = [&]() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+      if (ev_cmp[b]) cudaEventDestroy(ev_cmp[b]);
+      if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+    }
+    if (sin) cudaStreamDestroy(sin);
+    if (scmp) cudaStreamDestroy(scmp);
+    if (sout) cudaStreamDestroy(sout);
+  };
+  if ((ce = cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking)) != cudaSuccess ||
+      (ce = cudaStreamCreateWithFlags(&scmp, cudaStreamNonBlocking)) != cudaSuccess ||
+      (ce = cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking)) != cudaSuccess) {
+    cleanup();
+    return cuda_fail(ce, "stream create");
+  }
+  for (int b = 0; b < 2 && ce == cudaSuccess; ++b) {
+    if ((ce = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming)) != cudaSuccess) break;
+    if ((ce = cudaEventCreateWithFlags(&ev_cmp[b], cudaEventDisableTiming)) != cudaSuccess) break;
+    ce = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+  }
+  if (ce != cudaSuccess) {
+    cleanup();
+    return cuda_fail(ce, "event create");
+  }
+  int launches = 0;
+  for (int32_t i = 0; i < nsteps && rc == QSIM_OK; ++i) {
+    const int b = i & 1;
+    // k1[b] is free once step i-2's compute has read it
+    if (i >= 2 && (ce = cudaStreamWaitEvent(sin, ev_cmp[b], 0)) != cudaSuccess) break;
+    if ((ce = cudaMemcpyAsync(k1d[b], k1_hosts[i], bytes, cudaMemcpyHostToDevice, sin)) !=
+        cudaSuccess)
+      break;
+    if ((ce = cudaEventRecord(ev_in[b], sin)) != cudaSuccess) break;
+    // compute: its input is in, and k2[b] has been copied out by step i-2
+    if ((ce = cudaStreamWaitEvent(scmp, ev_in[b], 0)) != cudaSuccess) break;
+    if (i >= 2 && (ce = cudaStreamWaitEvent(scmp, ev_out[b], 0)) != cudaSuccess) break;
+    rc = mode == 0 ? map_gather_impl(&plan, gates, n_gates, perm_dev, k1d[b], k2d[b], workspace, scmp)
+                   : fused_planned_impl(&plan, gates, n_gates, k1d[b], k2d[b], workspace, scmp);
+    launches += g_launches;
+    if (rc) break;
+    if ((ce = cudaEventRecord(ev_cmp[b], scmp)) != cudaSuccess) break;
+    if ((ce = cudaStreamWaitEvent(sout, ev_cmp[b], 0)) != cudaSuccess) break;
+    if ((ce = cudaMemcpyAsync(k2_hosts[i], k2d[b], bytes, cudaMemcpyDeviceToHost, sout)) !=
+        cudaSuccess)
+      break;
+    if ((ce = cudaEventRecord(ev_out[b], sout)) != cudaSuccess) break;
+  }
+  cudaError_t ce2 = cudaStreamSynchronize(sin);
+  if (ce2 == cudaSuccess) ce2 = cudaStreamSynchronize(scmp);
+  if (ce2 == cudaSuccess) ce2 = cudaStreamSynchronize(sout);
+  cleanup();
+  if (rc) return rc;
+  if (ce != cudaSuccess) return cuda_fail(ce, "qsim_run_host_batch");
+  if (ce2 != cudaSuccess) return cuda_fail(ce2, "qsim_run_host_batch sync");
+  g_launches = launches;
+  return QSIM_OK;
+}
+
 int32_t qsim_last_launch_count(void) { return g_launches; }
 
 const char* qsim_last_kernel(void) { return g_last_kernel; }

@@ -296,3 +296,24 @@ def test_jit_sources_with_phase_and_swap_compile_without_gpu(q):
     for dt in (q.C64, q.C128):
         assert L.qsim_jit_check_compile_kron(g.ctypes.data, len(g), 20, dt) == q.OK, \
             L.qsim_last_error().decode()
+
+
+def test_run_host_batch_validation(q):
+    """The overlapped end-to-end call validates everything before any copy."""
+    L = q.lib()
+    g = np.ascontiguousarray(wl.random_gates(5, 10, 1))
+    hosts = (ctypes.c_void_p * 2)(FAKE, FAKE)
+    n = 1 << 10
+    args = [g.ctypes.data, 5, 10, q.C64, 0, 2, ctypes.cast(hosts, ctypes.c_void_p),
+            ctypes.cast(hosts, ctypes.c_void_p)]
+    devs = [FAKE * 8, FAKE * 8 + n * 8, FAKE * 8 + 2 * n * 8, FAKE * 8 + 3 * n * 8]
+    perm = FAKE * 8 + 4 * n * 8
+    assert L.qsim_run_host_batch(*args, *devs, None, None) == q.EINVAL          # mode 0 needs perm
+    assert L.qsim_run_host_batch(*args[:4], 2, 2, *args[6:], *devs, perm, None) == q.EINVAL
+    bad = list(devs)
+    bad[1] = devs[0] + 16                                                       # k1 buffers overlap
+    assert L.qsim_run_host_batch(*args, *bad, perm, None) == q.EALIAS
+    assert L.qsim_run_host_batch(*args[:5], 0, *args[6:], *devs, perm, None) == q.OK   # no steps
+    nulls = (ctypes.c_void_p * 2)(FAKE, None)
+    assert L.qsim_run_host_batch(*args[:6], ctypes.cast(nulls, ctypes.c_void_p), args[7], *devs,
+                                 perm, None) == q.EINVAL

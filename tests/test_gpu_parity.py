@@ -247,6 +247,29 @@ def test_run_host_end_to_end(q):
         assert k2_h.numpy().tobytes() == ref.tobytes(), mode
 
 
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_run_host_batch_overlapped(q, dtype):
+    """Serving form: several different states end to end with overlapped
+    copies and double-buffered device state; every step's k2 equals the
+    oracle's, in both modes, for odd and even step counts."""
+    M = 17
+    gates = wl.random_gates(64, M, 44)
+    e = 8 if dtype == "c64" else 16
+    states = [wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 50 + i)) for i in range(5)]
+    refs = [oracle.apply_map(oracle.build_map(gates, M), k) for k in states]
+    k1_h = [torch.from_numpy(k.view(np.uint8).copy()).pin_memory() for k in states]
+    k1_d = [torch.empty((1 << M) * e, dtype=torch.uint8, device=DEV) for _ in range(2)]
+    k2_d = [torch.empty_like(k1_d[0]) for _ in range(2)]
+    perm = _new_perm(1 << M)
+    for mode in (q.MATERIALISED, q.FUSED):
+        for ns in (1, 2, 5):
+            k2_h = [torch.empty_like(k1_h[0]).pin_memory() for _ in range(ns)]
+            q.run_host_batch(gates, M, mode, k1_h[:ns], k2_h, k1_d, k2_d, perm, q.workspace(),
+                             dtype=dtype)
+            for i in range(ns):
+                assert k2_h[i].numpy().tobytes() == refs[i].tobytes(), (mode, ns, i)
+
+
 def test_special_values_survive(q):
     """-0.0, NaN payloads, denormals, inf: moved as bits (R15)."""
     M = 11
