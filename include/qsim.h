@@ -277,9 +277,11 @@ int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_
  * products of gb qubits each (descending j; complex64: gb <= 10, e.g. 4
  * groups of 8 bits at M = 32, 4 of 10 at M = 40; complex128: gb <= 8), combined from the top
  * group down, ((T_{ng-1} T_{ng-2}) ...) T_0 -- the same in every walk; every
- * complex product is rounded as written (re = ar*br - ai*bi, im = ar*bi +
- * ai*br), no FMA.  Not bit-exact against a sequential double product: the
- * normwise relative error is at most (M-1)*sqrt(5)*u (u = 2^-24 for
+ * complex product is re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br)
+ * (the inner products rounded, then one fused rounding).  Not bit-exact
+ * against a sequential double product: each complex product has normwise
+ * relative error <= 2u with an FMA (Jeannerod, Kornerup, Louvet & Muller
+ * 2017), so M - 1 products stay within (M-1)*sqrt(5)*u (u = 2^-24 for
  * complex64, 2^-53 for complex128), the tolerance the tests use.          */
 int qsim_run_fused_kron(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
                         const double *qubits, uint64_t start, uint64_t count, void *k2_out,

@@ -760,8 +760,8 @@ qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ 
 // Natural-order fused walk with the input generated on the fly (Appendix 1,
 // P:L81-L89): k2_out[out - start] = k1(perm(out)) from tables of qubit
 // products, ng groups of gb address bits (same arithmetic and order as
-// qsim_kernels.cuh kron_tables / kron_element: products rounded as written,
-// no FMA contraction).  M > 32 (64-bit addresses; SURVEY 8f NEXT(2),
+// qsim_kernels.cuh kron_tables / kron_element: each complex product
+// re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br)).  M > 32 (64-bit addresses; SURVEY 8f NEXT(2),
 // "continuous portions"): 64 planes and two 32x32 transposes (low and
 // high address words).
 std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int ng) {
@@ -774,12 +774,12 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   s += buf;
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
-  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
-                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x))); }
+  return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
+                     __fmaf_rn(a.x, b.y, __fmul_rn(a.y, b.x))); }
 )" : R"(
 __device__ __forceinline__ C cmul(C a, C b) {
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))); }
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
+                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x))); }
 )";
   s += R"(
 struct Qubits { double v[64][4]; u32 M, gbits, ngroups; };
@@ -1150,6 +1150,9 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
       fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem, gbits, ngroups),
                              "qsim_jit_kron", err);
       if (!fn) return -1;
+      // write-only: shared memory for the tables of several resident CTAs
+      // (the gather kernels' 3 % carveout would allow one)
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 50);
       if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
         err = "cuFuncSetAttribute(max dynamic smem) failed";
         return -1;

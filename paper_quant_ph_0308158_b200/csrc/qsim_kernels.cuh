@@ -432,9 +432,8 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
 // <= 8 for complex128; chosen on the host, kron_groups in qsim_api.cu):
 // T_g[v] = product of q_j(bit) over the qubits of group g (j descending, the
 // Kronecker order), and k1(s) = ((T_{ng-1} T_{ng-2}) ...) T_0, evaluated in
-// the state precision without FMA contraction (each complex product rounded
-// as written: re = ar*br - ai*bi, im = ar*bi + ai*br).  M - 1 roundings in
-// all, the bound the tests use.
+// the state precision, each complex product as re = fma(ar, br, -(ai*bi)),
+// im = fma(ar, bi, ai*br) (error <= 2u per product; M - 1 products).
 struct Qubits {
   double v[64][4];  // qubit j (1-based) at v[j-1]: re q(0), im q(0), re q(1), im q(1)
   uint32_t M;
@@ -443,12 +442,12 @@ struct Qubits {
 };
 
 __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
-  return make_float2(__fsub_rn(__fmul_rn(a.x, b.x), __fmul_rn(a.y, b.y)),
-                     __fadd_rn(__fmul_rn(a.x, b.y), __fmul_rn(a.y, b.x)));
+  return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
+                     __fmaf_rn(a.x, b.y, __fmul_rn(a.y, b.x)));
 }
 __device__ __forceinline__ double2 cmul_rn(double2 a, double2 b) {
-  return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
-                      __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x)));
+  return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)),
+                      __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
 }
 template <typename C> __device__ __forceinline__ C cmake(double re, double im);
 template <> __device__ __forceinline__ float2 cmake<float2>(double re, double im) {

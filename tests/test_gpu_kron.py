@@ -1,13 +1,15 @@
 """GPU parity of the Appendix-1 path (input generated on the fly, fused
 with the map) against the oracle.
 
-The GPU forms the Kronecker product with byte tables in the state precision
+The GPU forms the Kronecker product with group tables in the state precision
 (header qsim.h, qsim_run_fused_kron), the oracle sequentially in double
-precision, so the bar is the rounding bound of the arithmetic: the normwise
-relative error of a product of M complex factors, each complex product
-rounded as written (no FMA), is at most (M-1)*sqrt(5)*u (Brent, Percival &
-Zimmermann 2007), u = 2^-24 (complex64) or 2^-53 (complex128).  Exact
-special cases (basis qubits) are compared bit for bit.
+precision, so the bar is the rounding bound of the arithmetic: a complex
+product formed as re = fma(ar, br, -ai*bi), im = fma(ar, bi, ai*br) has
+normwise relative error at most 2u (Jeannerod, Kornerup, Louvet & Muller
+2017), below the sqrt(5)*u of the plain formula (Brent, Percival &
+Zimmermann 2007); the test uses (M-1)*sqrt(5)*u over the M-1 products,
+u = 2^-24 (complex64) or 2^-53 (complex128).  Exact special cases (basis
+qubits) are compared bit for bit.
 """
 import math
 
