@@ -35,6 +35,18 @@
  *     (QSIM_EALIAS); all calls are out-of-place.
  *   - Thread safety: reentrant; concurrent calls on different streams are
  *     safe (no mutable module-scope device state).
+ *
+ * Environment (diagnostics and A/B switches; none is needed for normal use)
+ *   QSIM_NO_JIT=1            never use NVRTC (ahead-of-time kernels only)
+ *   QSIM_NVRTC=<path>        libnvrtc to load (default: the toolkit's)
+ *   QSIM_JIT_DUMP=<dir>      write each generated kernel source and cubin there
+ *   QSIM_JIT_PIPE=1          software pipeline in the fused kernel (measured neutral)
+ *   QSIM_PLAN_COVER_BITS=T   sector-cover size of new plans (default 13)
+ *   QSIM_PLAN_RUN_BITS=r     contiguous output bits kept in the cover (default 3)
+ *   QSIM_PLAN_LINEAR=1       linear-traversal plans (measured slower on cfg5)
+ *   QSIM_PLAN_PAIRS=1        lane-pair plans (measured slower on cfg5)
+ *   QSIM_NO_LINEAR=1         ignore a plan's linear traversal
+ *   QSIM_KRON_GROUP_BITS=b   product-table group size of the on-the-fly input
  */
 #ifndef QSIM_H
 #define QSIM_H
