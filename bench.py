@@ -177,7 +177,14 @@ def run_qsim(args):
 
     # ---- inputs: seeded on the host (pinned), copied once to HBM
     t_setup = time.perf_counter()
-    k1_host = torch.empty(N * e, dtype=torch.uint8, pin_memory=True)
+    def host_buffer(nbytes):
+        """Pinned host memory, else pageable (e.g. 8 ranks x 64 GiB pinned may not fit)."""
+        try:
+            return torch.empty(nbytes, dtype=torch.uint8, pin_memory=True), "pinned"
+        except RuntimeError:
+            return torch.empty(nbytes, dtype=torch.uint8), "pageable"
+
+    k1_host, k1_host_kind = host_buffer(N * e)
     wl.fill_state(cfg.state, k1_host.data_ptr())
     k1 = torch.empty(N * e, dtype=torch.uint8, device=dev)
     k1.copy_(k1_host, non_blocking=True)
@@ -306,7 +313,7 @@ def run_qsim(args):
     # (double-buffered device state)
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        k2_host = torch.empty(N * e, dtype=torch.uint8, pin_memory=True)
+        k2_host, k2_host_kind = host_buffer(N * e)
         k1b = torch.empty(N * e, dtype=torch.uint8, device=dev)
         k2b = torch.empty(N * e, dtype=torch.uint8, device=dev)
         ns = args.e2e_steps
@@ -320,6 +327,7 @@ def run_qsim(args):
         e2e = {"value": world * N * ns / dt, "unit": "entries/s",
                "h2d_bytes_per_step": N * e, "d2h_bytes_per_step": N * e,
                "ms_per_step": 1e3 * dt / ns, "steps": ns,
+               "host_memory": f"k1 {k1_host_kind}, k2 {k2_host_kind}",
                "path": "qsim_run_host_batch: per step H2D k1 (pinned) -> map_gather (perm + k2) -> "
                        "D2H k2, copies overlapped with compute across steps, synchronised at the end"}
         # the unpipelined single call, for reference
