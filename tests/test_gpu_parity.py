@@ -580,3 +580,50 @@ def test_lane_pairs(q, M):
         assert np.array_equal(_perm_np(pm), perm_plain), px
         assert out.cpu().numpy().tobytes() == ref_plain.tobytes(), px
         assert outf.cpu().numpy().tobytes() == ref.tobytes(), px
+
+
+@pytest.mark.parametrize("M", [16, 21])
+def test_structured_circuits(q, M):
+    """Circuits whose plans degenerate: gates only on high bits (whole blocks
+    move, every sector's readers are one output run), only on low bits
+    (in-run shuffles), the ripple cascade, NOT-only, and the empty list --
+    every call (natural and planned, both dtypes) equals the oracle."""
+    rng = np.random.default_rng(M)
+
+    def rand_on(bits, n):
+        rows = []
+        for _ in range(n):
+            kind = int(rng.integers(3))
+            b = rng.choice(bits, size=1 + kind, replace=False)
+            rows.append(wl.gate(kind, int(b[0]), *[int(x) for x in b[1:]]))
+        return wl.gates_array(rows)
+
+    circuits = {
+        "high": rand_on(list(range(M - 6, M)), 40),
+        "low": rand_on(list(range(0, 6)), 40),
+        "ripple": wl.ripple_gates(M, 3 * (M - 2)),
+        "not_only": wl.gates_array([wl.gate(wl.NOT, int(t)) for t in rng.integers(0, M, 9)]),
+        "empty": wl.gates_array([]),
+    }
+    for name, gates in circuits.items():
+        for dtype in ("c64", "c128"):
+            k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 70 + M))
+            perm_ref = oracle.build_map(gates, M)
+            ref = oracle.apply_map(perm_ref, k1)
+            k1_d = _to_dev(k1)
+            perm = _new_perm(1 << M)
+            q.build_map(gates, M, perm)
+            torch.cuda.synchronize()
+            assert np.array_equal(_perm_np(perm), perm_ref), name
+            plan = q.plan_create(gates, M, dtype)
+            for natural in (1, 0):
+                plan.flags = natural
+                outs = [torch.empty_like(k1_d) for _ in range(3)]
+                pm = _new_perm(1 << M)
+                q.apply_map_planned(plan, perm, k1_d, outs[0], q.workspace())
+                q.run_fused_planned(plan, gates, k1_d, outs[1], q.workspace())
+                q.map_gather_planned(plan, gates, pm, k1_d, outs[2], q.workspace())
+                torch.cuda.synchronize()
+                for o in outs:
+                    assert o.cpu().numpy().tobytes() == ref.tobytes(), (name, dtype, natural)
+                assert np.array_equal(_perm_np(pm), perm_ref), (name, dtype, natural)
