@@ -400,7 +400,7 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
     s += buf;
   }
   s += R"(
-      const u32 lo = tab[0][lane];   // output bits of the lane (= lane when sigma fixes 0..4)
+      const u32 lo = tab[0][lane];   // output bits of the lane: sigma(lane)
 )";
   if (from_perm)  // the apply: sources read from the materialised map (32-B runs)
     s += R"(

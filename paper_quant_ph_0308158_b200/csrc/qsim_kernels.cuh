@@ -161,7 +161,7 @@ k_walk_per_lane(const __grid_constant__ GateList<CAP> g, uint64_t start, uint64_
 
 // ------------------------------------------------------------ sigma tables
 struct SigmaParams {
-  uint8_t sigma[32];            // counter bit k -> output bit sigma[k]; sigma[k] = k for k < 5
+  uint8_t sigma[32];            // counter bit k -> output bit sigma[k] (bits 0..2 / 0..1 fixed)
   uint32_t chunk_log2;          // counters per CTA chunk
   uint32_t nbits;               // M
   unsigned long long* ticket;   // in-order chunk dispenser (zeroed), or null: grid-stride
@@ -198,10 +198,10 @@ __device__ __forceinline__ uint64_t next_chunk(const SigmaParams& sp, uint64_t c
 // ---------------------------------------------------------------- bit-sliced
 // A warp tile = 1024 counters: counter bits 0..4 are the lane, bits 5..9 the
 // word bit l, bits >= 10 the tile.  Lane L, word bit l handles output
-// out_base | Ltab[l] | L, where out_base = sigma(tile << 10) and Ltab[l] =
-// sigma(l << 5).  Initial plane b of a thread: lane bit b (b < 5), the
-// standard 0xAAAAAAAA.. pattern if b is the image of an l-bit, else the
-// (warp-uniform) bit b of out_base.
+// out_base | Ltab[l] | sigma(L), where out_base = sigma(tile << 10) and
+// Ltab[l] = sigma(l << 5).  Initial plane b of a thread: the lane bit that
+// sigma maps to b (lanebit[b]), the standard 0xAAAAAAAA.. pattern if b is
+// the image of an l-bit, else the (warp-uniform) bit b of out_base.
 constexpr int kBsThreads = 256;
 constexpr int kBsWarps = kBsThreads / 32;
 
