@@ -1,2 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_kron.py -q -x > gpurun_out/pytest_kron.log 2>&1
-{ for rc in 1 2 4 8 16; do QSIM_KRON_COPIES=$rc python tools/bench_kron.py 32 | sed "s/^/rc=$rc /"; QSIM_KRON_COPIES=$rc python tools/bench_kron.py 40 32 | sed "s/^/rc=$rc /"; done; python tools/bench_kron.py 32 32 c128; } > gpurun_out/diag14.log 2>&1
+{
+for m in map_gather fused; do
+python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=.cs /"
+QSIM_JIT_STORE="" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=wb /"
+QSIM_JIT_STORE=".cg" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=.cg /"
+QSIM_JIT_STORE=".L1::no_allocate" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=noalloc /"
+done
+} > gpurun_out/diag15.log 2>&1
