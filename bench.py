@@ -190,6 +190,8 @@ def run_qsim(args):
     import psutil
     need = world * 2 * N * e + (32 << 30)
     host_ok = psutil.virtual_memory().available >= need
+    if os.environ.get("QSIM_BENCH_LOW_HOST_MEM") == "1":  # exercise the low-memory setup
+        host_ok = False
     k1 = torch.empty(N * e, dtype=torch.uint8, device=dev)
     if host_ok:
         k1_host, k1_host_kind = host_buffer(N * e)
