@@ -1,8 +1,6 @@
 {
-for m in map_gather fused; do
-python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=.cs /"
-QSIM_JIT_STORE="" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=wb /"
-QSIM_JIT_STORE=".cg" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=.cg /"
-QSIM_JIT_STORE=".L1::no_allocate" python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/st=noalloc /"
+for m in map_gather fused apply; do
+python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/hint=0 /"
+QSIM_JIT_K1_HINT=1 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/hint=1 /"
 done
-} > gpurun_out/diag15.log 2>&1
+} > gpurun_out/diag16.log 2>&1
