@@ -325,6 +325,43 @@ def run_qsim(args):
                                                     args.warmup, per_kernel=True)
     clocks = sampler.summary()
 
+    # ---- launch-bound small state (cfg2, 2^20 entries, L2-resident): the
+    # planned step called directly vs replayed from a CUDA graph
+    launch_bound = None
+    if rank == 0:
+        c2 = wl.CONFIGS["cfg2"]
+        g2, n2 = c2.gates(), c2.N
+        a2 = torch.zeros(n2 * 8, dtype=torch.uint8, device=dev)
+        b2 = torch.empty_like(a2)
+        p2 = torch.empty(n2, dtype=torch.int32, device=dev)
+        plan2 = q.plan_create(g2, c2.M, c2.dtype)
+        reps = 100
+
+        def direct():
+            for _ in range(reps):
+                q.map_gather_planned(plan2, g2, p2, a2, b2, ws, stream=stream)
+        graph = q.Graph(plan2, g2, q.GRAPH_MAP_GATHER, p2, a2, b2, ws, reps=reps)
+
+        def replay():
+            graph.launch(stream=stream)
+        res = {}
+        for name, fn in (("direct", direct), ("graph", replay)):
+            with torch.cuda.stream(stream):
+                fn()
+                torch.cuda.synchronize()
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(stream)
+                fn()
+                t1.record(stream)
+            torch.cuda.synchronize()
+            res[name] = 1e3 * t0.elapsed_time(t1) / reps
+        graph.close()
+        launch_bound = {"config": "cfg2 (M = 20, 2^20 entries, L2-resident)",
+                        "call": "qsim_map_gather_planned", "direct_us_per_step": res["direct"],
+                        "graph_us_per_step": res["graph"],
+                        "note": "CUDA graph of 100 recorded steps (qsim_graph_*) vs 100 calls"}
+        del a2, b2, p2
+
     # ---- end to end through the C ABI from pinned host buffers: every step
     # copies its input in and its result out; qsim_run_host_batch overlaps
     # step i+1's copy in and step i-1's copy out with step i's compute
@@ -447,6 +484,7 @@ def run_qsim(args):
                 "note": "M = 40 qubits (64 random gates, seed 4): output portion "
                         "[2^39 - 2^31, 2^39 + 2^31) of 2^40, input on the fly, 64-bit walk"},
         },
+        "launch_bound": launch_bound,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mg,

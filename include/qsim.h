@@ -338,6 +338,23 @@ int qsim_run_host_batch(const qsim_gate *gates, int32_t n_gates, int32_t M, int3
                         void *const *k2_hosts, void *k1_dev0, void *k1_dev1, void *k2_dev0,
                         void *k2_dev1, uint32_t *perm_dev, void *workspace);
 
+/* CUDA graphs for launch-bound loops (small states: a 2^20-entry step runs
+ * in a few microseconds, less than its host-side launch path).
+ * qsim_graph_create records `reps` consecutive steps of one planned call --
+ * call 0: qsim_map_gather_planned, 1: qsim_run_fused_planned, 2:
+ * qsim_apply_map_planned -- on the given buffers into a CUDA graph (after one
+ * uncaptured step that validates the arguments and compiles the kernels; it
+ * synchronises).  qsim_graph_launch replays all reps on `stream`
+ * (asynchronous; the buffers must stay alive and unchanged in place);
+ * qsim_graph_destroy frees it.  `plan` and `gates` are read during create
+ * only.  reps in [1, 1024]; errors as the recorded call.                   */
+typedef struct qsim_graph qsim_graph;
+int qsim_graph_create(const qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, int32_t call,
+                      uint32_t *perm, const void *k1, void *k2, void *workspace, int32_t reps,
+                      qsim_graph **out);
+int qsim_graph_launch(qsim_graph *graph, void *stream);
+int qsim_graph_destroy(qsim_graph *graph);
+
 /* Number of kernel launches the last successful call on this thread
  * enqueued (for launch accounting in bench.py).                            */
 int32_t qsim_last_launch_count(void);

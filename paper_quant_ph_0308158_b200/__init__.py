@@ -83,6 +83,10 @@ def _load() -> ctypes.CDLL:
     }
     sig["qsim_build_map_signed"] = [vp, i32, i32, u64, u64, vp, vp, vp]
     sig["qsim_run_host_batch"] = [vp, i32, i32, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    sig["qsim_graph_create"] = [ctypes.POINTER(Plan), vp, i32, i32, vp, vp, vp, vp, i32,
+                                ctypes.POINTER(vp)]
+    sig["qsim_graph_launch"] = [vp, vp]
+    sig["qsim_graph_destroy"] = [vp]
     sig["qsim_apply_map_signed"] = [vp, vp, u64, i32, i32, vp, vp, vp]
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
     sig["qsim_apply_map_planned"] = [ctypes.POINTER(Plan), vp, vp, vp, vp, vp]
@@ -210,6 +214,36 @@ def run_fused_range(gates, M: int, start: int, count: int, k1, k2_out, stream=No
     code = _dtype_code(k1 if dtype is None else dtype)
     _check(_lib.qsim_run_fused_ex(gp, n, M, code, start, count, _ptr(k1), _ptr(k2_out), walk,
                                   _stream(stream)), "qsim_run_fused_ex")
+
+
+GRAPH_MAP_GATHER, GRAPH_FUSED, GRAPH_APPLY = 0, 1, 2
+
+
+class Graph:
+    """A CUDA graph of `reps` steps of one planned call (qsim_graph_*)."""
+
+    def __init__(self, plan: Plan, gates, call: int, perm, k1, k2, workspace, reps: int = 1):
+        self._g, gp, n = _gates(gates)
+        h = ctypes.c_void_p()
+        _check(_lib.qsim_graph_create(ctypes.byref(plan), gp, n, call, _ptr(perm), _ptr(k1),
+                                      _ptr(k2), _ptr(workspace), reps, ctypes.byref(h)),
+               "qsim_graph_create")
+        self._h = h
+        self._keep = (perm, k1, k2, workspace)   # the graph holds their addresses
+
+    def launch(self, stream=None) -> None:
+        _check(_lib.qsim_graph_launch(self._h, _stream(stream)), "qsim_graph_launch")
+
+    def close(self) -> None:
+        if self._h:
+            _check(_lib.qsim_graph_destroy(self._h), "qsim_graph_destroy")
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def run_host_batch(gates, M: int, mode: int, k1_hosts, k2_hosts, k1_devs, k2_devs, perm_dev=None,

@@ -878,6 +878,20 @@ void launch_apply_sigma(uint32_t ilp, uint32_t threads, int bps, unsigned blocks
   else launch_apply_sigma_t<T, 16>(threads, bps, blocks, sp, perm, N, k1, k2, st);
 }
 
+// A natural-order plan still runs the NVRTC kernels (one pass, the walk in
+// registers): identity sigma, no pairs / linear traversal, chunks of up to
+// 2^13 counters (all 8 warps of a CTA busy).
+qsim_plan natural_view(const qsim_plan* plan) {
+  qsim_plan p = *plan;
+  for (int k = 0; k < 32; ++k) p.sigma[k] = (uint8_t)k;
+  p.flags = 0;
+  p.pair_xor = 0;
+  p.lin_flags = 0;
+  p.blocks_per_sm = 1;
+  p.chunk_log2 = p.fused_chunk_log2 = (uint32_t)std::min(13, std::max(10, p.M - 7));
+  return p;
+}
+
 int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* k1, void* k2,
                        void* workspace, cudaStream_t st) {
   int rc = plan_validate(plan);
@@ -889,18 +903,24 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
   if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
   const uint64_t N = 1ull << M;
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e)) return QSIM_EALIAS;
-  if (plan_natural(plan)) return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
-  if (workspace) {  // NVRTC: the step kernel's traversal and batching, sources from perm
-    const uint64_t nchunks = N >> plan->fused_chunk_log2;
-    uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
+  const qsim_plan nat = natural_view(plan);
+  const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
+  if (workspace && (!plan_natural(plan) || M >= 13)) {
+    // NVRTC: the step kernel's traversal and batching, sources from perm
+    const uint64_t nchunks = N >> pp->fused_chunk_log2;
+    uint64_t blocks = (uint64_t)sm_count() * pp->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
     std::string err;
-    if (qsim::jit_apply(M, plan->sigma, plan->fused_chunk_log2, e, perm, k1, k2, workspace,
+    if (qsim::jit_apply(M, pp->sigma, pp->fused_chunk_log2, e, perm, k1, k2, workspace,
                         (int)blocks, st, err) == 0) {
       ++g_launches;
       g_last_kernel = "qsim_jit_apply";
       return QSIM_OK;
     }
+  }
+  if (plan_natural(plan)) {
+    g_last_kernel = "k_apply";
+    return apply_impl(perm, 1ull << M, M, plan->dtype, k1, k2, st);
   }
   g_last_kernel = "k_apply_sigma";
   const qsim::SigmaParams sp = plan_params(plan, workspace);
@@ -1007,8 +1027,18 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
     if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
     if (overlap(k1, (1ull << M) * e, k2, (1ull << M) * e)) return QSIM_EALIAS;
   }
-  if (plan_natural(plan))
+  if (plan_natural(plan)) {
+    if (workspace && M >= 13) {
+      const qsim_plan nat = natural_view(plan);
+      bool jit = false;
+      const int launches = g_launches;
+      if (fused_sigma_dispatch(&nat, gates, n, k1, k2, nullptr, workspace, st, &jit) == QSIM_OK && jit)
+        return QSIM_OK;
+      g_launches = launches;
+    }
+    g_last_kernel = "k_fused_bitsliced";
     return fused_impl(gates, n, M, plan->dtype, 0, 1ull << M, k1, k2, QSIM_WALK_AUTO, st);
+  }
   bool jit = false;
   return fused_sigma_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st, &jit);
 }
@@ -1031,10 +1061,12 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e) ||
       overlap(perm, N * 4, k1, N * e))
     return QSIM_EALIAS;
-  if (!plan_natural(plan) && workspace) {
+  if (workspace && (!plan_natural(plan) || M >= 13)) {
+    const qsim_plan nat = natural_view(plan);
+    const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
     bool jit = false;
     int launches = g_launches;
-    rc = fused_sigma_dispatch(plan, gates, n, k1, k2, perm, workspace, st, &jit);
+    rc = fused_sigma_dispatch(pp, gates, n, k1, k2, perm, workspace, st, &jit);
     if (rc == QSIM_OK && jit) return QSIM_OK;
     g_launches = launches;
   }
@@ -1296,6 +1328,75 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
   if (ce != cudaSuccess) return cuda_fail(ce, "qsim_run_host_batch");
   if (ce2 != cudaSuccess) return cuda_fail(ce2, "qsim_run_host_batch sync");
   g_launches = launches;
+  return QSIM_OK;
+}
+
+struct qsim_graph {
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  int32_t launches;
+};
+
+int qsim_graph_create(const qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, int32_t call,
+                      uint32_t* perm, const void* k1, void* k2, void* workspace, int32_t reps,
+                      qsim_graph** out) {
+  g_launches = 0;
+  if (!out || reps < 1 || reps > 1024 || call < 0 || call > 2) return QSIM_EINVAL;
+  *out = nullptr;
+  auto step = [&](cudaStream_t st) {
+    return call == 0   ? map_gather_impl(plan, gates, n_gates, perm, k1, k2, workspace, st)
+           : call == 1 ? fused_planned_impl(plan, gates, n_gates, k1, k2, workspace, st)
+                       : apply_planned_impl(plan, perm, k1, k2, workspace, st);
+  };
+  cudaStream_t st = nullptr;
+  cudaError_t ce = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (ce != cudaSuccess) return cuda_fail(ce, "stream create");
+  // one uncaptured step: validates, NVRTC-compiles and loads the kernels
+  int rc = step(st);
+  if (rc == QSIM_OK && (ce = cudaStreamSynchronize(st)) != cudaSuccess) rc = cuda_fail(ce, "warm-up");
+  cudaGraph_t graph = nullptr;
+  int32_t launches = 0;
+  if (rc == QSIM_OK) {
+    if ((ce = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) {
+      rc = cuda_fail(ce, "begin capture");
+    } else {
+      for (int32_t r = 0; r < reps && rc == QSIM_OK; ++r) {
+        rc = step(st);
+        launches += g_launches;
+      }
+      ce = cudaStreamEndCapture(st, &graph);
+      if (rc == QSIM_OK && ce != cudaSuccess) rc = cuda_fail(ce, "end capture");
+    }
+  }
+  cudaGraphExec_t exec = nullptr;
+  if (rc == QSIM_OK && (ce = cudaGraphInstantiate(&exec, graph, 0)) != cudaSuccess)
+    rc = cuda_fail(ce, "graph instantiate");
+  cudaStreamDestroy(st);
+  if (rc != QSIM_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  *out = new qsim_graph{graph, exec, launches};
+  g_launches = 0;
+  return QSIM_OK;
+}
+
+int qsim_graph_launch(qsim_graph* g, void* stream) {
+  g_launches = 0;
+  if (!g) return QSIM_EINVAL;
+  cudaError_t ce = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+  if (ce != cudaSuccess) return cuda_fail(ce, "graph launch");
+  g_launches = g->launches;
+  return QSIM_OK;
+}
+
+int qsim_graph_destroy(qsim_graph* g) {
+  g_launches = 0;
+  if (!g) return QSIM_OK;
+  cudaError_t e1 = cudaGraphExecDestroy(g->exec), e2 = cudaGraphDestroy(g->graph);
+  delete g;
+  if (e1 != cudaSuccess) return cuda_fail(e1, "graph exec destroy");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "graph destroy");
   return QSIM_OK;
 }
 

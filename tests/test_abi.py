@@ -317,3 +317,18 @@ def test_run_host_batch_validation(q):
     nulls = (ctypes.c_void_p * 2)(FAKE, None)
     assert L.qsim_run_host_batch(*args[:6], ctypes.cast(nulls, ctypes.c_void_p), args[7], *devs,
                                  perm, None) == q.EINVAL
+
+
+def test_graph_validation(q):
+    L = q.lib()
+    g = np.ascontiguousarray(wl.random_gates(5, 12, 1))
+    plan = q.plan_create(g, 12, "c64")
+    h = ctypes.c_void_p()
+    assert L.qsim_graph_create(ctypes.byref(plan), g.ctypes.data, 5, 0, FAKE, FAKE * 4, FAKE * 8,
+                               None, 0, ctypes.byref(h)) == q.EINVAL          # reps < 1
+    assert L.qsim_graph_create(ctypes.byref(plan), g.ctypes.data, 5, 3, FAKE, FAKE * 4, FAKE * 8,
+                               None, 1, ctypes.byref(h)) == q.EINVAL          # no such call
+    assert L.qsim_graph_create(ctypes.byref(plan), g.ctypes.data, 5, 0, FAKE, FAKE * 4, FAKE * 8,
+                               None, 1, None) == q.EINVAL
+    assert L.qsim_graph_launch(None, None) == q.EINVAL
+    assert L.qsim_graph_destroy(None) == q.OK

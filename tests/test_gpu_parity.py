@@ -627,3 +627,33 @@ def test_structured_circuits(q, M):
                 for o in outs:
                     assert o.cpu().numpy().tobytes() == ref.tobytes(), (name, dtype, natural)
                 assert np.array_equal(_perm_np(pm), perm_ref), (name, dtype, natural)
+
+
+@pytest.mark.parametrize("M,natural", [(16, 1), (16, 0), (20, 1)])
+def test_graphs_replay_planned_calls(q, M, natural):
+    """CUDA graphs of repeated planned calls (launch-bound small states):
+    replaying the recorded steps gives the oracle's bytes, for map + gather,
+    fused and apply, natural and plan order."""
+    gates = wl.random_gates(64, M, 1700 + M)
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 4 + M))
+    perm_ref = oracle.build_map(gates, M)
+    ref = oracle.apply_map(perm_ref, k1)
+    k1_d = _to_dev(k1)
+    plan = q.plan_create(gates, M, "c64")
+    plan.flags = natural
+    ws = q.workspace()
+    pm = _new_perm(1 << M)
+    for call in (q.GRAPH_MAP_GATHER, q.GRAPH_FUSED, q.GRAPH_APPLY):
+        out = torch.empty_like(k1_d)
+        if call == q.GRAPH_APPLY:
+            q.build_map(gates, M, pm)
+        g = q.Graph(plan, gates, call, pm, k1_d, out, ws, reps=3)
+        out.zero_()
+        torch.cuda.synchronize()
+        g.launch()
+        g.launch()
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == ref.tobytes(), call
+        if call == q.GRAPH_MAP_GATHER:
+            assert np.array_equal(_perm_np(pm), perm_ref)
+        g.close()
