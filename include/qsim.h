@@ -206,9 +206,14 @@ typedef struct qsim_plan {
     uint32_t chunk_log2;    /* counters per CTA chunk (default 16), within [10, M] */
     int32_t blocks_per_sm;  /* resident CTAs per SM (default 1), 1..8          */
     uint32_t flags;         /* bit 0: natural order (no sigma): set when the state is
-                               L2-resident (<= 64 MB), when natural order already keeps
-                               a line's readers within 2^20 outputs, or when sigma does
-                               not bring them under 2^24                         */
+                               L2-resident (<= 64 MB) or when the sector cover holds
+                               under 1/4 of the sampled pairs (no order helps).
+                               bit 1: the circuit keeps locality -- every target (and
+                               SWAP partner) bit is below T = 13 (complex64) / 12
+                               (complex128), so each aligned tile of 2^T outputs reads
+                               its own tile of k1: map+gather and fused use the
+                               shared-memory staged kernel (TMA bulk copies of k1
+                               tiles, double-buffered), re-checked on the gates given */
     uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
     uint16_t cta_threads;   /* apply kernel CTA size: 256, 512 or 1024 (0 = 256)    */
     uint16_t fused_chunk_log2; /* counters per CTA chunk of the fused kernel (default 16) */

@@ -739,6 +739,17 @@ void plan_pairs(const PlanGate* pg, int n, int M, uint32_t V, qsim_plan* plan) {
   plan->pair_xor = best & ~1u & ~(1u << plan->sigma[5]);
 }
 
+// Bits the walk can change: every target, and the partner bit of a SWAP.
+int moved_bits(const qsim_gate* gates, int32_t n) {
+  int top = 0;
+  for (int32_t k = 0; k < n; ++k) {
+    top = std::max(top, (int)gates[k].target + 1);
+    if (gates[k].kind == 6) top = std::max(top, (int)gates[k].c0 + 1);
+  }
+  return top;
+}
+int local_tile_bits(int32_t dtype) { return dtype == QSIM_C64 ? 13 : 12; }
+
 // bits of the sector cover (counter bits of one L1-resident block of work)
 int plan_cover_bits = 13;
 
@@ -831,6 +842,8 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   // small states are L2-resident: natural order, full parallelism
   if ((1ull << M) * (uint64_t)e <= (64ull << 20)) plan->flags = 1;
   plan->reserved_spread = (uint16_t)(nat | (sig << 8));
+  // locality-keeping circuit: every bit the walk changes lies below the tile
+  if (M >= local_tile_bits(dtype) && moved_bits(gates, n) <= local_tile_bits(dtype)) plan->flags |= 2u;
   // Lane pairs: opt-in (QSIM_PLAN_PAIRS=1).  On cfg5 half the 16-byte pairs
   // match, yet the step is slower: 22.0 vs 20.0 ms map+gather, 19.2 vs
   // 16.0 ms fused (profiles/r01_lane_pairs.txt).
@@ -876,6 +889,24 @@ void launch_apply_sigma(uint32_t ilp, uint32_t threads, int bps, unsigned blocks
   if (ilp == 8) launch_apply_sigma_t<T, 8>(threads, bps, blocks, sp, perm, N, k1, k2, st);
   else if (ilp == 32) launch_apply_sigma_t<T, 32>(threads, bps, blocks, sp, perm, N, k1, k2, st);
   else launch_apply_sigma_t<T, 16>(threads, bps, blocks, sp, perm, N, k1, k2, st);
+}
+
+
+// Locality-keeping circuits (plan flag bit 1, re-checked on the gates given):
+// the shared-memory staged kernel.  True if launched.
+bool local_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
+                    void* k2, uint32_t* perm_out, void* workspace, cudaStream_t st) {
+  const int T = local_tile_bits(plan->dtype);
+  if (!(plan->flags & 2u) || !workspace || plan->M < T || moved_bits(gates, n) > T) return false;
+  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+  pack_gates(gates, n, false, *gl);
+  std::string err;
+  if (qsim::jit_local(gl->w, n, plan->M, elem_bytes(plan->dtype), T, k1, k2, perm_out, sm_count(),
+                      st, err) != 0)
+    return false;
+  ++g_launches;
+  g_last_kernel = "qsim_jit_local";
+  return true;
 }
 
 // A natural-order plan still runs the NVRTC kernels (one pass, the walk in
@@ -1027,6 +1058,7 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
     if (workspace && !aligned16(workspace)) return QSIM_EINVAL;
     if (overlap(k1, (1ull << M) * e, k2, (1ull << M) * e)) return QSIM_EALIAS;
   }
+  if (local_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st)) return QSIM_OK;
   if (plan_natural(plan)) {
     if (workspace && M >= 13) {
       const qsim_plan nat = natural_view(plan);
@@ -1061,6 +1093,7 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e) ||
       overlap(perm, N * 4, k1, N * e))
     return QSIM_EALIAS;
+  if (local_dispatch(plan, gates, n, k1, k2, perm, workspace, st)) return QSIM_OK;
   if (workspace && (!plan_natural(plan) || M >= 13)) {
     const qsim_plan nat = natural_view(plan);
     const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
@@ -1436,6 +1469,12 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
                                     elem_bytes(plan->dtype) == 8 ? plan->pair_xor : 0u,
                                     elem_bytes(plan->dtype), err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
+    return QSIM_ECUDA;
+  }
+  if ((plan->flags & 2u) && qsim::jit_check_compile_local(gl->w, n_gates, plan->M,
+                                                          elem_bytes(plan->dtype),
+                                                          local_tile_bits(plan->dtype), err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit (local tiles): %s", err.c_str());
     return QSIM_ECUDA;
   }
   if ((plan->lin_flags & 1u) &&

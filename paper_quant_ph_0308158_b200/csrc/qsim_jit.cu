@@ -853,6 +853,93 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   return s;
 }
 
+// Circuits that keep locality (every target / SWAP bit below T): each aligned
+// tile of 2^T outputs reads exactly the same tile of k1 (the walk never
+// changes bits >= T).  One CTA per SM streams tiles: a TMA bulk copy
+// (cp.async.bulk, mbarrier completion) brings tile i+1 of k1 into shared
+// memory while the 8 warps walk tile i (planes in registers), read their
+// sources from shared memory and write k2 (and perm) with fully coalesced
+// 256-byte warp stores -- the gather of the north star "staged in shared
+// memory where the circuit keeps locality".
+std::string local_source(const uint32_t* w, int n, int M, int elem, int T) {
+  std::string s = kPrelude;
+  char buf[256];
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_LT %d\ntypedef %s E;\n", M, T,
+                elem == 8 ? "uint2" : "uint4");
+  s += buf;
+  s += R"(
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+extern "C" __global__ void __launch_bounds__(256, 1)
+qsim_jit_local(u64 ntiles, const E* __restrict__ k1, E* __restrict__ k2, u32* __restrict__ perm_out) {
+  extern __shared__ __align__(128) unsigned char lsm[];      // 2 stages x 2^T entries
+  __shared__ __align__(8) u64 bar[2];
+  const u32 tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const u32 TILE = 1u << QSIM_LT, BYTES = (u32)sizeof(E) << QSIM_LT;
+  E* stage0 = reinterpret_cast<E*>(lsm);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&bar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_addr(&bar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](u64 t, u32 st) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 :: "r"(smem_addr(&bar[st])), "r"(BYTES) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(smem_addr(stage0 + st * TILE)), "l"(k1 + (t << QSIM_LT)), "r"(BYTES),
+                    "r"(smem_addr(&bar[st])) : "memory");
+  };
+  if (tid == 0 && (u64)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  u32 i = 0;
+  for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    const u32 st = i & 1u;
+    if (tid == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, st ^ 1u);
+    {
+      const u32 bp = smem_addr(&bar[st]), par = (i >> 1) & 1u;
+      asm volatile("{\n.reg .pred P1;\nLW_%=:\n"
+                   "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                   "@!P1 bra LW_%=;\n}\n" :: "r"(bp), "r"(par) : "memory");
+    }
+    const E* sv = stage0 + st * TILE;
+    for (u32 wt = warp; wt < (TILE >> 10); wt += 8u) {
+      const u64 base = (t << QSIM_LT) | ((u64)wt << 10);
+)";
+  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+  for (int b = 0; b < 32; ++b) {
+    if (b >= M)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
+    else if (b < 5)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (b < 10)
+      std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[b - 5]);
+    else
+      std::snprintf(buf, sizeof buf, "      u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += "      u32 sg = 0u;\n";
+  s += walk_code(w, n, M);
+  s += "      u32 a[32] = {";
+  for (int b = 0; b < 32; ++b) {
+    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+    s += buf;
+  }
+  s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+  s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+  s += R"(
+      if (perm_out) {
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + base + 32u * l + lane, a[l]);
+      }
+      _Pragma("unroll") for (int l = 0; l < 32; ++l)
+        stcs(k2 + base + 32u * l + lane, negate_if(sv[a[l] & (TILE - 1u)], (sg >> l) & 1u));
+    }
+    __syncthreads();   // the stage is refilled two tiles later
+  }
+}
+)";
+  return s;
+}
+
 struct Entry {
   std::vector<uint32_t> words;
   int M;
@@ -1226,6 +1313,57 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
     return -1;
   }
   return 0;
+}
+
+int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,
+              uint32_t* perm_out, int sms, cudaStream_t st, std::string& err) {
+  const int smem = 2 * (elem << T);
+  CUfunction fn = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) {
+      err = g_status;
+      return -1;
+    }
+    std::vector<uint32_t> keyw(words, words + n);
+    keyw.push_back((uint32_t)elem);
+    keyw.push_back((uint32_t)T);
+    const uint64_t kind = 0x6c6f63616cull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+    for (const Entry& e : g_cache[key])
+      if (e.M == M && e.words == keyw) fn = e.fn;
+    if (!fn) {
+      fn = get_kernel_locked(kind, keyw, M, local_source(words, n, M, elem, T), "qsim_jit_local", err);
+      if (!fn) return -1;
+      if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
+        err = "cuFuncSetAttribute(max dynamic smem) failed";
+        return -1;
+      }
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
+    }
+  }
+  uint64_t ntiles = (1ull << M) >> T;
+  uint64_t blocks = (uint64_t)sms;
+  if (blocks > ntiles) blocks = ntiles;
+  void* args[] = {&ntiles, const_cast<void**>(&k1), &k2, &perm_out};
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args,
+                   nullptr) != CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(local_source(words, n, M, elem, T), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,

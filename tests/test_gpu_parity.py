@@ -657,3 +657,54 @@ def test_graphs_replay_planned_calls(q, M, natural):
         if call == q.GRAPH_MAP_GATHER:
             assert np.array_equal(_perm_np(pm), perm_ref)
         g.close()
+
+
+@pytest.mark.parametrize("dtype,M", [("c64", 13), ("c64", 17), ("c64", 22), ("c128", 12),
+                                     ("c128", 19)])
+def test_local_tiles_staged_in_shared_memory(q, M, dtype):
+    """Circuits that keep locality (every target and SWAP bit below the tile,
+    controls anywhere, phase steps included): the plan flags them and the
+    TMA-staged shared-memory kernel runs -- same map and k2 bytes as the
+    oracle; a circuit with one target above the tile does not take it."""
+    T = 13 if dtype == "c64" else 12
+    rng = np.random.default_rng(M + T)
+    rows = []
+    for _ in range(70):
+        kind = int(rng.integers(7))
+        nc = 1 if kind == 6 else kind % 3
+        t = int(rng.integers(T))
+        others = [b for b in range(M) if b != t] if kind != 6 else [b for b in range(T) if b != t]
+        cs = rng.choice(others, size=nc, replace=False)
+        rows.append(wl.gate(kind, t, *[int(c) for c in cs]))
+    gates = wl.gates_array(rows)
+    k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 30 + M))
+    perm_ref, signs_ref = oracle.build_map_signed(gates, M)
+    ref = oracle.apply_map_signed(perm_ref, signs_ref, k1)
+    plain = np.ascontiguousarray(gates[(gates[:, 0] < 3) | (gates[:, 0] == 6)])
+    perm_plain = oracle.build_map(plain, M)
+    ref_plain = oracle.apply_map(perm_plain, k1)
+    k1_d = _to_dev(k1)
+    plan = q.plan_create(gates, M, dtype)
+    assert plan.flags & 2
+    out = torch.empty_like(k1_d)
+    q.run_fused_planned(plan, gates, k1_d, out, q.workspace())
+    assert q.last_kernel() == "qsim_jit_local"
+    pm, out2 = _new_perm(1 << M), torch.empty_like(k1_d)
+    q.map_gather_planned(q.plan_create(plain, M, dtype), plain, pm, k1_d, out2, q.workspace())
+    assert q.last_kernel() == "qsim_jit_local"
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == ref.tobytes()
+    assert out2.cpu().numpy().tobytes() == ref_plain.tobytes()
+    assert np.array_equal(_perm_np(pm), perm_plain)
+    # a target above the tile: the plan is not local and the generic kernels run
+    if M == T:
+        return
+    far = np.concatenate([plain, wl.gates_array([wl.gate(wl.CNOT, M - 1, 0)])])
+    plan_far = q.plan_create(far, M, dtype)
+    assert not (plan_far.flags & 2)
+    plan.flags |= 2                                   # a stale plan: re-checked on the gates
+    out3 = torch.empty_like(k1_d)
+    q.run_fused_planned(plan, far, k1_d, out3, q.workspace())
+    assert q.last_kernel() != "qsim_jit_local"
+    torch.cuda.synchronize()
+    assert out3.cpu().numpy().tobytes() == oracle.apply_map(oracle.build_map(far, M), k1).tobytes()

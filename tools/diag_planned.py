@@ -1,7 +1,8 @@
 """Time the planned calls call by call (the first call includes NVRTC compile).
 
     python tools/diag_planned.py CFG MODE [key=value ...]
-      CFG   cfg1..cfg5 or rand:M (64 random gates over M bits, seed 4)
+      CFG   cfg1..cfg5, rand:M (64 random gates over M bits, seed 4), low:B / high:B
+            (M = 32, 64 random gates on bits < B / >= B)
       MODE  fused | map_gather | apply
       keys  order=plan|natural|sigma (sigma forces the plan's order),
             chunk=<log2>, bps=<blocks per SM>, T=<cover bits, informational>
@@ -20,6 +21,19 @@ kv = dict(a.split("=") for a in sys.argv[3:])
 if name.startswith("rand:"):
     M = int(name[5:])
     g, dtype = wl.random_gates(64, M, 4), "c64"
+elif name.startswith("low:") or name.startswith("high:"):
+    # M=32 circuits that keep locality: every gate on bits < B (low:B) or >= B (high:B)
+    kind, B = name.split(":")
+    M, dtype = 32, "c64"
+    bits = list(range(int(B))) if kind == "low" else list(range(int(B), 32))
+    import numpy as np
+    rng = np.random.default_rng(11)
+    rows = []
+    for _ in range(64):
+        k = int(rng.integers(3))
+        b = rng.choice(bits, size=1 + k, replace=False)
+        rows.append(wl.gate(k, int(b[0]), *[int(x) for x in b[1:]]))
+    g = wl.gates_array(rows)
 else:
     cfg = wl.CONFIGS[name]
     g, M, dtype = cfg.gates(), cfg.M, cfg.dtype

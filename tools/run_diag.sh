@@ -1,3 +1,4 @@
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1
-timeout 600 python tools/all_configs.py > gpurun_out/all_configs2.jsonl 2>&1
-timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bench_lb.json 2> gpurun_out/bench_lb.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "local or structured or planned" > gpurun_out/pytest_local.log 2>&1
+{
+for c in low:10 low:13; do for m in map_gather fused; do python tools/diag_planned.py $c $m | tail -1; done; done
+} > gpurun_out/diag18.log 2>&1
