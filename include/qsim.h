@@ -254,6 +254,19 @@ typedef struct qsim_plan {
 int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
                      qsim_plan *plan);
 
+/* qsim_plan_tune -- measure plan variants for this circuit on the caller's
+ * buffers (like an FFTW_MEASURE plan) and keep the fastest map + gather:
+ * the default cover rule and the full 13-bit cover, each with and without
+ * lanes on output bits 0..4, and full covers of 11 and 12 bits (distinct
+ * orders only).  Each variant runs qsim_map_gather_planned three times (the
+ * first compiles its kernel), so perm and k2 hold a valid result afterwards;
+ * the call synchronises `stream`.  plan: in (chunk sizes, residency kept) /
+ * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
+ * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit).
+ * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */
+int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
+                   const void *k1, void *k2, void *workspace, void *stream, int32_t *chosen);
+
 /* qsim_apply_map_planned -- qsim_apply_map (the same k2, bit for bit) in the
  * traversal order of `plan` (M and dtype are plan->M, plan->dtype).
  *   workspace  device scratch of QSIM_WORKSPACE_BYTES (16-B aligned), reset

@@ -86,6 +86,8 @@ def _load() -> ctypes.CDLL:
     sig["qsim_graph_create"] = [ctypes.POINTER(Plan), vp, i32, i32, vp, vp, vp, vp, i32,
                                 ctypes.POINTER(vp)]
     sig["qsim_graph_launch"] = [vp, vp]
+    sig["qsim_plan_tune"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp, vp,
+                             ctypes.POINTER(i32)]
     sig["qsim_graph_destroy"] = [vp]
     sig["qsim_apply_map_signed"] = [vp, vp, u64, i32, i32, vp, vp, vp]
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
@@ -279,6 +281,17 @@ def plan_create(gates, M: int, dtype="c64") -> Plan:
     _check(_lib.qsim_plan_create(gp, n, M, _dtype_code(dtype), ctypes.byref(plan)),
            "qsim_plan_create")
     return plan
+
+
+def plan_tune(plan: Plan, gates, perm, k1, k2, workspace, stream=None) -> int:
+    """Measure plan variants on these buffers and keep the fastest map + gather
+    in `plan` (returns the variant index; see qsim_plan_tune)."""
+    g, gp, n = _gates(gates)
+    chosen = ctypes.c_int32(-1)
+    _check(_lib.qsim_plan_tune(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
+                               _ptr(workspace), _stream(stream), ctypes.byref(chosen)),
+           "qsim_plan_tune")
+    return chosen.value
 
 
 def apply_map_planned(plan: Plan, perm, k1, k2, workspace=None, stream=None) -> None:

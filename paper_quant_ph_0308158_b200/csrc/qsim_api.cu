@@ -621,6 +621,38 @@ uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, q
   return V;
 }
 
+// Cover size: the smallest T in [10, Tmax] whose greedy cover holds >= 90 %
+// of the sampled pairs, else the T with the best containment (smallest on
+// ties) -- cover bits beyond what the pairs need cost more than they bring
+// (M = 32 seeds 4 / 7 / 8: profiles/r01_cover_size.txt).
+uint32_t plan_choose_cover(const PlanGate* pg, int n, int M, int dtype, int Tmax, bool fixed,
+                           qsim_plan* plan, std::vector<uint32_t>* top_patterns) {
+  const int lo = fixed ? Tmax : std::min(10, Tmax);
+  uint32_t best_v = 0;
+  float best_c = -1.0f;
+  int best_t = Tmax;
+  for (int T = lo; T <= Tmax; ++T) {
+    std::vector<uint32_t> pats;
+    const uint32_t V = plan_sector_cover(pg, n, M, dtype, T, plan, T == Tmax ? top_patterns : &pats);
+    const float c = plan->tile_contained;
+    if (c >= 0.9f) {
+      best_v = V;
+      best_c = c;
+      best_t = T;
+      if (T != Tmax && top_patterns) plan_sector_cover(pg, n, M, dtype, Tmax, plan, top_patterns);
+      break;
+    }
+    if (c > best_c + 1e-6f) {
+      best_v = V;
+      best_c = c;
+      best_t = T;
+    }
+  }
+  plan->tile_contained = best_c;
+  plan->tile_log2 = (uint8_t)best_t;
+  return best_v;
+}
+
 // Sampled distinct k1 sectors per warp load when the 32 lanes' outputs are
 // base ^ span(vecs) (averaged over fixed pseudo-random bases), per lane.
 double plan_lane_score(const PlanGate* pg, int n, int M, const std::vector<uint32_t>& vecs) {
@@ -750,10 +782,24 @@ int moved_bits(const qsim_gate* gates, int32_t n) {
 }
 int local_tile_bits(int32_t dtype) { return dtype == QSIM_C64 ? 13 : 12; }
 
-// bits of the sector cover (counter bits of one L1-resident block of work)
-int plan_cover_bits = 13;
+// Plan construction options (qsim_plan_create uses the defaults, with the
+// QSIM_PLAN_* environment switches; qsim_plan_tune measures variants).
+struct PlanOpts {
+  int cover_bits = 13;    // largest sector cover (counter bits of one L1-resident block)
+  bool fixed = false;     // always cover_bits (else the smallest cover holding >= 90 %)
+  bool lane_run = false;  // lanes on output bits 0..4 (bits 3, 4 added to the cover)
+};
 
-int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan) {
+PlanOpts default_plan_opts() {
+  PlanOpts o;
+  if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) o.cover_bits = std::atoi(cb);
+  if (const char* fx = std::getenv("QSIM_PLAN_COVER_FIXED")) o.fixed = fx[0] == '1';
+  if (const char* lr = std::getenv("QSIM_PLAN_LANE_RUN")) o.lane_run = lr[0] == '1';
+  return o;
+}
+
+int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan,
+              const PlanOpts& opts = default_plan_opts()) {
   std::memset(plan, 0, sizeof *plan);
   plan->M = M;
   plan->dtype = dtype;
@@ -805,11 +851,10 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   // first), so the readers of a k1 sector are handled by one CTA close in time
   // (its L1 serves them); then the other bits by how often a k1 line's readers
   // differ in them (the chunk front keeps its lines in L2)
-  int cover = plan_cover_bits;
-  if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) cover = std::atoi(cb);  // tuning
-  const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(cover, 20)));
+  const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(opts.cover_bits, 20)));
   std::vector<uint32_t> pats;
-  const uint32_t V = plan_sector_cover(pg.get(), n, M, dtype, T, plan, &pats);
+  uint32_t V = plan_choose_cover(pg.get(), n, M, dtype, T, opts.fixed, plan, &pats);
+  if (opts.lane_run && M >= 5) V |= 31u;  // lanes on output bits 0..4: 256-byte warp stores
   int order[32], m = 0, k = 0;
   for (int b = 0; b < M; ++b) {
     if ((V >> b) & 1u)
@@ -1361,6 +1406,86 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
   if (ce != cudaSuccess) return cuda_fail(ce, "qsim_run_host_batch");
   if (ce2 != cudaSuccess) return cuda_fail(ce2, "qsim_run_host_batch sync");
   g_launches = launches;
+  return QSIM_OK;
+}
+
+int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
+                   const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
+  g_launches = 0;
+  if (!plan || !workspace) return QSIM_EINVAL;
+  int rc = plan_validate(plan);
+  if (rc) return rc;
+  if ((rc = check_gates(gates, n_gates, plan->M))) return rc;
+  if (has_phase(gates, n_gates)) return QSIM_EINVAL;  // tunes the map + gather step
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // candidates: the default rule, the full cover, each with lanes on output bits 0..4,
+  // and smaller full covers
+  const PlanOpts base = default_plan_opts();
+  std::vector<PlanOpts> opts;
+  for (int fixed = 0; fixed < 2; ++fixed)
+    for (int run = 0; run < 2; ++run) {
+      PlanOpts o = base;
+      o.fixed = fixed != 0;
+      o.lane_run = run != 0;
+      opts.push_back(o);
+    }
+  for (int T = base.cover_bits - 2; T < base.cover_bits; ++T) {
+    PlanOpts o = base;
+    o.cover_bits = T;
+    o.fixed = true;
+    opts.push_back(o);
+  }
+  std::vector<qsim_plan> cands;
+  std::vector<int> idx;
+  for (size_t i = 0; i < opts.size(); ++i) {
+    qsim_plan p;
+    if ((rc = plan_fill(gates, n_gates, plan->M, plan->dtype, &p, opts[i]))) return rc;
+    p.chunk_log2 = plan->chunk_log2;
+    p.fused_chunk_log2 = plan->fused_chunk_log2;
+    p.blocks_per_sm = plan->blocks_per_sm;
+    bool dup = false;
+    for (const qsim_plan& c : cands)
+      dup = dup || (std::memcmp(c.sigma, p.sigma, 32) == 0 && c.flags == p.flags);
+    if (!dup) {
+      cands.push_back(p);
+      idx.push_back((int)i);
+    }
+  }
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaError_t ce;
+  if ((ce = cudaEventCreate(&a)) != cudaSuccess || (ce = cudaEventCreate(&b)) != cudaSuccess) {
+    if (a) cudaEventDestroy(a);
+    return cuda_fail(ce, "event create");
+  }
+  float best = 1e30f;
+  int best_i = -1;
+  for (size_t i = 0; i < cands.size() && rc == QSIM_OK; ++i) {
+    // one untimed call (compiles the kernel), then the best of two
+    rc = map_gather_impl(&cands[i], gates, n_gates, perm, k1, k2, workspace, st);
+    float t_best = 1e30f;
+    for (int r = 0; r < 2 && rc == QSIM_OK; ++r) {
+      cudaEventRecord(a, st);
+      rc = map_gather_impl(&cands[i], gates, n_gates, perm, k1, k2, workspace, st);
+      cudaEventRecord(b, st);
+      if ((ce = cudaEventSynchronize(b)) != cudaSuccess) {
+        rc = cuda_fail(ce, "tune sync");
+        break;
+      }
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, a, b);
+      t_best = std::min(t_best, ms);
+    }
+    if (rc == QSIM_OK && t_best < best) {
+      best = t_best;
+      best_i = (int)i;
+    }
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (rc) return rc;
+  *plan = cands[best_i];
+  if (chosen) *chosen = idx[best_i];
+  g_launches = 0;
   return QSIM_OK;
 }
 

@@ -708,3 +708,26 @@ def test_local_tiles_staged_in_shared_memory(q, M, dtype):
     assert q.last_kernel() != "qsim_jit_local"
     torch.cuda.synchronize()
     assert out3.cpu().numpy().tobytes() == oracle.apply_map(oracle.build_map(far, M), k1).tobytes()
+
+
+def test_plan_tune_keeps_a_valid_plan(q):
+    """qsim_plan_tune measures plan variants and keeps one: the result of its
+    own runs and of the tuned plan afterwards equal the oracle's bytes."""
+    M = 20
+    gates = wl.random_gates(64, M, 8)
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 8))
+    perm_ref = oracle.build_map(gates, M)
+    ref = oracle.apply_map(perm_ref, k1)
+    k1_d = _to_dev(k1)
+    plan = q.plan_create(gates, M, "c64")
+    plan.flags &= ~1
+    pm, out = _new_perm(1 << M), torch.empty_like(k1_d)
+    chosen = q.plan_tune(plan, gates, pm, k1_d, out, q.workspace())
+    assert 0 <= chosen <= 5
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == ref.tobytes()
+    assert np.array_equal(_perm_np(pm), perm_ref)
+    out2 = torch.empty_like(k1_d)
+    q.run_fused_planned(plan, gates, k1_d, out2, q.workspace())
+    torch.cuda.synchronize()
+    assert out2.cpu().numpy().tobytes() == ref.tobytes()

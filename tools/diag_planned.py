@@ -1,7 +1,8 @@
 """Time the planned calls call by call (the first call includes NVRTC compile).
 
     python tools/diag_planned.py CFG MODE [key=value ...]
-      CFG   cfg1..cfg5, rand:M (64 random gates over M bits, seed 4), low:B / high:B
+      CFG   cfg1..cfg5, rand:M (64 random gates over M bits, seed 4), seed:S (M = 32,
+            64 random gates, seed S), low:B / high:B
             (M = 32, 64 random gates on bits < B / >= B)
       MODE  fused | map_gather | apply
       keys  order=plan|natural|sigma (sigma forces the plan's order),
@@ -21,6 +22,9 @@ kv = dict(a.split("=") for a in sys.argv[3:])
 if name.startswith("rand:"):
     M = int(name[5:])
     g, dtype = wl.random_gates(64, M, 4), "c64"
+elif name.startswith("seed:"):
+    M, dtype = 32, "c64"
+    g = wl.random_gates(64, 32, int(name[5:]))
 elif name.startswith("low:") or name.startswith("high:"):
     # M=32 circuits that keep locality: every gate on bits < B (low:B) or >= B (high:B)
     kind, B = name.split(":")

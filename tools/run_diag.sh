@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "local or structured or planned" > gpurun_out/pytest_local.log 2>&1
-{
-for c in low:10 low:13; do for m in map_gather fused; do python tools/diag_planned.py $c $m | tail -1; done; done
-} > gpurun_out/diag18.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "tune" > gpurun_out/pytest_tune.log 2>&1
+timeout 1200 python tools/seed_sweep.py --M 32 --seeds 4,5,6,7,8,9 --tune > gpurun_out/seed32t.csv 2>&1
+timeout 900 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/bench_t.json 2> gpurun_out/bench_t.err
