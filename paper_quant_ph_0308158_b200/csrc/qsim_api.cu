@@ -1480,6 +1480,32 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       best_i = (int)i;
     }
   }
+  // second stage: the chunk size of the kept order (2^14 / 2^16 next to 2^15)
+  qsim_plan kept = cands[best_i];
+  const uint32_t c0 = kept.fused_chunk_log2;
+  for (int d = -1; d <= 1 && rc == QSIM_OK; d += 2) {
+    const int cl = (int)c0 + d;
+    if (cl < 10 || cl > kept.M || ((1ull << kept.M) >> cl) < (uint64_t)sm_count()) continue;
+    qsim_plan p = kept;
+    p.chunk_log2 = p.fused_chunk_log2 = (uint32_t)cl;
+    float t_best = 1e30f;
+    for (int r = 0; r < 2 && rc == QSIM_OK; ++r) {
+      cudaEventRecord(a, st);
+      rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st);
+      cudaEventRecord(b, st);
+      if ((ce = cudaEventSynchronize(b)) != cudaSuccess) {
+        rc = cuda_fail(ce, "tune sync");
+        break;
+      }
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, a, b);
+      t_best = std::min(t_best, ms);
+    }
+    if (rc == QSIM_OK && t_best < best * 0.99f) {  // only a clear win moves it
+      best = t_best;
+      cands[best_i] = p;
+    }
+  }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   if (rc) return rc;
