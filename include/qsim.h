@@ -397,6 +397,8 @@ int qsim_jit_check_compile_kron(const qsim_gate *gates, int32_t n_gates, int32_t
                                 int32_t dtype);
 int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
                                    int32_t n_gates);
+/* ABI version of this header / library: 6 (plans with the sector cover,
+ * phase / SWAP gates, M > 32 on-the-fly input, batch e2e, graphs, tuning).  */
 int32_t qsim_abi_version(void);
 
 #ifdef __cplusplus

@@ -1680,6 +1680,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 5; }
+int32_t qsim_abi_version(void) { return 6; }
 
 }  // extern "C"
