@@ -372,6 +372,20 @@ def _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d):
         assert np.array_equal(got, want)
 
 
+def _multiset_hash(t, chunk=1 << 28):
+    """Order-independent hash of a state's entries (as 8-byte words): the sum of
+    a mixing function, mod 2^64 -- equal for k1 and k2 when k2 is a permutation
+    of k1's entries (U is a permutation, the norm is kept)."""
+    w = t.view(torch.int64)
+    h = torch.zeros((), dtype=torch.int64, device=w.device)
+    for s0 in range(0, w.numel(), chunk):
+        x = w[s0:s0 + chunk]
+        y = (x ^ (x >> 31)) * 0x7FB5D329728EA185
+        y = (y ^ (y >> 27)) * 0x5A8D3F2B1C4E6F9B
+        h = h + (y ^ (y >> 33)).sum()
+    return int(h.item())
+
+
 def _full_config(q, name, fused):
     cfg = wl.CONFIGS[name]
     gates = cfg.gates()
@@ -388,6 +402,8 @@ def _full_config(q, name, fused):
         q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype=cfg.dtype)
     torch.cuda.synchronize()
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d)
+    if cfg.dtype == "c64":                      # the multiset of entries is kept
+        assert _multiset_hash(k1_d) == _multiset_hash(k2_d)
     if fused:
         assert torch.equal(k2_d, k2f_d)          # materialised == fused, every byte
     # the planned (sigma-ordered) calls bench.py times: same bytes
@@ -447,6 +463,7 @@ def test_cfg5_full_size_sampled(q):
     q.apply_map_planned(plan, perm_d, k1_d, k2_d, ws)       # the bench's launch config
     torch.cuda.synchronize()
     _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, None)
+    assert _multiset_hash(k1_d) == _multiset_hash(k2_d)    # a permutation of k1
     # every other path == the planned apply over all 2^32 entries (on device)
     k2f_d = torch.empty_like(k2_d)
     pm = torch.empty_like(perm_d)
