@@ -757,20 +757,36 @@ qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ 
   return s;
 }
 
-// Natural-order fused walk with the input generated on the fly (Appendix 1,
-// P:L81-L89): k2_out[out - start] = k1(perm(out)) from tables of qubit
-// products, ng groups of gb address bits (same arithmetic and order as
+// Fused walk with the input generated on the fly (Appendix 1):
+// k2_out[out - start] = k1(perm(out)) from tables of qubit products, ng
+// groups of gb table positions (same arithmetic and order as
 // qsim_kernels.cuh kron_tables / kron_element: each complex product
-// re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br)).  M > 32 (64-bit addresses; SURVEY 8f NEXT(2),
-// "continuous portions"): 64 planes and two 32x32 transposes (low and
-// high address words).
-std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int ng) {
+// re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br)); table position k holds
+// address bit pos[k] of the source.  M > 32 (64-bit addresses; SURVEY 8f
+// NEXT(2), "continuous portions"): 64 planes.
+//
+// Traversal (the layout, chosen on the host by kron_layout): a warp tile is
+// 1024 outputs = lanes on output bits 0..4 x the 32 bit positions of each
+// plane on output bits J[0..4]; tiles enumerate the other bits, 2^(L-10)
+// tiles per aligned block of 2^L outputs.  Stores stay 256-byte warp runs.
+// Fast path (nv > 0): when every source bit at table positions >= nv is
+// constant across a thread's 32 entries (checked per warp tile; the host
+// picked J so that it nearly always is), the product of groups ng-1..1 is
+// formed once per thread and each entry takes one lookup and one complex
+// product: cmul(C, T_0[x]) -- the same operations, in the same order, as the
+// general path, so both give identical bytes.
+std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int ng,
+                        const uint8_t* pos, const uint8_t* J, int L, int nv) {
   std::string s = kPrelude;
-  char buf[256];
+  char buf[320];
   const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M,
-                gb, ng);
+  std::snprintf(buf, sizeof buf,
+                "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n#define QSIM_L %d\n"
+                "#define QSIM_OFF(l) (((l) & 1 ? 1ull << %d : 0ull) | ((l) & 2 ? 1ull << %d : 0ull) | "
+                "((l) & 4 ? 1ull << %d : 0ull) | ((l) & 8 ? 1ull << %d : 0ull) | "
+                "((l) & 16 ? 1ull << %d : 0ull))\n",
+                M, gb, ng, L, J[0], J[1], J[2], J[3], J[4]);
   s += buf;
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
@@ -782,7 +798,7 @@ __device__ __forceinline__ C cmul(C a, C b) {
                       __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x))); }
 )";
   s += R"(
-struct Qubits { double v[64][4]; u32 M, gbits, ngroups; };
+struct Qubits { double v[64][4]; u32 M, gbits, ngroups; unsigned char pos[64]; u32 permuted; };
 extern "C" __global__ void __launch_bounds__(256)
 qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) {
   extern __shared__ __align__(16) unsigned char kt_smem[];
@@ -791,9 +807,9 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     const int g = x >> QSIM_GB, v = x & ((1 << QSIM_GB) - 1);
     C acc; bool first = true;
     for (int j = QSIM_GB - 1; j >= 0; --j) {
-      const int b = QSIM_GB * g + j;
-      if (b >= QSIM_M) continue;
-      const int bit = (v >> j) & 1;
+      const int k = QSIM_GB * g + j;
+      if (k >= QSIM_M) continue;
+      const int b = q.pos[k], bit = (v >> j) & 1;
       C f; f.x = (R)q.v[b][2 * bit]; f.y = (R)q.v[b][2 * bit + 1];
       acc = first ? f : cmul(acc, f);
       first = false;
@@ -804,29 +820,101 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
-    const u64 base = tile << 10;
+    u64 base = tile << 5;
 )";
+  // insert a zero at each in-thread output bit (ascending): base = the tile's
+  // output with lane and J bits clear
+  int Js[5];
+  for (int k = 0; k < 5; ++k) Js[k] = J[k];
+  for (int k = 0; k < 5; ++k) {
+    std::snprintf(buf, sizeof buf,
+                  "    base = (base & 0x%llxull) | ((base >> %d) << %d);\n",
+                  (unsigned long long)((1ull << Js[k]) - 1), Js[k], Js[k] + 1);
+    s += buf;
+  }
   const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
   const int np = wide ? 64 : 32;
   for (int b = 0; b < np; ++b) {
+    int jk = -1;
+    for (int k = 0; k < 5; ++k)
+      if (Js[k] == b) jk = k;
     if (b >= M)
       std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
     else if (b < 5)
       std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (b < 10)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
+    else if (jk >= 0)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[jk]);
     else
       std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
     s += buf;
   }
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
+  s += R"(
+    const u64 blk = base >> QSIM_L;
+    const bool full = (blk << QSIM_L) >= start && ((blk + 1ull) << QSIM_L) <= end;
+)";
+  auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
+  // 32 entries, stores hoisted out of the range test for whole blocks
+  auto entries = [&](const char* value, const char* ind) {
+    std::string e;
+    e += std::string(ind) + "C* const kq = k2 + (base + lane - start);\n";
+    e += std::string(ind) + "if (full) {\n";
+    e += std::string(ind) + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+    e += std::string(ind) + "    " + value + "\n";
+    e += std::string(ind) + "    __stcs(kq + QSIM_OFF(l), rv);\n";
+    e += std::string(ind) + "  }\n";
+    e += std::string(ind) + "} else {\n";
+    e += std::string(ind) + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+    e += std::string(ind) + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
+    e += std::string(ind) + "    if (addr >= start && addr < end) {\n";
+    e += std::string(ind) + "      " + value + "\n";
+    e += std::string(ind) + "      __stcs(kq + QSIM_OFF(l), rv);\n";
+    e += std::string(ind) + "    }\n";
+    e += std::string(ind) + "  }\n";
+    e += std::string(ind) + "}\n";
+    return e;
+  };
+  if (nv > 0 && ng >= 2) {
+    s += "    u32 un = 0u;\n";
+    for (int k = nv; k < M; ++k) {
+      std::snprintf(buf, sizeof buf, "    un |= %s ^ (0u - (%s & 1u));\n", P(k).c_str(), P(k).c_str());
+      s += buf;
+    }
+    s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n";
+    for (int g = 0; g < ng; ++g) {
+      std::snprintf(buf, sizeof buf, "      u32 i%d = 0u;\n", g);
+      s += buf;
+      for (int j = 0; j < gb; ++j) {
+        const int k = gb * g + j;
+        if (k >= M || k < nv) continue;
+        std::snprintf(buf, sizeof buf, "      i%d |= %s & 0x%xu;\n", g, P(k).c_str(), 1u << j);
+        s += buf;
+      }
+    }
+    std::snprintf(buf, sizeof buf, "      C cc = T[%d | i%d];\n", (ng - 1) << gb, ng - 1);
+    s += buf;
+    for (int g = ng - 2; g >= 1; --g) {
+      std::snprintf(buf, sizeof buf, "      cc = cmul(cc, T[%d | i%d]);\n", g << gb, g);
+      s += buf;
+    }
+    s += "      u32 a[32] = {";
+    for (int k = 0; k < 32; ++k) {
+      s += k < nv ? P(k) : std::string("0u");
+      s += k < 31 ? ", " : "};\n";
+    }
+    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+    s += entries("const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += "      continue;\n    }\n";
+  }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
     s += buf;
     for (int b = 0; b < 32; ++b) {
-      std::snprintf(buf, sizeof buf, "p%d%s", 32 * h + b, b < 31 ? ", " : "};\n");
-      s += buf;
+      const int k = 32 * h + b;
+      s += k < M ? P(k) : std::string("0u");
+      s += b < 31 ? ", " : "};\n";
     }
     std::snprintf(buf, sizeof buf,
                   "    QSIM_TS(16, 0x0000ffffu, a%d) QSIM_TS(8, 0x00ff00ffu, a%d) "
@@ -836,20 +924,17 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   }
   s += wide ? "#define QSIM_SRC(l) (((u64)a1[l] << 32) | a0[l])\n"
             : "#define QSIM_SRC(l) ((u64)a0[l])\n";
-  s += R"(
-    const bool full = base >= start && base + 1024u <= end;
-    const u64 gm = (1ull << QSIM_GB) - 1;
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u64 sv = QSIM_SRC(l);
-      C r = T[((QSIM_NG - 1) << QSIM_GB) | ((sv >> (QSIM_GB * (QSIM_NG - 1))) & gm)];
-      _Pragma("unroll") for (int g = QSIM_NG - 2; g >= 0; --g)
-        r = cmul(r, T[(g << QSIM_GB) | ((sv >> (QSIM_GB * g)) & gm)]);
-      const u64 addr = base + 32u * l + lane;
-      if (full || (addr >= start && addr < end)) __stcs(k2 + (addr - start), negate_if(r, (sg >> l) & 1u));
-    }
+  s += "    const u64 gm = (1ull << QSIM_GB) - 1;\n";
+  std::string gen = "const u64 sv = QSIM_SRC(l);";
+  std::snprintf(buf, sizeof buf, " C r = T[%d | ((sv >> %d) & gm)];", (ng - 1) << gb, gb * (ng - 1));
+  gen += buf;
+  for (int g = ng - 2; g >= 0; --g) {
+    std::snprintf(buf, sizeof buf, " r = cmul(r, T[%d | ((sv >> %d) & gm)]);", g << gb, gb * g);
+    gen += buf;
   }
-}
-)";
+  gen += " const C rv = negate_if(r, (sg >> l) & 1u);";
+  s += entries(gen.c_str(), "    ");
+  s += "  }\n}\n";
   return s;
 }
 
@@ -1214,8 +1299,9 @@ int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32
 }
 
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
-             int elem, int gbits, int ngroups, uint64_t start, uint64_t count, void* k2_out,
-             int sms, cudaStream_t st, std::string& err) {
+             int elem, int gbits, int ngroups, const uint8_t* pos, const uint8_t* J, int L, int nv,
+             uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
+             std::string& err) {
   const int smem = (ngroups << gbits) * (elem == 8 ? 8 : 16);
   CUfunction fn = nullptr;
   {
@@ -1229,12 +1315,16 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     keyw.push_back((uint32_t)elem);
     keyw.push_back((uint32_t)gbits);
     keyw.push_back((uint32_t)ngroups);
+    for (int k = 0; k < M; ++k) keyw.push_back(pos[k]);
+    for (int k = 0; k < 5; ++k) keyw.push_back(J[k]);
+    keyw.push_back((uint32_t)L);
+    keyw.push_back((uint32_t)nv);
     const uint64_t kind = 0x6b726f6eull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn) {
-      fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem, gbits, ngroups),
+      fn = get_kernel_locked(kind, keyw, M, kron_source(words, n, M, elem, gbits, ngroups, pos, J, L, nv),
                              "qsim_jit_kron", err);
       if (!fn) return -1;
       // write-only: shared memory for the tables of several resident CTAs
@@ -1247,11 +1337,12 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     }
   }
   if (count == 0) return 0;
-  uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  // whole blocks of 2^L outputs (the tiles of a block interleave its outputs)
+  uint64_t end = start + count;
+  uint64_t tb = (start >> L) << (L - 10), te = ((end + (1ull << L) - 1) >> L) << (L - 10);
   uint64_t blocks = (te - tb + 7) / 8;
   const uint64_t cap = (uint64_t)sms * 8;
   if (blocks > cap) blocks = cap;
-  uint64_t end = start + count;
   (void)qbytes;
   void* args[] = {&start, &end, &tb, &te, const_cast<void*>(qubits_struct), &k2_out};
   if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args,
@@ -1263,7 +1354,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
 }
 
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
-                           std::string& err) {
+                           const uint8_t* pos, const uint8_t* J, int L, int nv, std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nvrtc.ok) {
@@ -1271,7 +1362,8 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gb
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(kron_source(words, n, M, elem, gbits, ngroups), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(kron_source(words, n, M, elem, gbits, ngroups, pos, J, L, nv), cubin,
+                              err) ? 0 : -1;
 }
 
 // The planned apply from a materialised map: the fused kernel's traversal and

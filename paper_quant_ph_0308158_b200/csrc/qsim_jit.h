@@ -28,11 +28,16 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
 // k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
 // qsim::Qubits (passed by value as a kernel parameter).
+// Layout (host-chosen, kron_layout in qsim_api.cu): pos[k] = address bit at
+// table position k; J[0..4] = output bits walked inside a thread (ascending);
+// tiles fill aligned blocks of 2^L outputs; nv > 0 enables the per-thread
+// hoisted product (source bits at positions >= nv constant in a thread).
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
-             int elem, int gbits, int ngroups, uint64_t start, uint64_t count, void* k2_out,
-             int sms, cudaStream_t st, std::string& err);
+             int elem, int gbits, int ngroups, const uint8_t* pos, const uint8_t* J, int L, int nv,
+             uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
+             std::string& err);
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
-                           std::string& err);
+                           const uint8_t* pos, const uint8_t* J, int L, int nv, std::string& err);
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,
                             uint32_t pair_xor, int elem,
                             std::string& err);

@@ -434,11 +434,18 @@ k_fused_sigma(const __grid_constant__ GateList<CAP> g, const __grid_constant__ S
 // Kronecker order), and k1(s) = ((T_{ng-1} T_{ng-2}) ...) T_0, evaluated in
 // the state precision, each complex product as re = fma(ar, br, -(ai*bi)),
 // im = fma(ar, bi, ai*br) (error <= 2u per product; M - 1 products).
+// The tables index bits of s in a chosen order (the layout, kron_layout in
+// qsim_api.cu): table position k holds address bit pos[k] (identity unless
+// permuted), so group g covers the bits pos[gb*g .. gb*g + gb - 1].  The
+// product is the same set of factors in another grouping; every kernel of
+// one call uses the same layout (identical bytes across kernels).
 struct Qubits {
   double v[64][4];  // qubit j (1-based) at v[j-1]: re q(0), im q(0), re q(1), im q(1)
   uint32_t M;
   uint32_t gbits;   // bits per group
   uint32_t ngroups;
+  uint8_t pos[64];  // table position -> address bit
+  uint32_t permuted;
 };
 
 __device__ __forceinline__ float2 cmul_rn(float2 a, float2 b) {
@@ -465,10 +472,10 @@ __device__ __forceinline__ void kron_tables(const Qubits& q, C* T) {
     const int g = x >> gb, v = x & ((1 << gb) - 1);
     C acc = cmake<C>(1.0, 0.0);
     bool first = true;
-    for (int j = gb - 1; j >= 0; --j) {  // qubit index gb*g + j (0-based), descending
-      const int b = gb * g + j;
-      if (b >= (int)q.M) continue;
-      const int bit = (v >> j) & 1;
+    for (int j = gb - 1; j >= 0; --j) {  // table position gb*g + j, descending
+      const int k = gb * g + j;
+      if (k >= (int)q.M) continue;
+      const int b = q.pos[k], bit = (v >> j) & 1;
       const C f = cmake<C>(q.v[b][2 * bit], q.v[b][2 * bit + 1]);
       acc = first ? f : cmul_rn(acc, f);
       first = false;
@@ -478,7 +485,13 @@ __device__ __forceinline__ void kron_tables(const Qubits& q, C* T) {
 }
 
 template <typename C>
-__device__ __forceinline__ C kron_element(const C* T, uint64_t s, uint32_t gb, uint32_t ng) {
+__device__ __forceinline__ C kron_element(const C* T, uint64_t s, const Qubits& q) {
+  const uint32_t gb = q.gbits, ng = q.ngroups;
+  if (q.permuted) {  // address bits to table positions
+    uint64_t sp = 0;
+    for (uint32_t k = 0; k < q.M; ++k) sp |= ((s >> q.pos[k]) & 1ull) << k;
+    s = sp;
+  }
   const uint64_t mask = (1ull << gb) - 1;
   C r = T[((ng - 1) << gb) | ((s >> (gb * (ng - 1))) & mask)];
   for (int g = (int)ng - 2; g >= 0; --g) r = cmul_rn(r, T[((uint32_t)g << gb) | ((s >> (gb * g)) & mask)]);
@@ -515,7 +528,7 @@ k_fused_kron_bitsliced(const __grid_constant__ GateList<CAP> g,
       const uint64_t addr = base + 32u * l + lane;
       if (addr >= start && addr < end)
         k2_out[addr - start] =
-            negate_if(kron_element<C>(T, a[l], q.gbits, q.ngroups), (sgn >> l) & 1u);
+            negate_if(kron_element<C>(T, a[l], q), (sgn >> l) & 1u);
     }
   }
 }
@@ -552,7 +565,7 @@ k_fused_kron_perlane64(const __grid_constant__ GateList<CAP> g, const __grid_con
       }
       if ((~x & cm) == 0ull) x ^= tm;
     }
-    k2_out[r] = negate_if(kron_element<C>(T, x, q.gbits, q.ngroups), sg);
+    k2_out[r] = negate_if(kron_element<C>(T, x, q), sg);
   }
 }
 

@@ -163,3 +163,85 @@ def test_kron_64bit_kernel_equals_32bit_kernel_below_33(q):
             torch.cuda.synchronize()
             outs.append(out.cpu().numpy().tobytes())
         assert outs[0] == outs[1] == outs[2]
+
+
+def _kernel_nv(q):
+    name = q.last_kernel()
+    assert name.startswith("qsim_jit_kron"), name
+    return int(name.rsplit("nv ", 1)[1].rstrip(")"))
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+@pytest.mark.parametrize("kind", ["random", "structured"])
+def test_kron_thread_layout_fast_path(q, dtype, kind):
+    """The per-thread hoisted product (qsim_jit.cu kron_source, fast path):
+    the host picks 5 output bits whose flips move few source bits; every
+    kernel of the call uses the same table layout, so the NVRTC kernel (fast
+    path), the per-lane and the bit-sliced kernels give identical bytes, all
+    within the rounding bound of the oracle."""
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    M = 22
+    if kind == "random":    # 64 gates on 22 bits: the sampled |V| is 6..12 by seed
+        circuits = [wl.random_gates(64, M, sd) for sd in (122, 126, 127, 120)]
+    else:   # gates on bits 0..13 only: bits 14..21 move nothing but themselves
+        circuits = [wl.random_gates_ext(96, 14, 5)]
+    qb = wl.random_qubits(M, 31, dtype)
+    N = 1 << M
+    fast = 0
+    for gates in circuits:
+        outs = {}
+        for w in (q.WALK_JIT, q.WALK_PER_LANE, q.WALK_BITSLICED):
+            out = _out(N, dtype)
+            q.run_fused_kron(gates, M, qb, out, dtype=dtype, walk=w)
+            torch.cuda.synchronize()
+            if w == q.WALK_JIT:
+                fast += _kernel_nv(q) > 0
+            outs[w] = out.cpu().numpy()
+        assert outs[q.WALK_JIT].tobytes() == outs[q.WALK_PER_LANE].tobytes() == \
+            outs[q.WALK_BITSLICED].tobytes()
+    assert fast > 0
+    _check(outs[q.WALK_JIT], oracle.fused_kron(gates, qb), M, dtype)   # the last circuit, all 2^M
+
+
+def test_kron_thread_layout_general_path_on_missed_influence(q, monkeypatch):
+    """Sampling one point (QSIM_KRON_SAMPLES=1) misses most influences: the
+    per-warp check then sends tiles down the general path.  Both paths give
+    the bytes of the per-lane kernel, with and without phase gates."""
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    monkeypatch.setenv("QSIM_KRON_SAMPLES", "1")
+    M = 20
+    for seed in range(6):
+        gates = wl.random_gates_ext(48, M, 200 + seed)
+        qb = wl.random_qubits(M, seed, "c64")
+        a, b = _out(1 << M, "c64"), _out(1 << M, "c64")
+        q.run_fused_kron(gates, M, qb, a, dtype="c64", walk=q.WALK_JIT)
+        q.run_fused_kron(gates, M, qb, b, dtype="c64", walk=q.WALK_PER_LANE)
+        torch.cuda.synchronize()
+        assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes(), seed
+
+
+@pytest.mark.parametrize("start,count", [(0, 1 << 20), (12345, (1 << 20) - 777), ((1 << 21) - 99, 300000),
+                                         (1 << 19, 1 << 19)])
+def test_kron_thread_layout_ranges(q, start, count):
+    """Blocks of 2^L outputs hold whole tiles; ranges that cut blocks store
+    only their own outputs (bounds checked there): == the per-lane kernel
+    byte for byte, within the oracle's bound."""
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    M = 23
+    gates = wl.random_gates(64, M, 77)
+    qb = wl.random_qubits(M, 9, "c64")
+    guard = 64
+    a = _out(count + guard, "c64")
+    a.fill_(7.0)
+    b = _out(count, "c64")
+    q.run_fused_kron(gates, M, qb, a, start=start, count=count, dtype="c64", walk=q.WALK_JIT)
+    q.run_fused_kron(gates, M, qb, b, start=start, count=count, dtype="c64", walk=q.WALK_PER_LANE)
+    torch.cuda.synchronize()
+    ga = a.cpu().numpy()
+    assert ga[:count].tobytes() == b.cpu().numpy()[:count].tobytes()
+    assert np.all(ga[count:] == 7.0)        # nothing written past the range
+    sel = np.unique(np.concatenate([np.arange(min(count, 2000)), np.arange(count - min(count, 2000), count)]))
+    _check(ga[sel], oracle.fused_kron(gates, qb, start, count)[sel], M, "c64")
