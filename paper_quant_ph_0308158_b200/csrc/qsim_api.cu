@@ -208,8 +208,188 @@ int launch_walk(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, ui
 // is present; everything else (and any JIT failure under AUTO) uses the
 // shared-memory bit-sliced interpreter (kJitMinCount, top of file).
 
+// ---- In-thread output bits (the NVRTC build and on-the-fly input kernels)
+// Each NVRTC thread holds 32 outputs that differ in 5 output bits J (the bit
+// positions of its planes; lanes are output bits 0..4).  When the sources of
+// those 32 outputs differ only in a few address bits V, the kernels form
+// everything that depends on the other bits once per thread.  J is chosen
+// greedily from sampled single-bit influences (flip output bit j, see which
+// source bits change), then V is measured on all 32 combinations of the
+// chosen bits.  A sample can miss a rare influence: the kernels check per
+// warp tile and take the general path there (same bytes).  Host arithmetic
+// only samples the circuit.
+struct ThreadBits {
+  uint8_t J[5];
+  int L;                    // tiles fill aligned blocks of 2^L outputs
+  uint64_t V;               // 0: no fast path
+  std::vector<uint64_t> xs, s0;  // the sample (outputs, their sources)
+};
+
+// source address of output x (the walk, gates last to first; phase steps do
+// not move addresses)
+uint64_t walk_src(const qsim_gate* g, int n, uint64_t x) {
+  for (int k = n - 1; k >= 0; --k) {
+    const qsim_gate& q = g[k];
+    const uint64_t tm = 1ull << q.target;
+    if (q.kind == 6) {
+      if (((x >> q.target) ^ (x >> q.c0)) & 1ull) x ^= tm | (1ull << q.c0);
+      continue;
+    }
+    if (q.kind >= 3) continue;
+    const uint64_t cm = (q.kind >= 1 ? 1ull << q.c0 : 0ull) | (q.kind == 2 ? 1ull << q.c1 : 0ull);
+    if ((~x & cm) == 0ull) x ^= tm;
+  }
+  return x;
+}
+
+void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t count, int maxv,
+                 ThreadBits* tb) {
+  for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)(5 + k);
+  tb->L = 10;
+  tb->V = 0;
+  const char* env = std::getenv("QSIM_THREAD_BITS");  // A/B switch
+  if ((env && env[0] == '0') || M < 12 || count < (1ull << 16)) return;
+  const uint64_t end = start + count;
+  // blocks of 2^L outputs hold whole tiles: a range that is not aligned to
+  // them computes part of its first and last block for nothing -- allow
+  // that up to 1/8 of the count
+  int L = M;
+  auto ok = [&](int l) {
+    const uint64_t B = 1ull << l, m = B - 1;
+    return ((start & m) == 0 && (end & m) == 0) || (B <= count / 16);
+  };
+  while (L > 10 && !ok(L)) --L;
+  if (L <= 10) return;
+  uint64_t h = 0x9e3779b97f4a7c15ull ^ ((uint64_t)M << 32) ^ (uint64_t)n;
+  auto next = [&]() {  // splitmix64
+    uint64_t z = (h += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  int S = n > 1024 ? 16 : 64;
+  if (const char* se = std::getenv("QSIM_THREAD_BITS_SAMPLES")) S = std::max(1, std::atoi(se));  // tests
+  tb->xs.resize(S);
+  tb->s0.resize(S);
+  for (int i = 0; i < S; ++i) {
+    tb->xs[i] = start + next() % count;
+    tb->s0[i] = walk_src(g, n, tb->xs[i]);
+  }
+  uint64_t infl[64] = {0};
+  for (int j = 5; j < L; ++j)
+    for (int i = 0; i < S; ++i) infl[j] |= tb->s0[i] ^ walk_src(g, n, tb->xs[i] ^ (1ull << j));
+  uint64_t V = 0, Jm = 0;
+  int J[5];
+  for (int k = 0; k < 5; ++k) {
+    int best = -1, bc = 99;
+    for (int j = 5; j < L; ++j) {
+      if ((Jm >> j) & 1ull) continue;
+      const int c = __builtin_popcountll(V | infl[j]);
+      if (c < bc) bc = c, best = j;
+    }
+    J[k] = best;
+    Jm |= 1ull << best;
+    V |= infl[best];
+  }
+  std::sort(J, J + 5);
+  V = 0;
+  for (int i = 0; i < S; ++i) {
+    const uint64_t b0 = tb->xs[i] & ~Jm, sb = walk_src(g, n, b0);
+    for (int c = 1; c < 32; ++c) {
+      uint64_t x = b0;
+      for (int k = 0; k < 5; ++k)
+        if ((c >> k) & 1) x |= 1ull << J[k];
+      V |= sb ^ walk_src(g, n, x);
+    }
+  }
+  const int nv = __builtin_popcountll(V);
+  if (nv == 0 || nv > maxv) return;
+  for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)J[k];
+  tb->L = L;
+  tb->V = V;
+}
+
+// one-entry caches: repeated calls on the same circuit and range (a bench
+// loop, a batch) sample once
+struct ThreadBitsCache {
+  std::mutex mu;
+  std::vector<qsim_gate> gates;
+  std::string env;
+  int M = -1, maxv = 0;
+  uint64_t start = 0, count = 0;
+  ThreadBits tb;
+};
+ThreadBitsCache g_tb_cache[2];  // 0: build, 1: on-the-fly input
+
+void thread_bits_cached(int which, const qsim_gate* g, int n, int M, uint64_t start, uint64_t count,
+                        int maxv, ThreadBits* tb) {
+  ThreadBitsCache& c = g_tb_cache[which];
+  std::lock_guard<std::mutex> lk(c.mu);
+  const char* e1 = std::getenv("QSIM_THREAD_BITS");
+  const char* e2 = std::getenv("QSIM_THREAD_BITS_SAMPLES");
+  const std::string env = std::string(e1 ? e1 : "-") + "/" + (e2 ? e2 : "-");
+  const bool hit = c.env == env && c.M == M && c.maxv == maxv && c.start == start &&
+                   c.count == count && c.gates.size() == (size_t)n &&
+                   (n == 0 || std::memcmp(c.gates.data(), g, sizeof(qsim_gate) * n) == 0);
+  if (!hit) {
+    thread_bits(g, n, M, start, count, maxv, &c.tb);
+    c.gates.assign(g, g + n);
+    c.env = env;
+    c.M = M, c.maxv = maxv, c.start = start, c.count = count;
+  }
+  *tb = c.tb;
+}
+
+// On-the-fly input: the table layout.  Table 0 (one lookup per entry) is
+// indexed by V and gb - |V| more bits the lanes (output bits 0..4) do not
+// move, so that the 32 lanes of a warp read few distinct entries of table 0
+// (a broadcast rather than bank conflicts); the other groups' product is
+// formed once per thread.
+struct KronLayout {
+  uint8_t pos[64];
+  uint8_t J[5];
+  int L, nv;
+};
+
+void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t start, uint64_t count,
+                 bool cached, KronLayout* ly) {
+  for (int k = 0; k < 64; ++k) ly->pos[k] = (uint8_t)k;
+  ThreadBits tb;
+  if (ng < 2) {
+    thread_bits(g, n, M, start, 0, gb, &tb);  // default J (count 0: no sampling)
+  } else if (cached) {
+    thread_bits_cached(1, g, n, M, start, count, gb, &tb);
+  } else {
+    thread_bits(g, n, M, start, count, gb, &tb);
+  }
+  for (int k = 0; k < 5; ++k) ly->J[k] = tb.J[k];
+  ly->L = tb.L;
+  const uint64_t V = tb.V;
+  ly->nv = __builtin_popcountll(V);
+  if (!V) return;
+  uint64_t lanes = 0;
+  for (int j = 0; j < 5; ++j)
+    for (size_t i = 0; i < tb.xs.size(); ++i) lanes |= tb.s0[i] ^ walk_src(g, n, tb.xs[i] ^ (1ull << j));
+  uint64_t G0 = V;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int b = M - 1; b >= 0 && __builtin_popcountll(G0) < gb; --b)
+      if (!((G0 >> b) & 1ull) && (pass == 1 || !((lanes >> b) & 1ull))) G0 |= 1ull << b;
+  int k = 0;
+  for (int b = 0; b < M; ++b)
+    if ((V >> b) & 1ull) ly->pos[k++] = (uint8_t)b;
+  for (int b = 0; b < M; ++b)
+    if (((G0 & ~V) >> b) & 1ull) ly->pos[k++] = (uint8_t)b;
+  for (int b = 0; b < M; ++b)
+    if (!((G0 >> b) & 1ull)) ly->pos[k++] = (uint8_t)b;
+}
+
+// build kernel fast path up to this many varying address bits per thread
+constexpr int kBuildMaxV = 12;
+thread_local char g_build_name[96];
+
 int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
                uint32_t* perm_out, int32_t walk, cudaStream_t st) {
+  g_last_kernel = "";
   int rc = check_gates(gates, n, M);
   if (rc) return rc;
   if (has_phase(gates, n)) {  // the map alone would drop the -1 rows
@@ -223,8 +403,14 @@ int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uin
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n, false, *gl);
     std::string err;
-    if (qsim::jit_build(gl->w, n, M, start, count, perm_out, sm_count(), st, err) == 0) {
+    ThreadBits tb;
+    thread_bits_cached(0, gates, n, M, start, count, kBuildMaxV, &tb);
+    if (qsim::jit_build(gl->w, n, M, tb.J, tb.L, tb.V, start, count, perm_out, sm_count(), st,
+                        err) == 0) {
       if (count) ++g_launches;
+      std::snprintf(g_build_name, sizeof g_build_name, "qsim_jit_build (J %d.%d.%d.%d.%d, L %d, nv %d)",
+                    tb.J[0], tb.J[1], tb.J[2], tb.J[3], tb.J[4], tb.L, __builtin_popcountll(tb.V));
+      g_last_kernel = g_build_name;
       return QSIM_OK;
     }
     if (walk == QSIM_WALK_JIT) {
@@ -310,159 +496,6 @@ void kron_groups(int32_t M, int e, uint32_t* gbits, uint32_t* ngroups) {
   *gbits = (uint32_t)((M + ng - 1) / ng);
 }
 
-// Layout of the on-the-fly input (which output bits a thread walks, which
-// address bits index which table).  Each NVRTC thread holds 32 outputs that
-// differ in the output bits J; when the sources of those 32 outputs differ
-// only in a few address bits V (|V| <= gb), the tables put V at positions
-// 0..|V|-1 and the kernel forms the product of the other groups once per
-// thread (qsim_jit.cu kron_source).  J is chosen greedily from sampled
-// single-bit influences (flip output bit j, see which source bits change),
-// then V is measured on all 32 combinations of the chosen bits.  A sample can
-// miss a rare influence: the kernel checks per warp tile and takes the
-// general path there (same bytes).  Host arithmetic only samples the circuit.
-struct KronLayout {
-  uint8_t pos[64];
-  uint8_t J[5];
-  int L, nv;
-};
-
-// source address of output x (the walk, gates last to first; phase steps do
-// not move addresses)
-uint64_t kron_src(const qsim_gate* g, int n, uint64_t x) {
-  for (int k = n - 1; k >= 0; --k) {
-    const qsim_gate& q = g[k];
-    const uint64_t tm = 1ull << q.target;
-    if (q.kind == 6) {
-      if (((x >> q.target) ^ (x >> q.c0)) & 1ull) x ^= tm | (1ull << q.c0);
-      continue;
-    }
-    if (q.kind >= 3) continue;
-    const uint64_t cm = (q.kind >= 1 ? 1ull << q.c0 : 0ull) | (q.kind == 2 ? 1ull << q.c1 : 0ull);
-    if ((~x & cm) == 0ull) x ^= tm;
-  }
-  return x;
-}
-
-void kron_layout_default(int M, KronLayout* ly) {
-  for (int k = 0; k < 64; ++k) ly->pos[k] = (uint8_t)k;
-  for (int k = 0; k < 5; ++k) ly->J[k] = (uint8_t)(5 + k);
-  ly->L = 10;
-  ly->nv = 0;
-  (void)M;
-}
-
-void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t start, uint64_t count,
-                 KronLayout* ly) {
-  kron_layout_default(M, ly);
-  const char* env = std::getenv("QSIM_KRON_LAYOUT");  // A/B switch
-  if ((env && env[0] == '0') || ng < 2 || M < 12 || count < (1ull << 16)) return;
-  const uint64_t end = start + count;
-  // blocks of 2^L outputs hold whole tiles: a range that is not aligned to
-  // them computes part of its first and last block for nothing -- allow
-  // that up to 1/8 of the count
-  int L = M;
-  auto ok = [&](int l) {
-    const uint64_t B = 1ull << l, m = B - 1;
-    return ((start & m) == 0 && (end & m) == 0) || (B <= count / 16);
-  };
-  while (L > 10 && !ok(L)) --L;
-  if (L <= 10) return;
-  uint64_t h = 0x9e3779b97f4a7c15ull ^ ((uint64_t)M << 32) ^ (uint64_t)n;
-  auto next = [&]() {  // splitmix64
-    uint64_t z = (h += 0x9e3779b97f4a7c15ull);
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
-  };
-  int S = n > 1024 ? 16 : 64;
-  if (const char* se = std::getenv("QSIM_KRON_SAMPLES")) S = std::max(1, std::atoi(se));  // tests
-  std::vector<uint64_t> xs(S), s0(S);
-  for (int i = 0; i < S; ++i) {
-    xs[i] = start + next() % count;
-    s0[i] = kron_src(g, n, xs[i]);
-  }
-  uint64_t infl[64] = {0};
-  for (int j = 5; j < L; ++j)
-    for (int i = 0; i < S; ++i) infl[j] |= s0[i] ^ kron_src(g, n, xs[i] ^ (1ull << j));
-  uint64_t V = 0, Jm = 0;
-  int J[5];
-  for (int k = 0; k < 5; ++k) {
-    int best = -1, bc = 99;
-    for (int j = 5; j < L; ++j) {
-      if ((Jm >> j) & 1ull) continue;
-      const int c = __builtin_popcountll(V | infl[j]);
-      if (c < bc) bc = c, best = j;
-    }
-    J[k] = best;
-    Jm |= 1ull << best;
-    V |= infl[best];
-  }
-  std::sort(J, J + 5);
-  V = 0;
-  for (int i = 0; i < S; ++i) {
-    const uint64_t b0 = xs[i] & ~Jm, sb = kron_src(g, n, b0);
-    for (int c = 1; c < 32; ++c) {
-      uint64_t x = b0;
-      for (int k = 0; k < 5; ++k)
-        if ((c >> k) & 1) x |= 1ull << J[k];
-      V |= sb ^ kron_src(g, n, x);
-    }
-  }
-  const int nv = __builtin_popcountll(V);
-  if (nv == 0 || nv > gb) return;
-  // table 0 (one lookup per entry) is indexed by V and gb - nv more bits:
-  // take bits the lanes (output bits 0..4) do not move, so that the 32 lanes
-  // of a warp read few distinct entries of table 0 (a broadcast rather than
-  // bank conflicts)
-  uint64_t lanes = 0;
-  for (int j = 0; j < 5; ++j)
-    for (int i = 0; i < S; ++i) lanes |= s0[i] ^ kron_src(g, n, xs[i] ^ (1ull << j));
-  uint64_t G0 = V;
-  for (int pass = 0; pass < 2; ++pass)
-    for (int b = M - 1; b >= 0 && __builtin_popcountll(G0) < gb; --b)
-      if (!((G0 >> b) & 1ull) && (pass == 1 || !((lanes >> b) & 1ull))) G0 |= 1ull << b;
-  int k = 0;
-  for (int b = 0; b < M; ++b)
-    if ((V >> b) & 1ull) ly->pos[k++] = (uint8_t)b;
-  for (int b = 0; b < M; ++b)
-    if (((G0 & ~V) >> b) & 1ull) ly->pos[k++] = (uint8_t)b;
-  for (int b = 0; b < M; ++b)
-    if (!((G0 >> b) & 1ull)) ly->pos[k++] = (uint8_t)b;
-  for (int q = 0; q < 5; ++q) ly->J[q] = (uint8_t)J[q];
-  ly->L = L;
-  ly->nv = nv;
-}
-
-// one-entry cache: repeated calls on the same circuit and range (a bench
-// loop, a batch) sample once
-struct KronLayoutCache {
-  std::mutex mu;
-  std::vector<qsim_gate> gates;
-  std::string env;
-  int M = -1, gb = 0, ng = 0;
-  uint64_t start = 0, count = 0;
-  KronLayout ly;
-} g_kron_cache;
-
-void kron_layout_cached(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t start,
-                        uint64_t count, KronLayout* ly) {
-  std::lock_guard<std::mutex> lk(g_kron_cache.mu);
-  KronLayoutCache& c = g_kron_cache;
-  const char* e1 = std::getenv("QSIM_KRON_LAYOUT");
-  const char* e2 = std::getenv("QSIM_KRON_SAMPLES");
-  const std::string env = std::string(e1 ? e1 : "-") + "/" + (e2 ? e2 : "-");
-  const bool hit = c.env == env && c.M == M && c.gb == gb && c.ng == ng && c.start == start && c.count == count &&
-                   c.gates.size() == (size_t)n &&
-                   (n == 0 || std::memcmp(c.gates.data(), g, sizeof(qsim_gate) * n) == 0);
-  if (!hit) {
-    kron_layout(g, n, M, gb, ng, start, count, &c.ly);
-    c.gates.assign(g, g + n);
-    c.env = env;
-    c.M = M, c.gb = gb, c.ng = ng, c.start = start, c.count = count;
-  }
-  *ly = c.ly;
-}
-
 thread_local char g_kron_name[96];
 
 template <int CAP, typename C>
@@ -528,7 +561,7 @@ int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const
     for (int c = 0; c < 4; ++c) qb.v[j][c] = qubits[4 * j + c];
   if (count == 0) return QSIM_OK;
   KronLayout ly;
-  kron_layout_cached(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start, count, &ly);
+  kron_layout(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start, count, true, &ly);
   for (int k = 0; k < 64; ++k) {
     qb.pos[k] = ly.pos[k];
     if (ly.pos[k] != k) qb.permuted = 1;
@@ -1828,7 +1861,7 @@ int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t
   uint32_t gb = 0, ng = 0;
   kron_groups(M, elem_bytes(dtype), &gb, &ng);
   KronLayout ly;  // the layout of a call over all 2^M outputs
-  kron_layout(gates, n_gates, M, (int)gb, (int)ng, 0, 1ull << M, &ly);
+  kron_layout(gates, n_gates, M, (int)gb, (int)ng, 0, 1ull << M, false, &ly);
   if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), (int)gb, (int)ng, ly.pos,
                                    ly.J, ly.L, ly.nv, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
@@ -1844,7 +1877,9 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
-  if (qsim::jit_check_compile(gl->w, n_gates, M, err) != 0) {
+  ThreadBits tb;  // the in-thread bits of a call over all 2^M outputs
+  thread_bits(gates, n_gates, M, 0, 1ull << M, kBuildMaxV, &tb);
+  if (qsim::jit_check_compile(gl->w, n_gates, M, tb.J, tb.L, tb.V, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }

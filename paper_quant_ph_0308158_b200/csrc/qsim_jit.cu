@@ -243,50 +243,126 @@ std::string walk_code(const uint32_t* w, int n, int M) {
   return s;
 }
 
-std::string build_source(const uint32_t* w, int n, int M) {
+// In-thread output bits (qsim_api.cu thread_bits): a warp tile is 1024
+// outputs = lanes on output bits 0..4 x the 32 bit positions of each plane on
+// output bits J[0..4]; tiles enumerate the other bits, 2^(L-10) tiles per
+// aligned block of 2^L outputs.  Stores stay 128 / 256-byte warp runs.
+std::string thread_defs(const uint8_t* J, int L) {
+  char buf[320];
+  std::snprintf(buf, sizeof buf,
+                "#define QSIM_L %d\n"
+                "#define QSIM_OFF(l) (((l) & 1 ? 1ull << %d : 0ull) | ((l) & 2 ? 1ull << %d : 0ull) | "
+                "((l) & 4 ? 1ull << %d : 0ull) | ((l) & 8 ? 1ull << %d : 0ull) | "
+                "((l) & 16 ? 1ull << %d : 0ull))\n",
+                L, J[0], J[1], J[2], J[3], J[4]);
+  return buf;
+}
+
+// base = the tile's first output (lane and J bits clear), the initial planes
+// (address bits of the 32 x 32 outputs), the tile's block test
+std::string thread_planes(int M, const uint8_t* J, int np) {
+  std::string s = "    u64 base = tile << 5;\n";
+  char buf[200];
+  for (int k = 0; k < 5; ++k) {  // insert a zero at each in-thread bit, ascending
+    std::snprintf(buf, sizeof buf, "    base = (base & 0x%llxull) | ((base >> %d) << %d);\n",
+                  (unsigned long long)((1ull << J[k]) - 1), J[k], J[k] + 1);
+    s += buf;
+  }
+  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+  for (int b = 0; b < np; ++b) {
+    int jk = -1;
+    for (int k = 0; k < 5; ++k)
+      if (J[k] == b) jk = k;
+    if (b >= M)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
+    else if (b < 5)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+    else if (jk >= 0)
+      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[jk]);
+    else
+      std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
+    s += buf;
+  }
+  s += "    const u64 blk = base >> QSIM_L;\n"
+       "    const bool full = (blk << QSIM_L) >= start && ((blk + 1ull) << QSIM_L) <= end;\n";
+  return s;
+}
+
+// the 32 outputs of a thread: `value` defines rv for entry l; stores hoisted
+// out of the range test for whole blocks
+std::string thread_stores(const char* ptr, const char* value, const char* ind) {
+  const std::string i(ind);
+  std::string e;
+  e += i + "auto* const kq = " + ptr + " + (base + lane - start);\n";
+  e += i + "if (full) {\n";
+  e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+  e += i + "    " + value + "\n";
+  e += i + "    __stcs(kq + QSIM_OFF(l), rv);\n";
+  e += i + "  }\n";
+  e += i + "} else {\n";
+  e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+  e += i + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
+  e += i + "    if (addr >= start && addr < end) {\n";
+  e += i + "      " + value + "\n";
+  e += i + "      __stcs(kq + QSIM_OFF(l), rv);\n";
+  e += i + "    }\n";
+  e += i + "  }\n";
+  e += i + "}\n";
+  return e;
+}
+
+// transpose stages over the array `a`
+std::string transpose_code(const char* a, const char* ind) {
+  char buf[320];
+  std::snprintf(buf, sizeof buf,
+                "%sQSIM_TS(16, 0x0000ffffu, %s) QSIM_TS(8, 0x00ff00ffu, %s) QSIM_TS(4, 0x0f0f0f0fu, %s)\n"
+                "%sQSIM_TS(2, 0x33333333u, %s) QSIM_TS(1, 0x55555555u, %s)\n",
+                ind, a, a, a, ind, a, a);
+  return buf;
+}
+
+// The map: perm_out[out - start] = source of output out, M <= 32.
+// Fast path (V != 0): when every address bit outside V is constant across a
+// thread's 32 outputs (checked per warp tile), those bits are gathered once
+// per thread and only the |V| planes of V are transposed; otherwise all 32.
+std::string build_source(const uint32_t* w, int n, int M, const uint8_t* J, int L, uint64_t V) {
   std::string s = kPrelude;
+  s += thread_defs(J, L);
   s += R"(
 extern "C" __global__ void __launch_bounds__(256)
 qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
-    const u64 base = tile << 10;
-    const u32 b32 = (u32)base;
 )";
-  char buf[160];
-  for (int b = 0; b < 32; ++b) {
-    if (b < 5)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (b < 10) {
-      const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u",
-                            "0xffff0000u"};
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
-    } else
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((b32 >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    s += buf;
-  }
+  char buf[200];
+  s += thread_planes(M, J, 32);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
+  if (V != 0) {
+    s += "    u32 un = 0u, inv = 0u;\n";
+    for (int b = 0; b < M; ++b) {
+      if ((V >> b) & 1ull) continue;
+      std::snprintf(buf, sizeof buf, "    un |= p%d ^ (0u - (p%d & 1u)); inv |= p%d & 0x%xu;\n", b, b,
+                    b, 1u << b);
+      s += buf;
+    }
+    s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n      u32 a[32] = {";
+    for (int b = 0; b < 32; ++b) {
+      s += ((V >> b) & 1ull) ? "p" + std::to_string(b) : std::string("0u");
+      s += b < 31 ? ", " : "};\n";
+    }
+    s += transpose_code("a", "      ");
+    s += thread_stores("perm_out", "const u32 rv = a[l] | inv;", "      ");
+    s += "      continue;\n    }\n";
+  }
   s += "    u32 a[32] = {";
   for (int b = 0; b < 32; ++b) {
     std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
     s += buf;
   }
-  s += R"(
-    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
-    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
-    if (base >= start && base + 1024u <= end) {
-      _Pragma("unroll") for (int l = 0; l < 32; ++l)
-        __stcs(perm_out + (base - start + 32u * l + lane), a[l]);
-    } else {
-      _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-        const u64 addr = base + 32u * l + lane;
-        if (addr >= start && addr < end) __stcs(perm_out + (addr - start), a[l]);
-      }
-    }
-  }
-}
-)";
+  s += transpose_code("a", "    ");
+  s += thread_stores("perm_out", "const u32 rv = a[l];", "    ");
+  s += "  }\n}\n";
   return s;
 }
 
@@ -781,13 +857,10 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   char buf[320];
   const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf,
-                "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n#define QSIM_L %d\n"
-                "#define QSIM_OFF(l) (((l) & 1 ? 1ull << %d : 0ull) | ((l) & 2 ? 1ull << %d : 0ull) | "
-                "((l) & 4 ? 1ull << %d : 0ull) | ((l) & 8 ? 1ull << %d : 0ull) | "
-                "((l) & 16 ? 1ull << %d : 0ull))\n",
-                M, gb, ng, L, J[0], J[1], J[2], J[3], J[4]);
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M,
+                gb, ng);
   s += buf;
+  s += thread_defs(J, L);
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
   return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
@@ -820,61 +893,13 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
-    u64 base = tile << 5;
 )";
-  // insert a zero at each in-thread output bit (ascending): base = the tile's
-  // output with lane and J bits clear
-  int Js[5];
-  for (int k = 0; k < 5; ++k) Js[k] = J[k];
-  for (int k = 0; k < 5; ++k) {
-    std::snprintf(buf, sizeof buf,
-                  "    base = (base & 0x%llxull) | ((base >> %d) << %d);\n",
-                  (unsigned long long)((1ull << Js[k]) - 1), Js[k], Js[k] + 1);
-    s += buf;
-  }
-  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
   const int np = wide ? 64 : 32;
-  for (int b = 0; b < np; ++b) {
-    int jk = -1;
-    for (int k = 0; k < 5; ++k)
-      if (Js[k] == b) jk = k;
-    if (b >= M)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
-    else if (b < 5)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (jk >= 0)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[jk]);
-    else
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
-    s += buf;
-  }
+  s += thread_planes(M, J, np);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
-  s += R"(
-    const u64 blk = base >> QSIM_L;
-    const bool full = (blk << QSIM_L) >= start && ((blk + 1ull) << QSIM_L) <= end;
-)";
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
-  // 32 entries, stores hoisted out of the range test for whole blocks
-  auto entries = [&](const char* value, const char* ind) {
-    std::string e;
-    e += std::string(ind) + "C* const kq = k2 + (base + lane - start);\n";
-    e += std::string(ind) + "if (full) {\n";
-    e += std::string(ind) + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
-    e += std::string(ind) + "    " + value + "\n";
-    e += std::string(ind) + "    __stcs(kq + QSIM_OFF(l), rv);\n";
-    e += std::string(ind) + "  }\n";
-    e += std::string(ind) + "} else {\n";
-    e += std::string(ind) + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
-    e += std::string(ind) + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
-    e += std::string(ind) + "    if (addr >= start && addr < end) {\n";
-    e += std::string(ind) + "      " + value + "\n";
-    e += std::string(ind) + "      __stcs(kq + QSIM_OFF(l), rv);\n";
-    e += std::string(ind) + "    }\n";
-    e += std::string(ind) + "  }\n";
-    e += std::string(ind) + "}\n";
-    return e;
-  };
+
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
@@ -905,7 +930,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     }
     s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
     s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += entries("const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
     s += "      continue;\n    }\n";
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
@@ -933,7 +958,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     gen += buf;
   }
   gen += " const C rv = negate_if(r, (sg >> l) & 1u);";
-  s += entries(gen.c_str(), "    ");
+  s += thread_stores("k2", gen.c_str(), "    ");
   s += "  }\n}\n";
   return s;
 }
@@ -1144,7 +1169,8 @@ CUfunction get_kernel_locked(uint64_t kind, const std::vector<uint32_t>& keyw, i
   return fn;
 }
 
-int jit_check_compile(const uint32_t* words, int n, int M, std::string& err) {
+int jit_check_compile(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint64_t V,
+                      std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nvrtc.ok) {
@@ -1152,12 +1178,13 @@ int jit_check_compile(const uint32_t* words, int n, int M, std::string& err) {
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(build_source(words, n, M), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(build_source(words, n, M, J, L, V), cubin, err) ? 0 : -1;
 }
 
 // words: per-lane gate format (kind | t << 8 | c0 << 16 | c1 << 24).
-int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t count,
-              uint32_t* perm_out, int sms, cudaStream_t st, std::string& err) {
+int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint64_t V,
+              uint64_t start, uint64_t count, uint32_t* perm_out, int sms, cudaStream_t st,
+              std::string& err) {
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1166,23 +1193,28 @@ int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t coun
       err = g_status;
       return -1;
     }
-    const uint64_t key = fnv(words, n, 0x6275696c64ull);
+    std::vector<uint32_t> keyw(words, words + n);
+    for (int k = 0; k < 5; ++k) keyw.push_back(J[k]);
+    keyw.push_back((uint32_t)L);
+    keyw.push_back((uint32_t)V);
+    keyw.push_back((uint32_t)(V >> 32));
+    const uint64_t kind = 0x6275696c64ull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
-      if (e.M == M && (int)e.words.size() == n &&
-          std::memcmp(e.words.data(), words, n * sizeof(uint32_t)) == 0)
-        fn = e.fn;
+      if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn) {
-      fn = get_kernel_locked(0x6275696c64ull, std::vector<uint32_t>(words, words + n), M,
-                             build_source(words, n, M), "qsim_jit_build", err);
+      fn = get_kernel_locked(kind, keyw, M, build_source(words, n, M, J, L, V), "qsim_jit_build",
+                             err);
       if (!fn) return -1;
     }
   }
   if (count == 0) return 0;
-  uint64_t tb = start >> 10, te = (start + count + 1023) >> 10;
+  // whole blocks of 2^L outputs (the tiles of a block interleave its outputs)
+  uint64_t end = start + count;
+  uint64_t tb = (start >> L) << (L - 10), te = ((end + (1ull << L) - 1) >> L) << (L - 10);
   uint64_t blocks = (te - tb + 7) / 8;
   const uint64_t cap = (uint64_t)sms * 8;
   if (blocks > cap) blocks = cap;
-  uint64_t end = start + count;
   void* args[] = {&start, &end, &tb, &te, &perm_out};
   if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
       CUDA_SUCCESS) {

@@ -11,12 +11,17 @@ const char* jit_status();
 double jit_last_compile_ms();
 // NVRTC-compile the build kernel for this gate list without loading it
 // (works without a GPU); 0 on success.
-int jit_check_compile(const uint32_t* words, int n, int M, std::string& err);
+int jit_check_compile(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint64_t V,
+                      std::string& err);
 // Build perm for outputs [start, start+count) with a kernel compiled for this
 // exact gate list (per-lane word format).  Returns 0, or -1 with err set (the
 // caller then uses the interpreter kernel).
-int jit_build(const uint32_t* words, int n, int M, uint64_t start, uint64_t count,
-              uint32_t* perm_out, int sms, cudaStream_t st, std::string& err);
+// In-thread bits (qsim_api.cu thread_bits): J = output bits walked inside a
+// thread, tiles fill aligned blocks of 2^L outputs, V != 0 enables the fast
+// path (address bits outside V constant in a thread).
+int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint64_t V,
+              uint64_t start, uint64_t count, uint32_t* perm_out, int sms, cudaStream_t st,
+              std::string& err);
 // Sigma-ordered fused walk + gather over all 2^M outputs with a kernel
 // compiled for (circuit, sigma, element size); if perm_out != null the map is
 // stored as well (one-pass map + gather).  ticket: device scratch (reset on

@@ -205,12 +205,12 @@ def test_kron_thread_layout_fast_path(q, dtype, kind):
 
 
 def test_kron_thread_layout_general_path_on_missed_influence(q, monkeypatch):
-    """Sampling one point (QSIM_KRON_SAMPLES=1) misses most influences: the
+    """Sampling one point (QSIM_THREAD_BITS_SAMPLES=1) misses most influences: the
     per-warp check then sends tiles down the general path.  Both paths give
     the bytes of the per-lane kernel, with and without phase gates."""
     if not q.jit_status().startswith("ready"):
         pytest.skip("JIT unavailable")
-    monkeypatch.setenv("QSIM_KRON_SAMPLES", "1")
+    monkeypatch.setenv("QSIM_THREAD_BITS_SAMPLES", "1")
     M = 20
     for seed in range(6):
         gates = wl.random_gates_ext(48, M, 200 + seed)

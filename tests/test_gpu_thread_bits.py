@@ -1,0 +1,92 @@
+"""GPU parity of the in-thread output bits (qsim_api.cu thread_bits; the
+NVRTC build and on-the-fly input kernels): a thread's 32 outputs differ in 5
+output bits J chosen so that their sources differ in few address bits V;
+the fast path gathers the other bits once per thread.  The map is integer
+work: bit-exact against the oracle, with J at any position,
+ragged ranges, and tiles where a sampled-away influence sends the warp down
+the general path."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def q():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_native()
+    import paper_quant_ph_0308158_b200 as q
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    return q
+
+
+def _nv(name):
+    return int(name.rsplit("nv ", 1)[1].rstrip(")"))
+
+
+def _build(q, gates, M, start, count, guard=0):
+    out = torch.from_numpy(np.full(count + guard, 0xABCDEF01, dtype=np.uint32).view(np.int32)).to(DEV)
+    q.build_map_range(gates, M, start, count, out, walk=q.WALK_JIT)
+    torch.cuda.synchronize()
+    name = q.last_kernel()
+    return out.cpu().numpy().view(np.uint32), name
+
+
+@pytest.mark.parametrize("kind", ["random", "structured", "swaps"])
+def test_build_thread_bits_full(q, kind):
+    M = 22
+    if kind == "random":
+        circuits = [wl.random_gates(64, M, sd) for sd in (122, 126, 127, 120, 3)]
+    elif kind == "structured":      # bits 14..21 never move
+        circuits = [wl.random_gates(96, 14, 5)]
+    else:                           # SWAP renaming + NOT/CNOT/CCNOT
+        circuits = [wl.random_gates_ext(64, M, 9, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP))]
+    fast = 0
+    for gates in circuits:
+        got, name = _build(q, gates, M, 0, 1 << M)
+        assert name.startswith("qsim_jit_build"), name
+        fast += _nv(name) > 0
+        assert np.array_equal(got, oracle.build_map(gates, M))
+    assert fast > 0
+
+
+@pytest.mark.parametrize("start,count", [(0, 1 << 20), (12345, (1 << 20) - 777),
+                                         ((1 << 21) - 99, 300000), (1 << 19, 1 << 19)])
+def test_build_thread_bits_ranges(q, start, count):
+    """Blocks of 2^L outputs hold whole tiles; a range that cuts blocks
+    stores only its own outputs, nothing past the end."""
+    M = 23
+    gates = wl.random_gates(64, M, 77)
+    got, name = _build(q, gates, M, start, count, guard=64)
+    assert np.array_equal(got[:count], oracle.build_map(gates, M, start, count))
+    assert np.all(got[count:] == 0xABCDEF01)
+
+
+def test_build_thread_bits_general_path_on_missed_influence(q, monkeypatch):
+    """One sample point misses most influences: the per-warp check sends
+    tiles down the general path; the map stays exact."""
+    monkeypatch.setenv("QSIM_THREAD_BITS_SAMPLES", "1")
+    M = 20
+    for seed in range(6):
+        gates = wl.random_gates(48, M, 300 + seed)
+        got, _ = _build(q, gates, M, 0, 1 << M)
+        assert np.array_equal(got, oracle.build_map(gates, M)), seed
+
+
+def test_build_thread_bits_off_equals_on(q, monkeypatch):
+    """QSIM_THREAD_BITS=0 (J = 5..9, no fast path) gives the same map."""
+    M = 24
+    gates = wl.random_gates(64, M, 11)
+    on, name_on = _build(q, gates, M, 0, 1 << M)
+    monkeypatch.setenv("QSIM_THREAD_BITS", "0")
+    off, name_off = _build(q, gates, M, 0, 1 << M)
+    assert "J 5.6.7.8.9" in name_off and _nv(name_off) == 0
+    assert np.array_equal(on, off)

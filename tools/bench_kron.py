@@ -31,4 +31,4 @@ ms = min(times[2:])
 e = 8 if dtype == "c64" else 16
 print(f"M={M} count=2^{cl} {dtype} gb_env={os.environ.get('QSIM_KRON_GROUP_BITS', '-')}: {ms:.3f} ms "
       f"{count / ms * 1e3:.3e} entries/s {count * e / ms / 1e6:.0f} GB/s seed={seed} "
-      f"layout={os.environ.get('QSIM_KRON_LAYOUT', '-')} [{q.last_kernel()}]")
+      f"layout={os.environ.get('QSIM_THREAD_BITS', '-')} [{q.last_kernel()}]")
