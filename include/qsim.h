@@ -47,6 +47,10 @@
  *   QSIM_PLAN_PAIRS=1        lane-pair plans (measured slower on cfg5)
  *   QSIM_NO_LINEAR=1         ignore a plan's linear traversal
  *   QSIM_KRON_GROUP_BITS=b   product-table group size of the on-the-fly input
+ *   QSIM_THREAD_BITS=0       NVRTC threads walk output bits 5..9, no hoisted
+ *                            product (on-the-fly input 1.5-2x slower)
+ *   QSIM_THREAD_BITS_SAMPLES=k  circuit sample size of the in-thread bits (tests)
+ *   QSIM_BUILD_THREAD_BITS=1 in-thread bits in the build kernel (measured slower)
  */
 #ifndef QSIM_H
 #define QSIM_H
@@ -305,9 +309,14 @@ int qsim_run_fused_planned(const qsim_plan *plan, const qsim_gate *gates, int32_
  *           QSIM_WALK_PER_LANE (one 64-bit address per lane; the fallback
  *           for M > 32 without NVRTC, where BITSLICED means PER_LANE)
  * Arithmetic: the factors are grouped by bits of s into ng tables of
- * products of gb qubits each (descending j; complex64: gb <= 10, e.g. 4
+ * products of gb qubits each (descending table position; complex64: gb <= 10, e.g. 4
  * groups of 8 bits at M = 32, 4 of 10 at M = 40; complex128: gb <= 8), combined from the top
- * group down, ((T_{ng-1} T_{ng-2}) ...) T_0 -- the same in every walk; every
+ * group down, ((T_{ng-1} T_{ng-2}) ...) T_0 -- the same in every walk.  Which
+ * address bits form which group is chosen per call by sampling the circuit
+ * (the in-thread layout: table 0 holds the few source bits that vary across
+ * an NVRTC thread's 32 outputs, the product of the other groups is formed
+ * once per thread); every kernel of a call uses that grouping, so the walks
+ * give identical bytes, and the grouping of a call is deterministic.  Every
  * complex product is re = fma(ar, br, -(ai*bi)), im = fma(ar, bi, ai*br)
  * (the inner products rounded, then one fused rounding).  Not bit-exact
  * against a sequential double product: each complex product has normwise

@@ -16,6 +16,12 @@ pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
 
 
+@pytest.fixture(autouse=True)
+def _build_thread_bits(monkeypatch):
+    # the build kernel's in-thread bits are opt-in (measured slower by default)
+    monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "1")
+
+
 @pytest.fixture(scope="module")
 def q():
     if not torch.cuda.is_available():
@@ -88,5 +94,10 @@ def test_build_thread_bits_off_equals_on(q, monkeypatch):
     on, name_on = _build(q, gates, M, 0, 1 << M)
     monkeypatch.setenv("QSIM_THREAD_BITS", "0")
     off, name_off = _build(q, gates, M, 0, 1 << M)
+    monkeypatch.setenv("QSIM_THREAD_BITS", "1")
+    monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "0")
+    default, name_def = _build(q, gates, M, 0, 1 << M)
+    assert "J 5.6.7.8.9" in name_def
+    assert np.array_equal(on, default)
     assert "J 5.6.7.8.9" in name_off and _nv(name_off) == 0
     assert np.array_equal(on, off)
