@@ -326,8 +326,22 @@ def run_qsim(args):
                                                           per_kernel=True)
         ms_kron, launches_kron, kern_kron = timed_loop(step_kron, args.steps, args.warmup,
                                                        per_kernel=True)
+        kern_name_kron = q.last_kernel()
         ms_k40, launches_k40, kern_k40 = timed_loop(step_kron40, max(2, args.steps // 4),
                                                     args.warmup, per_kernel=True)
+        kern_name_k40 = q.last_kernel()
+        # write-only ceiling for the on-the-fly input's roofline: torch's fill
+        # of the same 2^M-entry output buffer (not our kernel; a denominator)
+        wz = []
+        for _ in range(4):
+            a0, b0 = ev(), ev()
+            a0.record(stream)
+            with torch.cuda.stream(stream):
+                k2.view(torch.float32).zero_()
+            b0.record(stream)
+            b0.synchronize()
+            wz.append(a0.elapsed_time(b0))
+        write_peak = N * e / (min(wz[1:]) * 1e-3) / 1e9
     clocks = sampler.summary()
 
     # ---- launch-bound small state (cfg2, 2^20 entries, L2-resident): the
@@ -481,14 +495,19 @@ def run_qsim(args):
             "fused_kron": {"ms": kron_ms, "GBps": gbps(N * e, kron_ms),
                            "entries_per_s": N / (kron_ms * 1e-3), "bytes_per_entry": e,
                            "frac_of_peak": gbps(N * e, kron_ms) / hbm,
+                           "frac_of_write_peak": gbps(N * e, kron_ms) / write_peak,
+                           "kernel": kern_name_kron,
                            "note": "qsim_run_fused_kron: Appendix-1 input generated on the fly "
                                    "(k1 never read), write-only"},
             "fused_kron_M40_portion": {
                 "ms": k40_ms, "GBps": gbps(N * e, k40_ms), "entries_per_s": N / (k40_ms * 1e-3),
                 "bytes_per_entry": e, "frac_of_peak": gbps(N * e, k40_ms) / hbm,
+                "frac_of_write_peak": gbps(N * e, k40_ms) / write_peak, "kernel": kern_name_k40,
                 "note": "M = 40 qubits (64 random gates, seed 4): output portion "
                         "[2^39 - 2^31, 2^39 + 2^31) of 2^40, input on the fly, 64-bit walk"},
         },
+        "write_peak": {"GBps": write_peak, "how": "torch zero_ of the 2^M-entry output buffer, "
+                                                 "best of 3 (write-only roofline of fused_kron)"},
         "launch_bound": launch_bound,
         "cpu_baseline": cpu,
         "e2e": e2e,
