@@ -177,6 +177,18 @@ def test_jit_source_compiles_without_gpu(q):
         assert rc == q.OK, L.qsim_last_error().decode()
 
 
+def test_jit_build_thread_bits_source_compiles_without_gpu(q, monkeypatch):
+    """The build kernel's opt-in in-thread fast path (QSIM_BUILD_THREAD_BITS=1)."""
+    monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "1")
+    L = q.lib()
+    for gates, M in ((wl.CONFIGS["cfg5"].gates(), 32), (wl.random_gates(96, 14, 5), 22)):
+        g = np.ascontiguousarray(gates)
+        rc = L.qsim_jit_check_compile(g.ctypes.data, len(g), M)
+        if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+            pytest.skip("NVRTC not available here")
+        assert rc == q.OK, L.qsim_last_error().decode()
+
+
 def test_jit_fused_source_compiles_without_gpu(q):
     L = q.lib()
     for name in ("cfg5", "cfg3"):
@@ -191,8 +203,12 @@ def test_jit_fused_source_compiles_without_gpu(q):
 
 def test_jit_kron_source_compiles_without_gpu(q):
     L = q.lib()
+    # cfg5: the in-thread layout (hoisted product) is generated; M = 40 / 63:
+    # 64 bit planes; phases: the sign plane in both paths
     for gates, M, dt in ((wl.CONFIGS["cfg5"].gates(), 32, q.C64), (wl.CONFIGS["cfg4"].gates(), 30, q.C128),
-                         (wl.random_gates(10, 9, 1), 9, q.C64)):
+                         (wl.random_gates(10, 9, 1), 9, q.C64), (wl.random_gates(64, 40, 80), 40, q.C64),
+                         (wl.random_gates_ext(48, 63, 2), 63, q.C128),
+                         (wl.random_gates_ext(64, 24, 8), 24, q.C64)):
         g = np.ascontiguousarray(gates)
         rc = L.qsim_jit_check_compile_kron(g.ctypes.data, len(g), M, dt)
         if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
