@@ -857,8 +857,10 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   char buf[320];
   const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M,
-                gb, ng);
+  int minb = 1;  // resident CTAs asked of ptxas (register cap); A/B via QSIM_KRON_MINB
+  if (const char* mb = std::getenv("QSIM_KRON_MINB")) minb = std::max(1, std::min(8, std::atoi(mb)));
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n"
+                "#define QSIM_MINB %d\n", M, gb, ng, minb);
   s += buf;
   s += thread_defs(J, L);
   s += f32 ? R"(
@@ -872,7 +874,7 @@ __device__ __forceinline__ C cmul(C a, C b) {
 )";
   s += R"(
 struct Qubits { double v[64][4]; u32 M, gbits, ngroups; unsigned char pos[64]; u32 permuted; };
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(256, QSIM_MINB)
 qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) {
   extern __shared__ __align__(16) unsigned char kt_smem[];
   C* T = reinterpret_cast<C*>(kt_smem);   // [QSIM_NG << QSIM_GB]
