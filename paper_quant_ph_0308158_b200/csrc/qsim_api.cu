@@ -248,7 +248,9 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
   tb->L = 10;
   tb->V = 0;
   const char* env = std::getenv("QSIM_THREAD_BITS");  // A/B switch
-  if ((env && env[0] == '0') || M < 12 || count < (1ull << 16)) return;
+  // from the count where AUTO takes the NVRTC kernels: below it the
+  // ahead-of-time kernels run, which would pay a per-entry bit permutation
+  if ((env && env[0] == '0') || M < 12 || count < kJitMinCount) return;
   const uint64_t end = start + count;
   // blocks of 2^L outputs hold whole tiles: a range that is not aligned to
   // them computes part of its first and last block for nothing -- allow

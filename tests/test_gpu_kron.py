@@ -211,7 +211,7 @@ def test_kron_thread_layout_general_path_on_missed_influence(q, monkeypatch):
     if not q.jit_status().startswith("ready"):
         pytest.skip("JIT unavailable")
     monkeypatch.setenv("QSIM_THREAD_BITS_SAMPLES", "1")
-    M = 20
+    M = 22
     for seed in range(6):
         gates = wl.random_gates_ext(48, M, 200 + seed)
         qb = wl.random_qubits(M, seed, "c64")
@@ -222,8 +222,8 @@ def test_kron_thread_layout_general_path_on_missed_influence(q, monkeypatch):
         assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes(), seed
 
 
-@pytest.mark.parametrize("start,count", [(0, 1 << 20), (12345, (1 << 20) - 777), ((1 << 21) - 99, 300000),
-                                         (1 << 19, 1 << 19)])
+@pytest.mark.parametrize("start,count", [(0, 1 << 22), (12345, (1 << 22) - 777),
+                                         ((1 << 21) - 99, (1 << 22) + 300000), (1 << 22, 1 << 22)])
 def test_kron_thread_layout_ranges(q, start, count):
     """Blocks of 2^L outputs hold whole tiles; ranges that cut blocks store
     only their own outputs (bounds checked there): == the per-lane kernel

@@ -64,8 +64,8 @@ def test_build_thread_bits_full(q, kind):
     assert fast > 0
 
 
-@pytest.mark.parametrize("start,count", [(0, 1 << 20), (12345, (1 << 20) - 777),
-                                         ((1 << 21) - 99, 300000), (1 << 19, 1 << 19)])
+@pytest.mark.parametrize("start,count", [(0, 1 << 22), (12345, (1 << 22) - 777),
+                                         ((1 << 21) - 99, (1 << 22) + 300000), (1 << 22, 1 << 22)])
 def test_build_thread_bits_ranges(q, start, count):
     """Blocks of 2^L outputs hold whole tiles; a range that cuts blocks
     stores only its own outputs, nothing past the end."""
@@ -80,7 +80,7 @@ def test_build_thread_bits_general_path_on_missed_influence(q, monkeypatch):
     """One sample point misses most influences: the per-warp check sends
     tiles down the general path; the map stays exact."""
     monkeypatch.setenv("QSIM_THREAD_BITS_SAMPLES", "1")
-    M = 20
+    M = 22
     for seed in range(6):
         gates = wl.random_gates(48, M, 300 + seed)
         got, _ = _build(q, gates, M, 0, 1 << M)

@@ -6,7 +6,12 @@ for M = 20..32 on 64 random NOT/CNOT/CCNOT gates (seed 4, the cfg5 recipe
 over M bits) and complex64 Gaussian states, and prints a CSV with the
 growth factor per added bit.
 
-    python tools/scaling_sweep.py [--mmin 20] [--mmax 32] > profiles/rNN_scaling.csv
+    python tools/scaling_sweep.py [--mmin 20] [--mmax 32] [--kron-max 40] > profiles/rNN_scaling.csv
+
+A second table times the input generated on the fly (Appendix 1): the whole
+2^M output for M <= 32, and for 32 < M <= --kron-max the 2^32-entry portion
+[0, 2^32) with the whole output extrapolated as 2^(M-32) such portions (the
+"continuous portions" of P:L13; nothing of size 2^M is ever stored).
 """
 import argparse
 import os
@@ -24,6 +29,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mmin", type=int, default=20)
     ap.add_argument("--mmax", type=int, default=32)
+    ap.add_argument("--kron-max", type=int, default=40)
     args = ap.parse_args()
     print("M,entries,map_gather_ms,build_ms,apply_ms,fused_ms,entries_per_s,growth_per_bit,"
           "plan_natural")
@@ -50,6 +56,20 @@ def main():
         prev = t_mg
         del k1, k2, perm
         torch.cuda.empty_cache()
+    print()
+    print("M,portion_entries,kron_portion_ms,kron_full_ms_extrapolated,entries_per_s,growth_per_bit,kernel")
+    prev = None
+    out = torch.empty(1 << min(args.kron_max, 32), dtype=torch.complex64, device="cuda")
+    for M in range(args.mmin, args.kron_max + 1):
+        count = 1 << min(M, 32)
+        gates = wl.random_gates(64, M, 4)
+        qb = wl.random_qubits(M, 2040, "c64")
+        t = timeit(lambda: q.run_fused_kron(gates, M, qb, out, start=0, count=count, dtype="c64"))
+        full = t * (1 << max(M - 32, 0))
+        growth = "" if prev is None else f"{full / prev:.3f}"
+        print(f"{M},{count},{t:.4f},{full:.4f},{count / t * 1e3:.4e},{growth},{q.last_kernel()}",
+              flush=True)
+        prev = full
 
 
 if __name__ == "__main__":
