@@ -758,7 +758,10 @@ uint32_t plan_forward_walk(const PlanGate* g, int n, uint32_t x) {
 // fraction of sampled pairs inside a V-block goes to plan->tile_contained.
 uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan,
                            std::vector<uint32_t>* top_patterns = nullptr) {
-  const int e = elem_bytes(dtype), eps = 32 / e, keep = plan_keep_bits(dtype);
+  const int e = elem_bytes(dtype), keep = plan_keep_bits(dtype);
+  int eps = 32 / e;  // entries per cover granule: a 32-byte sector
+  if (const char* gb = std::getenv("QSIM_PLAN_GRANULE_BYTES"))  // A/B: 64 / 128 (L1 lines)
+    eps = std::max(2, std::min(512, std::atoi(gb))) / e;
   const int samples = 2048;
   std::vector<uint32_t> diffs;
   diffs.reserve((size_t)samples * (eps - 1));
