@@ -245,3 +245,31 @@ def test_kron_thread_layout_ranges(q, start, count):
     assert np.all(ga[count:] == 7.0)        # nothing written past the range
     sel = np.unique(np.concatenate([np.arange(min(count, 2000)), np.arange(count - min(count, 2000), count)]))
     _check(ga[sel], oracle.fused_kron(gates, qb, start, count)[sel], M, "c64")
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_kron_thread_layout_beyond_32_qubits_ragged(q, dtype):
+    """M = 36, a 2^22 + 12345-entry portion at an unaligned start: 64-bit
+    planes, the in-thread layout with blocks of 2^L cut at both ends; the
+    NVRTC kernel == the per-lane 64-bit kernel byte for byte, within the
+    oracle's rounding bound on sampled outputs, nothing written past the end."""
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    M = 36
+    gates = wl.random_gates(64, M, 36)
+    qb = wl.random_qubits(M, 11, dtype)
+    start, count = (1 << 35) - 987654, (1 << 22) + 12345
+    guard = 32
+    a = _out(count + guard, dtype)
+    a.fill_(3.0)
+    b = _out(count, dtype)
+    q.run_fused_kron(gates, M, qb, a, start=start, count=count, dtype=dtype, walk=q.WALK_JIT)
+    name = q.last_kernel()
+    q.run_fused_kron(gates, M, qb, b, start=start, count=count, dtype=dtype, walk=q.WALK_PER_LANE)
+    torch.cuda.synchronize()
+    ga = a.cpu().numpy()
+    assert name.startswith("qsim_jit_kron"), name
+    assert ga[:count].tobytes() == b.cpu().numpy()[:count].tobytes()
+    assert np.all(ga[count:] == 3.0)
+    for s0, c0 in ((0, 3000), (count // 2, 3000), (count - 3000, 3000)):
+        _check(ga[s0:s0 + c0], oracle.fused_kron(gates, qb, start + s0, c0), M, dtype)
