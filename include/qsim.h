@@ -52,7 +52,7 @@
  *   QSIM_THREAD_BITS=0       NVRTC threads walk output bits 5..9, no hoisted
  *                            product (on-the-fly input 1.5-2x slower)
  *   QSIM_THREAD_BITS_SAMPLES=k  circuit sample size of the in-thread bits (tests)
- *   QSIM_BUILD_THREAD_BITS=1 in-thread bits in the build kernel (measured slower)
+ *   QSIM_BUILD_THREAD_BITS=0 build kernel without its in-thread affine fast path
  */
 #ifndef QSIM_H
 #define QSIM_H

@@ -243,7 +243,7 @@ uint64_t walk_src(const qsim_gate* g, int n, uint64_t x) {
 }
 
 void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t count, int maxv,
-                 ThreadBits* tb) {
+                 bool require_affine, ThreadBits* tb) {
   for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)(5 + k);
   tb->L = 10;
   tb->V = 0;
@@ -295,17 +295,29 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
   }
   std::sort(J, J + 5);
   V = 0;
+  int nonaffine = 0;  // samples whose 32 sources are not s0 ^ (a XOR of 5 columns)
   for (int i = 0; i < S; ++i) {
-    const uint64_t b0 = tb->xs[i] & ~Jm, sb = walk_src(g, n, b0);
-    for (int c = 1; c < 32; ++c) {
+    const uint64_t b0 = tb->xs[i] & ~Jm;
+    uint64_t sc[32];
+    for (int c = 0; c < 32; ++c) {
       uint64_t x = b0;
       for (int k = 0; k < 5; ++k)
         if ((c >> k) & 1) x |= 1ull << J[k];
-      V |= sb ^ walk_src(g, n, x);
+      sc[c] = walk_src(g, n, x);
+      V |= sc[0] ^ sc[c];
     }
+    bool aff = true;
+    for (int c = 1; c < 32 && aff; ++c) {
+      uint64_t lin = sc[0];
+      for (int k = 0; k < 5; ++k)
+        if ((c >> k) & 1) lin ^= sc[0] ^ sc[1 << k];
+      aff = lin == sc[c];
+    }
+    nonaffine += !aff;
   }
   const int nv = __builtin_popcountll(V);
   if (nv == 0 || nv > maxv) return;
+  if (require_affine && nonaffine * 16 > S) return;  // the affine fast path would mostly fail
   for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)J[k];
   tb->L = L;
   tb->V = V;
@@ -334,7 +346,7 @@ void thread_bits_cached(int which, const qsim_gate* g, int n, int M, uint64_t st
                    c.count == count && c.gates.size() == (size_t)n &&
                    (n == 0 || std::memcmp(c.gates.data(), g, sizeof(qsim_gate) * n) == 0);
   if (!hit) {
-    thread_bits(g, n, M, start, count, maxv, &c.tb);
+    thread_bits(g, n, M, start, count, maxv, which == 0, &c.tb);
     c.gates.assign(g, g + n);
     c.env = env;
     c.M = M, c.maxv = maxv, c.start = start, c.count = count;
@@ -358,11 +370,11 @@ void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t star
   for (int k = 0; k < 64; ++k) ly->pos[k] = (uint8_t)k;
   ThreadBits tb;
   if (ng < 2) {
-    thread_bits(g, n, M, start, 0, gb, &tb);  // default J (count 0: no sampling)
+    thread_bits(g, n, M, start, 0, gb, false, &tb);  // default J (count 0: no sampling)
   } else if (cached) {
     thread_bits_cached(1, g, n, M, start, count, gb, &tb);
   } else {
-    thread_bits(g, n, M, start, count, gb, &tb);
+    thread_bits(g, n, M, start, count, gb, false, &tb);
   }
   for (int k = 0; k < 5; ++k) ly->J[k] = tb.J[k];
   ly->L = tb.L;
@@ -386,7 +398,8 @@ void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t star
 }
 
 // build kernel fast path up to this many varying address bits per thread
-constexpr int kBuildMaxV = 12;
+// (each costs ~27 ops per thread; measured: |V| <= 6 faster, 8 neutral to slower)
+constexpr int kBuildMaxV = 6;
 thread_local char g_build_name[96];
 
 int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uint64_t count,
@@ -405,9 +418,9 @@ int build_impl(const qsim_gate* gates, int32_t n, int32_t M, uint64_t start, uin
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n, false, *gl);
     std::string err;
-    ThreadBits tb;  // default J = 5..9 unless QSIM_BUILD_THREAD_BITS=1 (measured 3-14 % slower)
+    ThreadBits tb;  // in-thread affine fast path (QSIM_BUILD_THREAD_BITS=0: J = 5..9, transpose)
     const char* bt = std::getenv("QSIM_BUILD_THREAD_BITS");
-    thread_bits_cached(0, gates, n, M, start, (bt && bt[0] == '1') ? count : 0, kBuildMaxV, &tb);
+    thread_bits_cached(0, gates, n, M, start, (bt && bt[0] == '0') ? 0 : count, kBuildMaxV, &tb);
     if (qsim::jit_build(gl->w, n, M, tb.J, tb.L, tb.V, start, count, perm_out, sm_count(), st,
                         err) == 0) {
       if (count) ++g_launches;
@@ -1883,9 +1896,9 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
-  ThreadBits tb;  // the in-thread bits of a call over all 2^M outputs (opt-in, as build_impl)
+  ThreadBits tb;  // the in-thread bits of a call over all 2^M outputs (as build_impl)
   const char* bt = std::getenv("QSIM_BUILD_THREAD_BITS");
-  thread_bits(gates, n_gates, M, 0, (bt && bt[0] == '1') ? 1ull << M : 0, kBuildMaxV, &tb);
+  thread_bits(gates, n_gates, M, 0, (bt && bt[0] == '0') ? 0 : 1ull << M, kBuildMaxV, true, &tb);
   if (qsim::jit_check_compile(gl->w, n_gates, M, tb.J, tb.L, tb.V, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;

@@ -323,8 +323,10 @@ std::string transpose_code(const char* a, const char* ind) {
 
 // The map: perm_out[out - start] = source of output out, M <= 32.
 // Fast path (V != 0): when every address bit outside V is constant across a
-// thread's 32 outputs (checked per warp tile), those bits are gathered once
-// per thread and only the |V| planes of V are transposed; otherwise all 32.
+// thread's 32 outputs and every bit in V is an affine function of the
+// thread's output bits J (checked per warp tile), the 32 sources follow from
+// one source and 5 difference columns, one XOR each; otherwise the 32x32
+// transpose.
 std::string build_source(const uint32_t* w, int n, int M, const uint8_t* J, int L, uint64_t V) {
   std::string s = kPrelude;
   s += thread_defs(J, L);
@@ -334,26 +336,62 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
 )";
-  char buf[200];
+  char buf[512];
   s += thread_planes(M, J, 32);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   if (V != 0) {
-    s += "    u32 un = 0u, inv = 0u;\n";
+    // affine fast path: every plane outside V constant in the thread, every
+    // plane in V an affine function of the thread's 5 output bits (checked
+    // with a bit-parallel XOR subset transform); then the 32 sources are
+    // s0 ^ (XOR of the columns of the set bits of l), taken in Gray-code
+    // order: one XOR per entry, no transpose
+    s += "    u32 un = 0u, s0 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u;\n";
     for (int b = 0; b < M; ++b) {
-      if ((V >> b) & 1ull) continue;
-      std::snprintf(buf, sizeof buf, "    un |= p%d ^ (0u - (p%d & 1u)); inv |= p%d & 0x%xu;\n", b, b,
-                    b, 1u << b);
-      s += buf;
+      if ((V >> b) & 1ull) {
+        std::snprintf(buf, sizeof buf,
+                      "    { const u32 d = p%d ^ (0u - (p%d & 1u)); u32 h = d & 0x00010116u;\n"
+                      "      h ^= (h << 1) & 0xaaaaaaaau; h ^= (h << 2) & 0xccccccccu; "
+                      "h ^= (h << 4) & 0xf0f0f0f0u;\n"
+                      "      h ^= (h << 8) & 0xff00ff00u; h ^= (h << 16) & 0xffff0000u; un |= h ^ d;\n",
+                      b, b);
+        s += buf;
+        std::snprintf(buf, sizeof buf,
+                      "      s0 |= (p%d & 1u) << %d; c0 |= ((d >> 1) & 1u) << %d; "
+                      "c1 |= ((d >> 2) & 1u) << %d;\n"
+                      "      c2 |= ((d >> 4) & 1u) << %d; c3 |= ((d >> 8) & 1u) << %d; "
+                      "c4 |= ((d >> 16) & 1u) << %d; }\n",
+                      b, b, b, b, b, b, b);
+        s += buf;
+      } else {
+        std::snprintf(buf, sizeof buf, "    un |= p%d ^ (u32)((int)p%d >> 31); s0 |= p%d & 0x%xu;\n",
+                      b, b, b, 1u << b);
+        s += buf;
+      }
     }
-    s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n      u32 a[32] = {";
-    for (int b = 0; b < 32; ++b) {
-      s += ((V >> b) & 1ull) ? "p" + std::to_string(b) : std::string("0u");
-      s += b < 31 ? ", " : "};\n";
+    s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n";
+    s += "      u32* const kq = perm_out + (base + lane - start);\n";
+    for (int pass = 0; pass < 2; ++pass) {
+      s += pass == 0 ? "      if (full) {\n" : "      } else {\n";
+      s += "        u32 sv = s0;\n";
+      for (int t = 0; t < 32; ++t) {
+        const int l = t ^ (t >> 1);
+        if (t) {
+          const int k = __builtin_ctz((unsigned)t);
+          std::snprintf(buf, sizeof buf, "        sv ^= c%d;\n", k);
+          s += buf;
+        }
+        if (pass == 0)
+          std::snprintf(buf, sizeof buf, "        __stcs(kq + QSIM_OFF(%d), sv);\n", l);
+        else
+          std::snprintf(buf, sizeof buf,
+                        "        { const u64 addr = base + lane + QSIM_OFF(%d); "
+                        "if (addr >= start && addr < end) __stcs(kq + QSIM_OFF(%d), sv); }\n",
+                        l, l);
+        s += buf;
+      }
     }
-    s += transpose_code("a", "      ");
-    s += thread_stores("perm_out", "const u32 rv = a[l] | inv;", "      ");
-    s += "      continue;\n    }\n";
+    s += "      }\n      continue;\n    }\n";
   }
   s += "    u32 a[32] = {";
   for (int b = 0; b < 32; ++b) {

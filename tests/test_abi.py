@@ -177,9 +177,8 @@ def test_jit_source_compiles_without_gpu(q):
         assert rc == q.OK, L.qsim_last_error().decode()
 
 
-def test_jit_build_thread_bits_source_compiles_without_gpu(q, monkeypatch):
-    """The build kernel's opt-in in-thread fast path (QSIM_BUILD_THREAD_BITS=1)."""
-    monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "1")
+def test_jit_build_thread_bits_source_compiles_without_gpu(q):
+    """The build kernel's in-thread affine fast path."""
     L = q.lib()
     for gates, M in ((wl.CONFIGS["cfg5"].gates(), 32), (wl.random_gates(96, 14, 5), 22)):
         g = np.ascontiguousarray(gates)

@@ -1,7 +1,8 @@
 """GPU parity of the in-thread output bits (qsim_api.cu thread_bits; the
 NVRTC build and on-the-fly input kernels): a thread's 32 outputs differ in 5
 output bits J chosen so that their sources differ in few address bits V;
-the fast path gathers the other bits once per thread.  The map is integer
+the build's fast path takes the 32 sources as one source XOR combinations
+of 5 difference columns (when V's planes are affine in J, checked per warp).  The map is integer
 work: bit-exact against the oracle, with J at any position,
 ragged ranges, and tiles where a sampled-away influence sends the warp down
 the general path."""
@@ -14,12 +15,6 @@ import workloads as wl
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 DEV = "cuda:0"
-
-
-@pytest.fixture(autouse=True)
-def _build_thread_bits(monkeypatch):
-    # the build kernel's in-thread bits are opt-in (measured slower by default)
-    monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "1")
 
 
 @pytest.fixture(scope="module")
@@ -53,8 +48,9 @@ def test_build_thread_bits_full(q, kind):
         circuits = [wl.random_gates(64, M, sd) for sd in (122, 126, 127, 120, 3)]
     elif kind == "structured":      # bits 14..21 never move
         circuits = [wl.random_gates(96, 14, 5)]
-    else:                           # SWAP renaming + NOT/CNOT/CCNOT
-        circuits = [wl.random_gates_ext(64, M, 9, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP))]
+    else:                           # SWAP renaming + NOT/CNOT/CCNOT (on bits 0..15, and on all)
+        kinds = (wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP)
+        circuits = [wl.random_gates_ext(64, 16, 9, kinds=kinds), wl.random_gates_ext(64, M, 9, kinds=kinds)]
     fast = 0
     for gates in circuits:
         got, name = _build(q, gates, M, 0, 1 << M)
@@ -96,8 +92,8 @@ def test_build_thread_bits_off_equals_on(q, monkeypatch):
     off, name_off = _build(q, gates, M, 0, 1 << M)
     monkeypatch.setenv("QSIM_THREAD_BITS", "1")
     monkeypatch.setenv("QSIM_BUILD_THREAD_BITS", "0")
-    default, name_def = _build(q, gates, M, 0, 1 << M)
-    assert "J 5.6.7.8.9" in name_def
-    assert np.array_equal(on, default)
+    plain, name_plain = _build(q, gates, M, 0, 1 << M)
+    assert "J 5.6.7.8.9" in name_plain
+    assert np.array_equal(on, plain)
     assert "J 5.6.7.8.9" in name_off and _nv(name_off) == 0
     assert np.array_equal(on, off)
