@@ -892,7 +892,7 @@ qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ 
 std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int ng,
                         const uint8_t* pos, const uint8_t* J, int L, int nv) {
   std::string s = kPrelude;
-  char buf[320];
+  char buf[640];
   const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
   int minb = 1;  // resident CTAs asked of ptxas (register cap); A/B via QSIM_KRON_MINB
@@ -940,11 +940,32 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   s += walk_code(w, n, M);
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
 
+  const char* aff_env = std::getenv("QSIM_KRON_AFFINE");  // A/B: affine fast path
+  const bool affine = aff_env && aff_env[0] == '1';
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
       std::snprintf(buf, sizeof buf, "    un |= %s ^ (0u - (%s & 1u));\n", P(k).c_str(), P(k).c_str());
       s += buf;
+    }
+    if (affine) {  // table-0 index of entry l = x0 ^ (columns of the set bits of l)
+      s += "    u32 x0 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u;\n";
+      for (int k = 0; k < nv; ++k) {
+        const std::string pk = P(k);
+        std::snprintf(buf, sizeof buf,
+                      "    { const u32 d = %s ^ (0u - (%s & 1u)); u32 h = d & 0x00010116u;\n"
+                      "      h ^= (h << 1) & 0xaaaaaaaau; h ^= (h << 2) & 0xccccccccu; "
+                      "h ^= (h << 4) & 0xf0f0f0f0u;\n"
+                      "      h ^= (h << 8) & 0xff00ff00u; h ^= (h << 16) & 0xffff0000u; un |= h ^ d;\n",
+                      pk.c_str(), pk.c_str());
+        s += buf;
+        std::snprintf(buf, sizeof buf,
+                      "      x0 |= (%s & 1u) << %d; c0 |= ((d >> 1) & 1u) << %d; c1 |= ((d >> 2) & 1u) << %d;\n"
+                      "      c2 |= ((d >> 4) & 1u) << %d; c3 |= ((d >> 8) & 1u) << %d; "
+                      "c4 |= ((d >> 16) & 1u) << %d; }\n",
+                      pk.c_str(), k, k, k, k, k, k);
+        s += buf;
+      }
     }
     s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n";
     for (int g = 0; g < ng; ++g) {
@@ -963,15 +984,41 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
       std::snprintf(buf, sizeof buf, "      cc = cmul(cc, T[%d | i%d]);\n", g << gb, g);
       s += buf;
     }
-    s += "      u32 a[32] = {";
-    for (int k = 0; k < 32; ++k) {
-      s += k < nv ? P(k) : std::string("0u");
-      s += k < 31 ? ", " : "};\n";
+    if (affine) {
+      s += "      C* const kq = k2 + (base + lane - start);\n";
+      for (int pass = 0; pass < 2; ++pass) {
+        s += pass == 0 ? "      if (full) {\n" : "      } else {\n";
+        s += "        u32 x = x0 | i0;\n";
+        for (int t = 0; t < 32; ++t) {
+          const int l = t ^ (t >> 1);
+          if (t) {
+            std::snprintf(buf, sizeof buf, "        x ^= c%d;\n", __builtin_ctz((unsigned)t));
+            s += buf;
+          }
+          if (pass == 0)
+            std::snprintf(buf, sizeof buf,
+                          "        __stcs(kq + QSIM_OFF(%d), negate_if(cmul(cc, T[x]), (sg >> %d) & 1u));\n",
+                          l, l);
+          else
+            std::snprintf(buf, sizeof buf,
+                          "        { const u64 addr = base + lane + QSIM_OFF(%d); if (addr >= start && "
+                          "addr < end) __stcs(kq + QSIM_OFF(%d), negate_if(cmul(cc, T[x]), (sg >> %d) & 1u)); }\n",
+                          l, l, l);
+          s += buf;
+        }
+      }
+      s += "      }\n      continue;\n    }\n";
+    } else {
+      s += "      u32 a[32] = {";
+      for (int k = 0; k < 32; ++k) {
+        s += k < nv ? P(k) : std::string("0u");
+        s += k < 31 ? ", " : "};\n";
+      }
+      s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+      s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+      s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+      s += "      continue;\n    }\n";
     }
-    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
-    s += "      continue;\n    }\n";
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
