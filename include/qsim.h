@@ -52,6 +52,8 @@
  *   QSIM_THREAD_BITS=0       NVRTC threads walk output bits 5..9, no hoisted
  *                            product (on-the-fly input 1.5-2x slower)
  *   QSIM_THREAD_BITS_SAMPLES=k  circuit sample size of the in-thread bits (tests)
+ *   QSIM_DEBUG_STORE=seq|none  TIMING EXPERIMENTS ONLY, results invalid: the planned
+ *                            fused kernel stores k2 in counter order / not at all
  *   QSIM_KRON_AFFINE=1       affine (Gray-code) fast path in the on-the-fly input
  *                            kernel instead of the V-plane transpose (measured neutral)
  *   QSIM_BUILD_THREAD_BITS=0 build kernel without its in-thread affine fast path

@@ -429,6 +429,12 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
                 elem == 8 && !pair && pipelined() ? 1 : 0, pair ? 1 : 0);
   s += buf;
   s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
+  {  // QSIM_DEBUG_STORE=seq|none: timing experiments on the store side (results invalid)
+    const char* ds = std::getenv("QSIM_DEBUG_STORE");
+    std::snprintf(buf, sizeof buf, "#define QSIM_DEBUG_STORE %d\n",
+                  ds && !std::strcmp(ds, "seq") ? 1 : ds && !std::strcmp(ds, "none") ? 2 : 0);
+    s += buf;
+  }
   s += "__constant__ unsigned int lt_g[32] = {";
   for (int l = 0; l < 32; ++l) {
     uint32_t o = (l & 1) ? pair_xor : 0u;
@@ -573,8 +579,17 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
+#if QSIM_DEBUG_STORE == 1   // timing experiment only (wrong result): k2 in counter order
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
+          stcs(k2 + (c + 32u * (h + l) + lane), negate_if(v[l], (sg >> (h + l)) & 1u));
+#elif QSIM_DEBUG_STORE == 2  // timing experiment only (wrong result): loads, no k2
+        u32 x = 0u;
+        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) x ^= v[l].x;
+        if (x == 0x9e3779b9u) stcs(k2 + c, v[0]);
+#else
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
           stcs(k2 + (ob ^ lt[h + l] ^ lo), negate_if(v[l], (sg >> (h + l)) & 1u));
+#endif
       }
 #endif
     }

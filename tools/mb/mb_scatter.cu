@@ -34,6 +34,22 @@ __global__ void __launch_bounds__(256) move(const uint4* __restrict__ src, uint4
   }
 }
 
+// read-only: random blocks, each read once, XOR-reduced (a store only if the
+// impossible value shows up)
+template <int B>
+__global__ void __launch_bounds__(256) readonly(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                uint64_t nchunks, int blk_bits) {
+  constexpr int CPB = B / 16;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks; i += stride) {
+    const uint64_t blk = i / CPB, c = i % CPB;
+    const uint4 v = src[mix(blk, blk_bits) * CPB + c];
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
+}
+
 template <typename F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -76,6 +92,9 @@ int main() {
     while ((1ull << bits) < BYTES / BB) ++bits;                                                    \
     rep("gather", BB, timeit([&] { move<BB, false><<<grid, 256>>>(src, dst, n, bits); }));        \
     rep("scatter", BB, timeit([&] { move<BB, true><<<grid, 256>>>(src, dst, n, bits); }));         \
+    { float ms = timeit([&] { readonly<BB><<<grid, 256>>>(src, dst, n, bits); });                  \
+      printf("{\"case\": \"readonly\", \"block_B\": %d, \"ms\": %.3f, \"GBps_read\": %.0f}\n", BB, ms, \
+             BYTES / (ms * 1e-3) / 1e9); }                                                          \
   }
   CASE(16) CASE(32) CASE(64) CASE(128) CASE(256) CASE(512) CASE(2048) CASE(8192)
   return 0;

@@ -1,0 +1,103 @@
+// mb_window.cu -- microbenchmark (NOT the product path): the step's k1 read
+// pattern in isolation.  Every 128-byte line of a 32 GiB buffer is read once,
+// as its four 32-byte sectors, by different threads at different times: the
+// lines are visited in a random order (a bijection), in windows of W lines;
+// inside a window all lines' sector 0 are read, then sector 1, ... (so a
+// line's sectors arrive W requests apart, well within L2 residency).  Loads
+// plain or with the .L2::128B / .L2::256B prefetch-size qualifier.  Decides
+// whether the L2 fetches a missing sector alone (four DRAM accesses per line)
+// and whether the qualifier makes it fetch the line.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o mb_window mb_window.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint64_t mix(uint64_t x, int bits) {
+  const uint64_t m = (1ull << bits) - 1;
+  x = (x * 0x9e3779b97f4a7c15ull) & m;
+  x ^= x >> (bits / 2);
+  x = (x * 0xbf58476d1ce4e5b9ull) & m;
+  x ^= x >> (bits / 3);
+  x = (x * 0x94d049bb133111ebull) & m;
+  return x;
+}
+
+template <int Q>
+__device__ __forceinline__ uint4 ld32(const uint4* p) {  // first 16 B of a sector
+  uint4 r;
+  if (Q == 0)
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  else if (Q == 1)
+    asm volatile("ld.global.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  else
+    asm volatile("ld.global.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
+// request r (0 .. 4 * nlines): window w = r / (4W), visit t = (r / W) % 4,
+// line = mix(w * W + r % W), sector (t + line) % 4 (the first-touched sector
+// of a line is random).  PF: 0 none; 1 prefetch.global.L2 of the line by
+// every request; 2 the same by sector-0 requests only; 3 cp.async.bulk
+// prefetch of the 128-byte line by sector-0 requests
+template <int Q, int PF>
+__global__ void __launch_bounds__(256) win(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                           uint64_t nreq, int line_bits, int wbits) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t acc = 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nreq; r += stride) {
+    const uint64_t w = r >> (wbits + 2), t = (r >> wbits) & 3, j = r & ((1ull << wbits) - 1);
+    const uint64_t line = mix((w << wbits) | j, line_bits);
+    const uint64_t c = (t + line) & 3;
+    const uint4* lp = src + line * 8;
+    if (PF == 1 || (PF == 2 && c == 0)) asm volatile("prefetch.global.L2 [%0];" ::"l"(lp));
+    if (PF == 3 && c == 0) asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(lp) : "memory");
+    const uint4 v = ld32<Q>(lp + c * 2);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
+}
+
+int main() {
+  const uint64_t BYTES = 32ull << 30, nlines = BYTES / 128, nreq = nlines * 4;
+  int line_bits = 0;
+  while ((1ull << line_bits) < nlines) ++line_bits;
+  uint4 *src, *dst;
+  if (cudaMalloc(&src, BYTES) != cudaSuccess || cudaMalloc(&dst, 64) != cudaSuccess) {
+    printf("oom\n");
+    return 1;
+  }
+  cudaMemset(src, 1, BYTES);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  struct Case { int q, pf; const char* name; };
+  const Case cases[] = {{0, 0, "-"}};
+  [[maybe_unused]] const Case unused[] = {{1, 0, "ld.L2::128B"}, {0, 1, "prefetch.L2 every request"},
+                        {0, 2, "prefetch.L2 by sector-0 requests"},
+                        {0, 3, "cp.async.bulk.prefetch 128 B by sector-0 requests"}};
+  for (int wbits : {0, 1, 2, 3, 4, 5, 6, 8, 10}) {
+    for (const Case& cs : cases) {
+      float best = 1e30f;
+      for (int rep = 0; rep < 3; ++rep) {
+        cudaEventRecord(a);
+        if (cs.q == 0 && cs.pf == 0) win<0, 0><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.q == 1 && cs.pf == 0) win<1, 0><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 1) win<0, 1><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 2) win<0, 2><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 3) win<0, 3><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep && ms < best) best = ms;
+      }
+      printf("{\"window_lines\": %llu, \"variant\": \"%s\", \"ms\": %.3f, \"line_GBps\": %.0f, \"err\": \"%s\"}\n",
+             1ull << wbits, cs.name, best, BYTES / (best * 1e-3) / 1e9,
+             cudaGetErrorString(cudaGetLastError()));
+      fflush(stdout);
+    }
+  }
+  return 0;
+}
