@@ -477,7 +477,10 @@ def run_qsim(args):
                      "frac": achieved / hbm, "frac_of_8TBps": achieved * 1e9 / 8e12,
                      "traffic": ncu_traffic(args.config, "map_gather"),
                      "algorithmic_bytes_per_launch": bytes_mg,
-                     "algorithmic_bytes_per_entry": 4 + 2 * e},
+                     "algorithmic_bytes_per_entry": 4 + 2 * e,
+                     "note": "DRAM traffic ~1.04x algorithmic (ncu); bound: the random k1 reads, "
+                             "fetched by L2 as separate 32-B sectors unless a line's sectors share "
+                             "one warp instruction (DESIGN.md section 6, profiles/r01_mb_window.jsonl)"},
         "modes": {
             "map_gather_1pass": {"ms": mg_ms, "GBps": achieved, "entries_per_s": N / (mg_ms * 1e-3),
                                  "launches_per_step": launches_mg / args.steps},
