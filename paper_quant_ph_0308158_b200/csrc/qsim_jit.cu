@@ -730,6 +730,10 @@ std::string fused_lt_source(const uint32_t* w, int n, int M, const uint32_t* lin
   }
   std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n", M);
   s += buf;
+  {  // QSIM_DEBUG_STORE=none: timing experiment on the store side (results invalid)
+    const char* ds = std::getenv("QSIM_DEBUG_STORE");
+    s += ds && !std::strcmp(ds, "none") ? "#define QSIM_DEBUG_STORE 2\n" : "#define QSIM_DEBUG_STORE 0\n";
+  }
   s += R"(
 extern "C" __global__ void __launch_bounds__(256)
 qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ k1,
@@ -839,6 +843,11 @@ qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ 
   s += R"(
       uint2 v[32];
       _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
+#if QSIM_DEBUG_STORE == 2   // timing experiment only (wrong result): loads, no stores
+      { u32 x = 0u; _Pragma("unroll") for (int l = 0; l < 32; ++l) x ^= v[l].x;
+        if (x == 0x9e3779b9u) k2[0] = v[0]; }
+      continue;
+#endif
       if (perm_out) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l) sp[wpc[l] ^ wpl] = a[l];
         __syncwarp();

@@ -1,10 +1,6 @@
-# cover granule A/B (QSIM_PLAN_GRANULE_BYTES: 32 = sector, the default; 64; 128 = L1 line)
+# reads-only time (QSIM_DEBUG_STORE=none, results invalid): sector-cover plan vs linear traversal
 {
-for gb in 32 64 128; do
-  for T in 12 13 14; do
-    for m in map_gather fused; do
-      QSIM_PLAN_GRANULE_BYTES=$gb QSIM_PLAN_COVER_BITS=$T QSIM_PLAN_COVER_FIXED=1 timeout 120 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/granule=$gb T=$T /"
-    done
-  done
+for env in "QSIM_DEBUG_STORE=none" "QSIM_DEBUG_STORE=none QSIM_PLAN_LINEAR=1 QSIM_PLAN_COVER_FIXED=1" "QSIM_PLAN_LINEAR=1 QSIM_PLAN_COVER_FIXED=1"; do
+  env $env timeout 120 python tools/diag_planned.py cfg5 fused | tail -1 | sed "s/^/$env /"
 done
-} > gpurun_out/diag_granule.log 2>&1
+} > gpurun_out/diag_lt2.log 2>&1
