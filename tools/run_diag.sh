@@ -1,6 +1,9 @@
-# reads-only time (QSIM_DEBUG_STORE=none, results invalid): sector-cover plan vs linear traversal
+# tile order inside a chunk (QSIM_JIT_TILE_ROT = r: the tile's low r bits pick the block)
 {
-for env in "QSIM_DEBUG_STORE=none" "QSIM_DEBUG_STORE=none QSIM_PLAN_LINEAR=1 QSIM_PLAN_COVER_FIXED=1" "QSIM_PLAN_LINEAR=1 QSIM_PLAN_COVER_FIXED=1"; do
-  env $env timeout 120 python tools/diag_planned.py cfg5 fused | tail -1 | sed "s/^/$env /"
+for r in 0 1 2; do
+  for m in map_gather fused; do
+    QSIM_JIT_TILE_ROT=$r timeout 120 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/rot=$r /"
+  done
+  QSIM_JIT_TILE_ROT=$r timeout 120 python tools/diag_planned.py cfg5 map_gather chunk=16 | tail -1 | sed "s/^/rot=$r /"
 done
-} > gpurun_out/diag_lt2.log 2>&1
+} > gpurun_out/diag_rot.log 2>&1
