@@ -318,6 +318,33 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
   const int nv = __builtin_popcountll(V);
   if (nv == 0 || nv > maxv) return;
   if (require_affine && nonaffine * 16 > S) return;  // the affine fast path would mostly fail
+  // the kernels check per warp (32 threads = output bits 0..4): one thread
+  // whose bits outside V move, or (build) whose sources are not affine in J,
+  // sends the whole warp tile down the general path -- sample whole warps
+  const int W = n > 1024 ? 4 : 16;
+  int failed = 0;
+  for (int w = 0; w < W; ++w) {
+    const uint64_t b0 = (start + next() % count) & ~Jm & ~31ull;
+    bool ok = true;
+    for (uint64_t lane = 0; lane < 32 && ok; ++lane) {
+      uint64_t sc[32];
+      for (int c = 0; c < 32; ++c) {
+        uint64_t x = b0 | lane;
+        for (int k = 0; k < 5; ++k)
+          if ((c >> k) & 1) x |= 1ull << J[k];
+        sc[c] = walk_src(g, n, x);
+        ok = ok && ((sc[0] ^ sc[c]) & ~V) == 0;
+      }
+      for (int c = 1; c < 32 && ok && require_affine; ++c) {
+        uint64_t lin = sc[0];
+        for (int k = 0; k < 5; ++k)
+          if ((c >> k) & 1) lin ^= sc[0] ^ sc[1 << k];
+        ok = lin == sc[c];
+      }
+    }
+    failed += !ok;
+  }
+  if (failed * 8 > W) return;  // more than 1 in 8 warp tiles would take the general path
   for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)J[k];
   tb->L = L;
   tb->V = V;

@@ -39,6 +39,26 @@ __global__ void k_store_tile16(uint32_t* out, uint64_t ntiles, uint32_t v) {
   }
 }
 
+// build-like tile with in-thread bits J: lane = output bits 0..4, store l at
+// the J-combination offset, tiles enumerate the other bits (zero-insertion)
+__global__ void k_store_tile_j(uint32_t* out, uint64_t ntiles, uint32_t v, int j0, int j1, int j2,
+                               int j3, int j4) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const int J[5] = {j0, j1, j2, j3, j4};
+  for (uint64_t tile = (uint64_t)blockIdx.x * 8u + warp; tile < ntiles; tile += (uint64_t)gridDim.x * 8u) {
+    uint64_t base = tile << 5;
+    for (int k = 0; k < 5; ++k) base = (base & ((1ull << J[k]) - 1)) | ((base >> J[k]) << (J[k] + 1));
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      uint64_t off = 0;
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        if ((l >> k) & 1) off |= 1ull << J[k];
+      __stcs(out + base + off + lane, v + l);
+    }
+  }
+}
+
 int main() {
   const uint64_t bytes = 16ull << 30, nwords = bytes / 4;
   uint32_t* out;
@@ -74,6 +94,13 @@ int main() {
     run(n, [&] { k_store_tile<<<sms * k, 256>>>(out, nwords >> 10, 1u); });
     snprintf(n, sizeof n, "tile u128 grid=%dxSM", k);
     run(n, [&] { k_store_tile16<<<sms * k, 256>>>(out, nwords >> 10, 1u); });
+  }
+  const int Js[5][5] = {{5, 6, 7, 8, 9}, {7, 8, 13, 26, 29}, {11, 13, 22, 23, 24}, {8, 13, 15, 21, 29},
+                        {5, 14, 21, 30, 31}};
+  for (int t = 0; t < 5; ++t) {
+    char n[96];
+    snprintf(n, sizeof n, "tile u32 J=%d.%d.%d.%d.%d grid=8xSM", Js[t][0], Js[t][1], Js[t][2], Js[t][3], Js[t][4]);
+    run(n, [&] { k_store_tile_j<<<sms * 8, 256>>>(out, nwords >> 10, 1u, Js[t][0], Js[t][1], Js[t][2], Js[t][3], Js[t][4]); });
   }
   cudaFree(out);
   return 0;
