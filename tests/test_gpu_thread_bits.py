@@ -97,3 +97,31 @@ def test_build_thread_bits_off_equals_on(q, monkeypatch):
     assert np.array_equal(on, plain)
     assert "J 5.6.7.8.9" in name_off and _nv(name_off) == 0
     assert np.array_equal(on, off)
+
+
+def test_thread_bits_long_circuit_on_quiet_bits(q):
+    """1500 gates (> 1024: the host samples 16 points and 4 warps) on bits
+    0..15 of M = 23: bits 16..22 are quiet, so both kernels take their fast
+    paths.  The map equals the ahead-of-time per-lane walk byte for byte and
+    the oracle on sampled outputs; the on-the-fly input equals the per-lane
+    kernel byte for byte."""
+    M = 23
+    gates = wl.random_gates(1500, 16, 21)
+    got, name = _build(q, gates, M, 0, 1 << M)
+    assert _nv(name) > 0, name
+    ref = torch.empty(1 << M, dtype=torch.int32, device=DEV)
+    q.build_map_range(gates, M, 0, 1 << M, ref, walk=q.WALK_PER_LANE)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, ref.cpu().numpy().view(np.uint32))
+    rng = np.random.default_rng(5)
+    idx = np.concatenate([np.arange(64), rng.integers(0, 1 << M, 3000), np.arange((1 << M) - 64, 1 << M)])
+    assert np.array_equal(got[idx], oracle.walk_many(gates, idx.astype(np.uint64)))
+    qb = wl.random_qubits(M, 3, "c64")
+    a = torch.empty(1 << M, dtype=torch.complex64, device=DEV)
+    b = torch.empty_like(a)
+    q.run_fused_kron(gates, M, qb, a, dtype="c64", walk=q.WALK_JIT)
+    kname = q.last_kernel()
+    q.run_fused_kron(gates, M, qb, b, dtype="c64", walk=q.WALK_PER_LANE)
+    torch.cuda.synchronize()
+    assert _nv(kname) > 0, kname
+    assert a.cpu().numpy().tobytes() == b.cpu().numpy().tobytes()
