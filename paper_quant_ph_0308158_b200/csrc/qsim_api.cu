@@ -1034,6 +1034,7 @@ struct PlanOpts {
   int cover_bits = 13;    // largest sector cover (counter bits of one L1-resident block)
   bool fixed = false;     // always cover_bits (else the smallest cover holding >= 90 %)
   bool lane_run = false;  // lanes on output bits 0..4 (bits 3, 4 added to the cover)
+  bool cover_order = false;  // cover bits by sector-mate weight (lanes, thread bits first)
 };
 
 PlanOpts default_plan_opts() {
@@ -1041,6 +1042,7 @@ PlanOpts default_plan_opts() {
   if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) o.cover_bits = std::atoi(cb);
   if (const char* fx = std::getenv("QSIM_PLAN_COVER_FIXED")) o.fixed = fx[0] == '1';
   if (const char* lr = std::getenv("QSIM_PLAN_LANE_RUN")) o.lane_run = lr[0] == '1';
+  if (const char* co = std::getenv("QSIM_PLAN_COVER_ORDER")) o.cover_order = co[0] == '1';
   return o;
 }
 
@@ -1107,6 +1109,30 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
       plan->sigma[k++] = (uint8_t)b;
     else
       order[m++] = b;
+  }
+  {
+    if (opts.cover_order) {
+      // cover bits beyond the kept ones ordered by how much of the sampled
+      // sector-mate reader differences they carry: the commonest land on the
+      // lane bits (counter 3, 4: same warp instruction) and the thread's bits
+      // (5..9: back-to-back instructions)
+      const int keep = plan_keep_bits(dtype);
+      double w[32] = {0};
+      const int e2 = elem_bytes(dtype), eps = 32 / e2;
+      for (int t = 0; t < 2048; ++t) {
+        const uint32_t i = (uint32_t)(plan_mix(0x0dd5ull + t) % (1ull << M));
+        const uint32_t src = plan_forward_walk(pg.get(), n, i);
+        for (int r = 1; r < eps; ++r) {
+          const uint32_t d = plan_inverse_walk(pg.get(), n, src ^ (uint32_t)r) ^ i;
+          if (d == 0 || (d & ~V)) continue;
+          const double wt = 1.0 / __builtin_popcount(d);
+          for (int b = 0; b < M; ++b)
+            if ((d >> b) & 1u) w[b] += wt;
+        }
+      }
+      std::stable_sort(plan->sigma + keep, plan->sigma + k,
+                       [&](uint8_t x, uint8_t y) { return w[x] > w[y]; });
+    }
   }
   std::stable_sort(order, order + m, [&](int x, int y) { return count[x] > count[y]; });
   for (int j = 0; j < m; ++j) plan->sigma[k++] = (uint8_t)order[j];
@@ -1694,6 +1720,7 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     o.fixed = true;
     opts.push_back(o);
   }
+
   std::vector<qsim_plan> cands;
   std::vector<int> idx;
   for (size_t i = 0; i < opts.size(); ++i) {

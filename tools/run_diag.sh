@@ -1,9 +1,10 @@
-# tile order inside a chunk (QSIM_JIT_TILE_ROT = r: the tile's low r bits pick the block)
+# cover-bit order inside the cover (QSIM_PLAN_COVER_ORDER=1: commonest sector-mate difference bits on lanes / thread bits)
 {
-for r in 0 1 2; do
-  for m in map_gather fused; do
-    QSIM_JIT_TILE_ROT=$r timeout 120 python tools/diag_planned.py cfg5 $m | tail -1 | sed "s/^/rot=$r /"
+for co in 0 1; do
+  for sd in 4 6 8; do
+    for m in map_gather fused; do
+      QSIM_PLAN_COVER_ORDER=$co timeout 120 python tools/diag_planned.py seed:$sd $m | tail -1 | sed "s/^/order=$co /"
+    done
   done
-  QSIM_JIT_TILE_ROT=$r timeout 120 python tools/diag_planned.py cfg5 map_gather chunk=16 | tail -1 | sed "s/^/rot=$r /"
 done
-} > gpurun_out/diag_rot.log 2>&1
+} > gpurun_out/diag_order.log 2>&1

@@ -28,17 +28,18 @@ def main():
     perm = torch.empty(N, dtype=torch.int32, device="cuda")
     ws = q.workspace()
     print("M,seed,map_gather_ms,apply_ms,entries_per_s,spread_nat_log2,spread_sigma_log2,"
-          "cover_contained,sigma")
+          "cover_contained,tuned_variant,sigma")
     for seed in map(int, args.seeds.split(",")):
         gates = wl.random_gates(args.ngates, M, seed)
         plan = q.plan_create(gates, M, "c64")
+        variant = -1
         if args.tune:
-            q.plan_tune(plan, gates, perm, k1, k2, ws)
+            variant = q.plan_tune(plan, gates, perm, k1, k2, ws)
         t = timeit(lambda: q.map_gather_planned(plan, gates, perm, k1, k2, ws), reps=3)
         ta = timeit(lambda: q.apply_map_planned(plan, perm, k1, k2, ws), reps=3)
         sp = plan.reserved_spread
         print(f"{M},{seed},{t:.3f},{ta:.3f},{N / t * 1e3:.3e},{sp & 255},{sp >> 8},"
-              f"{plan.tile_contained:.3f},{'-'.join(map(str, list(plan.sigma)[:M]))}", flush=True)
+              f"{plan.tile_contained:.3f},{variant},{'-'.join(map(str, list(plan.sigma)[:M]))}", flush=True)
 
 
 if __name__ == "__main__":
