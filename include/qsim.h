@@ -394,8 +394,10 @@ int qsim_graph_destroy(qsim_graph *graph);
 /* Number of kernel launches the last successful call on this thread
  * enqueued (for launch accounting in bench.py).                            */
 int32_t qsim_last_launch_count(void);
-/* Name of the last kernel the last planned call on this thread launched
- * ("qsim_jit_fused_lt", "qsim_jit_fused", "k_fused_sigma", ...; "" if none). */
+/* Name of the last kernel the last planned call, build_map or run_fused_kron
+ * call on this thread launched ("qsim_jit_fused", "k_fused_sigma",
+ * "qsim_jit_build (J 7.8.13.26.29, L 32, nv 5)" -- the in-thread output bits,
+ * block size and varying source bits --, ...; "" if none).                 */
 const char *qsim_last_kernel(void);
 
 const char *qsim_strerror(int32_t code);

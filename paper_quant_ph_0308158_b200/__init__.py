@@ -340,7 +340,8 @@ def workspace(device=None):
 
 
 def last_kernel() -> str:
-    """Kernel the last planned call on this thread launched (diagnostics)."""
+    """Kernel the last planned, build_map or run_fused_kron call on this thread
+    launched (diagnostics; see qsim_last_kernel in include/qsim.h)."""
     return _lib.qsim_last_kernel().decode()
 
 
