@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-log2", type=int, default=28,
+    ap.add_argument("--cpu-sample-log2", type=int, default=29,
                     help="outputs in the oracle's bounded sample (log2)")
     return ap.parse_args()
 
