@@ -43,8 +43,8 @@
  *   QSIM_JIT_PIPE=1          software pipeline in the fused kernel (measured neutral)
  *   QSIM_PLAN_COVER_BITS=T   sector-cover size of new plans (default 13)
  *   QSIM_PLAN_RUN_BITS=r     contiguous output bits kept in the cover (default 3)
- *   QSIM_PLAN_COVER_ORDER=1  new plans order the cover bits by sector-mate weight
- *                            (measured: never better than the tuned variants)
+ *   QSIM_PLAN_COVER_ORDER=1|2  new plans order the cover bits by sector-mate weight
+ *                            from counter bit 3 | 5 (measured: no better than tuned)
  *   QSIM_PLAN_GRANULE_BYTES=g  cover g-byte mates instead of 32-byte sector mates
  *                            (64 / 128 measured no faster)
  *   QSIM_PLAN_LINEAR=1       linear-traversal plans (measured slower on cfg5)

@@ -1034,7 +1034,7 @@ struct PlanOpts {
   int cover_bits = 13;    // largest sector cover (counter bits of one L1-resident block)
   bool fixed = false;     // always cover_bits (else the smallest cover holding >= 90 %)
   bool lane_run = false;  // lanes on output bits 0..4 (bits 3, 4 added to the cover)
-  bool cover_order = false;  // cover bits by sector-mate weight (lanes, thread bits first)
+  int cover_order = 0;  // cover bits by sector-mate weight: 1 from counter bit 3, 2 from bit 5
 };
 
 PlanOpts default_plan_opts() {
@@ -1042,7 +1042,7 @@ PlanOpts default_plan_opts() {
   if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) o.cover_bits = std::atoi(cb);
   if (const char* fx = std::getenv("QSIM_PLAN_COVER_FIXED")) o.fixed = fx[0] == '1';
   if (const char* lr = std::getenv("QSIM_PLAN_LANE_RUN")) o.lane_run = lr[0] == '1';
-  if (const char* co = std::getenv("QSIM_PLAN_COVER_ORDER")) o.cover_order = co[0] == '1';
+  if (const char* co = std::getenv("QSIM_PLAN_COVER_ORDER")) o.cover_order = std::atoi(co);
   return o;
 }
 
@@ -1130,7 +1130,8 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
             if ((d >> b) & 1u) w[b] += wt;
         }
       }
-      std::stable_sort(plan->sigma + keep, plan->sigma + k,
+      const int from = opts.cover_order == 2 ? std::min(k, 5) : keep;  // 2: lanes unchanged
+      std::stable_sort(plan->sigma + from, plan->sigma + k,
                        [&](uint8_t x, uint8_t y) { return w[x] > w[y]; });
     }
   }
