@@ -969,7 +969,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
-      std::snprintf(buf, sizeof buf, "    un |= %s ^ (0u - (%s & 1u));\n", P(k).c_str(), P(k).c_str());
+      std::snprintf(buf, sizeof buf, "    un |= %s ^ (u32)((int)%s >> 31);\n", P(k).c_str(), P(k).c_str());
       s += buf;
     }
     if (affine) {  // table-0 index of entry l = x0 ^ (columns of the set bits of l)
