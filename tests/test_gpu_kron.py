@@ -273,3 +273,29 @@ def test_kron_thread_layout_beyond_32_qubits_ragged(q, dtype):
     assert np.all(ga[count:] == 3.0)
     for s0, c0 in ((0, 3000), (count // 2, 3000), (count - 3000, 3000)):
         _check(ga[s0:s0 + c0], oracle.fused_kron(gates, qb, start + s0, c0), M, dtype)
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_kron_at_63_qubits(q, dtype):
+    """The largest M the 64-bit walk takes (M = 63): portions at both ends and
+    in the middle, and a 2^22 + 77 portion ending at the last output (the
+    in-thread layout with cut blocks), NVRTC == per-lane kernel byte for byte,
+    within the oracle's bound."""
+    if not q.jit_status().startswith("ready"):
+        pytest.skip("JIT unavailable")
+    M = 63
+    N = 1 << M
+    gates = wl.random_gates_ext(96, M, 63)
+    qb = wl.random_qubits(M, 17, dtype)
+    for start, count in ((0, 5000), (N - 5000, 5000), ((1 << 62) + 12345, 7777),
+                         (N - (1 << 22) - 77, (1 << 22) + 77)):
+        outs = {}
+        for w in (q.WALK_JIT, q.WALK_PER_LANE):
+            out = _out(count, dtype)
+            q.run_fused_kron(gates, M, qb, out, start=start, count=count, dtype=dtype, walk=w)
+            torch.cuda.synchronize()
+            outs[w] = out.cpu().numpy()[:count]
+        assert outs[q.WALK_JIT].tobytes() == outs[q.WALK_PER_LANE].tobytes(), (start, count)
+        for s0 in sorted({0, max(count - 3000, 0)}):
+            c0 = min(3000, count - s0)
+            _check(outs[q.WALK_JIT][s0:s0 + c0], oracle.fused_kron(gates, qb, start + s0, c0), M, dtype)
