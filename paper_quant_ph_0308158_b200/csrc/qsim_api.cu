@@ -1192,11 +1192,16 @@ void launch_apply_sigma_u(int bps, unsigned blocks, const qsim::SigmaParams& sp,
   qsim::k_apply_sigma<T, U, THREADS><<<blocks, THREADS, 0, st>>>(sp, perm, N, k1, k2);
 }
 
+// gathers in flight per thread, capped so the register budget of large CTAs
+// holds them without spills (complex128 entries take four registers each)
 template <typename T, int U>
 void launch_apply_sigma_t(uint32_t threads, int bps, unsigned blocks, const qsim::SigmaParams& sp,
                           const uint32_t* perm, uint64_t N, const T* k1, T* k2, cudaStream_t st) {
-  if (threads == 512) launch_apply_sigma_u<T, U, 512>(bps, blocks, sp, perm, N, k1, k2, st);
-  else if (threads == 1024) launch_apply_sigma_u<T, (U > 16 ? 16 : U), 1024>(bps, blocks, sp, perm, N, k1, k2, st);
+  constexpr bool wide = sizeof(T) == 16;
+  constexpr int U512 = wide && U > 16 ? 16 : U;
+  constexpr int U1024 = wide ? (U > 8 ? 8 : U) : (U > 16 ? 16 : U);
+  if (threads == 512) launch_apply_sigma_u<T, U512, 512>(bps, blocks, sp, perm, N, k1, k2, st);
+  else if (threads == 1024) launch_apply_sigma_u<T, U1024, 1024>(bps, blocks, sp, perm, N, k1, k2, st);
   else launch_apply_sigma_u<T, U, 256>(bps, blocks, sp, perm, N, k1, k2, st);
 }
 

@@ -748,3 +748,17 @@ def test_plan_tune_keeps_a_valid_plan(q):
     q.run_fused_planned(plan, gates, k1_d, out2, q.workspace())
     torch.cuda.synchronize()
     assert out2.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_aot_fallback_launch_shapes(q):
+    """Without NVRTC (QSIM_NO_JIT=1, a subprocess: the switch is read once per
+    process) the planned calls run the ahead-of-time kernels; every launch
+    shape (CTA threads x gathers in flight) gives the oracle's bytes."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QSIM_NO_JIT="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "aot_fallback_check.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "aot fallback ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
