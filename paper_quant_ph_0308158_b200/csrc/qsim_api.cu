@@ -603,8 +603,9 @@ int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const
   for (int j = 0; j < M; ++j)
     for (int c = 0; c < 4; ++c) qb.v[j][c] = qubits[4 * j + c];
   if (count == 0) return QSIM_OK;
-  KronLayout ly;
-  kron_layout(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start, count, true, &ly);
+  KronLayout ly;  // without NVRTC the ahead-of-time kernels run: keep their identity layout
+  kron_layout(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start,
+              qsim::jit_available() ? count : 0, true, &ly);
   for (int k = 0; k < 64; ++k) {
     qb.pos[k] = ly.pos[k];
     if (ly.pos[k] != k) qb.permuted = 1;

@@ -47,4 +47,18 @@ for dtype in ("c64", "c128"):
                 assert k2_d.cpu().numpy().tobytes() == ref, (dtype, threads, ilp, call, q.last_kernel())
                 if call == "map_gather":
                     assert np.array_equal(pm.cpu().numpy().view(np.uint32), perm_ref)
+# input on the fly without NVRTC (identity table layout), within the rounding bound
+import math  # noqa: E402
+Mk = 22
+gk = wl.random_gates(64, Mk, 8)
+for dtype in ("c64", "c128"):
+    qb = wl.random_qubits(Mk, 4, dtype)
+    out = torch.empty(1 << Mk, dtype=torch.complex64 if dtype == "c64" else torch.complex128, device="cuda")
+    q.run_fused_kron(gk, Mk, qb, out, dtype=dtype)
+    torch.cuda.synchronize()
+    assert q.last_kernel() == "k_fused_kron_bitsliced", q.last_kernel()
+    ref = oracle.fused_kron(gk, qb)
+    u = 2.0 ** -24 if dtype == "c64" else 2.0 ** -53
+    err = np.abs(out.cpu().numpy().astype(np.complex128) - ref)
+    assert np.all(err <= 1.01 * (Mk - 1) * math.sqrt(5.0) * u * np.abs(ref)), dtype
 print("aot fallback ok")
