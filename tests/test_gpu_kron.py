@@ -299,3 +299,23 @@ def test_kron_at_63_qubits(q, dtype):
         for s0 in sorted({0, max(count - 3000, 0)}):
             c0 = min(3000, count - s0)
             _check(outs[q.WALK_JIT][s0:s0 + c0], oracle.fused_kron(gates, qb, start + s0, c0), M, dtype)
+
+
+@pytest.mark.slow
+def test_kron_c128_full_size_sampled(q):
+    """complex128 at M = 32: 2^32 outputs, 64 GiB written without any input
+    in memory; sampled outputs within the oracle's bound."""
+    M, N = 32, 1 << 32
+    gates = wl.CONFIGS["cfg5"].gates()
+    qb = wl.random_qubits(M, 2025, "c128")
+    out = torch.empty(N, dtype=torch.complex128, device=DEV)
+    q.run_fused_kron(gates, M, qb, out, dtype="c128")
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    idx = np.concatenate([[0, 1, N - 1], rng.integers(0, N, 3000, dtype=np.uint64)]).astype(np.uint64)
+    src = oracle.walk_many(gates, idx)
+    ref = np.array([oracle.kron_element(qb, int(s)) for s in src])
+    got = out.index_select(0, torch.from_numpy(idx.astype(np.int64)).to(DEV)).cpu().numpy()
+    _check(got, ref, M, "c128")
+    del out
+    torch.cuda.empty_cache()

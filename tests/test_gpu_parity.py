@@ -762,3 +762,23 @@ def test_aot_fallback_launch_shapes(q):
     r = subprocess.run([sys.executable, os.path.join(root, "tests", "aot_fallback_check.py")],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "aot fallback ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.slow
+def test_build_max_gates_full_size(q):
+    """Maximum sizes together: M = 32 (2^32 outputs, perm 16 GiB) and the
+    largest gate list the parameter bank takes (QSIM_MAX_GATES), through the
+    NVRTC build kernel; sampled outputs against the oracle's walk, and the
+    map is a bijection on the samples' images (no two sampled outputs share
+    a source)."""
+    M, n = 32, q.MAX_GATES
+    gates = wl.random_gates(n, M, 404)
+    perm = torch.empty(1 << M, dtype=torch.int32, device=DEV)
+    q.build_map(gates, M, perm)
+    torch.cuda.synchronize()
+    idx = _sample_indices(M, 20000, 9)
+    got = perm.index_select(0, torch.from_numpy(idx.astype(np.int64)).to(DEV)).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, oracle.walk_many(gates, idx.astype(np.uint64)).astype(np.uint32))
+    assert len(np.unique(got)) == len(np.unique(idx))
+    del perm
+    torch.cuda.empty_cache()
