@@ -58,6 +58,46 @@ __global__ void __launch_bounds__(256) win(const uint4* __restrict__ src, uint4*
   if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
 }
 
+// PF == 4: sector-0 requests copy the whole 128-byte line into shared memory
+// with one TMA bulk copy (cp.async.bulk, mbarrier completion); every thread
+// then still loads its own sector.  Is a bulk copy one line-sized L2 request?
+__global__ void __launch_bounds__(256) win_tma(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                               uint64_t nreq, int line_bits, int wbits) {
+  __shared__ __align__(128) uint4 slot[256][8];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t bar_a = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_a), "r"(256u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t acc = 0, phase = 0;
+  for (uint64_t r0 = (uint64_t)blockIdx.x * blockDim.x; r0 < nreq; r0 += stride) {
+    const uint64_t r = r0 + tid;
+    const uint64_t w = r >> (wbits + 2), t = (r >> wbits) & 3, j = r & ((1ull << wbits) - 1);
+    const uint64_t line = mix((w << wbits) | j, line_bits);
+    const uint64_t c = (t + line) & 3;
+    const uint4* lp = src + line * 8;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&slot[tid][0]);
+    if (c == 0) {
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 128;" ::"r"(bar_a) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];"
+                   ::"r"(sa), "l"(lp), "r"(bar_a) : "memory");
+    } else {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_a) : "memory");
+    }
+    const uint4 v = ld32<0>(lp + c * 2);
+    acc ^= v.x ^ v.w;
+    asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+                 "@!P1 bra W_%=;\n}\n" ::"r"(bar_a), "r"(phase) : "memory");
+    phase ^= 1u;
+    acc ^= slot[tid][0].x;
+  }
+  if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
+}
+
 int main(int argc, char** argv) {
   const uint64_t BYTES = 32ull << 30, nlines = BYTES / 128, nreq = nlines * 4;
   int line_bits = 0;
@@ -90,6 +130,21 @@ int main(int argc, char** argv) {
   [[maybe_unused]] const Case unused[] = {{1, 0, "ld.L2::128B"}, {0, 1, "prefetch.L2 every request"},
                         {0, 2, "prefetch.L2 by sector-0 requests"},
                         {0, 3, "cp.async.bulk.prefetch 128 B by sector-0 requests"}};
+  for (int wbits : {5, 10, 14}) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      win_tma<<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (rep && ms < best) best = ms;
+    }
+    printf("{\"window_lines\": %llu, \"variant\": \"TMA bulk 128-B line copy by sector-0 requests\", \"ms\": %.3f, \"line_GBps\": %.0f, \"err\": \"%s\"}\n",
+           1ull << wbits, best, BYTES / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+  }
   for (int wbits : {0, 4, 5, 10, 14}) {
     for (const Case& cs : cases) {
       float best = 1e30f;
