@@ -98,6 +98,38 @@ __global__ void __launch_bounds__(256) win_tma(const uint4* __restrict__ src, ui
   if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
 }
 
+// PF == 5: the FIRST visit of each line (t == 0) is designated; the warp
+// loads every designated line whole with cooperative instructions (four lanes
+// per line, 16 bytes at each sector start: one instruction covers 8 lines),
+// then every thread loads its own sector.  Emulates a traversal in which a
+// line's first reader knows it is first.
+__global__ void __launch_bounds__(256) win_coop(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                uint64_t nreq, int line_bits, int wbits) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t acc = 0;
+  for (uint64_t r0 = (uint64_t)blockIdx.x * blockDim.x; r0 < nreq; r0 += stride) {
+    const uint64_t r = r0 + threadIdx.x;
+    const uint64_t w = r >> (wbits + 2), t = (r >> wbits) & 3, j = r & ((1ull << wbits) - 1);
+    const uint64_t line = mix((w << wbits) | j, line_bits);
+    const uint64_t c = (t + line) & 3;
+    const uint32_t mask = __ballot_sync(0xffffffffu, t == 0);
+    const int nd = __popc(mask);
+    for (int k = 0; k < nd; k += 8) {
+      const int jd = k + (int)(lane >> 2);
+      const int srcl = jd < nd ? (int)__fns(mask, 0, jd + 1) : 0;
+      const uint64_t ln = __shfl_sync(0xffffffffu, line, srcl);
+      if (jd < nd) {
+        const uint4 v = ld32<0>(src + ln * 8 + (lane & 3u) * 2);
+        acc ^= v.y;
+      }
+    }
+    const uint4 v = ld32<0>(src + line * 8 + c * 2);
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x9e3779b9u) dst[0] = make_uint4(acc, 0, 0, 0);
+}
+
 int main(int argc, char** argv) {
   const uint64_t BYTES = 32ull << 30, nlines = BYTES / 128, nreq = nlines * 4;
   int line_bits = 0;
@@ -130,11 +162,27 @@ int main(int argc, char** argv) {
   [[maybe_unused]] const Case unused[] = {{1, 0, "ld.L2::128B"}, {0, 1, "prefetch.L2 every request"},
                         {0, 2, "prefetch.L2 by sector-0 requests"},
                         {0, 3, "cp.async.bulk.prefetch 128 B by sector-0 requests"}};
+  const int bps = argc > 2 ? atoi(argv[2]) : 8;  // CTAs per SM (grid stride = time granularity)
+  for (int wbits : {14, 16, 17, 19}) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      win_coop<<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms;
+      cudaEventElapsedTime(&ms, a, b);
+      if (rep && ms < best) best = ms;
+    }
+    printf("{\"window_lines\": %llu, \"ctas_per_sm\": %d, \"variant\": \"first visit: warp-cooperative whole-line load\", \"ms\": %.3f, \"line_GBps\": %.0f, \"err\": \"%s\"}\n",
+           1ull << wbits, bps, best, BYTES / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+  }
   for (int wbits : {5, 10, 14}) {
     float best = 1e30f;
     for (int rep = 0; rep < 3; ++rep) {
       cudaEventRecord(a);
-      win_tma<<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+      win_tma<<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
@@ -145,16 +193,16 @@ int main(int argc, char** argv) {
            1ull << wbits, best, BYTES / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
     fflush(stdout);
   }
-  for (int wbits : {0, 4, 5, 10, 14}) {
+  for (int wbits : {0, 4, 5, 10, 14, 19, 20}) {
     for (const Case& cs : cases) {
       float best = 1e30f;
       for (int rep = 0; rep < 3; ++rep) {
         cudaEventRecord(a);
-        if (cs.q == 0 && cs.pf == 0) win<0, 0><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
-        if (cs.q == 1 && cs.pf == 0) win<1, 0><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
-        if (cs.pf == 1) win<0, 1><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
-        if (cs.pf == 2) win<0, 2><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
-        if (cs.pf == 3) win<0, 3><<<sms * 8, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.q == 0 && cs.pf == 0) win<0, 0><<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.q == 1 && cs.pf == 0) win<1, 0><<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 1) win<0, 1><<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 2) win<0, 2><<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
+        if (cs.pf == 3) win<0, 3><<<sms * bps, 256>>>(src, dst, nreq, line_bits, wbits);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms;
