@@ -242,8 +242,23 @@ uint64_t walk_src(const qsim_gate* g, int n, uint64_t x) {
   return x;
 }
 
+// Blocks of 2^L outputs hold whole tiles: a range that is not aligned to
+// them computes part of its first and last block for nothing -- allow that
+// up to 1/8 of the count.  Returns L (10 when no larger block fits).
+int range_block_bits(int M, uint64_t start, uint64_t count) {
+  const uint64_t end = start + count;
+  int L = M;
+  auto ok = [&](int l) {
+    const uint64_t B = 1ull << l, m = B - 1;
+    return ((start & m) == 0 && (end & m) == 0) || (B <= count / 16);
+  };
+  while (L > 10 && !ok(L)) --L;
+  return L;
+}
+
+// jmax: in-thread bits are chosen below min(L, jmax)
 void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t count, int maxv,
-                 bool require_affine, ThreadBits* tb) {
+                 bool require_affine, ThreadBits* tb, int jmax = 64) {
   for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)(5 + k);
   tb->L = 10;
   tb->V = 0;
@@ -251,17 +266,10 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
   // from the count where AUTO takes the NVRTC kernels: below it the
   // ahead-of-time kernels run, which would pay a per-entry bit permutation
   if ((env && env[0] == '0') || M < 12 || count < kJitMinCount) return;
-  const uint64_t end = start + count;
-  // blocks of 2^L outputs hold whole tiles: a range that is not aligned to
-  // them computes part of its first and last block for nothing -- allow
-  // that up to 1/8 of the count
-  int L = M;
-  auto ok = [&](int l) {
-    const uint64_t B = 1ull << l, m = B - 1;
-    return ((start & m) == 0 && (end & m) == 0) || (B <= count / 16);
-  };
-  while (L > 10 && !ok(L)) --L;
+  const int L = range_block_bits(M, start, count);
   if (L <= 10) return;
+  const int jtop = std::min(L, jmax);
+  if (jtop < 10) return;
   uint64_t h = 0x9e3779b97f4a7c15ull ^ ((uint64_t)M << 32) ^ (uint64_t)n;
   auto next = [&]() {  // splitmix64
     uint64_t z = (h += 0x9e3779b97f4a7c15ull);
@@ -278,13 +286,13 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
     tb->s0[i] = walk_src(g, n, tb->xs[i]);
   }
   uint64_t infl[64] = {0};
-  for (int j = 5; j < L; ++j)
+  for (int j = 5; j < jtop; ++j)
     for (int i = 0; i < S; ++i) infl[j] |= tb->s0[i] ^ walk_src(g, n, tb->xs[i] ^ (1ull << j));
   uint64_t V = 0, Jm = 0;
   int J[5];
   for (int k = 0; k < 5; ++k) {
     int best = -1, bc = 99;
-    for (int j = 5; j < L; ++j) {
+    for (int j = 5; j < jtop; ++j) {
       if ((Jm >> j) & 1ull) continue;
       const int c = __builtin_popcountll(V | infl[j]);
       if (c < bc) bc = c, best = j;
@@ -392,21 +400,39 @@ struct KronLayout {
   int L, nv;
 };
 
+// The table grouping decides the rounding of every entry, so it depends on
+// the circuit alone (never on the range or the call history): the in-thread
+// bits J and the varying source bits V are sampled once over the whole
+// output space [0, 2^M) with a fixed seed -- output portions then glue byte
+// for byte.  J is chosen below bit 28 when M > 32 (so 2^32-entry portions
+// aligned to 2^28 can use it).  The traversal of a range uses the circuit's J
+// when its blocks hold them (L > max J), else the default J and the general
+// path (same tables, same products, same bytes).
 void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t start, uint64_t count,
-                 bool cached, KronLayout* ly) {
+                 bool jit, KronLayout* ly) {
   for (int k = 0; k < 64; ++k) ly->pos[k] = (uint8_t)k;
+  for (int k = 0; k < 5; ++k) ly->J[k] = (uint8_t)(5 + k);
+  ly->L = 10;
+  ly->nv = 0;
+  if (ng < 2) return;
   ThreadBits tb;
-  if (ng < 2) {
-    thread_bits(g, n, M, start, 0, gb, false, &tb);  // default J (count 0: no sampling)
-  } else if (cached) {
-    thread_bits_cached(1, g, n, M, start, count, gb, &tb);
-  } else {
-    thread_bits(g, n, M, start, count, gb, false, &tb);
+  {
+    ThreadBitsCache& c = g_tb_cache[1];
+    std::lock_guard<std::mutex> lk(c.mu);
+    const char* e1 = std::getenv("QSIM_THREAD_BITS");
+    const char* e2 = std::getenv("QSIM_THREAD_BITS_SAMPLES");
+    const std::string env = std::string(e1 ? e1 : "-") + "/" + (e2 ? e2 : "-");
+    const bool hit = c.env == env && c.M == M && c.maxv == gb && c.gates.size() == (size_t)n &&
+                     (n == 0 || std::memcmp(c.gates.data(), g, sizeof(qsim_gate) * n) == 0);
+    if (!hit) {
+      thread_bits(g, n, M, 0, 1ull << M, gb, false, &c.tb, M > 32 ? 28 : 64);
+      c.gates.assign(g, g + n);
+      c.env = env;
+      c.M = M, c.maxv = gb, c.start = 0, c.count = 1ull << M;
+    }
+    tb = c.tb;
   }
-  for (int k = 0; k < 5; ++k) ly->J[k] = tb.J[k];
-  ly->L = tb.L;
   const uint64_t V = tb.V;
-  ly->nv = __builtin_popcountll(V);
   if (!V) return;
   uint64_t lanes = 0;
   for (int j = 0; j < 5; ++j)
@@ -422,6 +448,15 @@ void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t star
     if (((G0 & ~V) >> b) & 1ull) ly->pos[k++] = (uint8_t)b;
   for (int b = 0; b < M; ++b)
     if (!((G0 >> b) & 1ull)) ly->pos[k++] = (uint8_t)b;
+  // the range's traversal (speed only)
+  if (!jit || count < kJitMinCount) return;
+  const int L = range_block_bits(M, start, count);
+  int jhi = 0;
+  for (int j = 0; j < 5; ++j) jhi = std::max(jhi, (int)tb.J[j]);
+  if (L <= 10 || jhi >= L) return;
+  for (int j = 0; j < 5; ++j) ly->J[j] = tb.J[j];
+  ly->L = L;
+  ly->nv = __builtin_popcountll(V);
 }
 
 // build kernel fast path up to this many varying address bits per thread
@@ -603,9 +638,8 @@ int kron_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const
   for (int j = 0; j < M; ++j)
     for (int c = 0; c < 4; ++c) qb.v[j][c] = qubits[4 * j + c];
   if (count == 0) return QSIM_OK;
-  KronLayout ly;  // without NVRTC the ahead-of-time kernels run: keep their identity layout
-  kron_layout(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start,
-              qsim::jit_available() ? count : 0, true, &ly);
+  KronLayout ly;  // the table grouping is the circuit's (same bytes for every range and kernel)
+  kron_layout(gates, n, M, (int)qb.gbits, (int)qb.ngroups, start, count, qsim::jit_available(), &ly);
   for (int k = 0; k < 64; ++k) {
     qb.pos[k] = ly.pos[k];
     if (ly.pos[k] != k) qb.permuted = 1;
@@ -1704,11 +1738,20 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
 int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
                    const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
   g_launches = 0;
-  if (!plan || !workspace) return QSIM_EINVAL;
+  if (!plan || !workspace || !aligned16(workspace)) return QSIM_EINVAL;
   int rc = plan_validate(plan);
   if (rc) return rc;
   if ((rc = check_gates(gates, n_gates, plan->M))) return rc;
   if (has_phase(gates, n_gates)) return QSIM_EINVAL;  // tunes the map + gather step
+  {  // the buffers every trial call uses (validated once, before anything runs)
+    const uint64_t N = 1ull << plan->M;
+    const int e = elem_bytes(plan->dtype);
+    if (!perm || !k1 || !k2 || !aligned16(perm) || !aligned16(k1) || !aligned16(k2))
+      return QSIM_EINVAL;
+    if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e) ||
+        overlap(perm, N * 4, k1, N * e))
+      return QSIM_EALIAS;
+  }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // candidates: the default rule, the full cover, each with lanes on output bits 0..4,
   // and smaller full covers
@@ -1772,6 +1815,11 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       best = t_best;
       best_i = (int)i;
     }
+  }
+  if (rc != QSIM_OK || best_i < 0) {  // a trial failed: nothing was kept
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return rc != QSIM_OK ? rc : QSIM_EINVAL;
   }
   // second stage: the chunk size of the kept order (2^14 / 2^16 next to 2^15)
   qsim_plan kept = cands[best_i];
@@ -1915,6 +1963,10 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }
+  if (qsim::jit_check_compile_apply(plan->M, plan->sigma, elem_bytes(plan->dtype), err) != 0) {
+    std::snprintf(g_err, sizeof g_err, "jit (apply): %s", err.c_str());
+    return QSIM_ECUDA;
+  }
   if ((plan->flags & 2u) && qsim::jit_check_compile_local(gl->w, n_gates, plan->M,
                                                           elem_bytes(plan->dtype),
                                                           local_tile_bits(plan->dtype), err) != 0) {
@@ -1941,7 +1993,7 @@ int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t
   uint32_t gb = 0, ng = 0;
   kron_groups(M, elem_bytes(dtype), &gb, &ng);
   KronLayout ly;  // the layout of a call over all 2^M outputs
-  kron_layout(gates, n_gates, M, (int)gb, (int)ng, 0, 1ull << M, false, &ly);
+  kron_layout(gates, n_gates, M, (int)gb, (int)ng, 0, 1ull << M, true, &ly);
   if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), (int)gb, (int)ng, ly.pos,
                                    ly.J, ly.L, ly.nv, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());

@@ -408,6 +408,14 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // circuit and the traversal order compiled in).  If perm_out is non-null the
 // kernel also stores the map (one-pass materialised map + gather).
 // QSIM_JIT_PIPE=1 enables the software pipeline of the fused kernel (A/B)
+// CTA size of the gather kernels: 256, plus the dedicated prefetch warps of
+// the experimental QSIM_PF modes 5 / 6
+unsigned gather_threads() {
+  int m = 0, d = 0, g = 0, w = 2;
+  if (const char* pf = std::getenv("QSIM_PF")) std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
+  return m >= 5 ? 256u + 32u * (unsigned)w : 256u;
+}
+
 bool pipelined() {
   const char* v = std::getenv("QSIM_JIT_PIPE");
   return v && v[0] == '1';  // default off: measured neutral (map+gather) to 4 % slower (fused)
@@ -443,12 +451,132 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
     std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
     s += buf;
   }
+  // plane initialisation: output bit b comes from counter bit inv[b]: a lane
+  // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob);
+  // then the walk and the transpose: a[l] = source of the thread's entry l
+  auto walk_tile = [&]() {
+    std::string t;
+    const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
+    uint8_t inv[32];
+    for (int b = 0; b < 32; ++b) inv[b] = 255;
+    for (int k = 0; k < M; ++k) inv[sigma[k]] = (uint8_t)k;
+    for (int b = 0; b < 32; ++b) {
+      const int c = b < M ? inv[b] : 255;
+      if (c < 5)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, c);
+      else if (c < 10)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[c - 5]);
+      else if (c < 32)
+        std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
+      else
+        std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
+      t += buf;
+      if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
+        std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
+        t += buf;
+      }
+    }
+    t += "    u32 sg = 0u;\n";
+    t += walk_code(w, n, M);
+    t += "      u32 a[32] = {";
+    for (int b = 0; b < 32; ++b) {
+      std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
+      t += buf;
+    }
+    t += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+    t += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+    return t;
+  };
+  // Line prefetch ahead of the gather (experimental; QSIM_PF="mode,D,G"):
+  // while a CTA gathers chunk ch it walks chunk ch + D and, for every source
+  // whose low G bits are zero (one "leader" per 2^G-entry granule of k1),
+  // asks for the whole granule in one request, so the granule's readers
+  // find it in L2.  mode 1: warp-cooperative 16-B cp.async (8 / 16 lanes per
+  // 128 / 256-B granule); 2: cp.async.bulk.prefetch.L2 of the granule by the
+  // leader lane; 3: prefetch.global.L2 by the leader lane.
+  int pf_mode = 0, pf_d = 0, pf_g = elem == 8 ? 4 : 3, pf_w = 2;
+  if (const char* pf = std::getenv("QSIM_PF")) std::sscanf(pf, "%d,%d,%d,%d", &pf_mode, &pf_d, &pf_g, &pf_w);
+  // modes 5 / 6: the prefetch runs in pf_w dedicated warps (6: control, no loads)
+  std::snprintf(buf, sizeof buf, "#define QSIM_PF_MODE %d\n#define QSIM_PF_D %d\n#define QSIM_PF_G %d\n"
+                "#define QSIM_PF_W %d\n#define QSIM_PF_SPEC %d\n#define QSIM_THREADS %d\n",
+                pf_mode, pf_d, pf_g, pf_w, pf_mode >= 5 ? 1 : 0, pf_mode >= 5 ? 256 + 32 * pf_w : 256);
+  s += buf;
+  // the prefetch of one warp tile (1024 outputs of chunk pch): sources, then
+  // a whole-granule request for every source whose low G bits are zero
+  auto pf_sources = [&]() -> std::string {
+    if (from_perm)  // from the map (L2-resident when the gather re-reads it)
+      return R"(
+        u32 a[32];
+        { const u32 lo = tab[0][lane];
+          _Pragma("unroll") for (int l = 0; l < 32; ++l) a[l] = perm_out[ob ^ lt_g[l] ^ lo]; }
+)";
+    return walk_tile() + "        (void)sg;\n";
+  };
+  auto pf_issue = []() -> std::string {
+    return R"(
+        constexpr u32 GM = (1u << QSIM_PF_G) - 1u;
+        constexpr u32 GB = sizeof(QSIM_T) << QSIM_PF_G;   // granule bytes
+#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4 || QSIM_PF_MODE == 5 || QSIM_PF_MODE == 6
+        constexpr u32 LPG = GB / 16u;                     // lanes per granule
+        constexpr u32 GPI = 32u / LPG;                    // granules per instruction
+        u32 cnt = 0u;
+        const u32 ltm = (1u << lane) - 1u;
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+          const bool pr = (a[l] & GM) == 0u;
+          const u32 bal = __ballot_sync(0xffffffffu, pr);
+          if (pr) q[cnt + __popc(bal & ltm)] = a[l] >> QSIM_PF_G;
+          cnt += __popc(bal);
+        }
+        __syncwarp();
+        for (u32 j = 0; j < cnt; j += GPI) {
+          const u32 idx = j + lane / LPG;
+          if (idx < cnt) {
+            const u32 line = q[idx];
+#if QSIM_PF_MODE == 4 || QSIM_PF_MODE == 6   // control: the queue without the loads
+            if (line == 0xffffffffu)
+#endif
+            {
+              const char* src = reinterpret_cast<const char*>(k1) + (u64)line * GB + (lane % LPG) * 16u;
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
+                           :: "r"((u32)__cvta_generic_to_shared(scr + lane * 16u)), "l"(src)
+                           : "memory");
+            }
+          }
+        }
+        __syncwarp();
+#else
+        _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+          if ((a[l] & GM) == 0u) {
+            const char* src = reinterpret_cast<const char*>(k1 + a[l]);
+#if QSIM_PF_MODE == 2
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(GB) : "memory");
+#else
+            asm volatile("prefetch.global.L2 [%0];" :: "l"(src) : "memory");
+#endif
+          }
+        }
+#endif
+)";
+  };
   s += R"(
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(QSIM_THREADS)
 QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
            QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
   __shared__ u32 tab[4][256];
   __shared__ u64 s_chunk;
+#if QSIM_PF_SPEC
+  __shared__ u32 s_done;
+  __shared__ u32 pf_q[QSIM_PF_W * 1024];
+  __shared__ __align__(16) unsigned char pf_scratch[QSIM_PF_W * 512];
+  if (threadIdx.x == 0) { s_done = 0u; s_chunk = ~0ull; }
+#define QSIM_BAR() asm volatile("bar.sync 1, 256;" ::: "memory")
+#else
+#define QSIM_BAR() __syncthreads()
+#endif
+#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4
+  __shared__ u32 pf_q[8 * 1024];
+  __shared__ __align__(16) unsigned char pf_scratch[8 * 512];
+#endif
   for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
     const int b = x >> 8, v = x & 255;
     u32 r = 0;
@@ -466,50 +594,69 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   u32 pob = 0u, psg = 0u;
   bool pend = false;
 #endif
+#if QSIM_PF_SPEC
+  __syncthreads();
+  if (warp >= 8) {  // dedicated prefetch warps: follow the CTA's chunk, D chunks ahead
+    const u32 pw = warp - 8u;
+    u64 last = ~0ull;
+    for (;;) {
+      const u64 ch = *reinterpret_cast<volatile u64*>(&s_chunk);
+      if (*reinterpret_cast<volatile u32*>(&s_done)) break;
+      if (ch == last || ch == ~0ull) { __nanosleep(256); continue; }
+      last = ch;
+      const u64 pch = ch + QSIM_PF_D;
+      if (pch >= nchunks) continue;
+      for (u32 tt = pw; tt < tiles; tt += QSIM_PF_W) {
+        const u64 c = (pch << chunk_log2) + ((u64)tt << 10);
+        const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
+                       tab[3][(c >> 24) & 255];
+        u32* q = pf_q + pw * 1024u;
+        unsigned char* scr = pf_scratch + pw * 512u;
+)";
+    s += pf_sources() + pf_issue();
+    s += R"(
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+#endif
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
-    __syncthreads();
+    QSIM_BAR();
+    if (threadIdx.x == 0) {
+      s_chunk = atomicAdd(ticket, 1ull);
+#if QSIM_PF_SPEC
+      if (s_chunk >= nchunks) s_done = 1u;
+#endif
+    }
+    QSIM_BAR();
     const u64 ch = s_chunk;
     if (ch >= nchunks) break;
+)";
+  if (pf_mode >= 1 && pf_mode <= 4) {
+    s += R"(
+    if (ch + QSIM_PF_D < nchunks) {
+      const u64 pch = ch + QSIM_PF_D;
+      for (u32 tt = warp; tt < tiles; tt += 8u) {
+        const u64 c = (pch << chunk_log2) + ((u64)tt << 10);
+        const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
+                       tab[3][(c >> 24) & 255];
+        u32* q = pf_q + warp * 1024u;
+        unsigned char* scr = pf_scratch + warp * 512u;
+)";
+    s += pf_sources() + pf_issue();
+    s += R"(
+      }
+    }
+)";
+  }
+  s += R"(
     for (u32 tt = warp; tt < tiles; tt += 8u) {
       const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
       const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
                      tab[3][(c >> 24) & 255];
 )";
-  if (!from_perm) {
-  // plane initialisation: output bit b comes from counter bit inv[b]: a lane
-    // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob)
-    const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-    uint8_t inv[32];
-    for (int b = 0; b < 32; ++b) inv[b] = 255;
-    for (int k = 0; k < M; ++k) inv[sigma[k]] = (uint8_t)k;
-    for (int b = 0; b < 32; ++b) {
-      const int c = b < M ? inv[b] : 255;
-      if (c < 5)
-        std::snprintf(buf, sizeof buf, "      u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, c);
-      else if (c < 10)
-        std::snprintf(buf, sizeof buf, "      u32 p%d = %s;\n", b, pat[c - 5]);
-      else if (c < 32)
-        std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-      else
-        std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
-      s += buf;
-      if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
-        std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
-        s += buf;
-      }
-    }
-    s += "    u32 sg = 0u;\n";
-    s += walk_code(w, n, M);
-    s += "      u32 a[32] = {";
-    for (int b = 0; b < 32; ++b) {
-      std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-      s += buf;
-    }
-    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-  }
+  if (!from_perm) s += walk_tile();
   // output offsets of the 32 word bits: sigma(l << 5), compile-time
   s += "      const u32 lt[32] = {";
   for (int l = 0; l < 32; ++l) {
@@ -594,6 +741,9 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
 #endif
     }
   }
+#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4
+  asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
 #if QSIM_PIPE
   if (pend) {
     const u32 lo = tab[0][lane];
@@ -1351,6 +1501,14 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
     keyw.push_back((uint32_t)elem);
     keyw.push_back(pair_xor);
+    if (const char* pf = std::getenv("QSIM_PF")) {  // experimental prefetch (see fused_source)
+      int m = 0, d = 0, g = 0, w = 2;
+      std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
+      keyw.push_back(0x70660000u | (uint32_t)m);
+      keyw.push_back((uint32_t)d);
+      keyw.push_back((uint32_t)g);
+      keyw.push_back((uint32_t)w);
+    }
     // the source is only generated on a cache miss
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), 0x66757365ull);
     for (const Entry& e : g_cache[key])
@@ -1367,7 +1525,7 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     err = "ticket reset failed";
     return -1;
   }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, gather_threads(), 1, 1, 0, (CUstream)st, args, nullptr) !=
       CUDA_SUCCESS) {
     err = "cuLaunchKernel failed";
     return -1;
@@ -1525,6 +1683,14 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
     std::vector<uint32_t> keyw;
     for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
     keyw.push_back((uint32_t)elem);
+    if (const char* pf = std::getenv("QSIM_PF")) {  // experimental prefetch (see fused_source)
+      int m = 0, d = 0, g = 0, w = 2;
+      std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
+      keyw.push_back(0x70660000u | (uint32_t)m);
+      keyw.push_back((uint32_t)d);
+      keyw.push_back((uint32_t)g);
+      keyw.push_back((uint32_t)w);
+    }
     const uint64_t kind = 0x6170706c79ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
@@ -1542,7 +1708,7 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
     err = "ticket reset failed";
     return -1;
   }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, gather_threads(), 1, 1, 0, (CUstream)st, args, nullptr) !=
       CUDA_SUCCESS) {
     err = "cuLaunchKernel failed";
     return -1;
@@ -1599,6 +1765,17 @@ int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T
   }
   std::vector<char> cubin;
   return compile_cubin_locked(local_source(words, n, M, elem, T), cubin, err) ? 0 : -1;
+}
+
+int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& err) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nvrtc.ok) {
+    err = g_status;
+    return -1;
+  }
+  std::vector<char> cubin;
+  return compile_cubin_locked(fused_source(nullptr, 0, M, sigma, 0u, elem, true), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,

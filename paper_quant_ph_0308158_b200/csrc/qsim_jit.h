@@ -58,6 +58,7 @@ int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32
 int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,
               const void* k1, void* k2, void* ticket, int blocks, cudaStream_t st,
               std::string& err);
+int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& err);
 // Circuits whose targets all lie below bit T: tiles of 2^T outputs read their
 // own tile of k1, staged in shared memory by TMA bulk copies (double-buffered).
 int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,

@@ -1,0 +1,170 @@
+"""Full-size, element-by-element parity for BASELINE.json cfg3, cfg4 and cfg5.
+
+Every one of the 2^26 / 2^30 / 2^32 outputs of every mode is compared with the
+CPU oracle (perm as uint32, k2 as raw entry bytes; readings R14/R15):
+
+* the oracle (oracle/qsim_oracle.c, single-threaded C, driven on disjoint
+  output ranges from host threads by oracle/parallel.py) computes
+  perm[i] = f_1(...f_n(i)) and k2[i] = k1[perm[i]] for all i (P:L35, P:L43,
+  readings R1/R2) -- about 1.5 minutes per config on 16 host cores;
+* the CUDA path runs through the C ABI: the plain calls of the north star
+  (qsim_build_map, qsim_apply_map, qsim_run_fused), the planned calls with the
+  default plan (qsim_plan_create) AND with the plan qsim_plan_tune keeps (the
+  kernel instance bench.py times), and the end-to-end host-buffer call
+  (qsim_run_host);
+* each output is copied back in 512 MiB chunks and compared byte for byte;
+  a failure names the mode and the first mismatching output index.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import oracle.parallel as opar
+import workloads as wl
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+DEV = "cuda:0"
+CHUNK_BYTES = 1 << 29
+
+
+@pytest.fixture(scope="module")
+def q():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+    __graft_entry__.build_native()
+    import paper_quant_ph_0308158_b200 as q
+    return q
+
+
+def _first_mismatch(got: np.ndarray, want: np.ndarray, unit: int) -> int:
+    g = got.view(np.uint8).reshape(-1, unit)
+    w = want.view(np.uint8).reshape(-1, unit)
+    return int(np.flatnonzero((g != w).any(axis=1))[0])
+
+
+def _compare(dev_u8, ref: np.ndarray, unit: int, label: str) -> None:
+    """dev_u8: device uint8 tensor holding ref.nbytes bytes; unit: bytes per entry."""
+    ref_u8 = ref.view(np.uint8).reshape(-1)
+    assert dev_u8.numel() >= ref_u8.size, label
+    for s in range(0, ref_u8.size, CHUNK_BYTES):
+        e = min(ref_u8.size, s + CHUNK_BYTES)
+        got = dev_u8[s:e].cpu().numpy()
+        if not np.array_equal(got, ref_u8[s:e]):
+            i = s // unit + _first_mismatch(got, ref_u8[s:e], unit)
+            pytest.fail(f"{label}: first mismatch at output {i} "
+                        f"(got {got[(i * unit - s):(i * unit - s) + unit].tobytes().hex()}, "
+                        f"want {ref_u8[i * unit:(i + 1) * unit].tobytes().hex()})")
+
+
+def _host_compare(got: np.ndarray, ref: np.ndarray, unit: int, label: str) -> None:
+    a, b = got.view(np.uint8).reshape(-1), ref.view(np.uint8).reshape(-1)
+    for s in range(0, b.size, CHUNK_BYTES):
+        e = min(b.size, s + CHUNK_BYTES)
+        if not np.array_equal(a[s:e], b[s:e]):
+            i = s // unit + _first_mismatch(a[s:e], b[s:e], unit)
+            pytest.fail(f"{label}: first mismatch at output {i}")
+
+
+def _run_config(q, name):
+    cfg = wl.CONFIGS[name]
+    gates, M, N = cfg.gates(), cfg.M, cfg.N
+    e = 8 if cfg.dtype == "c64" else 16
+    # ---- the oracle over every output (host)
+    k1_host = np.empty(N, dtype=wl.NP_DTYPE[cfg.dtype])
+    wl.fill_state(cfg.state, k1_host.ctypes.data)
+    perm_ref = opar.build_map(gates, M)
+    k2_ref = opar.apply_map(perm_ref, k1_host)
+    # the oracle's own sampled walk agrees with its materialised map (sanity)
+    idx = np.array([0, 1, N // 2, N - 1], dtype=np.uint64)
+    assert np.array_equal(oracle.walk_many(gates, idx), perm_ref[idx.astype(np.int64)])
+
+    # ---- device buffers
+    k1 = torch.empty(N * e, dtype=torch.uint8, device=DEV)
+    step = 1 << 28
+    for s in range(0, N, step):
+        k1[s * e:(s + step) * e].copy_(torch.from_numpy(k1_host[s:s + step].view(np.uint8)))
+    k2 = torch.empty(N * e, dtype=torch.uint8, device=DEV)
+    perm = torch.empty(N, dtype=torch.int32, device=DEV)
+    ws = q.workspace()
+    perm_u8 = perm.view(torch.uint8)
+
+    def check_perm(label):
+        torch.cuda.synchronize()
+        _compare(perm_u8, perm_ref, 4, f"{name} {label} perm")
+
+    def check_k2(label):
+        torch.cuda.synchronize()
+        _compare(k2, k2_ref, e, f"{name} {label} k2")
+        k2.fill_(0xA5)                                  # stale bytes cannot pass the next mode
+
+    # the north star's plain calls
+    perm.fill_(-1)
+    q.build_map(gates, M, perm)
+    check_perm("qsim_build_map")
+    q.apply_map(perm, M, k1, k2, dtype=cfg.dtype)
+    check_k2("qsim_apply_map")
+    q.run_fused(gates, M, k1, k2, dtype=cfg.dtype)
+    check_k2("qsim_run_fused")
+    # the planned calls with the default plan
+    plan = q.plan_create(gates, M, cfg.dtype)
+    q.apply_map_planned(plan, perm, k1, k2, ws)
+    check_k2(f"qsim_apply_map_planned (plan_create, sigma {list(plan.sigma)[:8]}...)")
+    q.run_fused_planned(plan, gates, k1, k2, ws)
+    check_k2("qsim_run_fused_planned (plan_create)")
+    perm.fill_(-1)
+    q.map_gather_planned(plan, gates, perm, k1, k2, ws)
+    check_perm("qsim_map_gather_planned (plan_create)")
+    check_k2("qsim_map_gather_planned (plan_create)")
+    # the plan bench.py times (qsim_plan_tune keeps the fastest variant)
+    tuned = q.plan_create(gates, M, cfg.dtype)
+    variant = q.plan_tune(tuned, gates, perm, k1, k2, ws)
+    label = f"tuned plan (variant {variant}, sigma {list(tuned.sigma)[:13]}, chunk {tuned.fused_chunk_log2})"
+    perm.fill_(-1)
+    k2.fill_(0xA5)
+    q.map_gather_planned(tuned, gates, perm, k1, k2, ws)
+    check_perm("qsim_map_gather_planned " + label)
+    check_k2("qsim_map_gather_planned " + label)
+    q.run_fused_planned(tuned, gates, k1, k2, ws)
+    check_k2("qsim_run_fused_planned " + label)
+    q.apply_map_planned(tuned, perm, k1, k2, ws)
+    check_k2("qsim_apply_map_planned " + label)
+    # end to end from host buffers (the e2e leg of bench.py)
+    k2_host = np.empty_like(k1_host)
+    for mode in (q.MATERIALISED, q.FUSED):
+        k2_host.view(np.uint8)[:] = 0xA5
+        q.run_host(gates, M, mode, k1_host, k2_host, k1, k2, perm, ws, dtype=cfg.dtype)
+        _host_compare(k2_host, k2_ref, e, f"{name} qsim_run_host mode {mode} k2 (host)")
+    del k2_host
+    return cfg, perm, k1, k2
+
+
+def test_cfg3_every_output(q):
+    """cfg3: M = 26, 256 random gates, complex128 (materialised map then gather)."""
+    _run_config(q, "cfg3")
+    torch.cuda.empty_cache()
+
+
+def test_cfg4_every_output(q):
+    """cfg4: M = 30, 256-gate ripple cascade, complex64 (fused vs materialised)."""
+    _run_config(q, "cfg4")
+    torch.cuda.empty_cache()
+
+
+def test_cfg5_every_output(q):
+    """cfg5: M = 32, 64 random gates, complex64 -- the bench's workload."""
+    cfg, perm, k1, k2 = _run_config(q, "cfg5")
+    # group identity at full size as well: perm(rev G)[perm(G)[i]] == i
+    del k1, k2
+    torch.cuda.empty_cache()
+    q.build_map(cfg.gates(), cfg.M, perm)
+    rev = torch.empty_like(perm)
+    q.build_map(cfg.gates()[::-1].copy(), cfg.M, rev)
+    step = 1 << 28
+    for s in range(0, cfg.N, step):
+        p = perm[s:s + step].to(torch.int64) & 0xFFFFFFFF
+        comp = rev.index_select(0, p).to(torch.int64) & 0xFFFFFFFF
+        assert torch.equal(comp, torch.arange(s, s + step, device=DEV, dtype=torch.int64))
+    torch.cuda.empty_cache()

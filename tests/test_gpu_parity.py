@@ -6,9 +6,9 @@ floats (R15).
 
 * small and medium sizes: every output compared with the oracle, both walk
   algorithms, complex64 and complex128, ragged ranges, edge cases;
-* BASELINE.json configs: cfg1/cfg2 in full; cfg3/cfg4/cfg5 at full size in
-  the launch configuration bench.py uses, on sampled outputs the oracle
-  computes one by one, plus properties that hold at any size.
+* BASELINE.json configs: cfg1/cfg2 in full here; cfg3/cfg4/cfg5 every output
+  at full size in tests/test_gpu_fullsize.py, plus the index-tagged M = 32
+  gather below.
 """
 import numpy as np
 import pytest
@@ -356,141 +356,8 @@ def _sample_indices(M, n=1 << 15, seed=0):
     return idx
 
 
-def _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d):
-    gates = cfg.gates()
-    idx = _sample_indices(cfg.M)
-    src = oracle.walk_many(gates, idx)
-    it = torch.from_numpy(idx.astype(np.int64)).to(DEV)
-    got_perm = perm_d.index_select(0, it).cpu().numpy().view(np.uint32)
-    assert np.array_equal(got_perm.astype(np.uint64), src)
-    e = 8 if cfg.dtype == "c64" else 16
-    want = k1_host.view(np.uint8).reshape(-1, e)[src.astype(np.int64)]
-    for out in (k2_d, k2f_d):
-        if out is None:
-            continue
-        got = out.view(-1, e).index_select(0, it).cpu().numpy()
-        assert np.array_equal(got, want)
-
-
-def _multiset_hash(t, chunk=1 << 28):
-    """Order-independent hash of a state's entries (as 8-byte words): the sum of
-    a mixing function, mod 2^64 -- equal for k1 and k2 when k2 is a permutation
-    of k1's entries (U is a permutation, the norm is kept)."""
-    w = t.view(torch.int64)
-    h = torch.zeros((), dtype=torch.int64, device=w.device)
-    for s0 in range(0, w.numel(), chunk):
-        x = w[s0:s0 + chunk]
-        y = (x ^ (x >> 31)) * 0x7FB5D329728EA185
-        y = (y ^ (y >> 27)) * 0x5A8D3F2B1C4E6F9B
-        h = h + (y ^ (y >> 33)).sum()
-    return int(h.item())
-
-
-def _full_config(q, name, fused):
-    cfg = wl.CONFIGS[name]
-    gates = cfg.gates()
-    e = 8 if cfg.dtype == "c64" else 16
-    k1_host = wl.make_state(cfg.state)
-    k1_d = torch.from_numpy(k1_host.view(np.uint8)).to(DEV)
-    perm_d = torch.empty(cfg.N, dtype=torch.int32, device=DEV)
-    k2_d = torch.empty(cfg.N * e, dtype=torch.uint8, device=DEV)
-    q.build_map(gates, cfg.M, perm_d)
-    q.apply_map(perm_d, cfg.M, k1_d, k2_d, dtype=cfg.dtype)
-    k2f_d = None
-    if fused:
-        k2f_d = torch.empty_like(k2_d)
-        q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype=cfg.dtype)
-    torch.cuda.synchronize()
-    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, k2f_d)
-    if cfg.dtype == "c64":                      # the multiset of entries is kept (P:L35)
-        assert _multiset_hash(k1_d) == _multiset_hash(k2_d)
-    if fused:
-        assert torch.equal(k2_d, k2f_d)          # materialised == fused, every byte
-    # the planned (sigma-ordered) calls bench.py times: same bytes
-    plan = q.plan_create(gates, cfg.M, cfg.dtype)
-    ws = q.workspace()
-    k2p = torch.empty_like(k2_d)
-    q.apply_map_planned(plan, perm_d, k1_d, k2p, ws)
-    torch.cuda.synchronize()
-    assert torch.equal(k2_d, k2p)
-    q.run_fused_planned(plan, gates, k1_d, k2p, ws)
-    torch.cuda.synchronize()
-    assert torch.equal(k2_d, k2p)
-    pm = torch.empty_like(perm_d)
-    q.map_gather_planned(plan, gates, pm, k1_d, k2p, ws)
-    torch.cuda.synchronize()
-    assert torch.equal(k2_d, k2p) and torch.equal(perm_d, pm)
-    del k2p, pm
-    # perm(reverse G) o perm(G) == identity over all 2^M outputs (group identity)
-    rev_d = torch.empty_like(perm_d)
-    q.build_map(gates[::-1].copy(), cfg.M, rev_d)
-    p64 = perm_d.view(torch.int32).to(torch.int64) & 0xFFFFFFFF
-    comp = rev_d.index_select(0, p64)
-    del p64
-    ident = torch.arange(cfg.N, device=DEV, dtype=torch.int64).to(torch.int32)
-    assert torch.equal(comp, ident)
-    return cfg
-
-
-def test_cfg3_full_size_sampled(q):
-    _full_config(q, "cfg3", fused=False)
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.slow
-def test_cfg4_full_size_sampled(q):
-    _full_config(q, "cfg4", fused=True)
-    torch.cuda.empty_cache()
-
-
-@pytest.mark.slow
-def test_cfg5_full_size_sampled(q):
-    """M = 32: 2^32 entries, 16 GiB perm, 32 GiB k1 and k2 (BASELINE cfg5)."""
-    cfg = wl.CONFIGS["cfg5"]
-    gates = cfg.gates()
-    N = cfg.N
-    k1_host = np.empty(N, dtype=np.complex64)
-    wl.fill_state(cfg.state, k1_host.ctypes.data)
-    k1_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
-    chunk = 1 << 28
-    for s in range(0, N, chunk):
-        k1_d[s * 8:(s + chunk) * 8].copy_(torch.from_numpy(k1_host[s:s + chunk].view(np.uint8)))
-    perm_d = torch.empty(N, dtype=torch.int32, device=DEV)
-    k2_d = torch.empty(N * 8, dtype=torch.uint8, device=DEV)
-    plan = q.plan_create(gates, cfg.M, "c64")
-    ws = q.workspace()
-    q.build_map(gates, cfg.M, perm_d)
-    q.apply_map_planned(plan, perm_d, k1_d, k2_d, ws)       # the bench's launch config
-    torch.cuda.synchronize()
-    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2_d, None)
-    assert _multiset_hash(k1_d) == _multiset_hash(k2_d)    # a permutation of k1 (P:L35)
-    # every other path == the planned apply over all 2^32 entries (on device)
-    k2f_d = torch.empty_like(k2_d)
-    pm = torch.empty_like(perm_d)
-    q.map_gather_planned(plan, gates, pm, k1_d, k2f_d, ws)       # one-pass map + gather
-    torch.cuda.synchronize()
-    assert torch.equal(pm, perm_d)
-    for s in range(0, N * 8, 1 << 32):
-        assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
-    del pm
-    for run in (lambda: q.run_fused_planned(plan, gates, k1_d, k2f_d, ws),
-                lambda: q.apply_map(perm_d, cfg.M, k1_d, k2f_d, dtype="c64"),
-                lambda: q.run_fused(gates, cfg.M, k1_d, k2f_d, dtype="c64")):
-        k2f_d.zero_()
-        run()
-        torch.cuda.synchronize()
-        for s in range(0, N * 8, 1 << 32):
-            assert torch.equal(k2_d[s:s + (1 << 32)], k2f_d[s:s + (1 << 32)])
-    _check_sampled(q, cfg, k1_host, k1_d, perm_d, k2f_d, None)
-    del k2f_d, k2_d, k1_d
-    # group identity at full size: perm(rev G)[perm(G)[i]] == i for all 2^32 i
-    rev_d = torch.empty_like(perm_d)
-    q.build_map(gates[::-1].copy(), cfg.M, rev_d)
-    for s in range(0, N, chunk):
-        p = perm_d[s:s + chunk].to(torch.int64) & 0xFFFFFFFF
-        comp = rev_d.index_select(0, p).to(torch.int64) & 0xFFFFFFFF
-        assert torch.equal(comp, torch.arange(s, s + chunk, device=DEV, dtype=torch.int64))
-    torch.cuda.empty_cache()
+# cfg3 / cfg4 / cfg5 at full size: every output against the oracle in
+# tests/test_gpu_fullsize.py (these configs were sampled here before).
 
 
 @pytest.mark.slow
