@@ -158,6 +158,101 @@ def cpu_oracle_rate(gates, k1_host: np.ndarray, start: int, count: int, threads:
     return count / dt, dt
 
 
+def verify_sample(gates, M, e, perm, k2, k1_host, cfg, dev, n=1 << 16, seed=2025):
+    """Post-timing check of the timed step: 2^16 seeded output indices (plus
+    the first and last 64) of perm and k2 against the oracle's walk
+    (oracle.walk_many) and k1 at the oracle's sources (the host copy, or the
+    counter-based generator entry by entry when no host copy exists)."""
+    import torch
+    import oracle
+    import workloads as wl
+    N = 1 << M
+    rng = np.random.default_rng(seed)
+    idx = np.unique(np.concatenate([np.arange(min(64, N)), np.arange(max(0, N - 64), N),
+                                    rng.integers(0, N, size=n)]).astype(np.uint64))
+    src = oracle.walk_many(gates, idx)
+    it = torch.from_numpy(idx.astype(np.int64)).to(dev)
+    got_perm = perm.index_select(0, it).cpu().numpy().view(np.uint32).astype(np.uint64)
+    got_k2 = k2.view(-1, e).index_select(0, it).cpu().numpy()
+    if k1_host is not None:
+        want = k1_host.numpy().reshape(-1, e)[src.astype(np.int64)]
+    else:
+        scale = cfg.state.scale()
+        want = np.stack([wl.make_state(cfg.state, int(j), 1, scale=scale).view(np.uint8)
+                         for j in src])
+    ok_perm = bool(np.array_equal(got_perm, src))
+    ok_k2 = bool(np.array_equal(got_k2, want))
+    return {"ok": ok_perm and ok_k2, "outputs_checked": int(idx.size), "perm_equal": ok_perm,
+            "k2_bytes_equal": ok_k2,
+            "how": "after the timed loop: perm[i] and k2[i] at 2^16 seeded outputs (+ first/last 64) "
+                   "vs oracle.walk_many (single-threaded C walk, P:L43) and k1[perm_oracle[i]]"}
+
+
+def host_info():
+    info = {"cpu_model": None, "host_ram_gb": None, "nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    info["cpu_model"] = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    info["host_ram_gb"] = round(int(ln.split()[1]) / (1 << 20), 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
+def cpu_single_core(gates, k1_np: np.ndarray, count: int):
+    """The oracle (build walk + apply gather) on ONE host core (the process
+    pinned to core 0 for the call, like taskset -c 0), outputs [0, count)."""
+    import oracle
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    try:
+        t0 = time.perf_counter()
+        perm = oracle.build_map(gates, k1_np.shape[0].bit_length() - 1, 0, count)
+        oracle.apply_map(perm, k1_np)
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
+    return count / dt, dt, core
+
+
+def cpu_accumulate(gates, k1_np: np.ndarray, n_gates: int):
+    """The paper's "basic accumulation method" (oracle_accumulate,
+    gate-by-gate pair swaps over the whole state) on one core, for the first
+    n_gates steps over the full state, in place; the same steps then run in
+    reverse order (each step is an involution), which restores k1
+    exactly (checked on a sample).  Returns entry-steps/s and seconds."""
+    import ctypes
+    import oracle
+    lib = oracle._load()
+    M = k1_np.shape[0].bit_length() - 1
+    e = k1_np.dtype.itemsize
+    g = np.ascontiguousarray(gates[:n_gates], dtype=np.uint8)
+    gr = np.ascontiguousarray(g[::-1])
+    probe = np.array(k1_np[:: max(1, k1_np.shape[0] // 4096)], copy=True)
+    old = os.sched_getaffinity(0)
+    os.sched_setaffinity(0, {min(old)})
+    try:
+        t0 = time.perf_counter()
+        lib.oracle_accumulate(g.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n_gates, M, e,
+                              k1_np.ctypes.data)
+        dt = time.perf_counter() - t0
+        lib.oracle_accumulate(gr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), n_gates, M, e,
+                              k1_np.ctypes.data)
+    finally:
+        os.sched_setaffinity(0, old)
+    restored = bool(np.array_equal(probe.view(np.uint8),
+                                   k1_np[:: max(1, k1_np.shape[0] // 4096)].view(np.uint8)))
+    return k1_np.shape[0] * n_gates / dt, dt, restored
+
+
 # ----------------------------------------------------------------- main arm
 def run_qsim(args):
     import torch
@@ -215,6 +310,7 @@ def run_qsim(args):
     # measured plan (like an FFTW_MEASURE plan): variants timed on these buffers,
     # the fastest map + gather kept; once per circuit, outside the timed region
     t_tune = time.perf_counter()
+    torch.cuda.synchronize()                     # k1's H2D copy (default stream) is complete
     tuned = q.plan_tune(plan, gates, perm, k1, k2, ws, stream=stream) if not (plan.flags & 1) else -1
     t_tune = time.perf_counter() - t_tune
     torch.cuda.synchronize()
@@ -316,14 +412,44 @@ def run_qsim(args):
                 marks.append(("run_fused", a, b))
         return n
 
+    def step_plain_fused(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.run_fused(gates, M, k1, k2, stream=stream, dtype=cfg.dtype)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("plain_run_fused", a, b))
+        return n
+
+    def step_plain_apply(marks):
+        with torch.cuda.stream(stream):
+            a = ev() if marks is not None else None
+            q.apply_map(perm, M, k1, k2, stream=stream, dtype=cfg.dtype)
+            n = q.last_launch_count()
+            b = ev() if marks is not None else None
+            if marks is not None:
+                marks.append(("plain_apply_map", a, b))
+        return n
+
     sampler = ClockSampler(local)
     with sampler:
         ms_mg, launches_mg, kern_mg = timed_loop(step_map_gather, args.steps, args.warmup,
                                                  per_kernel=True)
+        # the timed step's own output, checked against the oracle before any
+        # other loop overwrites perm / k2
+        verified = verify_sample(gates, M, e, perm, k2, k1_host, cfg, dev)
         ms_mat, launches_mat, kern_mat = timed_loop(step_materialised, args.steps, args.warmup,
                                                     per_kernel=True)
         ms_fused, launches_fused, kern_fused = timed_loop(step_fused, args.steps, args.warmup,
                                                           per_kernel=True)
+        plain_steps = max(2, args.steps // 4)
+        ms_pf, launches_pf, kern_pf = timed_loop(step_plain_fused, plain_steps, args.warmup,
+                                                 per_kernel=True)
+        kern_name_pf = q.last_kernel()
+        q.build_map(gates, M, perm, stream=stream)
+        ms_pa, launches_pa, kern_pa = timed_loop(step_plain_apply, plain_steps, min(args.warmup, 1),
+                                                 per_kernel=True)
         ms_kron, launches_kron, kern_kron = timed_loop(step_kron, args.steps, args.warmup,
                                                        per_kernel=True)
         kern_name_kron = q.last_kernel()
@@ -375,10 +501,31 @@ def run_qsim(args):
             torch.cuda.synchronize()
             res[name] = 1e3 * t0.elapsed_time(t1) / reps
         graph.close()
+        # warm (back to back, the 20 MiB working set stays in L2) vs flushed
+        # (a 256 MiB scrub written between steps evicts it)
+        scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        warm, flushed = [], []
+        for _ in range(12):
+            for lst, flush in ((warm, False), (flushed, True)):
+                with torch.cuda.stream(stream):
+                    if flush:
+                        scrub.fill_(1)
+                    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    t0.record(stream)
+                    q.map_gather_planned(plan2, g2, p2, a2, b2, ws, stream=stream)
+                    t1.record(stream)
+                torch.cuda.synchronize()
+                lst.append(t0.elapsed_time(t1))
+        del scrub
         launch_bound = {"config": "cfg2 (M = 20, 2^20 entries, L2-resident)",
                         "call": "qsim_map_gather_planned", "direct_us_per_step": res["direct"],
                         "graph_us_per_step": res["graph"],
-                        "note": "CUDA graph of 100 recorded steps (qsim_graph_*) vs 100 calls"}
+                        "warm_us": 1e3 * statistics.median(warm[2:]),
+                        "flushed_us": 1e3 * statistics.median(flushed[2:]),
+                        "kernel": q.last_kernel(),
+                        "note": "CUDA graph of 100 recorded steps (qsim_graph_*) vs 100 calls; "
+                                "warm = back to back (L2-resident), flushed = 256 MiB written "
+                                "between steps (one call, CUDA events around the kernel)"}
         del a2, b2, p2
 
     # ---- end to end through the C ABI from pinned host buffers: every step
@@ -420,14 +567,29 @@ def run_qsim(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and k1_host is not None:
         import workloads as wl2
         k1_np = k1_host.numpy().view(wl2.NP_DTYPE[cfg.dtype])
-        threads = os.cpu_count() or 1
+        threads = len(os.sched_getaffinity(0))
         count = min(N, 1 << args.cpu_sample_log2)
         rate, dt = cpu_oracle_rate(gates, k1_np, 0, count, threads)
+        c1 = min(N, 1 << 24)
+        rate1, dt1, core = cpu_single_core(gates, k1_np, c1)
+        acc_rate, acc_dt, restored = cpu_accumulate(gates, k1_np, 1)
         cpu = {"value": rate, "unit": "entries/s", "cores": threads, "kind": "oracle",
                "seconds": dt,
                "sample": f"output entries [0, 2^{args.cpu_sample_log2}) of {args.config} "
                          f"(build_map walk + apply gather, oracle C -O2, one thread per core "
-                         f"on disjoint sub-ranges)"}
+                         f"on disjoint sub-ranges)",
+               "single_core": {"value": rate1, "unit": "entries/s", "cores": 1, "core": core,
+                               "seconds": dt1,
+                               "sample": f"output entries [0, 2^{c1.bit_length() - 1}) of "
+                                         f"{args.config}, build walk + apply gather, process "
+                                         f"pinned to one core (taskset -c {core} equivalent)",
+                               "projected_full_s": N / rate1},
+               "accumulate": {"value": acc_rate, "unit": "entry-steps/s", "cores": 1,
+                              "seconds": acc_dt, "k1_restored": restored,
+                              "sample": f"the paper's basic accumulation method (P:L59), step 1 of "
+                                        f"{args.config} over all 2^{M} entries, one core",
+                              "projected_full_s": N * int(gates.shape[0]) / acc_rate},
+               **host_info()}
 
     if rank != 0:
         return
@@ -495,6 +657,20 @@ def run_qsim(args):
             "run_fused": {"ms": fused_ms, "GBps": gbps(bytes_fused, fused_ms),
                           "entries_per_s": N / (fused_ms * 1e-3), "bytes_per_entry": 2 * e,
                           "frac_of_peak": gbps(bytes_fused, fused_ms) / hbm},
+            "plain_run_fused": {
+                "ms": statistics.mean(kern_pf["plain_run_fused"]),
+                "entries_per_s": N / (statistics.mean(kern_pf["plain_run_fused"]) * 1e-3),
+                "GBps": gbps(bytes_fused, statistics.mean(kern_pf["plain_run_fused"])),
+                "kernel": kern_name_pf,
+                "note": "qsim_run_fused (north-star call, no plan argument): plans internally, "
+                        "plan cached per circuit, round-robin chunks (no workspace)"},
+            "plain_apply_map": {
+                "ms": statistics.mean(kern_pa["plain_apply_map"]),
+                "entries_per_s": N / (statistics.mean(kern_pa["plain_apply_map"]) * 1e-3),
+                "GBps": gbps(bytes_apply, statistics.mean(kern_pa["plain_apply_map"])),
+                "note": "qsim_apply_map (north-star call): natural output order, k_apply; it "
+                        "receives no gates, so it cannot plan -- the fast form of the same "
+                        "call is qsim_apply_map_planned (modes.apply_map)"},
             "fused_kron": {"ms": kron_ms, "GBps": gbps(N * e, kron_ms),
                            "entries_per_s": N / (kron_ms * 1e-3), "bytes_per_entry": e,
                            "frac_of_peak": gbps(N * e, kron_ms) / hbm,
@@ -512,10 +688,12 @@ def run_qsim(args):
         "write_peak": {"GBps": write_peak, "how": "torch zero_ of the 2^M-entry output buffer, "
                                                  "best of 3 (write-only roofline of fused_kron)"},
         "launch_bound": launch_bound,
+        "verified": verified,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mg,
         "gpu_launches_other_loops": {"two_call": launches_mat, "fused": launches_fused,
+                                     "plain_run_fused": launches_pf, "plain_apply_map": launches_pa,
                                      "fused_kron": launches_kron, "fused_kron_M40": launches_k40},
         "clocks": clocks,
         "setup_s": t_setup,

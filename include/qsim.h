@@ -36,28 +36,14 @@
  *   - Thread safety: reentrant; concurrent calls on different streams are
  *     safe (no mutable module-scope device state).
  *
- * Environment (diagnostics and A/B switches; none is needed for normal use)
+ * Environment (diagnostics and test switches; none is needed for normal use,
+ * none changes a result)
  *   QSIM_NO_JIT=1            never use NVRTC (ahead-of-time kernels only)
  *   QSIM_NVRTC=<path>        libnvrtc to load (default: the toolkit's)
  *   QSIM_JIT_DUMP=<dir>      write each generated kernel source and cubin there
- *   QSIM_JIT_PIPE=1          software pipeline in the fused kernel (measured neutral)
- *   QSIM_PLAN_COVER_BITS=T   sector-cover size of new plans (default 13)
- *   QSIM_PLAN_RUN_BITS=r     contiguous output bits kept in the cover (default 3)
- *   QSIM_PLAN_COVER_ORDER=1|2  new plans order the cover bits by sector-mate weight
- *                            from counter bit 3 | 5 (measured: no better than tuned)
- *   QSIM_PLAN_GRANULE_BYTES=g  cover g-byte mates instead of 32-byte sector mates
- *                            (64 / 128 measured no faster)
- *   QSIM_PLAN_LINEAR=1       linear-traversal plans (measured slower on cfg5)
- *   QSIM_PLAN_PAIRS=1        lane-pair plans (measured slower on cfg5)
- *   QSIM_NO_LINEAR=1         ignore a plan's linear traversal
- *   QSIM_KRON_GROUP_BITS=b   product-table group size of the on-the-fly input
- *   QSIM_THREAD_BITS=0       NVRTC threads walk output bits 5..9, no hoisted
- *                            product (on-the-fly input 1.5-2x slower)
+ *   QSIM_THREAD_BITS=0       NVRTC build / on-the-fly input threads walk output
+ *                            bits 5..9 (no fast path; same bytes)
  *   QSIM_THREAD_BITS_SAMPLES=k  circuit sample size of the in-thread bits (tests)
- *   QSIM_DEBUG_STORE=seq|none  TIMING EXPERIMENTS ONLY, results invalid: the planned
- *                            fused kernel stores k2 in counter order / not at all
- *   QSIM_KRON_AFFINE=1       affine (Gray-code) fast path in the on-the-fly input
- *                            kernel instead of the V-plane transpose (measured neutral)
  *   QSIM_BUILD_THREAD_BITS=0 build kernel without its in-thread affine fast path
  */
 #ifndef QSIM_H
@@ -240,27 +226,6 @@ typedef struct qsim_plan {
     uint8_t tile_reserved[3];
     float tile_contained;   /* sampled fraction of (reader, sector-mate reader) pairs
                                that differ only in those bits                        */
-    /* Linear traversal (ABI 4, complex64, NVRTC kernels of the planned calls):
-     * when lin_flags bit 0 is set, output = XOR of lin[k] over the set counter
-     * bits k (an invertible GF(2) map instead of the bit permutation sigma).
-     * lin[0..4] (the lanes of a warp) are the commonest differences between the
-     * readers of one 32-byte k1 sector, so a warp load touches fewer sectors;
-     * lin[0..12] span the sector cover, lin[13..] = 1 << sigma[13..]; the span
-     * of lin[0..9] holds output bits 0..3, and k2 / perm are written through a
-     * per-warp shared-memory transpose in 128-byte runs.  lanes_sectors: sampled
-     * distinct k1 sectors per warp load with lin (32 = every lane its own).   */
-    uint32_t lin[32];
-    uint32_t lin_flags;
-    float lanes_sectors;
-    /* Lane pairs (ABI 5, complex64, NVRTC kernels): when pair_xor != 0 the
-     * traversal XORs pair_xor into the output when counter bit 5 (word bit 0)
-     * is set, so lane L's word l and lane L^1's word l^1 hold outputs o and
-     * o ^ d, d = the commonest difference between the readers of k1 entries
-     * 2m and 2m+1 (pair_frac of them, sampled).  Such a pair is read with ONE
-     * 16-byte load and split with a lane shuffle.  sigma still defines the
-     * order for the ahead-of-time kernels (another bijection, same k2).      */
-    uint32_t pair_xor;
-    float pair_frac;
 } qsim_plan;
 
 int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
@@ -416,8 +381,9 @@ int qsim_jit_check_compile_kron(const qsim_gate *gates, int32_t n_gates, int32_t
                                 int32_t dtype);
 int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
                                    int32_t n_gates);
-/* ABI version of this header / library: 6 (plans with the sector cover,
- * phase / SWAP gates, M > 32 on-the-fly input, batch e2e, graphs, tuning).  */
+/* ABI version of this header / library: 7 (plans with the sector cover,
+ * phase / SWAP gates, M > 32 on-the-fly input, batch e2e, graphs, tuning;
+ * 7: the measured-slower linear-traversal and lane-pair plan fields removed). */
 int32_t qsim_abi_version(void);
 
 #ifdef __cplusplus

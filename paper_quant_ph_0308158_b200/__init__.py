@@ -57,10 +57,7 @@ class Plan(ctypes.Structure):
                 ("reserved_spread", ctypes.c_uint16),
                 ("sigma", ctypes.c_uint8 * 32), ("change_freq", ctypes.c_float * 32),
                 ("tile_log2", ctypes.c_uint8), ("tile_reserved", ctypes.c_uint8 * 3),
-                ("tile_contained", ctypes.c_float),
-                ("lin", ctypes.c_uint32 * 32), ("lin_flags", ctypes.c_uint32),
-                ("lanes_sectors", ctypes.c_float),
-                ("pair_xor", ctypes.c_uint32), ("pair_frac", ctypes.c_float)]
+                ("tile_contained", ctypes.c_float)]
 
 
 def _load() -> ctypes.CDLL:

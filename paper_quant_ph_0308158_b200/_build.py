@@ -18,8 +18,7 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
 
 TARGETS = {
     LIB: (os.path.join(CSRC, "*.cu"), os.path.join(CSRC, "*.h*"), "qsim.h"),
-    MB_LIB: ([os.path.join(CSRC, "mb", "*.cu"), os.path.join(CSRC, "qsim_tma_host.cu")],
-             os.path.join(CSRC, "*.cuh"), "qsim_mb.h"),
+    MB_LIB: (os.path.join(CSRC, "mb", "*.cu"), os.path.join(CSRC, "mb", "*.cuh"), "qsim_mb.h"),
 }
 
 

@@ -111,7 +111,7 @@ extern "C" int qsim_mb_gather_c64(const uint32_t* idx, uint64_t count, const voi
 // into shared memory, 4 rows per instruction, STAGES-deep mbarrier ring.
 // Warp 0 produces (each lane one gather4 per instruction), warps 1..4
 // consume (select the 8-byte half, store k2 coalesced).
-#include "../qsim_tma.cuh"
+#include "qsim_tma.cuh"
 
 namespace {
 

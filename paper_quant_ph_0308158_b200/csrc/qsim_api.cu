@@ -568,7 +568,6 @@ int fused_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, uint
 // 11.7 ms (larger tables cost more than the product they save).
 void kron_groups(int32_t M, int e, uint32_t* gbits, uint32_t* ngroups) {
   int maxb = e == 8 ? 10 : 8;
-  if (const char* gb = std::getenv("QSIM_KRON_GROUP_BITS")) maxb = std::max(1, std::min(12, std::atoi(gb)));  // tuning
   const int ng = (M + maxb - 1) / maxb;
   *ngroups = (uint32_t)ng;
   *gbits = (uint32_t)((M + ng - 1) / ng);
@@ -732,22 +731,6 @@ uint32_t plan_inverse_walk(const PlanGate* g, int n, uint32_t x) {
   return x;
 }
 
-// ---- GF(2) helpers for the linear traversal
-// Insert v into an echelon basis (pivot = highest bit); false if v is in the span.
-bool gf2_insert(std::vector<uint32_t>& ech, uint32_t v) {
-  for (uint32_t b : ech)
-    if ((v ^ b) < v) v ^= b;  // b's pivot bit is set in v
-  if (v == 0) return false;
-  ech.push_back(v);
-  std::sort(ech.begin(), ech.end(), [](uint32_t x, uint32_t y) { return x > y; });
-  return true;
-}
-bool gf2_in_span(const std::vector<uint32_t>& ech, uint32_t v) {
-  for (uint32_t b : ech)
-    if ((v ^ b) < v) v ^= b;
-  return v == 0;
-}
-
 // counter bits that stay output bits: 32-byte runs of k2 and perm (8
 // complex64 / 2 complex128 entries: 64 / 32 bytes of k2, 32 / 8 bytes of perm)
 int plan_keep_bits(int32_t dtype) { return dtype == QSIM_C64 ? 3 : 2; }
@@ -772,22 +755,6 @@ int plan_validate(const qsim_plan* p) {
       p->cta_threads != 1024)
     return QSIM_EINVAL;
   if (p->ilp == 32 && p->cta_threads == 1024) return QSIM_EINVAL;  // register file
-  if (p->pair_xor) {  // counter bit 5 -> sigma[5] ^ pair_xor stays invertible
-    if (p->dtype != QSIM_C64 || p->M < 12 || ((uint64_t)p->pair_xor >> p->M) ||
-        ((p->pair_xor >> p->sigma[5]) & 1u))
-      return QSIM_EINVAL;
-  }
-  if (p->lin_flags & 1u) {  // invertible on the M address bits, output bits 0..3 in the warp tile
-    if (p->dtype != QSIM_C64 || p->M < 14) return QSIM_EINVAL;
-    std::vector<uint32_t> ech, ten;
-    for (int k = 0; k < p->M; ++k) {
-      if ((uint64_t)p->lin[k] >> p->M) return QSIM_EINVAL;
-      if (!gf2_insert(ech, p->lin[k])) return QSIM_EINVAL;
-      if (k < 10) gf2_insert(ten, p->lin[k]);
-    }
-    for (int b = 0; b < 4; ++b)
-      if (!gf2_in_span(ten, 1u << b)) return QSIM_EINVAL;
-  }
   return QSIM_OK;
 }
 
@@ -831,12 +798,9 @@ uint32_t plan_forward_walk(const PlanGate* g, int n, uint32_t x) {
 // start from the kept bits, repeatedly add the pattern with the best gain in
 // contained pairs per added bit until T bits.  Returns the bit set V; the
 // fraction of sampled pairs inside a V-block goes to plan->tile_contained.
-uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan,
-                           std::vector<uint32_t>* top_patterns = nullptr) {
+uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, qsim_plan* plan) {
   const int e = elem_bytes(dtype), keep = plan_keep_bits(dtype);
-  int eps = 32 / e;  // entries per cover granule: a 32-byte sector
-  if (const char* gb = std::getenv("QSIM_PLAN_GRANULE_BYTES"))  // A/B: 64 / 128 (L1 lines)
-    eps = std::max(2, std::min(512, std::atoi(gb))) / e;
+  const int eps = 32 / e;  // entries per cover granule: a 32-byte sector
   const int samples = 2048;
   std::vector<uint32_t> diffs;
   diffs.reserve((size_t)samples * (eps - 1));
@@ -859,16 +823,13 @@ uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, q
     return x.second != y.second ? x.second > y.second : x.first < y.first;
   });
   if (pats.size() > 512) pats.resize(512);  // candidates: the frequent patterns
-  if (top_patterns)
-    for (const auto& pc : pats) top_patterns->push_back(pc.first);
   auto contained = [&](uint32_t V) {
     uint64_t c = 0;
     for (const auto& pc : pats)
       if ((pc.first & ~V) == 0) c += pc.second;
     return c;
   };
-  int run = keep;  // low output bits in the cover: contiguous output runs of 2^run entries
-  if (const char* rb = std::getenv("QSIM_PLAN_RUN_BITS")) run = std::max(keep, std::min(T, std::atoi(rb)));  // tuning
+  const int run = keep;  // low output bits in the cover: contiguous output runs of 2^run entries
   uint32_t V = (1u << run) - 1;
   int bits = run;
   while (bits < T) {
@@ -907,20 +868,18 @@ uint32_t plan_sector_cover(const PlanGate* pg, int n, int M, int dtype, int T, q
 // ties) -- cover bits beyond what the pairs need cost more than they bring
 // (M = 32 seeds 4 / 7 / 8: profiles/r01_cover_size.txt).
 uint32_t plan_choose_cover(const PlanGate* pg, int n, int M, int dtype, int Tmax, bool fixed,
-                           qsim_plan* plan, std::vector<uint32_t>* top_patterns) {
+                           qsim_plan* plan) {
   const int lo = fixed ? Tmax : std::min(10, Tmax);
   uint32_t best_v = 0;
   float best_c = -1.0f;
   int best_t = Tmax;
   for (int T = lo; T <= Tmax; ++T) {
-    std::vector<uint32_t> pats;
-    const uint32_t V = plan_sector_cover(pg, n, M, dtype, T, plan, T == Tmax ? top_patterns : &pats);
+    const uint32_t V = plan_sector_cover(pg, n, M, dtype, T, plan);
     const float c = plan->tile_contained;
     if (c >= 0.9f) {
       best_v = V;
       best_c = c;
       best_t = T;
-      if (T != Tmax && top_patterns) plan_sector_cover(pg, n, M, dtype, Tmax, plan, top_patterns);
       break;
     }
     if (c > best_c + 1e-6f) {
@@ -934,124 +893,6 @@ uint32_t plan_choose_cover(const PlanGate* pg, int n, int M, int dtype, int Tmax
   return best_v;
 }
 
-// Sampled distinct k1 sectors per warp load when the 32 lanes' outputs are
-// base ^ span(vecs) (averaged over fixed pseudo-random bases), per lane.
-double plan_lane_score(const PlanGate* pg, int n, int M, const std::vector<uint32_t>& vecs) {
-  const int k = (int)vecs.size(), nb = 48;
-  const uint64_t N = 1ull << M;
-  std::vector<uint32_t> sec(1u << k);
-  double tot = 0.0;
-  for (int b = 0; b < nb; ++b) {
-    const uint32_t base = (uint32_t)(plan_mix(0xb45eull + b) % N);
-    for (uint32_t i = 0; i < (1u << k); ++i) {
-      uint32_t o = base;
-      for (int j = 0; j < k; ++j)
-        if ((i >> j) & 1u) o ^= vecs[j];
-      sec[i] = plan_forward_walk(pg, n, o) >> 2;
-    }
-    std::sort(sec.begin(), sec.end());
-    tot += (double)(std::unique(sec.begin(), sec.end()) - sec.begin());
-  }
-  return tot / nb / (double)(1u << k);
-}
-
-// Linear traversal for complex64 (qsim_plan.lin): lanes = the vectors in the
-// cover span that most reduce the sectors a warp load touches (greedy over
-// the frequent sector-mate difference patterns and their pairwise XORs),
-// words = output bits 0..3 (runs for the transposed stores) completed from
-// the cover, warp bits = the rest of the cover; higher counter bits keep sigma.
-void plan_linear(const PlanGate* pg, int n, int M, uint32_t V, const std::vector<uint32_t>& pats,
-                 qsim_plan* plan) {
-  plan->lin_flags = 0;
-  for (int k = 0; k < 32; ++k) plan->lin[k] = k < M ? 1u << plan->sigma[k] : 0u;
-  const int T = __builtin_popcount(V);
-  if (plan->dtype != QSIM_C64 || M < 14 || T < 13 || (V & 15u) != 15u) return;
-  std::vector<uint32_t> cand;
-  const size_t top = std::min<size_t>(pats.size(), 12);
-  for (size_t a = 0; a < top; ++a) {
-    if ((pats[a] & ~V) == 0) cand.push_back(pats[a]);
-    for (size_t b = a + 1; b < top; ++b)
-      if (((pats[a] ^ pats[b]) & ~V) == 0) cand.push_back(pats[a] ^ pats[b]);
-  }
-  for (int b = 0; b < M; ++b)
-    if ((V >> b) & 1u) cand.push_back(1u << b);
-  std::sort(cand.begin(), cand.end());
-  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-  std::vector<uint32_t> lanes, ech;
-  for (int step = 0; step < 5; ++step) {
-    double best = 1e9;
-    uint32_t bv = 0;
-    for (uint32_t c : cand) {
-      if (c == 0 || gf2_in_span(ech, c)) continue;
-      std::vector<uint32_t> t(lanes);
-      t.push_back(c);
-      const double sc = plan_lane_score(pg, n, M, t);
-      if (sc < best - 1e-9) {
-        best = sc;
-        bv = c;
-      }
-    }
-    if (bv == 0) return;
-    lanes.push_back(bv);
-    gf2_insert(ech, bv);
-  }
-  std::vector<uint32_t> cols(lanes);
-  for (int b = 0; b < 4; ++b)  // words: output bits 0..3 first
-    if (gf2_insert(ech, 1u << b)) cols.push_back(1u << b);
-  for (int b = 0; b < M && (int)cols.size() < T; ++b)
-    if (((V >> b) & 1u) && gf2_insert(ech, 1u << b)) cols.push_back(1u << b);
-  if ((int)cols.size() != T || (int)cols.size() < 10) return;
-  const double sc = plan_lane_score(pg, n, M, lanes);
-  std::vector<uint32_t> unit;
-  for (int j = 0; j < 5; ++j) unit.push_back(1u << plan->sigma[j]);
-  const double sc_sigma = plan_lane_score(pg, n, M, unit);
-  plan->lanes_sectors = (float)(sc * 32.0);
-  if (sc >= 0.85 * sc_sigma) return;  // not worth the transposed stores
-  for (int k = 0; k < T; ++k) plan->lin[k] = cols[k];
-  plan->lin_flags = 1;
-}
-
-// Lane pairs: d = the commonest difference g(s ^ 1) ^ i between the readers
-// of the two entries of an aligned 16-byte pair (bit 0 of d is always set);
-// put one other bit b of d at counter bit 5 (swapping within the cover) and
-// XOR the rest of d into the output with counter bit 5, so lane L / word l and
-// lane L^1 / word l^1 are o and o ^ d.  Enabled when the sampled share of
-// such pairs is at least 1/4.
-void plan_pairs(const PlanGate* pg, int n, int M, uint32_t V, qsim_plan* plan) {
-  plan->pair_xor = 0;
-  plan->pair_frac = 0.0f;
-  if (plan->dtype != QSIM_C64 || M < 12) return;
-  const int samples = 2048;
-  const uint64_t N = 1ull << M;
-  std::vector<uint32_t> d(samples);
-  for (int k = 0; k < samples; ++k) {
-    const uint32_t i = (uint32_t)(plan_mix(0x9a17ull + k) % N);
-    d[k] = plan_inverse_walk(pg, n, plan_forward_walk(pg, n, i) ^ 1u) ^ i;
-  }
-  std::vector<uint32_t> srt(d);
-  std::sort(srt.begin(), srt.end());
-  uint32_t best = 0;
-  size_t bc = 0;
-  for (size_t a = 0; a < srt.size();) {
-    size_t b = a;
-    while (b < srt.size() && srt[b] == srt[a]) ++b;
-    if (b - a > bc) {
-      bc = b - a;
-      best = srt[a];
-    }
-    a = b;
-  }
-  plan->pair_frac = (float)bc / samples;
-  if (plan->pair_frac < 0.25f || !(best & 1u) || best == 1u) return;
-  // a bit of d (not bit 0, not a lane bit) to sit at counter bit 5
-  int pos = -1;
-  for (int k = 5; k < M && pos < 0; ++k)
-    if (((best >> plan->sigma[k]) & 1u) && ((V >> plan->sigma[k]) & 1u)) pos = k;
-  if (pos < 0) return;
-  std::swap(plan->sigma[5], plan->sigma[pos]);
-  plan->pair_xor = best & ~1u & ~(1u << plan->sigma[5]);
-}
-
 // Bits the walk can change: every target, and the partner bit of a SWAP.
 int moved_bits(const qsim_gate* gates, int32_t n) {
   int top = 0;
@@ -1063,26 +904,16 @@ int moved_bits(const qsim_gate* gates, int32_t n) {
 }
 int local_tile_bits(int32_t dtype) { return dtype == QSIM_C64 ? 13 : 12; }
 
-// Plan construction options (qsim_plan_create uses the defaults, with the
-// QSIM_PLAN_* environment switches; qsim_plan_tune measures variants).
+// Plan construction options (qsim_plan_create uses the defaults;
+// qsim_plan_tune measures variants).
 struct PlanOpts {
   int cover_bits = 13;    // largest sector cover (counter bits of one L1-resident block)
   bool fixed = false;     // always cover_bits (else the smallest cover holding >= 90 %)
   bool lane_run = false;  // lanes on output bits 0..4 (bits 3, 4 added to the cover)
-  int cover_order = 0;  // cover bits by sector-mate weight: 1 from counter bit 3, 2 from bit 5
 };
 
-PlanOpts default_plan_opts() {
-  PlanOpts o;
-  if (const char* cb = std::getenv("QSIM_PLAN_COVER_BITS")) o.cover_bits = std::atoi(cb);
-  if (const char* fx = std::getenv("QSIM_PLAN_COVER_FIXED")) o.fixed = fx[0] == '1';
-  if (const char* lr = std::getenv("QSIM_PLAN_LANE_RUN")) o.lane_run = lr[0] == '1';
-  if (const char* co = std::getenv("QSIM_PLAN_COVER_ORDER")) o.cover_order = std::atoi(co);
-  return o;
-}
-
 int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* plan,
-              const PlanOpts& opts = default_plan_opts()) {
+              const PlanOpts& opts = PlanOpts()) {
   std::memset(plan, 0, sizeof *plan);
   plan->M = M;
   plan->dtype = dtype;
@@ -1135,8 +966,7 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   // (its L1 serves them); then the other bits by how often a k1 line's readers
   // differ in them (the chunk front keeps its lines in L2)
   const int T = std::max(plan_keep_bits(dtype), std::min(M, std::min(opts.cover_bits, 20)));
-  std::vector<uint32_t> pats;
-  uint32_t V = plan_choose_cover(pg.get(), n, M, dtype, T, opts.fixed, plan, &pats);
+  uint32_t V = plan_choose_cover(pg.get(), n, M, dtype, T, opts.fixed, plan);
   if (opts.lane_run && M >= 5) V |= 31u;  // lanes on output bits 0..4: 256-byte warp stores
   int order[32], m = 0, k = 0;
   for (int b = 0; b < M; ++b) {
@@ -1144,31 +974,6 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
       plan->sigma[k++] = (uint8_t)b;
     else
       order[m++] = b;
-  }
-  {
-    if (opts.cover_order) {
-      // cover bits beyond the kept ones ordered by how much of the sampled
-      // sector-mate reader differences they carry: the commonest land on the
-      // lane bits (counter 3, 4: same warp instruction) and the thread's bits
-      // (5..9: back-to-back instructions)
-      const int keep = plan_keep_bits(dtype);
-      double w[32] = {0};
-      const int e2 = elem_bytes(dtype), eps = 32 / e2;
-      for (int t = 0; t < 2048; ++t) {
-        const uint32_t i = (uint32_t)(plan_mix(0x0dd5ull + t) % (1ull << M));
-        const uint32_t src = plan_forward_walk(pg.get(), n, i);
-        for (int r = 1; r < eps; ++r) {
-          const uint32_t d = plan_inverse_walk(pg.get(), n, src ^ (uint32_t)r) ^ i;
-          if (d == 0 || (d & ~V)) continue;
-          const double wt = 1.0 / __builtin_popcount(d);
-          for (int b = 0; b < M; ++b)
-            if ((d >> b) & 1u) w[b] += wt;
-        }
-      }
-      const int from = opts.cover_order == 2 ? std::min(k, 5) : keep;  // 2: lanes unchanged
-      std::stable_sort(plan->sigma + from, plan->sigma + k,
-                       [&](uint8_t x, uint8_t y) { return w[x] > w[y]; });
-    }
   }
   std::stable_sort(order, order + m, [&](int x, int y) { return count[x] > count[y]; });
   for (int j = 0; j < m; ++j) plan->sigma[k++] = (uint8_t)order[j];
@@ -1197,21 +1002,39 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   plan->reserved_spread = (uint16_t)(nat | (sig << 8));
   // locality-keeping circuit: every bit the walk changes lies below the tile
   if (M >= local_tile_bits(dtype) && moved_bits(gates, n) <= local_tile_bits(dtype)) plan->flags |= 2u;
-  // Lane pairs: opt-in (QSIM_PLAN_PAIRS=1).  On cfg5 half the 16-byte pairs
-  // match, yet the step is slower: 22.0 vs 20.0 ms map+gather, 19.2 vs
-  // 16.0 ms fused (profiles/r01_lane_pairs.txt).
-  if (!(plan->flags & 1u)) {
-    const char* po = std::getenv("QSIM_PLAN_PAIRS");
-    if (po && po[0] == '1') plan_pairs(pg.get(), n, M, V, plan);
+  return QSIM_OK;
+}
+
+// Plans of recent circuits (qsim_run_fused, qsim_run_host*): the host
+// sampling runs once per (circuit, M, dtype); a few entries, most recent first.
+struct PlanCacheEntry {
+  std::vector<qsim_gate> gates;
+  int32_t M, dtype;
+  qsim_plan plan;
+};
+std::mutex g_plan_mu;
+std::vector<PlanCacheEntry> g_plan_cache;
+
+int cached_plan(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_plan* out) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (size_t i = 0; i < g_plan_cache.size(); ++i) {
+    const PlanCacheEntry& c = g_plan_cache[i];
+    if (c.M == M && c.dtype == dtype && c.gates.size() == (size_t)n &&
+        (n == 0 || std::memcmp(c.gates.data(), gates, sizeof(qsim_gate) * n) == 0)) {
+      *out = c.plan;
+      std::rotate(g_plan_cache.begin(), g_plan_cache.begin() + i, g_plan_cache.begin() + i + 1);
+      return QSIM_OK;
+    }
   }
-  // Linear traversal: opt-in (QSIM_PLAN_LINEAR=1).  Measured on cfg5 it cuts the
-  // L1 sector lookups of the gather 2.6x (32 -> 12.5 per warp load) but loses
-  // the L1 hits (45 % -> 10 %) and 64 KB of L1 to the transposes: 23.8 ms vs
-  // 19.9 ms for the bit-permutation plan (profiles/r01_linear_traversal.txt).
-  if (!(plan->flags & 1u)) {
-    const char* lo = std::getenv("QSIM_PLAN_LINEAR");
-    if (lo && lo[0] == '1') plan_linear(pg.get(), n, M, V, pats, plan);
-  }
+  PlanCacheEntry c;
+  int rc = plan_fill(gates, n, M, dtype, &c.plan);
+  if (rc) return rc;
+  c.gates.assign(gates, gates + n);
+  c.M = M;
+  c.dtype = dtype;
+  *out = c.plan;
+  g_plan_cache.insert(g_plan_cache.begin(), std::move(c));
+  if (g_plan_cache.size() > 8) g_plan_cache.pop_back();
   return QSIM_OK;
 }
 
@@ -1255,7 +1078,7 @@ void launch_apply_sigma(uint32_t ilp, uint32_t threads, int bps, unsigned blocks
 bool local_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
                     void* k2, uint32_t* perm_out, void* workspace, cudaStream_t st) {
   const int T = local_tile_bits(plan->dtype);
-  if (!(plan->flags & 2u) || !workspace || plan->M < T || moved_bits(gates, n) > T) return false;
+  if (!(plan->flags & 2u) || plan->M < T || moved_bits(gates, n) > T) return false;
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n, false, *gl);
   std::string err;
@@ -1268,14 +1091,12 @@ bool local_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t n, co
 }
 
 // A natural-order plan still runs the NVRTC kernels (one pass, the walk in
-// registers): identity sigma, no pairs / linear traversal, chunks of up to
+// registers): identity sigma, chunks of up to
 // 2^13 counters (all 8 warps of a CTA busy).
 qsim_plan natural_view(const qsim_plan* plan) {
   qsim_plan p = *plan;
   for (int k = 0; k < 32; ++k) p.sigma[k] = (uint8_t)k;
   p.flags = 0;
-  p.pair_xor = 0;
-  p.lin_flags = 0;
   p.blocks_per_sm = 1;
   p.chunk_log2 = p.fused_chunk_log2 = (uint32_t)std::min(13, std::max(10, p.M - 7));
   return p;
@@ -1294,7 +1115,7 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
   if (overlap(k1, N * e, k2, N * e) || overlap(perm, N * 4, k2, N * e)) return QSIM_EALIAS;
   const qsim_plan nat = natural_view(plan);
   const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
-  if (workspace && (!plan_natural(plan) || M >= 13)) {
+  if (!plan_natural(plan) || M >= 13) {
     // NVRTC: the step kernel's traversal and batching, sources from perm
     const uint64_t nchunks = N >> pp->fused_chunk_log2;
     uint64_t blocks = (uint64_t)sm_count() * pp->blocks_per_sm;
@@ -1370,25 +1191,15 @@ int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t 
                          bool* used_jit) {
   *used_jit = false;
   const int e = elem_bytes(plan->dtype);
-  if (workspace) {
+  {  // workspace == nullptr: the kernel takes its chunks round-robin by CTA
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n, false, *gl);
     std::string err;
     const uint64_t nchunks = (1ull << plan->M) >> plan->fused_chunk_log2;
     uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
-    const char* lt_off = std::getenv("QSIM_NO_LINEAR");  // A/B switch
-    if ((plan->lin_flags & 1u) && e == 8 && !(lt_off && lt_off[0] == '1') &&
-        qsim::jit_fused_lt(gl->w, n, plan->M, plan->lin, plan->fused_chunk_log2, k1, k2, perm_out,
-                           workspace, (int)blocks, st, err) == 0) {
-      ++g_launches;
-      *used_jit = true;
-      g_last_kernel = "qsim_jit_fused_lt";
-      return QSIM_OK;
-    }
-    if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, e == 8 ? plan->pair_xor : 0u,
-                        plan->fused_chunk_log2, e, k1, k2, perm_out, workspace, (int)blocks, st,
-                        err) == 0) {
+    if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2, perm_out,
+                        workspace, (int)blocks, st, err) == 0) {
       ++g_launches;
       *used_jit = true;
       g_last_kernel = "qsim_jit_fused";
@@ -1418,7 +1229,7 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
   }
   if (local_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st)) return QSIM_OK;
   if (plan_natural(plan)) {
-    if (workspace && M >= 13) {
+    if (M >= 13) {
       const qsim_plan nat = natural_view(plan);
       bool jit = false;
       const int launches = g_launches;
@@ -1452,7 +1263,7 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
       overlap(perm, N * 4, k1, N * e))
     return QSIM_EALIAS;
   if (local_dispatch(plan, gates, n, k1, k2, perm, workspace, st)) return QSIM_OK;
-  if (workspace && (!plan_natural(plan) || M >= 13)) {
+  if (!plan_natural(plan) || M >= 13) {
     const qsim_plan nat = natural_view(plan);
     const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
     bool jit = false;
@@ -1513,7 +1324,18 @@ int qsim_apply_map_range(const uint32_t* perm_in, uint64_t count, int32_t M, int
 int qsim_run_fused(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype,
                    const void* k1, void* k2, void* stream) {
   g_launches = 0;
+  g_last_kernel = "";
   if (M < 1 || M > 32) return QSIM_ERANGE;
+  // the whole output: planned internally (plan cached per circuit), the
+  // NVRTC kernel in the plan's order -- the same bytes as every other path
+  int rc = check_gates(gates, n_gates, M);
+  if (rc == QSIM_OK && M >= 13 && elem_bytes(dtype) != 0 && qsim::jit_available()) {
+    qsim_plan plan;
+    if ((rc = cached_plan(gates, n_gates, M, dtype, &plan))) return rc;
+    return fused_planned_impl(&plan, gates, n_gates, k1, k2, nullptr,
+                              static_cast<cudaStream_t>(stream));
+  }
+  g_last_kernel = "k_fused_bitsliced";
   return fused_impl(gates, n_gates, M, dtype, 0, 1ull << M, k1, k2, QSIM_WALK_AUTO,
                     static_cast<cudaStream_t>(stream));
 }
@@ -1612,7 +1434,7 @@ int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dt
                      overlap(perm_dev, N * 4, k1_dev, bytes))))
     return QSIM_EALIAS;
   qsim_plan plan;
-  if ((rc = plan_fill(gates, n_gates, M, dtype, &plan))) return rc;
+  if ((rc = cached_plan(gates, n_gates, M, dtype, &plan))) return rc;
   cudaError_t ce = cudaMemcpyAsync(k1_dev, k1_host, bytes, cudaMemcpyHostToDevice, st);
   if (ce != cudaSuccess) return cuda_fail(ce, "H2D k1");
   int launches = 0;
@@ -1658,7 +1480,7 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
       if (overlap(bufs[a], sz[a], bufs[b], sz[b])) return QSIM_EALIAS;
   if (nsteps == 0) return QSIM_OK;
   qsim_plan plan;
-  if ((rc = plan_fill(gates, n_gates, M, dtype, &plan))) return rc;
+  if ((rc = cached_plan(gates, n_gates, M, dtype, &plan))) return rc;
   // three streams: copies in, compute, copies out; step i uses buffer i & 1
   cudaStream_t sin = nullptr, scmp = nullptr, sout = nullptr;
   cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_cmp[2] = {nullptr, nullptr},
@@ -1755,7 +1577,7 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   // candidates: the default rule, the full cover, each with lanes on output bits 0..4,
   // and smaller full covers
-  const PlanOpts base = default_plan_opts();
+  const PlanOpts base;
   std::vector<PlanOpts> opts;
   for (int fixed = 0; fixed < 2; ++fixed)
     for (int run = 0; run < 2; ++run) {
@@ -1793,15 +1615,14 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     if (a) cudaEventDestroy(a);
     return cuda_fail(ce, "event create");
   }
-  float best = 1e30f;
-  int best_i = -1;
-  for (size_t i = 0; i < cands.size() && rc == QSIM_OK; ++i) {
-    // one untimed call (compiles the kernel), then the best of two
-    rc = map_gather_impl(&cands[i], gates, n_gates, perm, k1, k2, workspace, st);
+  // best of `reps` timed map + gather calls with plan p (one untimed call
+  // first when `warm`: it compiles the kernel)
+  auto time_plan = [&](const qsim_plan& p, bool warm, int reps) -> float {
+    if (warm && (rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st))) return 1e30f;
     float t_best = 1e30f;
-    for (int r = 0; r < 2 && rc == QSIM_OK; ++r) {
+    for (int r = 0; r < reps && rc == QSIM_OK; ++r) {
       cudaEventRecord(a, st);
-      rc = map_gather_impl(&cands[i], gates, n_gates, perm, k1, k2, workspace, st);
+      rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st);
       cudaEventRecord(b, st);
       if ((ce = cudaEventSynchronize(b)) != cudaSuccess) {
         rc = cuda_fail(ce, "tune sync");
@@ -1811,8 +1632,14 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       cudaEventElapsedTime(&ms, a, b);
       t_best = std::min(t_best, ms);
     }
-    if (rc == QSIM_OK && t_best < best) {
-      best = t_best;
+    return rc == QSIM_OK ? t_best : 1e30f;
+  };
+  float best = 1e30f;
+  int best_i = -1;
+  for (size_t i = 0; i < cands.size() && rc == QSIM_OK; ++i) {
+    const float t = time_plan(cands[i], true, 2);
+    if (rc == QSIM_OK && t < best) {
+      best = t;
       best_i = (int)i;
     }
   }
@@ -1829,23 +1656,52 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     if (cl < 10 || cl > kept.M || ((1ull << kept.M) >> cl) < (uint64_t)sm_count()) continue;
     qsim_plan p = kept;
     p.chunk_log2 = p.fused_chunk_log2 = (uint32_t)cl;
-    float t_best = 1e30f;
-    for (int r = 0; r < 2 && rc == QSIM_OK; ++r) {
-      cudaEventRecord(a, st);
-      rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st);
-      cudaEventRecord(b, st);
-      if ((ce = cudaEventSynchronize(b)) != cudaSuccess) {
-        rc = cuda_fail(ce, "tune sync");
-        break;
-      }
-      float ms = 0.0f;
-      cudaEventElapsedTime(&ms, a, b);
-      t_best = std::min(t_best, ms);
-    }
-    if (rc == QSIM_OK && t_best < best * 0.99f) {  // only a clear win moves it
-      best = t_best;
+    const float t = time_plan(p, false, 2);
+    if (rc == QSIM_OK && t < best * 0.99f) {  // only a clear win moves it
+      best = t;
       cands[best_i] = p;
     }
+  }
+  // third stage: the order of the counter bits above the cover (runtime
+  // kernel parameter, no recompiles).  The plan orders them for the k1 reads
+  // (a line's readers close in time); moving a low output bit down next to
+  // the cover also brings neighbouring k2 / perm lines into the same chunk
+  // front, so their DRAM writes meet in the same rows (measured on cfg5:
+  // output bit 4 at counter bit 15: 19.06 vs 19.85 ms,
+  // profiles/r02_sigma_tail_moves.txt).  Greedy: each low output bit in the
+  // tail tried at each of the 6 positions above the cover, kept on a clear
+  // (>= 1 %) win; two rounds.
+  qsim_plan cur = cands[best_i];
+  const int from = std::max(10, (int)cur.tile_log2 + 0);
+  if (!(cur.flags & 1u) && cur.M >= from + 4) {
+    for (int round = 0; round < 2 && rc == QSIM_OK; ++round) {
+      bool moved = false;
+      for (int bit = 3; bit < 12 && rc == QSIM_OK; ++bit) {
+        int at = -1;
+        for (int k = from; k < cur.M; ++k)
+          if (cur.sigma[k] == bit) at = k;
+        if (at < 0) continue;  // in the cover (or >= M)
+        for (int pos = from; pos < std::min(cur.M, from + 6) && rc == QSIM_OK; ++pos) {
+          if (pos == at) continue;
+          qsim_plan p = cur;
+          uint8_t rest[32];
+          int m = 0;
+          for (int k = from; k < cur.M; ++k)
+            if (k != at) rest[m++] = cur.sigma[k];
+          for (int k = from, r = 0; k < cur.M; ++k)
+            p.sigma[k] = k == pos ? (uint8_t)bit : rest[r++];
+          const float t = time_plan(p, false, 2);
+          if (rc == QSIM_OK && t < best * 0.99f) {
+            best = t;
+            cur = p;
+            moved = true;
+            at = pos;
+          }
+        }
+      }
+      if (!moved) break;
+    }
+    if (rc == QSIM_OK) cands[best_i] = cur;
   }
   cudaEventDestroy(a);
   cudaEventDestroy(b);
@@ -1957,9 +1813,8 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
   std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
-  if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma,
-                                    elem_bytes(plan->dtype) == 8 ? plan->pair_xor : 0u,
-                                    elem_bytes(plan->dtype), err) != 0) {
+  if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma, elem_bytes(plan->dtype),
+                                    err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }
@@ -1971,11 +1826,6 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
                                                           elem_bytes(plan->dtype),
                                                           local_tile_bits(plan->dtype), err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit (local tiles): %s", err.c_str());
-    return QSIM_ECUDA;
-  }
-  if ((plan->lin_flags & 1u) &&
-      qsim::jit_check_compile_fused_lt(gl->w, n_gates, plan->M, plan->lin, err) != 0) {
-    std::snprintf(g_err, sizeof g_err, "jit (linear traversal): %s", err.c_str());
     return QSIM_ECUDA;
   }
   return QSIM_OK;
@@ -2019,6 +1869,6 @@ int qsim_jit_check_compile(const qsim_gate* gates, int32_t n_gates, int32_t M) {
   return QSIM_OK;
 }
 
-int32_t qsim_abi_version(void) { return 6; }
+int32_t qsim_abi_version(void) { return 7; }
 
 }  // extern "C"

@@ -405,57 +405,64 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 }
 
 // Sigma-ordered fused walk + gather (qsim_kernels.cuh k_fused_sigma, with the
-// circuit and the traversal order compiled in).  If perm_out is non-null the
-// kernel also stores the map (one-pass materialised map + gather).
-// QSIM_JIT_PIPE=1 enables the software pipeline of the fused kernel (A/B)
-// CTA size of the gather kernels: 256, plus the dedicated prefetch warps of
-// the experimental QSIM_PF modes 5 / 6
-unsigned gather_threads() {
-  int m = 0, d = 0, g = 0, w = 2;
-  if (const char* pf = std::getenv("QSIM_PF")) std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
-  return m >= 5 ? 256u + 32u * (unsigned)w : 256u;
-}
-
-bool pipelined() {
-  const char* v = std::getenv("QSIM_JIT_PIPE");
-  return v && v[0] == '1';  // default off: measured neutral (map+gather) to 4 % slower (fused)
-}
-
-std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
-                         int elem, bool from_perm = false) {
+// circuit compiled in).  If perm_out is non-null the kernel also stores the
+// map (one-pass materialised map + gather); from_perm: the planned apply, the
+// sources read from a stored map instead of walked.
+//
+// Counter c -> output sigma(c): counter bits 0..4 are the lanes, 5..9 the 32
+// entries a thread holds (bit positions of its planes), 10.. the warp tile,
+// the CTA's 8 warps and the chunk.  Only sigma[0..9] shape the generated
+// code (which output bits are lane / word bits); the rest of sigma is a
+// kernel parameter (the tile offset `ob` comes from 4 shared-memory tables
+// built from it), so qsim_plan_tune can try orders of the high counter bits
+// without recompiling.
+std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem,
+                         bool from_perm) {
   std::string s = kPrelude;
   char buf[256];
-  const char* T = elem == 8 ? "uint2" : "uint4";
-  const bool pair = elem == 8 && pair_xor != 0;
-  s += "__constant__ unsigned char kSigma[32] = {";
-  for (int k = 0; k < 32; ++k) {
-    std::snprintf(buf, sizeof buf, "%u%s", (unsigned)sigma[k], k < 31 ? "," : "};\n");
-    s += buf;
-  }
-  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n"
-                "#define QSIM_PIPE %d\n#define QSIM_PAIR %d\n", T, M, elem == 8 ? 32 : 16,
-                elem == 8 && !pair && pipelined() ? 1 : 0, pair ? 1 : 0);
+  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n",
+                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16);
   s += buf;
   s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
-  {  // QSIM_DEBUG_STORE=seq|none: timing experiments on the store side (results invalid)
-    const char* ds = std::getenv("QSIM_DEBUG_STORE");
-    std::snprintf(buf, sizeof buf, "#define QSIM_DEBUG_STORE %d\n",
-                  ds && !std::strcmp(ds, "seq") ? 1 : ds && !std::strcmp(ds, "none") ? 2 : 0);
-    s += buf;
+  s += R"(
+struct Sigma { unsigned char s[32]; };
+extern "C" __global__ void __launch_bounds__(256)
+QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
+           QSIM_T* __restrict__ k2, u32* __restrict__ perm_out, const Sigma sig) {
+  __shared__ u32 tab[4][256];
+  __shared__ u64 s_chunk;
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
+    const int b = x >> 8, v = x & 255;
+    u32 r = 0;
+    for (int j = 0; j < 8; ++j)
+      if (((v >> j) & 1) && 8 * b + j < QSIM_M) r |= 1u << sig.s[8 * b + j];
+    tab[b][v] = r;
   }
-  s += "__constant__ unsigned int lt_g[32] = {";
-  for (int l = 0; l < 32; ++l) {
-    uint32_t o = (l & 1) ? pair_xor : 0u;
-    for (int j = 0; j < 5 && 5 + j < M; ++j)
-      if ((l >> j) & 1) o ^= 1u << sigma[5 + j];
-    std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  // plane initialisation: output bit b comes from counter bit inv[b]: a lane
-  // bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit (ob);
-  // then the walk and the transpose: a[l] = source of the thread's entry l
-  auto walk_tile = [&]() {
-    std::string t;
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const u64 nchunks = N >> chunk_log2;
+  const u32 tiles = 1u << (chunk_log2 - 10);
+  // chunks in counter order: from a device ticket (dynamic), or without a
+  // workspace round-robin by CTA (static; the front still moves in order)
+  for (u64 it = 0;; ++it) {
+    u64 ch;
+    if (ticket) {
+      __syncthreads();
+      if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
+      __syncthreads();
+      ch = s_chunk;
+    } else {
+      ch = (u64)blockIdx.x + it * gridDim.x;
+    }
+    if (ch >= nchunks) break;
+    for (u32 tt = warp; tt < tiles; tt += 8u) {
+      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
+      const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
+                     tab[3][(c >> 24) & 255];
+)";
+  if (!from_perm) {
+    // plane initialisation: output bit b comes from counter bit inv[b]: a
+    // lane bit (< 5), a word bit (5..9, compile-time pattern) or a tile bit
+    // (ob); then the walk and the transpose: a[l] = source of entry l
     const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
     uint8_t inv[32];
     for (int b = 0; b < 32; ++b) inv[b] = 255;
@@ -470,197 +477,22 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
         std::snprintf(buf, sizeof buf, "      u32 p%d = ((ob >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
       else
         std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
-      t += buf;
-      if ((pair_xor >> b) & 1u) {  // word bit 0 also toggles the pair difference
-        std::snprintf(buf, sizeof buf, "      p%d ^= 0xaaaaaaaau;\n", b);
-        t += buf;
-      }
+      s += buf;
     }
-    t += "    u32 sg = 0u;\n";
-    t += walk_code(w, n, M);
-    t += "      u32 a[32] = {";
+    s += "      u32 sg = 0u;\n";
+    s += walk_code(w, n, M);
+    s += "      u32 a[32] = {";
     for (int b = 0; b < 32; ++b) {
       std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-      t += buf;
+      s += buf;
     }
-    t += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-    t += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    return t;
-  };
-  // Line prefetch ahead of the gather (experimental; QSIM_PF="mode,D,G"):
-  // while a CTA gathers chunk ch it walks chunk ch + D and, for every source
-  // whose low G bits are zero (one "leader" per 2^G-entry granule of k1),
-  // asks for the whole granule in one request, so the granule's readers
-  // find it in L2.  mode 1: warp-cooperative 16-B cp.async (8 / 16 lanes per
-  // 128 / 256-B granule); 2: cp.async.bulk.prefetch.L2 of the granule by the
-  // leader lane; 3: prefetch.global.L2 by the leader lane.
-  int pf_mode = 0, pf_d = 0, pf_g = elem == 8 ? 4 : 3, pf_w = 2;
-  if (const char* pf = std::getenv("QSIM_PF")) std::sscanf(pf, "%d,%d,%d,%d", &pf_mode, &pf_d, &pf_g, &pf_w);
-  // modes 5 / 6: the prefetch runs in pf_w dedicated warps (6: control, no loads)
-  std::snprintf(buf, sizeof buf, "#define QSIM_PF_MODE %d\n#define QSIM_PF_D %d\n#define QSIM_PF_G %d\n"
-                "#define QSIM_PF_W %d\n#define QSIM_PF_SPEC %d\n#define QSIM_THREADS %d\n",
-                pf_mode, pf_d, pf_g, pf_w, pf_mode >= 5 ? 1 : 0, pf_mode >= 5 ? 256 + 32 * pf_w : 256);
-  s += buf;
-  // the prefetch of one warp tile (1024 outputs of chunk pch): sources, then
-  // a whole-granule request for every source whose low G bits are zero
-  auto pf_sources = [&]() -> std::string {
-    if (from_perm)  // from the map (L2-resident when the gather re-reads it)
-      return R"(
-        u32 a[32];
-        { const u32 lo = tab[0][lane];
-          _Pragma("unroll") for (int l = 0; l < 32; ++l) a[l] = perm_out[ob ^ lt_g[l] ^ lo]; }
-)";
-    return walk_tile() + "        (void)sg;\n";
-  };
-  auto pf_issue = []() -> std::string {
-    return R"(
-        constexpr u32 GM = (1u << QSIM_PF_G) - 1u;
-        constexpr u32 GB = sizeof(QSIM_T) << QSIM_PF_G;   // granule bytes
-#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4 || QSIM_PF_MODE == 5 || QSIM_PF_MODE == 6
-        constexpr u32 LPG = GB / 16u;                     // lanes per granule
-        constexpr u32 GPI = 32u / LPG;                    // granules per instruction
-        u32 cnt = 0u;
-        const u32 ltm = (1u << lane) - 1u;
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-          const bool pr = (a[l] & GM) == 0u;
-          const u32 bal = __ballot_sync(0xffffffffu, pr);
-          if (pr) q[cnt + __popc(bal & ltm)] = a[l] >> QSIM_PF_G;
-          cnt += __popc(bal);
-        }
-        __syncwarp();
-        for (u32 j = 0; j < cnt; j += GPI) {
-          const u32 idx = j + lane / LPG;
-          if (idx < cnt) {
-            const u32 line = q[idx];
-#if QSIM_PF_MODE == 4 || QSIM_PF_MODE == 6   // control: the queue without the loads
-            if (line == 0xffffffffu)
-#endif
-            {
-              const char* src = reinterpret_cast<const char*>(k1) + (u64)line * GB + (lane % LPG) * 16u;
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;"
-                           :: "r"((u32)__cvta_generic_to_shared(scr + lane * 16u)), "l"(src)
-                           : "memory");
-            }
-          }
-        }
-        __syncwarp();
-#else
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-          if ((a[l] & GM) == 0u) {
-            const char* src = reinterpret_cast<const char*>(k1 + a[l]);
-#if QSIM_PF_MODE == 2
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(src), "r"(GB) : "memory");
-#else
-            asm volatile("prefetch.global.L2 [%0];" :: "l"(src) : "memory");
-#endif
-          }
-        }
-#endif
-)";
-  };
-  s += R"(
-extern "C" __global__ void __launch_bounds__(QSIM_THREADS)
-QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
-           QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
-  __shared__ u32 tab[4][256];
-  __shared__ u64 s_chunk;
-#if QSIM_PF_SPEC
-  __shared__ u32 s_done;
-  __shared__ u32 pf_q[QSIM_PF_W * 1024];
-  __shared__ __align__(16) unsigned char pf_scratch[QSIM_PF_W * 512];
-  if (threadIdx.x == 0) { s_done = 0u; s_chunk = ~0ull; }
-#define QSIM_BAR() asm volatile("bar.sync 1, 256;" ::: "memory")
-#else
-#define QSIM_BAR() __syncthreads()
-#endif
-#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4
-  __shared__ u32 pf_q[8 * 1024];
-  __shared__ __align__(16) unsigned char pf_scratch[8 * 512];
-#endif
-  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
-    const int b = x >> 8, v = x & 255;
-    u32 r = 0;
-    for (int j = 0; j < 8; ++j)
-      if (((v >> j) & 1) && 8 * b + j < QSIM_M) r |= 1u << kSigma[8 * b + j];
-    tab[b][v] = r;
+    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
   }
-  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const u64 nchunks = N >> chunk_log2;
-  const u32 tiles = 1u << (chunk_log2 - 10);
-#if QSIM_PIPE
-  // software pipeline: a warp tile's 32 gathers stay in flight while the
-  // warp walks its next tile; they are stored after that walk
-  QSIM_T v[32];
-  u32 pob = 0u, psg = 0u;
-  bool pend = false;
-#endif
-#if QSIM_PF_SPEC
-  __syncthreads();
-  if (warp >= 8) {  // dedicated prefetch warps: follow the CTA's chunk, D chunks ahead
-    const u32 pw = warp - 8u;
-    u64 last = ~0ull;
-    for (;;) {
-      const u64 ch = *reinterpret_cast<volatile u64*>(&s_chunk);
-      if (*reinterpret_cast<volatile u32*>(&s_done)) break;
-      if (ch == last || ch == ~0ull) { __nanosleep(256); continue; }
-      last = ch;
-      const u64 pch = ch + QSIM_PF_D;
-      if (pch >= nchunks) continue;
-      for (u32 tt = pw; tt < tiles; tt += QSIM_PF_W) {
-        const u64 c = (pch << chunk_log2) + ((u64)tt << 10);
-        const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
-                       tab[3][(c >> 24) & 255];
-        u32* q = pf_q + pw * 1024u;
-        unsigned char* scr = pf_scratch + pw * 512u;
-)";
-    s += pf_sources() + pf_issue();
-    s += R"(
-      }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    return;
-  }
-#endif
-  for (;;) {
-    QSIM_BAR();
-    if (threadIdx.x == 0) {
-      s_chunk = atomicAdd(ticket, 1ull);
-#if QSIM_PF_SPEC
-      if (s_chunk >= nchunks) s_done = 1u;
-#endif
-    }
-    QSIM_BAR();
-    const u64 ch = s_chunk;
-    if (ch >= nchunks) break;
-)";
-  if (pf_mode >= 1 && pf_mode <= 4) {
-    s += R"(
-    if (ch + QSIM_PF_D < nchunks) {
-      const u64 pch = ch + QSIM_PF_D;
-      for (u32 tt = warp; tt < tiles; tt += 8u) {
-        const u64 c = (pch << chunk_log2) + ((u64)tt << 10);
-        const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
-                       tab[3][(c >> 24) & 255];
-        u32* q = pf_q + warp * 1024u;
-        unsigned char* scr = pf_scratch + warp * 512u;
-)";
-    s += pf_sources() + pf_issue();
-    s += R"(
-      }
-    }
-)";
-  }
-  s += R"(
-    for (u32 tt = warp; tt < tiles; tt += 8u) {
-      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
-      const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
-                     tab[3][(c >> 24) & 255];
-)";
-  if (!from_perm) s += walk_tile();
   // output offsets of the 32 word bits: sigma(l << 5), compile-time
   s += "      const u32 lt[32] = {";
   for (int l = 0; l < 32; ++l) {
-    uint32_t o = (l & 1) ? pair_xor : 0u;
+    uint32_t o = 0u;
     for (int j = 0; j < 5 && 5 + j < M; ++j)
       if ((l >> j) & 1) o ^= 1u << sigma[5 + j];
     std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
@@ -682,362 +514,12 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
       }
 )";
   s += R"(
-#if QSIM_PAIR
-      // lane L word l and lane L^1 word l^1 hold outputs o and o ^ d: when their
-      // sources are the two entries of one aligned 16-byte pair, the lane with
-      // the even source loads both and hands the odd one over
-      _Pragma("unroll") for (int h = 0; h < 32; h += 16) {
-        uint4 w4[16];
-        bool take[16];
-        _Pragma("unroll") for (int j = 0; j < 16; j += 2) {
-          const u32 x0 = a[h + j], x1 = a[h + j + 1];
-          const u32 p0 = __shfl_xor_sync(0xffffffffu, x1, 1);  // partner's word l+1: pairs with my l
-          const u32 p1 = __shfl_xor_sync(0xffffffffu, x0, 1);  // partner's word l: pairs with my l+1
-          take[j] = ((x0 ^ p0) == 1u) && (x0 & 1u);
-          take[j + 1] = ((x1 ^ p1) == 1u) && (x1 & 1u);
-          w4[j] = make_uint4(0u, 0u, 0u, 0u);
-          w4[j + 1] = make_uint4(0u, 0u, 0u, 0u);
-          if (!take[j]) w4[j] = ldg(reinterpret_cast<const uint4*>(k1) + (x0 >> 1));
-          if (!take[j + 1]) w4[j + 1] = ldg(reinterpret_cast<const uint4*>(k1) + (x1 >> 1));
-        }
-        _Pragma("unroll") for (int j = 0; j < 16; j += 2) {
-          const int l = h + j;
-          const uint4 q0 = w4[j], q1 = w4[j + 1];
-          const u32 s0x = __shfl_xor_sync(0xffffffffu, q1.z, 1), s0y = __shfl_xor_sync(0xffffffffu, q1.w, 1);
-          const u32 s1x = __shfl_xor_sync(0xffffffffu, q0.z, 1), s1y = __shfl_xor_sync(0xffffffffu, q0.w, 1);
-          const uint2 v0 = take[j] ? make_uint2(s0x, s0y)
-                                   : ((a[l] & 1u) ? make_uint2(q0.z, q0.w) : make_uint2(q0.x, q0.y));
-          const uint2 v1 = take[j + 1] ? make_uint2(s1x, s1y)
-                                       : ((a[l + 1] & 1u) ? make_uint2(q1.z, q1.w) : make_uint2(q1.x, q1.y));
-          stcs(k2 + (ob ^ lt[l] ^ lo), negate_if(v0, (sg >> l) & 1u));
-          stcs(k2 + (ob ^ lt[l + 1] ^ lo), negate_if(v1, (sg >> (l + 1)) & 1u));
-        }
-      }
-#elif QSIM_PIPE
-      if (pend) {
-        _Pragma("unroll") for (int l = 0; l < 32; ++l)
-          stcs(k2 + (pob ^ lt[l] ^ lo), negate_if(v[l], (psg >> l) & 1u));
-      }
-      _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
-      pob = ob;
-      psg = sg;
-      pend = true;
-#else
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
-#if QSIM_DEBUG_STORE == 1   // timing experiment only (wrong result): k2 in counter order
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
-          stcs(k2 + (c + 32u * (h + l) + lane), negate_if(v[l], (sg >> (h + l)) & 1u));
-#elif QSIM_DEBUG_STORE == 2  // timing experiment only (wrong result): loads, no k2
-        u32 x = 0u;
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) x ^= v[l].x;
-        if (x == 0x9e3779b9u) stcs(k2 + c, v[0]);
-#else
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
           stcs(k2 + (ob ^ lt[h + l] ^ lo), negate_if(v[l], (sg >> (h + l)) & 1u));
-#endif
       }
-#endif
-    }
-  }
-#if QSIM_PF_MODE == 1 || QSIM_PF_MODE == 4
-  asm volatile("cp.async.wait_all;" ::: "memory");
-#endif
-#if QSIM_PIPE
-  if (pend) {
-    const u32 lo = tab[0][lane];
-    _Pragma("unroll") for (int l = 0; l < 32; ++l)
-      stcs(k2 + (pob ^ lt_g[l] ^ lo), negate_if(v[l], (psg >> l) & 1u));
-  }
-#endif
-}
-)";
-  return s;
-}
-
-// Linear-traversal fused walk + gather (complex64): output = XOR of lin[k]
-// over the set bits k of the counter (qsim_plan.lin).  The lanes of a warp
-// differ by the commonest sector-mate differences, so one warp load touches
-// ~12 instead of 32 k1 sectors; the warp's 1024 outputs are a union of
-// 16-entry runs (lin[0..9] span output bits 0..3) and are written through a
-// per-warp shared-memory transpose: entry (lane, l) sits at l*32 + lane, the
-// write order u (bits 0..3 = output bits 0..3) reads it at B.u (B = the
-// coordinates of the write basis W in lin[0..9]).
-namespace {
-struct LtWrite {
-  uint32_t W[10], B[10];
-  uint32_t Sk[6], Sp[5];  // bank swizzles: k2 view (8-B entries), perm view (4-B entries)
-};
-// rank over GF(2) of a set of vectors
-int gf2_rank(std::vector<uint32_t> v) {
-  int r = 0;
-  for (int bit = 31; bit >= 0; --bit) {
-    int piv = -1;
-    for (size_t i = r; i < v.size(); ++i)
-      if ((v[i] >> bit) & 1u) {
-        piv = (int)i;
-        break;
-      }
-    if (piv < 0) continue;
-    std::swap(v[r], v[piv]);
-    for (size_t i = 0; i < v.size(); ++i)
-      if ((int)i != r && ((v[i] >> bit) & 1u)) v[i] ^= v[r];
-    ++r;
-  }
-  return r;
-}
-// position of counter offset q in a view whose banks are the low `lb` bits:
-// q ^ S(q >> lb), S linear (columns S[j] for bit j of q >> lb)
-uint32_t swz(uint32_t q, const uint32_t* S, int lb, int hb) {
-  uint32_t r = q;
-  for (int j = 0; j < hb; ++j)
-    if ((q >> (lb + j)) & 1u) r ^= S[j];
-  return r;
-}
-// choose S so that lanes reading q = sum lane_j L[j] hit distinct banks
-void pick_swizzle(const uint32_t* L, int lb, int hb, uint32_t* S) {
-  uint64_t z = 0x243f6a8885a308d3ull;
-  for (int tries = 0; tries < 4096; ++tries) {
-    for (int j = 0; j < hb; ++j) {
-      if (tries == 0) {
-        S[j] = 0;
-        continue;
-      }
-      z = z * 6364136223846793005ull + 1442695040888963407ull;
-      S[j] = (uint32_t)(z >> 40) & ((1u << lb) - 1u);
-    }
-    std::vector<uint32_t> low;
-    for (int j = 0; j < 5; ++j) low.push_back(swz(L[j], S, lb, hb) & ((1u << lb) - 1u));
-    if (gf2_rank(low) >= lb) return;
-  }
-}
-bool lt_write_basis(const uint32_t* lin, LtWrite& wb) {
-  // echelon of lin[0..9] with coordinates
-  std::vector<std::pair<uint32_t, uint32_t>> ech;  // (vector, coords)
-  auto reduce = [&](uint32_t v, uint32_t c, uint32_t& vo, uint32_t& co) {
-    for (const auto& e : ech)
-      if ((v ^ e.first) < v) {
-        v ^= e.first;
-        c ^= e.second;
-      }
-    vo = v;
-    co = c;
-  };
-  for (int j = 0; j < 10; ++j) {
-    uint32_t v, c;
-    reduce(lin[j], 1u << j, v, c);
-    if (v == 0) return false;
-    ech.push_back({v, c});
-    std::sort(ech.begin(), ech.end(),
-              [](const std::pair<uint32_t, uint32_t>& x, const std::pair<uint32_t, uint32_t>& y) {
-                return x.first > y.first;
-              });
-  }
-  auto coords = [&](uint32_t w, uint32_t& c) {
-    uint32_t v;
-    reduce(w, 0u, v, c);
-    return v == 0;
-  };
-  int k = 0;
-  std::vector<uint32_t> wech;
-  auto winsert = [&](uint32_t v) {
-    for (uint32_t b : wech)
-      if ((v ^ b) < v) v ^= b;
-    if (v == 0) return false;
-    wech.push_back(v);
-    std::sort(wech.begin(), wech.end(), [](uint32_t x, uint32_t y) { return x > y; });
-    return true;
-  };
-  for (int b = 0; b < 4; ++b) {
-    wb.W[k] = 1u << b;
-    if (!coords(wb.W[k], wb.B[k]) || !winsert(wb.W[k])) return false;
-    ++k;
-  }
-  for (int j = 0; j < 10 && k < 10; ++j) {
-    const uint32_t w = lin[j] & ~15u;  // output bits 0..3 come from u bits 0..3 only
-    if (!winsert(w)) continue;
-    wb.W[k] = w;
-    if (!coords(w, wb.B[k])) return false;
-    ++k;
-  }
-  if (k != 10) return false;
-  pick_swizzle(wb.B + 1, 4, 6, wb.Sk);  // k2 reads: lanes -> u bits 1..5
-  pick_swizzle(wb.B + 2, 5, 5, wb.Sp);  // perm reads: lanes -> u bits 2..6
-  return true;
-}
-}  // namespace
-
-std::string fused_lt_source(const uint32_t* w, int n, int M, const uint32_t* lin) {
-  std::string s = kPrelude;
-  char buf[256];
-  LtWrite wb;
-  if (!lt_write_basis(lin, wb)) return std::string();
-  s += "__constant__ unsigned int kLin[32] = {";
-  for (int k = 0; k < 32; ++k) {
-    std::snprintf(buf, sizeof buf, "%uu%s", k < M ? lin[k] : 0u, k < 31 ? "," : "};\n");
-    s += buf;
-  }
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n", M);
-  s += buf;
-  {  // QSIM_DEBUG_STORE=none: timing experiment on the store side (results invalid)
-    const char* ds = std::getenv("QSIM_DEBUG_STORE");
-    s += ds && !std::strcmp(ds, "none") ? "#define QSIM_DEBUG_STORE 2\n" : "#define QSIM_DEBUG_STORE 0\n";
-  }
-  s += R"(
-extern "C" __global__ void __launch_bounds__(256)
-qsim_jit_fused_lt(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ k1,
-                  uint2* __restrict__ k2, u32* __restrict__ perm_out) {
-  extern __shared__ __align__(16) uint2 stage_all[];   // [8 warps][1024]
-  __shared__ u32 tab[4][256];
-  __shared__ u64 s_chunk;
-  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
-    const int b = x >> 8, v = x & 255;
-    u32 r = 0;
-    for (int j = 0; j < 8; ++j)
-      if (((v >> j) & 1) && 8 * b + j < QSIM_M) r ^= kLin[8 * b + j];
-    tab[b][v] = r;
-  }
-  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint2* sv = stage_all + warp * 1024u;
-  u32* sp = reinterpret_cast<u32*>(sv);
-  const u64 nchunks = N >> chunk_log2;
-  const u32 tiles = 1u << (chunk_log2 - 10);
-)";
-  // per-thread lane words and write-back offsets
-  for (int j = 0; j < 5; ++j) {
-    std::snprintf(buf, sizeof buf, "  const u32 lw%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", j, j);
-    s += buf;
-  }
-  auto lanexor = [&](const char* name, const uint32_t* vec, int off) {
-    std::string t = std::string("  const u32 ") + name + " = 0u";
-    for (int j = 0; j < 5; ++j) {
-      std::snprintf(buf, sizeof buf, " ^ (lw%d & %uu)", j, vec[off + j]);
-      t += buf;
-    }
-    return t + ";\n";
-  };
-  // shared-memory positions are bank-swizzled (linear): k2 view q ^ Sk(q >> 4),
-  // perm view q ^ Sp(q >> 5); everything below is already swizzled
-  uint32_t Bk[10], Bp[10];
-  for (int j = 0; j < 10; ++j) {
-    Bk[j] = swz(wb.B[j], wb.Sk, 4, 6);
-    Bp[j] = swz(wb.B[j], wb.Sp, 5, 5);
-  }
-  s += lanexor("qkl", Bk, 1);     // k2: u = it*64 + lane*2  (lane -> u bits 1..5)
-  s += lanexor("okl", wb.W, 1);
-  s += lanexor("qpl", Bp, 2);     // perm: u = it*128 + lane*4 (lane -> u bits 2..6)
-  s += lanexor("opl", wb.W, 2);
-  // writes: entry (lane, l) at q = 32 l + lane -> swizzled lane part + per-l constant
-  {
-    uint32_t lk[5], lp[5];
-    for (int j = 0; j < 5; ++j) {
-      lk[j] = swz(1u << j, wb.Sk, 4, 6);
-      lp[j] = swz(1u << j, wb.Sp, 5, 5);
-    }
-    s += lanexor("wkl", lk, 0);
-    s += lanexor("wpl", lp, 0);
-  }
-  std::snprintf(buf, sizeof buf, "#define QB0 %uu\n#define QB1 %uu\n#define PB0 %uu\n#define PB1 %uu\n",
-                Bk[0], Bk[1], Bp[0], Bp[1]);
-  s += buf;
-  s += "  const u32 wkc[32] = {";
-  for (int l = 0; l < 32; ++l) {
-    std::snprintf(buf, sizeof buf, "%uu%s", swz(32u * l, wb.Sk, 4, 6), l < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += "  const u32 wpc[32] = {";
-  for (int l = 0; l < 32; ++l) {
-    std::snprintf(buf, sizeof buf, "%uu%s", swz(32u * l, wb.Sp, 5, 5), l < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += R"(
-  for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
-    __syncthreads();
-    const u64 ch = s_chunk;
-    if (ch >= nchunks) break;
-    for (u32 tt = warp; tt < tiles; tt += 8u) {
-      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
-      const u32 ob = tab[1][(c >> 8) & 255] ^ tab[2][(c >> 16) & 255] ^ tab[3][(c >> 24) & 255];
-)";
-  // planes: XOR of the lane words, word patterns and ob bits
-  const uint32_t pat[5] = {0xaaaaaaaau, 0xccccccccu, 0xf0f0f0f0u, 0xff00ff00u, 0xffff0000u};
-  for (int b = 0; b < 32; ++b) {
-    if (b >= M) {
-      std::snprintf(buf, sizeof buf, "      u32 p%d = 0u;\n", b);
-      s += buf;
-      continue;
-    }
-    std::string e = "      u32 p" + std::to_string(b) + " = ((ob >> " + std::to_string(b) +
-                    ") & 1u ? 0xffffffffu : 0u)";
-    uint32_t wordc = 0;
-    for (int j = 0; j < 10 && j < M; ++j)
-      if ((lin[j] >> b) & 1u) {
-        if (j < 5) e += " ^ lw" + std::to_string(j);
-        else wordc ^= pat[j - 5];
-      }
-    std::snprintf(buf, sizeof buf, " ^ %uu;\n", wordc);
-    s += e + buf;
-  }
-  s += "      u32 sg = 0u;\n";
-  s += walk_code(w, n, M);
-  s += "      u32 a[32] = {";
-  for (int b = 0; b < 32; ++b) {
-    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-  s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-  s += R"(
-      uint2 v[32];
-      _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = ldg(k1 + a[l]);
-#if QSIM_DEBUG_STORE == 2   // timing experiment only (wrong result): loads, no stores
-      { u32 x = 0u; _Pragma("unroll") for (int l = 0; l < 32; ++l) x ^= v[l].x;
-        if (x == 0x9e3779b9u) k2[0] = v[0]; }
-      continue;
-#endif
-      if (perm_out) {
-        _Pragma("unroll") for (int l = 0; l < 32; ++l) sp[wpc[l] ^ wpl] = a[l];
-        __syncwarp();
-)";
-  for (int it = 0; it < 8; ++it) {
-    uint32_t qc = 0, oc = 0;
-    for (int j = 0; j < 3; ++j)
-      if ((it >> j) & 1) {
-        qc ^= Bp[7 + j];
-        oc ^= wb.W[7 + j];
-      }
-    std::snprintf(buf, sizeof buf,
-                  "        { const u32 q0 = qpl ^ %uu; const u32 o = ob ^ opl ^ %uu;\n"
-                  "          __stcs(reinterpret_cast<uint4*>(perm_out + o), make_uint4(sp[q0], "
-                  "sp[q0 ^ PB0], sp[q0 ^ PB1], sp[q0 ^ PB0 ^ PB1])); }\n",
-                  qc, oc);
-    s += buf;
-  }
-  s += R"(
-        __syncwarp();
-      }
-      _Pragma("unroll") for (int l = 0; l < 32; ++l) sv[wkc[l] ^ wkl] = negate_if(v[l], (sg >> l) & 1u);
-      __syncwarp();
-)";
-  for (int it = 0; it < 16; ++it) {
-    uint32_t qc = 0, oc = 0;
-    for (int j = 0; j < 4; ++j)
-      if ((it >> j) & 1) {
-        qc ^= Bk[6 + j];
-        oc ^= wb.W[6 + j];
-      }
-    std::snprintf(buf, sizeof buf,
-                  "      { const u32 q0 = qkl ^ %uu; const uint2 y0 = sv[q0], y1 = sv[q0 ^ QB0];\n"
-                  "        stcs(reinterpret_cast<uint4*>(k2 + (ob ^ okl ^ %uu)), "
-                  "make_uint4(y0.x, y0.y, y1.x, y1.y)); }\n",
-                  qc, oc);
-    s += buf;
-  }
-  s += R"(
-      __syncwarp();
     }
   }
 }
@@ -1069,10 +551,8 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   char buf[640];
   const bool f32 = elem == 8, wide = M > 32;
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  int minb = 1;  // resident CTAs asked of ptxas (register cap); A/B via QSIM_KRON_MINB
-  if (const char* mb = std::getenv("QSIM_KRON_MINB")) minb = std::max(1, std::min(8, std::atoi(mb)));
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n"
-                "#define QSIM_MINB %d\n", M, gb, ng, minb);
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M, gb,
+                ng);
   s += buf;
   s += thread_defs(J, L);
   s += f32 ? R"(
@@ -1086,7 +566,7 @@ __device__ __forceinline__ C cmul(C a, C b) {
 )";
   s += R"(
 struct Qubits { double v[64][4]; u32 M, gbits, ngroups; unsigned char pos[64]; u32 permuted; };
-extern "C" __global__ void __launch_bounds__(256, QSIM_MINB)
+extern "C" __global__ void __launch_bounds__(256, 1)
 qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) {
   extern __shared__ __align__(16) unsigned char kt_smem[];
   C* T = reinterpret_cast<C*>(kt_smem);   // [QSIM_NG << QSIM_GB]
@@ -1114,32 +594,11 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   s += walk_code(w, n, M);
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
 
-  const char* aff_env = std::getenv("QSIM_KRON_AFFINE");  // A/B: affine fast path
-  const bool affine = aff_env && aff_env[0] == '1';
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
       std::snprintf(buf, sizeof buf, "    un |= %s ^ (u32)((int)%s >> 31);\n", P(k).c_str(), P(k).c_str());
       s += buf;
-    }
-    if (affine) {  // table-0 index of entry l = x0 ^ (columns of the set bits of l)
-      s += "    u32 x0 = 0u, c0 = 0u, c1 = 0u, c2 = 0u, c3 = 0u, c4 = 0u;\n";
-      for (int k = 0; k < nv; ++k) {
-        const std::string pk = P(k);
-        std::snprintf(buf, sizeof buf,
-                      "    { const u32 d = %s ^ (0u - (%s & 1u)); u32 h = d & 0x00010116u;\n"
-                      "      h ^= (h << 1) & 0xaaaaaaaau; h ^= (h << 2) & 0xccccccccu; "
-                      "h ^= (h << 4) & 0xf0f0f0f0u;\n"
-                      "      h ^= (h << 8) & 0xff00ff00u; h ^= (h << 16) & 0xffff0000u; un |= h ^ d;\n",
-                      pk.c_str(), pk.c_str());
-        s += buf;
-        std::snprintf(buf, sizeof buf,
-                      "      x0 |= (%s & 1u) << %d; c0 |= ((d >> 1) & 1u) << %d; c1 |= ((d >> 2) & 1u) << %d;\n"
-                      "      c2 |= ((d >> 4) & 1u) << %d; c3 |= ((d >> 8) & 1u) << %d; "
-                      "c4 |= ((d >> 16) & 1u) << %d; }\n",
-                      pk.c_str(), k, k, k, k, k, k);
-        s += buf;
-      }
     }
     s += "    if (__all_sync(0xffffffffu, un == 0u)) {\n";
     for (int g = 0; g < ng; ++g) {
@@ -1158,41 +617,15 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
       std::snprintf(buf, sizeof buf, "      cc = cmul(cc, T[%d | i%d]);\n", g << gb, g);
       s += buf;
     }
-    if (affine) {
-      s += "      C* const kq = k2 + (base + lane - start);\n";
-      for (int pass = 0; pass < 2; ++pass) {
-        s += pass == 0 ? "      if (full) {\n" : "      } else {\n";
-        s += "        u32 x = x0 | i0;\n";
-        for (int t = 0; t < 32; ++t) {
-          const int l = t ^ (t >> 1);
-          if (t) {
-            std::snprintf(buf, sizeof buf, "        x ^= c%d;\n", __builtin_ctz((unsigned)t));
-            s += buf;
-          }
-          if (pass == 0)
-            std::snprintf(buf, sizeof buf,
-                          "        __stcs(kq + QSIM_OFF(%d), negate_if(cmul(cc, T[x]), (sg >> %d) & 1u));\n",
-                          l, l);
-          else
-            std::snprintf(buf, sizeof buf,
-                          "        { const u64 addr = base + lane + QSIM_OFF(%d); if (addr >= start && "
-                          "addr < end) __stcs(kq + QSIM_OFF(%d), negate_if(cmul(cc, T[x]), (sg >> %d) & 1u)); }\n",
-                          l, l, l);
-          s += buf;
-        }
-      }
-      s += "      }\n      continue;\n    }\n";
-    } else {
-      s += "      u32 a[32] = {";
-      for (int k = 0; k < 32; ++k) {
-        s += k < nv ? P(k) : std::string("0u");
-        s += k < 31 ? ", " : "};\n";
-      }
-      s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-      s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-      s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
-      s += "      continue;\n    }\n";
+    s += "      u32 a[32] = {";
+    for (int k = 0; k < 32; ++k) {
+      s += k < nv ? P(k) : std::string("0u");
+      s += k < 31 ? ", " : "};\n";
     }
+    s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
+    s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
+    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += "      continue;\n    }\n";
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
@@ -1485,8 +918,44 @@ int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint
   return 0;
 }
 
-int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
-              uint32_t chunk_log2,
+namespace {
+// the kernel parameter carrying the whole traversal order (see fused_source)
+struct SigmaArg {
+  unsigned char s[32];
+};
+
+// one chunk ticket reset + launch of a gather kernel (fused / apply)
+int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log2, const void* k1,
+                  void* k2, uint32_t* perm, void* ticket, int blocks, cudaStream_t st,
+                  std::string& err) {
+  uint64_t N = 1ull << M;
+  uint32_t cl = chunk_log2;
+  SigmaArg sg;
+  std::memcpy(sg.s, sigma, 32);
+  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &perm, &sg};
+  if (ticket && cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
+    err = "ticket reset failed";
+    return -1;
+  }
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+      CUDA_SUCCESS) {
+    err = "cuLaunchKernel failed";
+    return -1;
+  }
+  return 0;
+}
+
+// cache key of a gather kernel: what shapes its code (sigma[0..9], the dtype
+// and, for the fused walk, the gates)
+std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem) {
+  std::vector<uint32_t> keyw(words, words + n);
+  for (int k = 0; k < 10; ++k) keyw.push_back(sigma[k]);
+  keyw.push_back((uint32_t)elem);
+  return keyw;
+}
+}  // namespace
+
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err) {
   CUfunction fn = nullptr;
@@ -1497,106 +966,17 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
       err = g_status;
       return -1;
     }
-    std::vector<uint32_t> keyw(words, words + n);
-    for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
-    keyw.push_back((uint32_t)elem);
-    keyw.push_back(pair_xor);
-    if (const char* pf = std::getenv("QSIM_PF")) {  // experimental prefetch (see fused_source)
-      int m = 0, d = 0, g = 0, w = 2;
-      std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
-      keyw.push_back(0x70660000u | (uint32_t)m);
-      keyw.push_back((uint32_t)d);
-      keyw.push_back((uint32_t)g);
-      keyw.push_back((uint32_t)w);
-    }
-    // the source is only generated on a cache miss
-    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), 0x66757365ull);
-    for (const Entry& e : g_cache[key])
+    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem);
+    const uint64_t kind = 0x66757365ull;
+    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+    for (const Entry& e : g_cache[key])  // the source is only generated on a cache miss
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(0x66757365ull, keyw, M, fused_source(words, n, M, sigma, pair_xor, elem),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false),
                              "qsim_jit_fused", err);
     if (!fn) return -1;
   }
-  uint64_t N = 1ull << M;
-  uint32_t cl = chunk_log2;
-  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &perm_out};
-  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
-    err = "ticket reset failed";
-    return -1;
-  }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, gather_threads(), 1, 1, 0, (CUstream)st, args, nullptr) !=
-      CUDA_SUCCESS) {
-    err = "cuLaunchKernel failed";
-    return -1;
-  }
-  return 0;
-}
-
-int jit_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin, uint32_t chunk_log2,
-                 const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
-                 cudaStream_t st, std::string& err) {
-  const int smem = 8 * 1024 * 8;  // per-warp transposes
-  CUfunction fn = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    init_locked();
-    if (!(g_nvrtc.ok && g_drv.ok)) {
-      err = g_status;
-      return -1;
-    }
-    std::vector<uint32_t> keyw(words, words + n);
-    for (int k = 0; k < 32; ++k) keyw.push_back(lin[k]);
-    const uint64_t kind = 0x6c696e6561ull;
-    const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
-    for (const Entry& e : g_cache[key])
-      if (e.M == M && e.words == keyw) fn = e.fn;
-    if (!fn) {
-      const std::string src = fused_lt_source(words, n, M, lin);
-      if (src.empty()) {
-        err = "linear traversal: no write basis";
-        return -1;
-      }
-      fn = get_kernel_locked(kind, keyw, M, src, "qsim_jit_fused_lt", err);
-      if (!fn) return -1;
-      if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
-        err = "cuFuncSetAttribute(max dynamic smem) failed";
-        return -1;
-      }
-      // shared memory for the transposes, the rest of the array stays L1
-      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 31);
-    }
-  }
-  uint64_t N = 1ull << M;
-  uint32_t cl = chunk_log2;
-  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &perm_out};
-  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
-    err = "ticket reset failed";
-    return -1;
-  }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, args,
-                   nullptr) != CUDA_SUCCESS) {
-    err = "cuLaunchKernel failed";
-    return -1;
-  }
-  return 0;
-}
-
-int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin,
-                               std::string& err) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  init_locked();
-  if (!g_nvrtc.ok) {
-    err = g_status;
-    return -1;
-  }
-  const std::string src = fused_lt_source(words, n, M, lin);
-  if (src.empty()) {
-    err = "linear traversal: no write basis";
-    return -1;
-  }
-  std::vector<char> cubin;
-  return compile_cubin_locked(src, cubin, err) ? 0 : -1;
+  return launch_gather(fn, M, sigma, chunk_log2, k1, k2, perm_out, ticket, blocks, st, err);
 }
 
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,
@@ -1680,40 +1060,18 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
       err = g_status;
       return -1;
     }
-    std::vector<uint32_t> keyw;
-    for (int k = 0; k < 32; ++k) keyw.push_back(sigma[k]);
-    keyw.push_back((uint32_t)elem);
-    if (const char* pf = std::getenv("QSIM_PF")) {  // experimental prefetch (see fused_source)
-      int m = 0, d = 0, g = 0, w = 2;
-      std::sscanf(pf, "%d,%d,%d,%d", &m, &d, &g, &w);
-      keyw.push_back(0x70660000u | (uint32_t)m);
-      keyw.push_back((uint32_t)d);
-      keyw.push_back((uint32_t)g);
-      keyw.push_back((uint32_t)w);
-    }
+    const std::vector<uint32_t> keyw = gather_key(nullptr, 0, sigma, elem);
     const uint64_t kind = 0x6170706c79ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, 0u, elem, true),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true),
                              "qsim_jit_apply", err);
     if (!fn) return -1;
   }
-  uint64_t N = 1ull << M;
-  uint32_t cl = chunk_log2;
-  uint32_t* pm = const_cast<uint32_t*>(perm);
-  void* args[] = {&N, &cl, &ticket, const_cast<void**>(&k1), &k2, &pm};
-  if (cudaMemsetAsync(ticket, 0, sizeof(unsigned long long), st) != cudaSuccess) {
-    err = "ticket reset failed";
-    return -1;
-  }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, gather_threads(), 1, 1, 0, (CUstream)st, args, nullptr) !=
-      CUDA_SUCCESS) {
-    err = "cuLaunchKernel failed";
-    return -1;
-  }
-  return 0;
+  return launch_gather(fn, M, sigma, chunk_log2, k1, k2, const_cast<uint32_t*>(perm), ticket,
+                       blocks, st, err);
 }
 
 int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,
@@ -1775,11 +1133,10 @@ int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(nullptr, 0, M, sigma, 0u, elem, true), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(nullptr, 0, M, sigma, elem, true), cubin, err) ? 0 : -1;
 }
 
-int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,
-                            uint32_t pair_xor, int elem,
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
                             std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
@@ -1788,7 +1145,7 @@ int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(words, n, M, sigma, pair_xor, elem), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(words, n, M, sigma, elem, false), cubin, err) ? 0 : -1;
 }
 
 }  // namespace qsim

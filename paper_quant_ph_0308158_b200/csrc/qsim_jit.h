@@ -23,11 +23,10 @@ int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint
               uint64_t start, uint64_t count, uint32_t* perm_out, int sms, cudaStream_t st,
               std::string& err);
 // Sigma-ordered fused walk + gather over all 2^M outputs with a kernel
-// compiled for (circuit, sigma, element size); if perm_out != null the map is
-// stored as well (one-pass map + gather).  ticket: device scratch (reset on
-// st).  Returns 0 or -1 with err.
-int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t pair_xor,
-              uint32_t chunk_log2,
+// compiled for (circuit, sigma[0..9], element size); sigma[10..] is a kernel
+// parameter.  If perm_out != null the map is stored as well (one-pass map +
+// gather).  ticket: device scratch (reset on st).  Returns 0 or -1 with err.
+int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err);
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
@@ -43,16 +42,8 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
              std::string& err);
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
                            const uint8_t* pos, const uint8_t* J, int L, int nv, std::string& err);
-int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma,
-                            uint32_t pair_xor, int elem,
+int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
                             std::string& err);
-// Linear-traversal variant (complex64, qsim_plan.lin): one pass of walk,
-// gather and (optionally) map store, writes through per-warp transposes.
-int jit_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin, uint32_t chunk_log2,
-                 const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
-                 cudaStream_t st, std::string& err);
-int jit_check_compile_fused_lt(const uint32_t* words, int n, int M, const uint32_t* lin,
-                               std::string& err);
 // Planned apply from a materialised map (NVRTC; sigma order, the fused
 // kernel's batching).  Returns 0 or -1 with err.
 int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(q):
     lib = ctypes.CDLL(q.LIB_PATH)
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.qsim_abi_version() == 6
+    assert lib.qsim_abi_version() == 7
 
 
 def test_strerror_covers_every_status(q):

@@ -12,8 +12,9 @@ CPU oracle (perm as uint32, k2 as raw entry bytes; readings R14/R15):
   default plan (qsim_plan_create) AND with the plan qsim_plan_tune keeps (the
   kernel instance bench.py times), and the end-to-end host-buffer call
   (qsim_run_host);
-* each output is copied back in 512 MiB chunks and compared byte for byte;
-  a failure names the mode and the first mismatching output index.
+* the oracle's perm and k2 are copied to the device once and each mode's
+  output is compared with them byte for byte (torch.equal on 512 MiB
+  chunks); a failure names the mode and the first mismatching output index.
 """
 import numpy as np
 import pytest
@@ -39,24 +40,27 @@ def q():
     return q
 
 
-def _first_mismatch(got: np.ndarray, want: np.ndarray, unit: int) -> int:
-    g = got.view(np.uint8).reshape(-1, unit)
-    w = want.view(np.uint8).reshape(-1, unit)
-    return int(np.flatnonzero((g != w).any(axis=1))[0])
-
-
-def _compare(dev_u8, ref: np.ndarray, unit: int, label: str) -> None:
-    """dev_u8: device uint8 tensor holding ref.nbytes bytes; unit: bytes per entry."""
-    ref_u8 = ref.view(np.uint8).reshape(-1)
-    assert dev_u8.numel() >= ref_u8.size, label
-    for s in range(0, ref_u8.size, CHUNK_BYTES):
-        e = min(ref_u8.size, s + CHUNK_BYTES)
-        got = dev_u8[s:e].cpu().numpy()
-        if not np.array_equal(got, ref_u8[s:e]):
-            i = s // unit + _first_mismatch(got, ref_u8[s:e], unit)
+def _compare(dev_u8, ref_u8, unit: int, label: str) -> None:
+    """dev_u8 (the CUDA path's output) and ref_u8 (the oracle's, copied to the
+    device once) are uint8 tensors; unit: bytes per entry."""
+    assert dev_u8.numel() >= ref_u8.numel(), label
+    for s in range(0, ref_u8.numel(), CHUNK_BYTES):
+        e = min(ref_u8.numel(), s + CHUNK_BYTES)
+        a, b = dev_u8[s:e], ref_u8[s:e]
+        if not torch.equal(a, b):
+            bad = (a.view(-1, unit) != b.view(-1, unit)).any(dim=1).nonzero()[0, 0].item()
+            i = s // unit + bad
             pytest.fail(f"{label}: first mismatch at output {i} "
-                        f"(got {got[(i * unit - s):(i * unit - s) + unit].tobytes().hex()}, "
-                        f"want {ref_u8[i * unit:(i + 1) * unit].tobytes().hex()})")
+                        f"(got {dev_u8[i * unit:(i + 1) * unit].cpu().numpy().tobytes().hex()}, "
+                        f"want {ref_u8[i * unit:(i + 1) * unit].cpu().numpy().tobytes().hex()})")
+
+
+def _to_device(a: np.ndarray):
+    out = torch.empty(a.nbytes, dtype=torch.uint8, device=DEV)
+    flat = a.view(np.uint8).reshape(-1)
+    for s in range(0, flat.size, 1 << 30):
+        out[s:s + (1 << 30)].copy_(torch.from_numpy(flat[s:s + (1 << 30)]))
+    return out
 
 
 def _host_compare(got: np.ndarray, ref: np.ndarray, unit: int, label: str) -> None:
@@ -64,8 +68,8 @@ def _host_compare(got: np.ndarray, ref: np.ndarray, unit: int, label: str) -> No
     for s in range(0, b.size, CHUNK_BYTES):
         e = min(b.size, s + CHUNK_BYTES)
         if not np.array_equal(a[s:e], b[s:e]):
-            i = s // unit + _first_mismatch(a[s:e], b[s:e], unit)
-            pytest.fail(f"{label}: first mismatch at output {i}")
+            bad = np.flatnonzero((a[s:e].reshape(-1, unit) != b[s:e].reshape(-1, unit)).any(axis=1))
+            pytest.fail(f"{label}: first mismatch at output {s // unit + int(bad[0])}")
 
 
 def _run_config(q, name):
@@ -81,11 +85,11 @@ def _run_config(q, name):
     idx = np.array([0, 1, N // 2, N - 1], dtype=np.uint64)
     assert np.array_equal(oracle.walk_many(gates, idx), perm_ref[idx.astype(np.int64)])
 
-    # ---- device buffers
-    k1 = torch.empty(N * e, dtype=torch.uint8, device=DEV)
-    step = 1 << 28
-    for s in range(0, N, step):
-        k1[s * e:(s + step) * e].copy_(torch.from_numpy(k1_host[s:s + step].view(np.uint8)))
+    # ---- device buffers (the oracle's perm and k2 are copied to the device
+    # once, so each mode is compared there, byte for byte)
+    k1 = _to_device(k1_host)
+    perm_ref_d = _to_device(perm_ref)
+    k2_ref_d = _to_device(k2_ref)
     k2 = torch.empty(N * e, dtype=torch.uint8, device=DEV)
     perm = torch.empty(N, dtype=torch.int32, device=DEV)
     ws = q.workspace()
@@ -93,11 +97,11 @@ def _run_config(q, name):
 
     def check_perm(label):
         torch.cuda.synchronize()
-        _compare(perm_u8, perm_ref, 4, f"{name} {label} perm")
+        _compare(perm_u8, perm_ref_d, 4, f"{name} {label} perm")
 
     def check_k2(label):
         torch.cuda.synchronize()
-        _compare(k2, k2_ref, e, f"{name} {label} k2")
+        _compare(k2, k2_ref_d, e, f"{name} {label} k2")
         k2.fill_(0xA5)                                  # stale bytes cannot pass the next mode
 
     # the north star's plain calls
@@ -137,7 +141,7 @@ def _run_config(q, name):
         k2_host.view(np.uint8)[:] = 0xA5
         q.run_host(gates, M, mode, k1_host, k2_host, k1, k2, perm, ws, dtype=cfg.dtype)
         _host_compare(k2_host, k2_ref, e, f"{name} qsim_run_host mode {mode} k2 (host)")
-    del k2_host
+    del k2_host, perm_ref_d, k2_ref_d
     return cfg, perm, k1, k2
 
 

@@ -188,7 +188,8 @@ def test_planned_orders_moving_lane_bits(q, M, dtype):
     """Traversal orders whose lane bits are not output bits 3..4 (the sector
     cover puts other bits there; only 0..2 / 0..1 are kept): the plan's own
     sigma and a sigma reversing every non-kept bit, through the NVRTC kernels
-    (workspace) and the ahead-of-time ones (no workspace) -- same bytes."""
+    with the chunk ticket (workspace) and with round-robin chunks (no
+    workspace) -- same bytes."""
     gates = wl.random_gates(80, M, 300 + M)
     k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 11 + M))
     perm_ref = oracle.build_map(gates, M)
@@ -213,6 +214,29 @@ def test_planned_orders_moving_lane_bits(q, M, dtype):
             for o in (out, outf, outm):
                 assert o.cpu().numpy().tobytes() == ref.tobytes(), (sig, w is None)
             assert np.array_equal(_perm_np(pm), perm_ref)
+
+
+@pytest.mark.parametrize("dtype,M,ext", [("c64", 13, False), ("c64", 18, False), ("c128", 16, False),
+                                         ("c64", 17, True)])
+def test_plain_run_fused_is_planned(q, M, dtype, ext):
+    """qsim_run_fused over the whole output plans internally (plan cached per
+    circuit) and runs the NVRTC kernel in the plan's order: same bytes as
+    the oracle, also for phase / SWAP circuits (R17) and on repeated calls."""
+    gates = (wl.random_gates_ext(70, M, 40 + M) if ext else wl.random_gates(70, M, 40 + M))
+    k1 = wl.make_state(wl.StateSpec(M, dtype, wl.GAUSS, 5 + M))
+    if ext:
+        perm, signs = oracle.build_map_signed(gates, M)
+        ref = oracle.apply_map_signed(perm, signs, k1)
+    else:
+        ref = oracle.apply_map(oracle.build_map(gates, M), k1)
+    k1_d = _to_dev(k1)
+    for _ in range(2):
+        out = torch.empty_like(k1_d)
+        q.run_fused(gates, M, k1_d, out, dtype=dtype)
+        torch.cuda.synchronize()
+        if q.jit_status().startswith("ready"):
+            assert q.last_kernel() in ("qsim_jit_fused", "qsim_jit_local"), q.last_kernel()
+        assert out.cpu().numpy().tobytes() == ref.tobytes()
 
 
 def test_planned_small_M_falls_back_to_natural(q):
@@ -388,82 +412,6 @@ def test_tagged_gather_m32(q):
     assert np.array_equal(words[:, 0].index_select(0, it).cpu().numpy().view(np.uint32)
                           .astype(np.uint64), src)
     torch.cuda.empty_cache()
-
-
-@pytest.mark.parametrize("M", [14, 17, 20])
-def test_linear_traversal(q, M):
-    """Plans with a linear (GF(2)) traversal, complex64: lanes of a warp differ
-    by sector-mate differences, stores go through per-warp shared-memory
-    transposes -- the map, the fused result and the one-pass map + gather
-    equal the oracle byte for byte (the plan's own basis when it takes one,
-    and a hand-made basis with mixed lane vectors)."""
-    gates = wl.random_gates_ext(80, M, 1200 + M, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP))
-    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 3 + M))
-    perm_ref = oracle.build_map(gates, M)
-    ref = oracle.apply_map(perm_ref, k1)
-    k1_d = _to_dev(k1)
-    plan = q.plan_create(gates, M, "c64")
-    plan.flags = 0
-    bases = []
-    if plan.lin_flags & 1:
-        bases.append(list(plan.lin))
-    cols = [1 | 1 << 5, 2 | 1 << 7, 1 << 6, 1 << 8 | 1 << 9, 1 << 10, 1, 2, 4, 8, 1 << 4, 1 << 9]
-    cols += [1 << b for b in range(11, M)] + [0] * (32 - M)
-    bases.append(cols)
-    for basis in bases:
-        for k, v in enumerate(basis):
-            plan.lin[k] = v
-        plan.lin_flags = 1
-        for cl in (12, min(M, 15)):
-            plan.chunk_log2 = plan.fused_chunk_log2 = cl
-            pm = _new_perm(1 << M)
-            out, outf = torch.empty_like(k1_d), torch.empty_like(k1_d)
-            q.map_gather_planned(plan, gates, pm, k1_d, out, q.workspace())
-            assert q.last_kernel() == "qsim_jit_fused_lt"
-            q.run_fused_planned(plan, gates, k1_d, outf, q.workspace())
-            assert q.last_kernel() == "qsim_jit_fused_lt"
-            torch.cuda.synchronize()
-            assert np.array_equal(_perm_np(pm), perm_ref), (basis[:5], cl)
-            assert out.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)
-            assert outf.cpu().numpy().tobytes() == ref.tobytes(), (basis[:5], cl)
-
-
-@pytest.mark.parametrize("M", [12, 15, 18])
-def test_lane_pairs(q, M):
-    """Plans with lane pairs (pair_xor): lane L word l and lane L^1 word l^1
-    read the two entries of one 16-byte pair with one load and a shuffle when
-    the circuit puts them there -- same map and k2 bytes as the oracle, for
-    the plan's own pair difference and for forced ones (pairs rarely
-    matching: every load still correct)."""
-    gates = wl.random_gates_ext(70, M, 1500 + M, kinds=(wl.NOT, wl.CNOT, wl.CCNOT, wl.SWAP, wl.Z))
-    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 9 + M))
-    perm_ref, signs_ref = oracle.build_map_signed(gates, M)
-    ref = oracle.apply_map_signed(perm_ref, signs_ref, k1)
-    plain = np.ascontiguousarray(gates[gates[:, 0] != wl.Z])
-    perm_plain = oracle.build_map(plain, M)
-    ref_plain = oracle.apply_map(perm_plain, k1)
-    k1_d = _to_dev(k1)
-    base = q.plan_create(plain, M, "c64")
-    base.flags = 0
-    cases = []
-    if base.pair_xor:
-        cases.append((list(base.sigma), base.pair_xor))
-    sig = list(range(M))
-    cases.append((sig, (1 << 7) | (1 << (M - 1))))          # counter bit 5 -> bit 5 ^ {7, M-1}
-    cases.append((sig, 1 << 6))
-    for sg, px in cases:
-        plan = q.Plan.from_buffer_copy(base)
-        for k, b in enumerate(sg):
-            plan.sigma[k] = b
-        plan.pair_xor = px
-        out, outf, pm = torch.empty_like(k1_d), torch.empty_like(k1_d), _new_perm(1 << M)
-        q.map_gather_planned(plan, plain, pm, k1_d, out, q.workspace())
-        assert q.last_kernel() == "qsim_jit_fused"
-        q.run_fused_planned(plan, gates, k1_d, outf, q.workspace())    # with a phase step
-        torch.cuda.synchronize()
-        assert np.array_equal(_perm_np(pm), perm_plain), px
-        assert out.cpu().numpy().tobytes() == ref_plain.tobytes(), px
-        assert outf.cpu().numpy().tobytes() == ref.tobytes(), px
 
 
 @pytest.mark.parametrize("M", [16, 21])

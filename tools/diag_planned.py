@@ -73,4 +73,4 @@ for i in range(4):
     print(f"{name} {mode} {' '.join(sys.argv[3:])} call {i}: {ms:.3f} ms  entries/s {N / ms * 1e3:.3e}"
           f"  launches {q.lib().qsim_last_launch_count()}  natural {plan.flags & 1}"
           f"  chunk {plan.chunk_log2}  contained {plan.tile_contained:.3f}"
-          f"  lin {plan.lin_flags} lane_sectors {plan.lanes_sectors:.1f}  [{q.last_kernel()}]", flush=True)
+          f"  [{q.last_kernel()}]", flush=True)

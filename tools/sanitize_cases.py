@@ -35,17 +35,10 @@ def main():
             ok &= out.cpu().numpy().tobytes() == ref[3:-2].tobytes()
         plan = q.plan_create(gates, M, "c64")
         plan.flags = 0
-        for lin in (0, 1):
-            if lin:
-                cols = [1 | 1 << 5, 2 | 1 << 7, 1 << 6, 1 << 8 | 1 << 9, 1 << 10, 1, 2, 4, 8, 1 << 4, 1 << 9]
-                cols += [1 << b for b in range(11, M)] + [0] * (32 - M)
-                for k, v in enumerate(cols):
-                    plan.lin[k] = v
-            plan.lin_flags = lin
-            out = torch.empty_like(k1_d)
-            q.run_fused_planned(plan, gates, k1_d, out, q.workspace())
-            torch.cuda.synchronize()
-            ok &= out.cpu().numpy().tobytes() == ref.tobytes()
+        out = torch.empty_like(k1_d)
+        q.run_fused_planned(plan, gates, k1_d, out, q.workspace())
+        torch.cuda.synchronize()
+        ok &= out.cpu().numpy().tobytes() == ref.tobytes()
         perm = torch.empty(1 << M, dtype=torch.int32, device=dev)
         signs = torch.empty((1 << M) // 32, dtype=torch.int32, device=dev)
         q.build_map_signed(gates, M, 0, 1 << M, perm, signs)
