@@ -248,8 +248,8 @@ def cpu_accumulate(gates, k1_np: np.ndarray, n_gates: int):
                               k1_np.ctypes.data)
     finally:
         os.sched_setaffinity(0, old)
-    restored = bool(np.array_equal(probe.view(np.uint8),
-                                   k1_np[:: max(1, k1_np.shape[0] // 4096)].view(np.uint8)))
+    after = np.array(k1_np[:: max(1, k1_np.shape[0] // 4096)], copy=True)
+    restored = bool(np.array_equal(probe.view(np.uint8), after.view(np.uint8)))
     return k1_np.shape[0] * n_gates / dt, dt, restored
 
 
