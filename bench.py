@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     ap.add_argument("--cpu-sample-log2", type=int, default=29,
                     help="outputs in the oracle's bounded sample (log2)")
     return ap.parse_args()
@@ -251,6 +252,72 @@ def cpu_accumulate(gates, k1_np: np.ndarray, n_gates: int):
     after = np.array(k1_np[:: max(1, k1_np.shape[0] // 4096)], copy=True)
     restored = bool(np.array_equal(probe.view(np.uint8), after.view(np.uint8)))
     return k1_np.shape[0] * n_gates / dt, dt, restored
+
+
+def other_configs(q, wl, dev, stream, names=("cfg3", "cfg4")):
+    """The other large BASELINE configs on the same GPU (parity cases, not the
+    headline): per call, the median of 5 CUDA-event timings after 2 warm-ups,
+    algorithmic GB/s and the fraction of the measured copy bandwidth."""
+    import torch
+    hbm, _ = peaks()
+    out = {}
+    for name in names:
+        cfg = wl.CONFIGS[name]
+        g, M, N = cfg.gates(), cfg.M, cfg.N
+        e = 8 if cfg.dtype == "c64" else 16
+        k1 = torch.empty(N * e, dtype=torch.uint8, device=dev)
+        scale = cfg.state.scale() if M <= 30 else None
+        stage = torch.empty(min(N, 1 << 26) * e, dtype=torch.uint8, pin_memory=True)
+        for s0 in range(0, N, 1 << 26):
+            c = min(N - s0, 1 << 26)
+            wl.fill_state(cfg.state, stage.data_ptr(), s0, c, scale=scale)
+            k1[s0 * e:(s0 + c) * e].copy_(stage[:c * e])
+        del stage
+        k2 = torch.empty_like(k1)
+        perm = torch.empty(N, dtype=torch.int32, device=dev)
+        ws = q.workspace(dev)
+        plan = q.plan_create(g, M, cfg.dtype)
+        torch.cuda.synchronize()
+        if not (plan.flags & 1):
+            q.plan_tune(plan, g, perm, k1, k2, ws, stream=stream)
+        q.build_map(g, M, perm, stream=stream)
+        calls = {
+            "map_gather_planned": (lambda: q.map_gather_planned(plan, g, perm, k1, k2, ws, stream=stream),
+                                   4 + 2 * e),
+            "run_fused_planned": (lambda: q.run_fused_planned(plan, g, k1, k2, ws, stream=stream), 2 * e),
+            "apply_map_planned": (lambda: q.apply_map_planned(plan, perm, k1, k2, ws, stream=stream),
+                                  4 + 2 * e),
+        }
+        scratches = []
+        for wp in (False, True):
+            nb = q.bucket_scratch_bytes(M, cfg.dtype, wp)
+            if nb:
+                sc = torch.empty(nb, dtype=torch.uint8, device=dev)
+                scratches.append(sc)
+                calls["bucketed" + ("_map_gather" if wp else "_fused")] = (
+                    (lambda sc=sc, wp=wp: q.run_bucketed(g, M, k1, k2, sc, perm_out=perm if wp else None,
+                                                         stream=stream, dtype=cfg.dtype)),
+                    2 * e + (4 if wp else 0))
+        res = {"M": M, "dtype": cfg.dtype, "natural_order_plan": bool(plan.flags & 1)}
+        for call, (f, bpe) in calls.items():
+            ts = []
+            for i in range(7):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    a.record(stream)
+                    f()
+                    b.record(stream)
+                torch.cuda.synchronize()
+                if i >= 2:
+                    ts.append(a.elapsed_time(b))
+            ms = statistics.median(ts)
+            gbps = N * bpe / (ms * 1e-3) / 1e9
+            res[call] = {"ms": ms, "entries_per_s": N / (ms * 1e-3), "GBps": gbps,
+                         "bytes_per_entry": bpe, "frac_of_peak": gbps / hbm, "kernel": q.last_kernel()}
+        out[name] = res
+        del k1, k2, perm, scratches, calls
+        torch.cuda.empty_cache()
+    return out
 
 
 # ----------------------------------------------------------------- main arm
@@ -562,6 +629,11 @@ def run_qsim(args):
         del k2_host, k1b, k2b
         torch.cuda.empty_cache()
 
+    # ---- the other large configs (rank 0): cfg3 (well-mixed, bucketed) and cfg4
+    others = None
+    if rank == 0 and args.config == "cfg5" and not args.no_other_configs:
+        others = other_configs(q, wl, dev, stream)
+
     # ---- cpu baseline: the oracle on a bounded sample (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and k1_host is not None:
@@ -689,6 +761,7 @@ def run_qsim(args):
                                                  "best of 3 (write-only roofline of fused_kron)"},
         "launch_bound": launch_bound,
         "verified": verified,
+        "other_configs": others,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches_mg,

@@ -28,8 +28,11 @@
  *     except qsim_run_host (see there).  Faults inside kernels surface at
  *     the caller's next synchronisation.
  *   - Ownership: all buffers are caller-owned.  The library allocates no
- *     device memory.  `gates` is a host array read during the call (copied
- *     into the launch's kernel-parameter bank); it may be freed on return.
+ *     device memory for data; the one exception is qsim_run_fused's 256-byte
+ *     chunk ticket per (device, stream), allocated on first use and kept for
+ *     the life of the process.  `gates` is a host array read during the call
+ *     (copied into the launch's kernel-parameter bank); it may be freed on
+ *     return.
  *   - Device pointers (perm, k1, k2) must be 16-byte aligned
  *     (QSIM_EINVAL otherwise) and must not overlap each other
  *     (QSIM_EALIAS); all calls are out-of-place.
@@ -144,7 +147,10 @@ int qsim_apply_map_range(const uint32_t *perm_in, uint64_t count, int32_t M,
 
 /* qsim_run_fused -- k2[i] = k1[f_1(...f_n(i))] without storing the map:
  * the memory-for-processing trade-off.  Same arguments as
- * build + apply; no perm buffer.                                           */
+ * build + apply; no perm buffer.  For M >= 13 with NVRTC the call plans the
+ * traversal itself (qsim_plan_create, cached per circuit) and runs the
+ * planned kernel with a per-stream chunk ticket -- the same k2 bytes as
+ * every other path, at the planned call's speed.                          */
 int qsim_run_fused(const qsim_gate *gates, int32_t n_gates, int32_t M,
                    int32_t dtype, const void *k1, void *k2, void *stream);
 

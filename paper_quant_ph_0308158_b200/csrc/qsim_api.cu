@@ -1005,6 +1005,34 @@ int plan_fill(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, qsim_
   return QSIM_OK;
 }
 
+// The chunk ticket of the planned kernels when the caller passes no
+// workspace (qsim_run_fused): 256 bytes per (device, stream), allocated on
+// first use and kept for the process -- calls on one stream are ordered by
+// the stream, so they can share it.  During stream capture nothing is
+// allocated (nullptr: round-robin chunks).
+std::mutex g_ticket_mu;
+std::vector<std::pair<std::pair<int, cudaStream_t>, void*>> g_tickets;
+
+void* stream_ticket(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_ticket_mu);
+  for (const auto& t : g_tickets)
+    if (t.first.first == dev && t.first.second == st) return t.second;
+  void* p = nullptr;
+  if (cudaMalloc(&p, 256) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  g_tickets.push_back({{dev, st}, p});
+  return p;
+}
+
 // Plans of recent circuits (qsim_run_fused, qsim_run_host*): the host
 // sampling runs once per (circuit, M, dtype); a few entries, most recent first.
 struct PlanCacheEntry {
@@ -1397,8 +1425,8 @@ int qsim_run_fused(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t d
   if (rc == QSIM_OK && M >= 13 && elem_bytes(dtype) != 0 && qsim::jit_available()) {
     qsim_plan plan;
     if ((rc = cached_plan(gates, n_gates, M, dtype, &plan))) return rc;
-    return fused_planned_impl(&plan, gates, n_gates, k1, k2, nullptr,
-                              static_cast<cudaStream_t>(stream));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return fused_planned_impl(&plan, gates, n_gates, k1, k2, stream_ticket(st), st);
   }
   g_last_kernel = "k_fused_bitsliced";
   return fused_impl(gates, n_gates, M, dtype, 0, 1ull << M, k1, k2, QSIM_WALK_AUTO,
