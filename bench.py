@@ -577,6 +577,9 @@ def run_qsim(args):
                 with torch.cuda.stream(stream):
                     if flush:
                         scrub.fill_(1)
+                    # keep the GPU busy while the call is enqueued, so the events
+                    # bracket the kernel and not the host's launch latency
+                    torch.cuda._sleep(100000)
                     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     t0.record(stream)
                     q.map_gather_planned(plan2, g2, p2, a2, b2, ws, stream=stream)
@@ -592,7 +595,8 @@ def run_qsim(args):
                         "kernel": q.last_kernel(),
                         "note": "CUDA graph of 100 recorded steps (qsim_graph_*) vs 100 calls; "
                                 "warm = back to back (L2-resident), flushed = 256 MiB written "
-                                "between steps (one call, CUDA events around the kernel)"}
+                                "between steps; one call each, CUDA events around the kernel "
+                                "(a GPU sleep before the start event hides the launch latency)"}
         del a2, b2, p2
 
     # ---- end to end through the C ABI from pinned host buffers: every step

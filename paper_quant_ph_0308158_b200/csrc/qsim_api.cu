@@ -1316,8 +1316,10 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
 // so pass 2's scattered writes land in L2 (qsim_jit.cu bucket_source).
 int bucket_bits(int32_t M, int32_t dtype, bool with_perm) {
   const int per = elem_bytes(dtype) + (with_perm ? 4 : 0);
+  int mb = 32;
+  if (const char* e = std::getenv("QSIM_BUCKET_MB")) mb = std::max(1, std::atoi(e));  // experiment
   int rb = 0;
-  while ((per << (rb + 1)) <= (32 << 20)) ++rb;
+  while (((uint64_t)per << (rb + 1)) <= ((uint64_t)mb << 20)) ++rb;
   return std::min(rb, (int)M);
 }
 
@@ -1808,6 +1810,16 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
         }
       }
       if (!moved) break;
+    }
+    // then swaps of neighbouring counter bits above the cover (one sweep)
+    for (int k = from; k + 1 < std::min(cur.M, from + 12) && rc == QSIM_OK; ++k) {
+      qsim_plan p = cur;
+      std::swap(p.sigma[k], p.sigma[k + 1]);
+      const float t = time_plan(p, false, 2);
+      if (rc == QSIM_OK && t < best * 0.99f) {
+        best = t;
+        cur = p;
+      }
     }
     if (rc == QSIM_OK) cands[best_i] = cur;
   }

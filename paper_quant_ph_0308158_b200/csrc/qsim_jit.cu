@@ -528,6 +528,27 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   return s;
 }
 
+// CTA staging of the on-the-fly input's stores (kron_stage_runs): the 8
+// warps of a CTA hold 8192 outputs -- lanes on output bits 0..4, the
+// in-thread bits J, and as warp bits the 3 lowest remaining bits W.  When
+// those 13 bits include 0..r-1 with r >= 7, the CTA's outputs are 2^(13-r)
+// runs of 2^r consecutive entries: the values go to shared memory first and
+// each warp then writes whole runs front to back (1 KB .. 64 KB), instead
+// of 32 separate 256-byte pieces per thread -- sequential DRAM writes.
+// Returns r (0: no staging) and fills W.
+int kron_stage_runs(const uint8_t* J, int L, int M, uint8_t* W) {
+  uint64_t set = 31ull;
+  for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
+  int k = 0;
+  for (int b = 5; b < M && k < 3; ++b)
+    if (!((set >> b) & 1ull)) W[k++] = (uint8_t)b;
+  if (k < 3 || L < 13) return 0;
+  for (int i = 0; i < 3; ++i) set |= 1ull << W[i];
+  int r = 0;
+  while (r < 13 && ((set >> r) & 1ull)) ++r;
+  return r >= 7 ? r : 0;
+}
+
 // Fused walk with the input generated on the fly (Appendix 1):
 // k2_out[out - start] = k1(perm(out)) from tables of qubit products, ng
 // groups of gb table positions (same arithmetic and order as
@@ -539,7 +560,8 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
 // Traversal (the layout, chosen on the host by kron_layout): a warp tile is
 // 1024 outputs = lanes on output bits 0..4 x the 32 bit positions of each
 // plane on output bits J[0..4]; tiles enumerate the other bits, 2^(L-10)
-// tiles per aligned block of 2^L outputs.  Stores stay 256-byte warp runs.
+// tiles per aligned block of 2^L outputs; the 8 warps of a CTA take 8
+// consecutive tiles (stores staged per CTA, kron_stage_runs).
 // Fast path (nv > 0): when every source bit at table positions >= nv is
 // constant across a thread's 32 entries (checked per warp tile; the host
 // picked J so that it nearly always is), the product of groups ng-1..1 is
@@ -551,11 +573,44 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   std::string s = kPrelude;
   char buf[640];
   const bool f32 = elem == 8, wide = M > 32;
+  uint8_t W[3] = {0, 0, 0};
+  const int runb = kron_stage_runs(J, L, M, W);
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M, gb,
-                ng);
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n"
+                "#define QSIM_STAGE %d\n#define QSIM_RUNB %d\n", M, gb, ng, runb ? 1 : 0, runb);
   s += buf;
   s += thread_defs(J, L);
+  if (runb) {
+    // rank of each staged bit among the CTA's 13 bits (ascending): smem index
+    uint64_t set = 31ull;
+    for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
+    for (int k = 0; k < 3; ++k) set |= 1ull << W[k];
+    auto rank = [&](int b) { return __builtin_popcountll(set & ((1ull << b) - 1)); };
+    std::snprintf(buf, sizeof buf,
+                  "#define QSIM_CIDX(l) (((l) & 1 ? %du : 0u) | ((l) & 2 ? %du : 0u) | ((l) & 4 ? %du : 0u) | "
+                  "((l) & 8 ? %du : 0u) | ((l) & 16 ? %du : 0u))\n",
+                  1 << rank(J[0]), 1 << rank(J[1]), 1 << rank(J[2]), 1 << rank(J[3]), 1 << rank(J[4]));
+    s += buf;
+    std::snprintf(buf, sizeof buf,
+                  "#define QSIM_WIDX(w) (((w) & 1 ? %du : 0u) | ((w) & 2 ? %du : 0u) | ((w) & 4 ? %du : 0u))\n"
+                  "#define QSIM_WMASK %lluull\n",
+                  1 << rank(W[0]), 1 << rank(W[1]), 1 << rank(W[2]),
+                  (unsigned long long)((1ull << W[0]) | (1ull << W[1]) | (1ull << W[2])));
+    s += buf;
+    // output offset of each run (bits ranked >= r deposited into the set)
+    std::vector<int> hi;
+    for (int b = 0; b < 64; ++b)
+      if (((set >> b) & 1ull) && rank(b) >= runb) hi.push_back(b);
+    const int nruns = 1 << (13 - runb);
+    s += "__constant__ u64 kRunOff[" + std::to_string(nruns) + "] = {";
+    for (int r = 0; r < nruns; ++r) {
+      uint64_t off = 0;
+      for (size_t i = 0; i < hi.size(); ++i)
+        if ((r >> i) & 1) off |= 1ull << hi[i];
+      std::snprintf(buf, sizeof buf, "%lluull%s", (unsigned long long)off, r < nruns - 1 ? ", " : "};\n");
+      s += buf;
+    }
+  }
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
   return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
@@ -587,14 +642,42 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   }
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#if QSIM_STAGE
+  C* const stg = T + (QSIM_NG << QSIM_GB);   // [8192] the CTA's outputs in address order
+  const u32 widx = QSIM_WIDX(warp);
+  for (u64 r0 = blockIdx.x; tb + r0 * 8u < te; r0 += gridDim.x) {
+    const u64 tile = tb + r0 * 8u + warp;
+#else
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
+#endif
 )";
   const int np = wide ? 64 : 32;
   s += thread_planes(M, J, np);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
-
+  // the 32 values of a thread: staged (whole blocks) or stored directly
+  auto stores = [&](const std::string& value, const char* ind) {
+    const std::string i(ind);
+    std::string e;
+    e += i + "auto* const kq = k2 + (base + lane - start);\n";
+    e += i + "if (full) {\n";
+    e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+    e += i + "    " + value + "\n";
+    e += runb ? i + "    stg[lane | QSIM_CIDX(l) | widx] = rv;\n" : i + "    __stcs(kq + QSIM_OFF(l), rv);\n";
+    e += i + "  }\n";
+    e += i + "} else {\n";
+    e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
+    e += i + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
+    e += i + "    if (addr >= start && addr < end) {\n";
+    e += i + "      " + value + "\n";
+    e += i + "      __stcs(kq + QSIM_OFF(l), rv);\n";
+    e += i + "    }\n";
+    e += i + "  }\n";
+    e += i + "}\n";
+    return e;
+  };
+  bool fast_open = false;
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
@@ -625,8 +708,9 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     }
     s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
     s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
-    s += "      continue;\n    }\n";
+    s += stores("const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += "    } else {\n";
+    fast_open = true;
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
@@ -653,7 +737,21 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     gen += buf;
   }
   gen += " const C rv = negate_if(r, (sg >> l) & 1u);";
-  s += thread_stores("k2", gen.c_str(), "    ");
+  s += stores(gen, "    ");
+  if (fast_open) s += "    }\n";
+  if (runb)  // the CTA's 8192 staged outputs to k2 as whole runs (full blocks: CTA-uniform)
+    s += R"(
+    if (full) {
+      __syncthreads();
+      const u64 cbase = base & ~QSIM_WMASK;
+      for (u32 run = warp; run < (1u << (13 - QSIM_RUNB)); run += 8u) {
+        C* const dst = k2 + (cbase + kRunOff[run] - start);
+        const C* const src = stg + (run << QSIM_RUNB);
+        _Pragma("unroll 4") for (u32 x = lane; x < (1u << QSIM_RUNB); x += 32u) __stcs(dst + x, src[x]);
+      }
+      __syncthreads();
+    }
+)";
   s += "  }\n}\n";
   return s;
 }
@@ -1161,7 +1259,9 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
              int elem, int gbits, int ngroups, const uint8_t* pos, const uint8_t* J, int L, int nv,
              uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
              std::string& err) {
-  const int smem = (ngroups << gbits) * (elem == 8 ? 8 : 16);
+  uint8_t Wb[3];
+  const bool staged = kron_stage_runs(J, L, M, Wb) != 0;  // + the CTA's 8192 staged outputs
+  const int smem = ((ngroups << gbits) + (staged ? 8192 : 0)) * (elem == 8 ? 8 : 16);
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1188,7 +1288,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
       if (!fn) return -1;
       // write-only: shared memory for the tables of several resident CTAs
       // (the gather kernels' 3 % carveout would allow one)
-      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 50);
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, staged ? 100 : 50);
       if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
         err = "cuFuncSetAttribute(max dynamic smem) failed";
         return -1;
