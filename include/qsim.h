@@ -387,34 +387,6 @@ int qsim_jit_check_compile_kron(const qsim_gate *gates, int32_t n_gates, int32_t
                                 int32_t dtype);
 int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
                                    int32_t n_gates);
-int qsim_jit_check_compile_bucketed(const qsim_gate *gates, int32_t n_gates, int32_t M,
-                                    int32_t dtype, int32_t with_perm);
-/* qsim_run_bucketed -- k2 = U k1 (and, when perm_out != NULL, the map, as
- * qsim_map_gather_planned) in TWO passes through destination buckets, for
- * well-mixed circuits where no traversal order keeps a k1 sector's readers
- * together (the plan's natural-order flag, e.g. BASELINE cfg3: 256 random
- * gates on 26 bits) and a one-pass gather is bound by random 32-byte DRAM
- * accesses:
- *   pass 1 streams k1 in address order, walks each source s forward to its
- *     output d (perm(d) = s; Step 1 first), and appends (k1[s] with the row
- *     value applied, d[, s]) to the scratch region of bucket d >> RB, in
- *     runs per CTA (shared-memory counting sort of 8192 entries);
- *   pass 2 streams the scratch bucket by bucket and writes k2[d] (perm[d]);
- *     a bucket's output range (<= 32 MB) stays in L2 while it fills.
- * Same bytes as qsim_run_fused / qsim_map_gather_planned.
- *   M        13..32; at most 256 buckets (QSIM_ERANGE otherwise: 2^M entries
- *            with buckets of <= 32 MB of output, e.g. complex128 M <= 29)
- *   k1, k2   device, 2^M entries; perm_out device, 2^M uint32, or NULL
- *   scratch  device, >= qsim_bucket_scratch_bytes(M, dtype, perm_out != NULL)
- *            bytes (2^M * (e + 4 [+ 4]) + cursors), 16-B aligned, caller-owned,
- *            contents undefined afterwards; must not overlap k1 / k2 / perm
- * Phase steps (R17) are allowed without perm_out (QSIM_EINVAL with it).
- * Without NVRTC the call runs the ahead-of-time kernels (same bytes).       */
-uint64_t qsim_bucket_scratch_bytes(int32_t M, int32_t dtype, int32_t with_perm);
-int qsim_run_bucketed(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
-                      const void *k1, void *k2, uint32_t *perm_out, void *scratch,
-                      uint64_t scratch_bytes, void *stream);
-
 /* ABI version of this header / library: 7 (plans with the sector cover,
  * phase / SWAP gates, M > 32 on-the-fly input, batch e2e, graphs, tuning;
  * 7: the measured-slower linear-traversal and lane-pair plan fields removed). */

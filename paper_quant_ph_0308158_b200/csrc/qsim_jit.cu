@@ -528,27 +528,6 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   return s;
 }
 
-// CTA staging of the on-the-fly input's stores (kron_stage_runs): the 8
-// warps of a CTA hold 8192 outputs -- lanes on output bits 0..4, the
-// in-thread bits J, and as warp bits the 3 lowest remaining bits W.  When
-// those 13 bits include 0..r-1 with r >= 7, the CTA's outputs are 2^(13-r)
-// runs of 2^r consecutive entries: the values go to shared memory first and
-// each warp then writes whole runs front to back (1 KB .. 64 KB), instead
-// of 32 separate 256-byte pieces per thread -- sequential DRAM writes.
-// Returns r (0: no staging) and fills W.
-int kron_stage_runs(const uint8_t* J, int L, int M, uint8_t* W) {
-  uint64_t set = 31ull;
-  for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
-  int k = 0;
-  for (int b = 5; b < M && k < 3; ++b)
-    if (!((set >> b) & 1ull)) W[k++] = (uint8_t)b;
-  if (k < 3 || L < 13) return 0;
-  for (int i = 0; i < 3; ++i) set |= 1ull << W[i];
-  int r = 0;
-  while (r < 13 && ((set >> r) & 1ull)) ++r;
-  return r >= 7 ? r : 0;
-}
-
 // Fused walk with the input generated on the fly (Appendix 1):
 // k2_out[out - start] = k1(perm(out)) from tables of qubit products, ng
 // groups of gb table positions (same arithmetic and order as
@@ -560,8 +539,7 @@ int kron_stage_runs(const uint8_t* J, int L, int M, uint8_t* W) {
 // Traversal (the layout, chosen on the host by kron_layout): a warp tile is
 // 1024 outputs = lanes on output bits 0..4 x the 32 bit positions of each
 // plane on output bits J[0..4]; tiles enumerate the other bits, 2^(L-10)
-// tiles per aligned block of 2^L outputs; the 8 warps of a CTA take 8
-// consecutive tiles (stores staged per CTA, kron_stage_runs).
+// tiles per aligned block of 2^L outputs.  Stores stay 256-byte warp runs.
 // Fast path (nv > 0): when every source bit at table positions >= nv is
 // constant across a thread's 32 entries (checked per warp tile; the host
 // picked J so that it nearly always is), the product of groups ng-1..1 is
@@ -573,44 +551,11 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
   std::string s = kPrelude;
   char buf[640];
   const bool f32 = elem == 8, wide = M > 32;
-  uint8_t W[3] = {0, 0, 0};
-  const int runb = kron_stage_runs(J, L, M, W);
   s += f32 ? "typedef float2 C; typedef float R;\n" : "typedef double2 C; typedef double R;\n";
-  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n"
-                "#define QSIM_STAGE %d\n#define QSIM_RUNB %d\n", M, gb, ng, runb ? 1 : 0, runb);
+  std::snprintf(buf, sizeof buf, "#define QSIM_M %d\n#define QSIM_GB %d\n#define QSIM_NG %d\n", M, gb,
+                ng);
   s += buf;
   s += thread_defs(J, L);
-  if (runb) {
-    // rank of each staged bit among the CTA's 13 bits (ascending): smem index
-    uint64_t set = 31ull;
-    for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
-    for (int k = 0; k < 3; ++k) set |= 1ull << W[k];
-    auto rank = [&](int b) { return __builtin_popcountll(set & ((1ull << b) - 1)); };
-    std::snprintf(buf, sizeof buf,
-                  "#define QSIM_CIDX(l) (((l) & 1 ? %du : 0u) | ((l) & 2 ? %du : 0u) | ((l) & 4 ? %du : 0u) | "
-                  "((l) & 8 ? %du : 0u) | ((l) & 16 ? %du : 0u))\n",
-                  1 << rank(J[0]), 1 << rank(J[1]), 1 << rank(J[2]), 1 << rank(J[3]), 1 << rank(J[4]));
-    s += buf;
-    std::snprintf(buf, sizeof buf,
-                  "#define QSIM_WIDX(w) (((w) & 1 ? %du : 0u) | ((w) & 2 ? %du : 0u) | ((w) & 4 ? %du : 0u))\n"
-                  "#define QSIM_WMASK %lluull\n",
-                  1 << rank(W[0]), 1 << rank(W[1]), 1 << rank(W[2]),
-                  (unsigned long long)((1ull << W[0]) | (1ull << W[1]) | (1ull << W[2])));
-    s += buf;
-    // output offset of each run (bits ranked >= r deposited into the set)
-    std::vector<int> hi;
-    for (int b = 0; b < 64; ++b)
-      if (((set >> b) & 1ull) && rank(b) >= runb) hi.push_back(b);
-    const int nruns = 1 << (13 - runb);
-    s += "__constant__ u64 kRunOff[" + std::to_string(nruns) + "] = {";
-    for (int r = 0; r < nruns; ++r) {
-      uint64_t off = 0;
-      for (size_t i = 0; i < hi.size(); ++i)
-        if ((r >> i) & 1) off |= 1ull << hi[i];
-      std::snprintf(buf, sizeof buf, "%lluull%s", (unsigned long long)off, r < nruns - 1 ? ", " : "};\n");
-      s += buf;
-    }
-  }
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
   return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
@@ -642,42 +587,14 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   }
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-#if QSIM_STAGE
-  C* const stg = T + (QSIM_NG << QSIM_GB);   // [8192] the CTA's outputs in address order
-  const u32 widx = QSIM_WIDX(warp);
-  for (u64 r0 = blockIdx.x; tb + r0 * 8u < te; r0 += gridDim.x) {
-    const u64 tile = tb + r0 * 8u + warp;
-#else
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
-#endif
 )";
   const int np = wide ? 64 : 32;
   s += thread_planes(M, J, np);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
-  // the 32 values of a thread: staged (whole blocks) or stored directly
-  auto stores = [&](const std::string& value, const char* ind) {
-    const std::string i(ind);
-    std::string e;
-    e += i + "auto* const kq = k2 + (base + lane - start);\n";
-    e += i + "if (full) {\n";
-    e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
-    e += i + "    " + value + "\n";
-    e += runb ? i + "    stg[lane | QSIM_CIDX(l) | widx] = rv;\n" : i + "    __stcs(kq + QSIM_OFF(l), rv);\n";
-    e += i + "  }\n";
-    e += i + "} else {\n";
-    e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
-    e += i + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
-    e += i + "    if (addr >= start && addr < end) {\n";
-    e += i + "      " + value + "\n";
-    e += i + "      __stcs(kq + QSIM_OFF(l), rv);\n";
-    e += i + "    }\n";
-    e += i + "  }\n";
-    e += i + "}\n";
-    return e;
-  };
-  bool fast_open = false;
+
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
     for (int k = nv; k < M; ++k) {
@@ -708,9 +625,8 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     }
     s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
     s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += stores("const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
-    s += "    } else {\n";
-    fast_open = true;
+    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += "      continue;\n    }\n";
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
@@ -737,21 +653,7 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     gen += buf;
   }
   gen += " const C rv = negate_if(r, (sg >> l) & 1u);";
-  s += stores(gen, "    ");
-  if (fast_open) s += "    }\n";
-  if (runb)  // the CTA's 8192 staged outputs to k2 as whole runs (full blocks: CTA-uniform)
-    s += R"(
-    if (full) {
-      __syncthreads();
-      const u64 cbase = base & ~QSIM_WMASK;
-      for (u32 run = warp; run < (1u << (13 - QSIM_RUNB)); run += 8u) {
-        C* const dst = k2 + (cbase + kRunOff[run] - start);
-        const C* const src = stg + (run << QSIM_RUNB);
-        _Pragma("unroll 4") for (u32 x = lane; x < (1u << QSIM_RUNB); x += 32u) __stcs(dst + x, src[x]);
-      }
-      __syncthreads();
-    }
-)";
+  s += thread_stores("k2", gen.c_str(), "    ");
   s += "  }\n}\n";
   return s;
 }
@@ -837,183 +739,6 @@ qsim_jit_local(u64 ntiles, const E* __restrict__ k1, E* __restrict__ k2, u32* __
         stcs(k2 + base + 32u * l + lane, negate_if(sv[a[l] & (TILE - 1u)], (sg >> l) & 1u));
     }
     __syncthreads();   // the stage is refilled two tiles later
-  }
-}
-)";
-  return s;
-}
-
-// Two passes through destination buckets, for well-mixed circuits (no
-// traversal order keeps a k1 sector's readers together, e.g. cfg3: 256
-// random gates on 26 bits): a single-pass gather there is bound by random
-// 32-byte DRAM accesses.  Instead
-//   pass 1 streams k1 in address order (coalesced), walks every source s
-//     FORWARD (g = perm^-1: Step 1 first, the gate list reversed into
-//     walk_code; each step is an involution) to its output d = g(s),
-//     sorts the CTA's 8192 entries by bucket d >> RB in shared memory, and
-//     appends each bucket's run (value, d mod 2^RB [, s]) to that bucket's
-//     region of the scratch (an atomic cursor per bucket) -- runs of
-//     ~8192 / NB entries, coalesced;
-//   pass 2 streams the scratch bucket by bucket and scatters
-//     k2[d] = value (and perm[d] = s): one bucket's output range (<= 32 MB)
-//     stays in L2 while its entries land, so the L2 merges the 16-/8-byte
-//     writes into whole lines before they go to DRAM.
-// A row value -1 (phase steps, R17) is applied in pass 1: the product of
-// the step values met along the forward walk equals the backward walk's
-// (phase steps do not move the address).  Every entry carries its own d,
-// so the result is the same bytes whatever order the atomics give.
-std::string bucket_source(const uint32_t* w, int n, int M, int elem, int RB, bool with_src) {
-  std::string s = kPrelude;
-  char buf[256];
-  std::snprintf(buf, sizeof buf,
-                "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_RB %d\n#define QSIM_NB %d\n"
-                "#define QSIM_SRC %d\n",
-                elem == 8 ? "uint2" : "uint4", M, RB, 1 << (M - RB), with_src ? 1 : 0);
-  s += buf;
-  s += R"(
-#define QSIM_TILE 8192u
-extern "C" __global__ void __launch_bounds__(256, 1)
-qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32* __restrict__ bidx,
-                  u32* __restrict__ bsrc, u32* __restrict__ cursor) {
-  extern __shared__ __align__(16) unsigned char bsm[];
-  QSIM_T* sval = reinterpret_cast<QSIM_T*>(bsm);                        // [TILE]
-  u32* sidx = reinterpret_cast<u32*>(sval + QSIM_TILE);                 // [TILE]
-  unsigned char* sbk = reinterpret_cast<unsigned char*>(sidx + QSIM_TILE);  // [TILE] bucket of a slot
-  __shared__ u32 cnt[QSIM_NB], start[QSIM_NB], gbase[QSIM_NB];
-  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const u64 ntiles = (1ull << QSIM_M) / QSIM_TILE;
-  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (u32 b = threadIdx.x; b < QSIM_NB; b += blockDim.x) cnt[b] = 0u;
-    __syncthreads();
-    const u64 base = tile * QSIM_TILE + (u64)warp * 1024u;   // this warp's 1024 sources
-)";
-  // planes of the sources base + 32 l + lane: lanes on bits 0..4, the
-  // thread's 32 entries on bits 5..9, the rest constant in the warp
-  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-  for (int b = 0; b < 32; ++b) {
-    if (b >= M)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
-    else if (b < 5)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (b < 10)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
-    else
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
-    s += buf;
-  }
-  s += "    u32 sg = 0u;\n";
-  {  // forward walk: Step 1 first (the list reversed into the last -> first emitter)
-    std::vector<uint32_t> rev(w, w + n);
-    std::reverse(rev.begin(), rev.end());
-    s += walk_code(rev.data(), n, M);
-  }
-  s += "    u32 a[32] = {";
-  for (int b = 0; b < 32; ++b) {
-    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += R"(
-    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
-    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
-    // a[l] = d = g(base + 32 l + lane); a slot in its bucket (warp-aggregated)
-    u32 slot[32];
-    const u32 ltm = (1u << lane) - 1u;
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u32 b = a[l] >> QSIM_RB;
-      const u32 m = __match_any_sync(0xffffffffu, b);
-      const u32 leader = __ffs(m) - 1u;
-      u32 first = 0u;
-      if (lane == leader) first = atomicAdd(&cnt[b], (u32)__popc(m));
-      slot[l] = __shfl_sync(m, first, leader) + __popc(m & ltm);
-    }
-    __syncthreads();
-    if (warp == 0) {  // exclusive scan of the bucket counts; reserve the runs in the scratch
-      u32 carry = 0u;
-      for (u32 b0 = 0; b0 < QSIM_NB; b0 += 32u) {
-        const u32 b = b0 + lane;
-        const u32 c = b < QSIM_NB ? cnt[b] : 0u;
-        u32 x = c;
-        _Pragma("unroll") for (int o = 1; o < 32; o <<= 1) {
-          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= (u32)o) x += y;
-        }
-        if (b < QSIM_NB) {
-          start[b] = carry + x - c;
-          gbase[b] = c ? atomicAdd(&cursor[b], c) : 0u;
-        }
-        carry += __shfl_sync(0xffffffffu, x, 31);
-      }
-    }
-    __syncthreads();
-    // values (coalesced loads in batches of 8) to their slots
-    _Pragma("unroll") for (int h = 0; h < 32; h += 8) {
-      QSIM_T v[8];
-      _Pragma("unroll") for (int l = 0; l < 8; ++l) v[l] = ldg(k1 + base + 32u * (h + l) + lane);
-      _Pragma("unroll") for (int l = 0; l < 8; ++l) {
-        const u32 d = a[h + l], b = d >> QSIM_RB, pos = start[b] + slot[h + l];
-        sval[pos] = negate_if(v[l], (sg >> (h + l)) & 1u);
-        sidx[pos] = d;
-        sbk[pos] = (unsigned char)b;
-      }
-    }
-    __syncthreads();
-    // runs out: slot pos of bucket b -> scratch b * 2^RB + gbase[b] + (pos - start[b])
-    for (u32 pos = threadIdx.x; pos < QSIM_TILE; pos += blockDim.x) {
-      const u32 b = sbk[pos], d = sidx[pos];
-      const u64 g = ((u64)b << QSIM_RB) + gbase[b] + (pos - start[b]);
-      stcs(bval + g, sval[pos]);
-      __stcs(bidx + g, d);
-    }
-#if QSIM_SRC
-    // the map as well: the sources of the slots, in a second sweep over
-    // the same shared-memory index array
-    __syncthreads();
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u32 d = a[l], b = d >> QSIM_RB, pos = start[b] + slot[l];
-      sidx[pos] = (u32)(base + 32u * l + lane);
-    }
-    __syncthreads();
-    for (u32 pos = threadIdx.x; pos < QSIM_TILE; pos += blockDim.x) {
-      const u32 b = sbk[pos];
-      const u64 g = ((u64)b << QSIM_RB) + gbase[b] + (pos - start[b]);
-      __stcs(bsrc + g, sidx[pos]);
-    }
-#endif
-    __syncthreads();
-  }
-}
-
-// pass 2: the scratch in order (bucket-major), k2[d] = value (perm[d] = s)
-extern "C" __global__ void __launch_bounds__(256)
-qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
-                  const u32* __restrict__ bsrc, QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
-  const u64 N = 1ull << QSIM_M;
-  const u64 stride = (u64)gridDim.x * blockDim.x * 4u;
-  for (u64 i0 = ((u64)blockIdx.x * blockDim.x + threadIdx.x); i0 < N; i0 += stride) {
-    QSIM_T v[4];
-    u32 d[4];
-#if QSIM_SRC
-    u32 sr[4];
-#endif
-    _Pragma("unroll") for (int j = 0; j < 4; ++j) {
-      const u64 i = i0 + (u64)j * gridDim.x * blockDim.x;
-      if (i < N) {
-        v[j] = __ldcs(bval + i);
-        d[j] = __ldcs(bidx + i);
-#if QSIM_SRC
-        sr[j] = __ldcs(bsrc + i);
-#endif
-      }
-    }
-    _Pragma("unroll") for (int j = 0; j < 4; ++j) {
-      const u64 i = i0 + (u64)j * gridDim.x * blockDim.x;
-      if (i < N) {
-        k2[d[j]] = v[j];
-#if QSIM_SRC
-        perm_out[d[j]] = sr[j];
-#endif
-      }
-    }
   }
 }
 )";
@@ -1259,9 +984,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
              int elem, int gbits, int ngroups, const uint8_t* pos, const uint8_t* J, int L, int nv,
              uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
              std::string& err) {
-  uint8_t Wb[3];
-  const bool staged = kron_stage_runs(J, L, M, Wb) != 0;  // + the CTA's 8192 staged outputs
-  const int smem = ((ngroups << gbits) + (staged ? 8192 : 0)) * (elem == 8 ? 8 : 16);
+  const int smem = (ngroups << gbits) * (elem == 8 ? 8 : 16);
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1288,7 +1011,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
       if (!fn) return -1;
       // write-only: shared memory for the tables of several resident CTAs
       // (the gather kernels' 3 % carveout would allow one)
-      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, staged ? 100 : 50);
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 50);
       if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
         err = "cuFuncSetAttribute(max dynamic smem) failed";
         return -1;
@@ -1390,80 +1113,6 @@ int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* 
     return -1;
   }
   return 0;
-}
-
-// Bucketed two-pass fused gather (bucket_source).  scratch: bval (2^M elem
-// bytes), bidx (2^M u32), bsrc (2^M u32, when perm_out), cursor (NB u32),
-// laid out by the caller (qsim_api.cu).
-int jit_bucketed(const uint32_t* words, int n, int M, int elem, int RB, const void* k1, void* k2,
-                 uint32_t* perm_out, void* bval, uint32_t* bidx, uint32_t* bsrc, uint32_t* cursor,
-                 int sms, cudaStream_t st, std::string& err) {
-  const bool with_src = perm_out != nullptr;
-  const int smem = 8192 * (elem + 4 + 1);
-  CUfunction f1 = nullptr, f2 = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    init_locked();
-    if (!(g_nvrtc.ok && g_drv.ok)) {
-      err = g_status;
-      return -1;
-    }
-    std::vector<uint32_t> keyw(words, words + n);
-    keyw.push_back((uint32_t)elem);
-    keyw.push_back((uint32_t)RB);
-    keyw.push_back(with_src ? 1u : 0u);
-    const uint64_t k1d = 0x62756b31ull, k2d = 0x62756b32ull;
-    const uint64_t h1 = fnv(keyw.data(), (int)keyw.size(), k1d), h2 = fnv(keyw.data(), (int)keyw.size(), k2d);
-    for (const Entry& e : g_cache[h1])
-      if (e.M == M && e.words == keyw) f1 = e.fn;
-    for (const Entry& e : g_cache[h2])
-      if (e.M == M && e.words == keyw) f2 = e.fn;
-    if (!f1 || !f2) {
-      const std::string src = bucket_source(words, n, M, elem, RB, with_src);
-      f1 = get_kernel_locked(k1d, keyw, M, src, "qsim_bucket_pass1", err);
-      if (!f1) return -1;
-      f2 = get_kernel_locked(k2d, keyw, M, src, "qsim_bucket_pass2", err);
-      if (!f2) return -1;
-    }
-    if (g_drv.setattr(f1, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
-      err = "cuFuncSetAttribute(max dynamic smem) failed";
-      return -1;
-    }
-    g_drv.setattr(f1, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
-  }
-  const int NB = 1 << (M - RB);
-  if (cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * NB, st) != cudaSuccess) {
-    err = "bucket cursor reset failed";
-    return -1;
-  }
-  const uint64_t ntiles = (1ull << M) / 8192;
-  uint64_t b1 = std::min<uint64_t>(ntiles, (uint64_t)sms);
-  void* a1[] = {const_cast<void**>(&k1), &bval, &bidx, &bsrc, &cursor};
-  if (g_drv.launch(f1, (unsigned)b1, 1, 1, 256, 1, 1, (unsigned)smem, (CUstream)st, a1, nullptr) !=
-      CUDA_SUCCESS) {
-    err = "cuLaunchKernel (bucket pass 1) failed";
-    return -1;
-  }
-  uint64_t b2 = std::min<uint64_t>(((1ull << M) + 1023) / 1024, (uint64_t)sms * 4);
-  void* a2[] = {&bval, &bidx, &bsrc, &k2, &perm_out};
-  if (g_drv.launch(f2, (unsigned)b2, 1, 1, 256, 1, 1, 0, (CUstream)st, a2, nullptr) !=
-      CUDA_SUCCESS) {
-    err = "cuLaunchKernel (bucket pass 2) failed";
-    return -1;
-  }
-  return 0;
-}
-
-int jit_check_compile_bucketed(const uint32_t* words, int n, int M, int elem, int RB, bool with_src,
-                               std::string& err) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  init_locked();
-  if (!g_nvrtc.ok) {
-    err = g_status;
-    return -1;
-  }
-  std::vector<char> cubin;
-  return compile_cubin_locked(bucket_source(words, n, M, elem, RB, with_src), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T, std::string& err) {

@@ -55,12 +55,4 @@ int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& 
 int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,
               uint32_t* perm_out, int sms, cudaStream_t st, std::string& err);
 int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T, std::string& err);
-// Well-mixed circuits: two passes through destination buckets of 2^RB
-// outputs (pass 1 streams k1, walks forward, appends (value, d[, s]) runs per
-// bucket; pass 2 scatters one L2-resident bucket at a time).  Returns 0 or -1.
-int jit_bucketed(const uint32_t* words, int n, int M, int elem, int RB, const void* k1, void* k2,
-                 uint32_t* perm_out, void* bval, uint32_t* bidx, uint32_t* bsrc, uint32_t* cursor,
-                 int sms, cudaStream_t st, std::string& err);
-int jit_check_compile_bucketed(const uint32_t* words, int n, int M, int elem, int RB, bool with_src,
-                               std::string& err);
 }  // namespace qsim

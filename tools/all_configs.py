@@ -1,5 +1,4 @@
-"""Steady-state time of every planned call (and the two-pass bucketed call where
-it applies) on every BASELINE config (CUDA events, median of 5 after 2
+"""Steady-state time of every planned call on every BASELINE config (CUDA events, median of 5 after 2
 warm-ups); one JSON line per (config, call)."""
 import json
 import os
@@ -42,13 +41,6 @@ for name in sys.argv[1:] or ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"]:
         "run_fused_planned": (lambda: q.run_fused_planned(plan, g, k1, k2, ws), 2 * e),
         "map_gather_planned": (lambda: q.map_gather_planned(plan, g, perm, k1, k2, ws), 4 + 2 * e),
     }
-    for wp in (False, True):
-        nb = q.bucket_scratch_bytes(M, cfg.dtype, wp)
-        if nb:
-            scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
-            calls["bucketed" + ("_with_map" if wp else "")] = (
-                (lambda s=scratch, w=wp: q.run_bucketed(g, M, k1, k2, s, perm_out=perm if w else None,
-                                                        dtype=cfg.dtype)), 2 * e + (4 if wp else 0))
     for call, (fn, bpe) in calls.items():
         ms = timeit(fn)
         print(json.dumps({"config": name, "M": M, "dtype": cfg.dtype, "call": call,
