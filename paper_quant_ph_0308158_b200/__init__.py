@@ -160,15 +160,47 @@ def _check(rc: int, where: str) -> None:
         raise QsimError(rc, where)
 
 
+_ELEM = {C64: 8, C128: 16}
+
+
+def _need(x, nbytes: int, what: str, device: bool = True) -> None:
+    """Argument check before the C call (the ABI cannot see sizes): a torch
+    tensor must be on CUDA (device buffers) and hold at least nbytes; a numpy
+    array must hold at least nbytes.  Raw integer addresses are passed on."""
+    if x is None or isinstance(x, int):
+        return
+    if isinstance(x, np.ndarray):
+        have = x.nbytes
+    else:
+        if device and not x.is_cuda:
+            raise ValueError(f"{what} must be a CUDA tensor (got device {x.device})")
+        have = x.numel() * x.element_size()
+    if have < nbytes:
+        raise ValueError(f"{what} holds {have} bytes, the call needs {nbytes}")
+
+
+def _tensor_dtype(x):
+    """C64 / C128 from a complex tensor or array, else None (raw bytes)."""
+    s = str(getattr(x, "dtype", ""))
+    if "complex64" in s:
+        return C64
+    if "complex128" in s:
+        return C128
+    return None
+
+
 # ---------------------------------------------------------------------- calls
 def build_map(gates, M: int, perm, stream=None) -> None:
     g, gp, n = _gates(gates)
+    if 1 <= M <= 32:
+        _need(perm, 4 << M, "perm")
     _check(_lib.qsim_build_map(gp, n, M, _ptr(perm), _stream(stream)), "qsim_build_map")
 
 
 def build_map_range(gates, M: int, start: int, count: int, perm_out, stream=None,
                     walk: int = WALK_AUTO) -> None:
     g, gp, n = _gates(gates)
+    _need(perm_out, 4 * count, "perm_out")
     _check(_lib.qsim_build_map_ex(gp, n, M, start, count, _ptr(perm_out), walk,
                                   _stream(stream)), "qsim_build_map_ex")
 
@@ -190,6 +222,10 @@ def apply_map_signed(perm_in, signs, count: int, M: int, k1, k2_out, stream=None
 
 def apply_map(perm, M: int, k1, k2, stream=None, dtype=None) -> None:
     code = _dtype_code(k1 if dtype is None else dtype)
+    if 1 <= M <= 32 and code in _ELEM:
+        _need(perm, 4 << M, "perm")
+        _need(k1, _ELEM[code] << M, "k1")
+        _need(k2, _ELEM[code] << M, "k2")
     _check(_lib.qsim_apply_map(_ptr(perm), M, code, _ptr(k1), _ptr(k2), _stream(stream)),
            "qsim_apply_map")
 
@@ -203,6 +239,9 @@ def apply_map_range(perm_in, count: int, M: int, k1, k2_out, stream=None, dtype=
 def run_fused(gates, M: int, k1, k2, stream=None, dtype=None) -> None:
     g, gp, n = _gates(gates)
     code = _dtype_code(k1 if dtype is None else dtype)
+    if 1 <= M <= 32 and code in _ELEM:
+        _need(k1, _ELEM[code] << M, "k1")
+        _need(k2, _ELEM[code] << M, "k2")
     _check(_lib.qsim_run_fused(gp, n, M, code, _ptr(k1), _ptr(k2), _stream(stream)),
            "qsim_run_fused")
 
@@ -301,6 +340,7 @@ def apply_map_planned(plan: Plan, perm, k1, k2, workspace=None, stream=None) -> 
 def run_fused_planned(plan: Plan, gates, k1, k2, workspace=None, stream=None) -> None:
     """qsim_run_fused in the plan's traversal order (same k2 bytes)."""
     g, gp, n = _gates(gates)
+    _need_plan(plan, k1, k2, None, workspace)
     _check(_lib.qsim_run_fused_planned(ctypes.byref(plan), gp, n, _ptr(k1), _ptr(k2),
                                        _ptr(workspace), _stream(stream)),
            "qsim_run_fused_planned")
@@ -309,13 +349,14 @@ def run_fused_planned(plan: Plan, gates, k1, k2, workspace=None, stream=None) ->
 def map_gather_planned(plan: Plan, gates, perm, k1, k2, workspace=None, stream=None) -> None:
     """perm (materialised map) and k2 = k1[perm] in one call (one kernel when JIT)."""
     g, gp, n = _gates(gates)
+    _need_plan(plan, k1, k2, perm, workspace)
     _check(_lib.qsim_map_gather_planned(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
                                         _ptr(workspace), _stream(stream)),
            "qsim_map_gather_planned")
 
 
 def run_fused_kron(gates, M: int, qubits, k2_out, start: int = 0, count: int | None = None,
-                   dtype="c64", walk: int = WALK_AUTO, stream=None) -> None:
+                   dtype=None, walk: int = WALK_AUTO, stream=None) -> None:
     """k2_out[r] = k1(perm[start + r]) with k1 = q_M (x) ... (x) q_1 generated on
     the fly (Appendix 1).  qubits: (M, 2) complex, row j-1 = [q_j(0), q_j(1)]."""
     q = np.ascontiguousarray(np.asarray(qubits, dtype=np.complex128).reshape(-1, 2))
@@ -324,8 +365,17 @@ def run_fused_kron(gates, M: int, qubits, k2_out, start: int = 0, count: int | N
     qd = np.ascontiguousarray(q.view(np.float64).reshape(-1))
     if count is None:
         count = (1 << M) - start
+    if dtype is None:                    # from the output tensor, else complex64
+        dtype = _tensor_dtype(k2_out)
+        dtype = C64 if dtype is None else dtype
+    code = _dtype_code(dtype)
+    td = _tensor_dtype(k2_out)
+    if td is not None and td != code:
+        raise ValueError(f"k2_out is {k2_out.dtype} but dtype says {dtype}")
+    if code in _ELEM:
+        _need(k2_out, _ELEM[code] * count, "k2_out")
     g, gp, n = _gates(gates)
-    _check(_lib.qsim_run_fused_kron(gp, n, M, _dtype_code(dtype), qd.ctypes.data, start, count,
+    _check(_lib.qsim_run_fused_kron(gp, n, M, code, qd.ctypes.data, start, count,
                                     _ptr(k2_out), walk, _stream(stream)), "qsim_run_fused_kron")
 
 

@@ -360,3 +360,19 @@ def test_plan_tune_validation(q):
     plan2 = q.plan_create(ph, 16, "c64")
     assert L.qsim_plan_tune(ctypes.byref(plan2), ph.ctypes.data, 1, FAKE, FAKE * 4, FAKE * 8,
                             FAKE * 16, None, None) == q.EINVAL                # phase circuit
+
+
+def test_binding_checks_before_the_c_call(q):
+    """The ctypes binding checks what the C ABI cannot see: device
+    buffers must be CUDA tensors of at least the bytes the call writes, and
+    the on-the-fly input's dtype follows its output tensor."""
+    import torch
+    g = wl.random_gates(5, 10, 1)
+    with pytest.raises(ValueError, match="CUDA"):
+        q.build_map(g, 10, torch.empty(1 << 10, dtype=torch.int32))          # host tensor
+    with pytest.raises(ValueError, match="CUDA"):
+        q.run_fused(g, 10, torch.empty(1 << 10, dtype=torch.complex64),
+                    torch.empty(1 << 10, dtype=torch.complex64))
+    qb = wl.random_qubits(10, 1, "c64")
+    with pytest.raises(ValueError, match="dtype"):
+        q.run_fused_kron(g, 10, qb, torch.empty(1 << 10, dtype=torch.complex128), dtype="c64")

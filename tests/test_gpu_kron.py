@@ -319,3 +319,41 @@ def test_kron_c128_full_size_sampled(q):
     _check(got, ref, M, "c128")
     del out
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_kron_portions_glue_at_32_qubits(q, dtype):
+    """The table grouping is the circuit's, not the range's: at
+    M = 32 the whole output in one call equals, byte for byte, portions
+    computed by separate calls below 2^22 outputs (ahead-of-time kernels),
+    above it (NVRTC, in-thread layout), misaligned and ragged -- and a
+    sampled set of outputs lies within the oracle's rounding bound."""
+    M, N = 32, 1 << 32
+    gates = wl.CONFIGS["cfg5"].gates()
+    qb = wl.random_qubits(M, 2024, dtype)
+    e = 8 if dtype == "c64" else 16
+    if dtype == "c128":              # 64 GiB: check the upper half as "the whole" range instead
+        whole_start, whole_count = N // 2, N // 2
+    else:
+        whole_start, whole_count = 0, N
+    whole = torch.empty(whole_count * e, dtype=torch.uint8, device=DEV)
+    q.run_fused_kron(gates, M, qb, whole, start=whole_start, count=whole_count, dtype=dtype)
+    torch.cuda.synchronize()
+    portions = [(whole_start, 1 << 21), (whole_start + (1 << 30) - 12345, (1 << 23) + 77),
+                (whole_start + whole_count - (1 << 22) - 5, (1 << 22) + 5),
+                (whole_start + (1 << 28), 1 << 26), (whole_start + 3, 1000)]
+    for start, count in portions:
+        part = torch.empty(count * e, dtype=torch.uint8, device=DEV)
+        q.run_fused_kron(gates, M, qb, part, start=start, count=count, dtype=dtype)
+        torch.cuda.synchronize()
+        off = (start - whole_start) * e
+        assert torch.equal(part, whole[off:off + count * e]), (start, count, q.last_kernel())
+    rng = np.random.default_rng(3)
+    idx = np.unique(rng.integers(whole_start, whole_start + whole_count, 2000, dtype=np.uint64))
+    ref = np.array([oracle.fused_kron(gates, qb, int(i), 1)[0] for i in idx])
+    got = whole.view(-1, e)[torch.from_numpy((idx - whole_start).astype(np.int64)).to(DEV)]
+    got = got.cpu().numpy().reshape(-1).view(wl.NP_DTYPE[dtype])
+    _check(got, ref, M, dtype)
+    del whole
+    torch.cuda.empty_cache()
