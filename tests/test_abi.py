@@ -376,3 +376,23 @@ def test_binding_checks_before_the_c_call(q):
     qb = wl.random_qubits(10, 1, "c64")
     with pytest.raises(ValueError, match="dtype"):
         q.run_fused_kron(g, 10, qb, torch.empty(1 << 10, dtype=torch.complex128), dtype="c64")
+
+
+def test_binding_wrappers_reach_their_checks(q):
+    """Every wrapper that takes device buffers rejects host tensors with a
+    ValueError before the C call (catches wrapper bugs without a GPU)."""
+    import torch
+    M = 12
+    g = wl.random_gates(5, M, 2)
+    plan = q.plan_create(g, M, "c64")
+    k = torch.empty(1 << M, dtype=torch.complex64)
+    p = torch.empty(1 << M, dtype=torch.int32)
+    ws = torch.empty(q.WORKSPACE_BYTES, dtype=torch.uint8)
+    calls = [lambda: q.apply_map(p, M, k, k), lambda: q.apply_map_planned(plan, p, k, k, ws),
+             lambda: q.run_fused_planned(plan, g, k, k, ws),
+             lambda: q.map_gather_planned(plan, g, p, k, k, ws),
+             lambda: q.run_bucketed(g, M, k, k, ws, dtype="c64"),
+             lambda: q.build_map_range(g, M, 0, 1 << M, p)]
+    for c in calls:
+        with pytest.raises(ValueError):
+            c()
