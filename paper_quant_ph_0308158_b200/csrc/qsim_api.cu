@@ -1323,7 +1323,7 @@ int bucket_log_count(int32_t M, int32_t dtype, bool with_perm, int C) {
 bool bucket_supported(int32_t M, int32_t dtype, bool with_perm) {
   if (M < 13 || M > 32 || elem_bytes(dtype) == 0) return false;
   const int l16 = bucket_log_count(M, dtype, with_perm, 16);
-  return l16 >= 0 && l16 <= 9;
+  return l16 >= 0 && l16 <= 10;
 }
 
 uint64_t bucket_scratch_bytes(int32_t M, int32_t dtype, bool with_perm) {

@@ -799,6 +799,9 @@ qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32*
     for (u32 x = threadIdx.x; x < 4u * QSIM_NB; x += blockDim.x) wcnt[x] = 0u;
     __syncthreads();
     const u64 base = tile * QSIM_TILE + (u64)warp * 1024u;   // this warp's 1024 sources
+    // the 32 values first (coalesced; they arrive while the walk runs)
+    QSIM_T v[32];
+    _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = __ldcs(k1 + base + 32u * l + lane);
 )";
   // planes of the sources base + 32 l + lane: lanes on bits 0..4, the
   // thread's 32 entries on bits 5..9, the rest constant in the warp
@@ -829,9 +832,11 @@ qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32*
     QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
     QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
     // a[l] = d = g(base + 32 l + lane); its rank among this warp pair's entries of its bucket
-    u32 slot[32];
+    u32 slot[16];   // two 16-bit ranks per word (< 8192)
     u32* const wc = wcnt + (warp >> 1) * QSIM_NB;
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) slot[l] = atomicAdd(&wc[a[l] >> QSIM_LOGBK], 1u);
+    _Pragma("unroll") for (int l = 0; l < 32; l += 2)
+      slot[l >> 1] = atomicAdd(&wc[a[l] >> QSIM_LOGBK], 1u) |
+                     (atomicAdd(&wc[a[l + 1] >> QSIM_LOGBK], 1u) << 16);
     __syncthreads();
     // per bucket: warp offsets, tile total; then offsets over the buckets and the scratch runs
     for (u32 b = threadIdx.x; b < QSIM_NB; b += blockDim.x) {
@@ -862,19 +867,15 @@ qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32*
       }
     }
     __syncthreads();
-    // values (coalesced loads in batches of 8) to their bucket-sorted slots
-    _Pragma("unroll") for (int h = 0; h < 32; h += 8) {
-      QSIM_T v[8];
-      _Pragma("unroll") for (int l = 0; l < 8; ++l) v[l] = __ldcs(k1 + base + 32u * (h + l) + lane);
-      _Pragma("unroll") for (int l = 0; l < 8; ++l) {
-        const u32 d = a[h + l], b = d >> QSIM_LOGBK;
-        const u32 pos = start[b] + wc[b] + slot[h + l];
-        sval[pos] = negate_if(v[l], (sg >> (h + l)) & 1u);
-        sidx[pos] = d;
+    // values to their bucket-sorted slots
+    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
+      const u32 d = a[l], b = d >> QSIM_LOGBK;
+      const u32 pos = start[b] + wc[b] + ((slot[l >> 1] >> (16 * (l & 1))) & 0xffffu);
+      sval[pos] = negate_if(v[l], (sg >> l) & 1u);
+      sidx[pos] = d;
 #if QSIM_SRC
-        ssrc[pos] = (u32)(base + 32u * (h + l) + lane);
+      ssrc[pos] = (u32)(base + 32u * l + lane);
 #endif
-      }
     }
     __syncthreads();
     // runs out: slot pos of bucket b -> scratch b * Bk + gbase[b] + (pos - start[b])
@@ -894,7 +895,8 @@ qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32*
 // pass 2: cluster b (of C CTAs, one bucket of Bk = C * S outputs) scatters the
 // bucket's entries into its distributed shared memory, then each CTA writes
 // its S outputs as one run
-extern "C" __global__ void __cluster_dims__(QSIM_C, 1, 1) __launch_bounds__(256, 1)
+#define QSIM_P2T 1024u
+extern "C" __global__ void __cluster_dims__(QSIM_C, 1, 1) __launch_bounds__(1024, 1)
 qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
                   const u32* __restrict__ bsrc, QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
   extern __shared__ __align__(16) unsigned char bsm[];
@@ -911,19 +913,8 @@ qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
 #if QSIM_SRC
   const u32 p_sh = smem_u32(slp);
 #endif
-  // the remote shared-memory window of every CTA of the cluster
-  u32 rv[QSIM_C];
-#if QSIM_SRC
-  u32 rp[QSIM_C];
-#endif
-  _Pragma("unroll") for (int c = 0; c < QSIM_C; ++c) {
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv[c]) : "r"(v_sh), "r"(c));
-#if QSIM_SRC
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rp[c]) : "r"(p_sh), "r"(c));
-#endif
-  }
-  const u32 stride = QSIM_C * 256u;
-  for (u32 i0 = rank * 256u + threadIdx.x; i0 < Bk; i0 += stride * 8u) {
+  const u32 stride = QSIM_C * QSIM_P2T;
+  for (u32 i0 = rank * QSIM_P2T + threadIdx.x; i0 < Bk; i0 += stride * 8u) {
     QSIM_T v[8];
     u32 d[8];
 #if QSIM_SRC
@@ -943,21 +934,21 @@ qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
       const u32 i = i0 + (u32)j * stride;
       if (i < Bk) {
         const u32 rel = (u32)(d[j] - base), own = rel >> QSIM_LOGS, off = rel & (S - 1u);
-        u32 ra = 0u;
-        _Pragma("unroll") for (int c = 0; c < QSIM_C; ++c) ra = own == (u32)c ? rv[c] : ra;
+        u32 ra;   // the owner CTA's slot in the cluster's shared-memory window
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(v_sh + off * (u32)sizeof(QSIM_T)), "r"(own));
 #if QSIM_SRC
-        u32 rpa = 0u;
-        _Pragma("unroll") for (int c = 0; c < QSIM_C; ++c) rpa = own == (u32)c ? rp[c] : rpa;
-        asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(rpa + off * 4u), "r"(sr[j]) : "memory");
+        u32 rpa;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpa) : "r"(p_sh + off * 4u), "r"(own));
+        asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(rpa), "r"(sr[j]) : "memory");
 #endif
         if (sizeof(QSIM_T) == 16) {
           const uint4 x = *reinterpret_cast<const uint4*>(&v[j]);
           asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
-                       :: "r"(ra + off * 16u), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w) : "memory");
+                       :: "r"(ra), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w) : "memory");
         } else {
           const uint2 x = *reinterpret_cast<const uint2*>(&v[j]);
           asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};"
-                       :: "r"(ra + off * 8u), "r"(x.x), "r"(x.y) : "memory");
+                       :: "r"(ra), "r"(x.x), "r"(x.y) : "memory");
         }
       }
     }
@@ -965,7 +956,7 @@ qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   // this CTA's S outputs, one contiguous run
   const u64 o0 = base + (u64)rank * S;
-  for (u32 j = threadIdx.x; j < S; j += 256u) {
+  for (u32 j = threadIdx.x; j < S; j += QSIM_P2T) {
     stcs(k2 + o0 + j, slv[j]);
 #if QSIM_SRC
     __stcs(perm_out + o0 + j, slp[j]);
@@ -1353,8 +1344,10 @@ int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* 
 int bucket_geometry(int M, int elem, bool with_src, int C, int* logS) {
   // S outputs per CTA: its values (and map entries) in at most 160 KB of smem
   const int per = elem + (with_src ? 4 : 0);
+  int kb = 160;
+  if (const char* e = std::getenv("QSIM_BUCKET_SLICE_KB")) kb = std::atoi(e);  // experiment
   int ls = 0;
-  while ((per << (ls + 1)) <= (160 << 10)) ++ls;
+  while ((per << (ls + 1)) <= (kb << 10)) ++ls;
   *logS = ls;
   const int logBk = ls + __builtin_ctz((unsigned)C);
   return M - logBk;  // log2 of the bucket count
@@ -1367,7 +1360,7 @@ int jit_bucketed(const uint32_t* words, int n, int M, int elem, const void* k1, 
   for (int C : {16, 8}) {
     int logS = 0;
     const int lnb = bucket_geometry(M, elem, with_src, C, &logS);
-    if (lnb < 0 || lnb > 10) {
+    if (lnb < 0 || lnb > 11) {
       err = "bucket count out of range";
       return -1;
     }
@@ -1385,6 +1378,7 @@ int jit_bucketed(const uint32_t* words, int n, int M, int elem, const void* k1, 
       std::vector<uint32_t> keyw(words, words + n);
       keyw.push_back((uint32_t)elem);
       keyw.push_back((uint32_t)C);
+      keyw.push_back((uint32_t)logS);
       keyw.push_back(with_src ? 1u : 0u);
       const uint64_t k1d = 0x62756b31ull, k2d = 0x62756b32ull;
       const uint64_t h1 = fnv(keyw.data(), (int)keyw.size(), k1d), h2 = fnv(keyw.data(), (int)keyw.size(), k2d);
@@ -1421,7 +1415,7 @@ int jit_bucketed(const uint32_t* words, int n, int M, int elem, const void* k1, 
       return -1;
     }
     void* a2[] = {&bval, &bidx, &bsrc, &k2, &perm_out};
-    if (g_drv.launch(f2, (unsigned)(NB * C), 1, 1, 256, 1, 1, (unsigned)smem2, (CUstream)st, a2,
+    if (g_drv.launch(f2, (unsigned)(NB * C), 1, 1, 1024, 1, 1, (unsigned)smem2, (CUstream)st, a2,
                      nullptr) == CUDA_SUCCESS)
       return 0;
     err = "cuLaunchKernel (bucket pass 2, cluster " + std::to_string(C) + ") failed";
