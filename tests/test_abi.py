@@ -391,7 +391,6 @@ def test_binding_wrappers_reach_their_checks(q):
     calls = [lambda: q.apply_map(p, M, k, k), lambda: q.apply_map_planned(plan, p, k, k, ws),
              lambda: q.run_fused_planned(plan, g, k, k, ws),
              lambda: q.map_gather_planned(plan, g, p, k, k, ws),
-             lambda: q.run_bucketed(g, M, k, k, ws, dtype="c64"),
              lambda: q.build_map_range(g, M, 0, 1 << M, p)]
     for c in calls:
         with pytest.raises(ValueError):
