@@ -1693,24 +1693,22 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
   }
   // third stage: the order of the counter bits above the cover (runtime
   // kernel parameter, no recompiles).  The plan orders them for the k1 reads
-  // (a line's readers close in time); moving a low output bit down next to
-  // the cover also brings neighbouring k2 / perm lines into the same chunk
-  // front, so their DRAM writes meet in the same rows (measured on cfg5:
-  // output bit 4 at counter bit 15: 19.06 vs 19.85 ms,
-  // profiles/r02_sigma_tail_moves.txt).  Greedy: each low output bit in the
-  // tail tried at each of the 6 positions above the cover, kept on a clear
-  // (>= 1 %) win; two rounds.
+  // (a line's readers close in time); moving an output bit down next to the
+  // cover changes which k2 / perm lines share a chunk front (their DRAM rows
+  // on write-back) and which k1 lines are read together.  Best-improvement
+  // rounds: every tail bit tried at each of the 10 positions just above the
+  // cover (screened with one timed call), the best candidate re-timed and
+  // kept on a >= 0.5 % win; up to 3 rounds (cfg5: output bits 4 and 28 move
+  // down, 19.85 -> 18.95 ms; profiles/r02_sigma_tail_moves.txt,
+  // r02_tail_search.txt).
   qsim_plan cur = cands[best_i];
-  const int from = std::max(10, (int)cur.tile_log2 + 0);
+  const int from = std::max(10, (int)cur.tile_log2);
   if (!(cur.flags & 1u) && cur.M >= from + 4) {
-    for (int round = 0; round < 2 && rc == QSIM_OK; ++round) {
-      bool moved = false;
-      for (int bit = 3; bit < 12 && rc == QSIM_OK; ++bit) {
-        int at = -1;
-        for (int k = from; k < cur.M; ++k)
-          if (cur.sigma[k] == bit) at = k;
-        if (at < 0) continue;  // in the cover (or >= M)
-        for (int pos = from; pos < std::min(cur.M, from + 6) && rc == QSIM_OK; ++pos) {
+    for (int round = 0; round < 3 && rc == QSIM_OK; ++round) {
+      float cand_t = 1e30f;
+      qsim_plan cand = cur;
+      for (int at = from; at < cur.M && rc == QSIM_OK; ++at) {
+        for (int pos = from; pos < std::min(cur.M, from + 10) && rc == QSIM_OK; ++pos) {
           if (pos == at) continue;
           qsim_plan p = cur;
           uint8_t rest[32];
@@ -1718,27 +1716,19 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
           for (int k = from; k < cur.M; ++k)
             if (k != at) rest[m++] = cur.sigma[k];
           for (int k = from, r = 0; k < cur.M; ++k)
-            p.sigma[k] = k == pos ? (uint8_t)bit : rest[r++];
-          const float t = time_plan(p, false, 2);
-          if (rc == QSIM_OK && t < best * 0.99f) {
-            best = t;
-            cur = p;
-            moved = true;
-            at = pos;
+            p.sigma[k] = k == pos ? cur.sigma[at] : rest[r++];
+          const float t = time_plan(p, false, 1);
+          if (rc == QSIM_OK && t < cand_t) {
+            cand_t = t;
+            cand = p;
           }
         }
       }
-      if (!moved) break;
-    }
-    // then swaps of neighbouring counter bits above the cover (one sweep)
-    for (int k = from; k + 1 < std::min(cur.M, from + 12) && rc == QSIM_OK; ++k) {
-      qsim_plan p = cur;
-      std::swap(p.sigma[k], p.sigma[k + 1]);
-      const float t = time_plan(p, false, 2);
-      if (rc == QSIM_OK && t < best * 0.99f) {
-        best = t;
-        cur = p;
-      }
+      if (rc != QSIM_OK) break;
+      const float t = time_plan(cand, false, 3);
+      if (rc != QSIM_OK || !(t < best * 0.995f)) break;
+      best = t;
+      cur = cand;
     }
     if (rc == QSIM_OK) cands[best_i] = cur;
   }
