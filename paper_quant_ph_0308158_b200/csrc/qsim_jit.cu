@@ -249,13 +249,19 @@ std::string walk_code(const uint32_t* w, int n, int M) {
 // aligned block of 2^L outputs.  Stores stay 128 / 256-byte warp runs.
 std::string thread_defs(const uint8_t* J, int L) {
   char buf[320];
+  std::string st = "#define QSIM_ST(p, v) __stcs(p, v)\n";
+  if (const char* e = std::getenv("QSIM_KRON_ST")) {  // experiment: store policy
+    if (!std::strcmp(e, "wb")) st = "#define QSIM_ST(p, v) (*(p) = (v))\n";
+    else if (!std::strcmp(e, "cg")) st = "#define QSIM_ST(p, v) __stcg(p, v)\n";
+    else if (!std::strcmp(e, "wt")) st = "#define QSIM_ST(p, v) __stwt(p, v)\n";
+  }
   std::snprintf(buf, sizeof buf,
                 "#define QSIM_L %d\n"
                 "#define QSIM_OFF(l) (((l) & 1 ? 1ull << %d : 0ull) | ((l) & 2 ? 1ull << %d : 0ull) | "
                 "((l) & 4 ? 1ull << %d : 0ull) | ((l) & 8 ? 1ull << %d : 0ull) | "
                 "((l) & 16 ? 1ull << %d : 0ull))\n",
                 L, J[0], J[1], J[2], J[3], J[4]);
-  return buf;
+  return st + buf;
 }
 
 // base = the tile's first output (lane and J bits clear), the initial planes
@@ -297,14 +303,14 @@ std::string thread_stores(const char* ptr, const char* value, const char* ind) {
   e += i + "if (full) {\n";
   e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
   e += i + "    " + value + "\n";
-  e += i + "    __stcs(kq + QSIM_OFF(l), rv);\n";
+  e += i + "    QSIM_ST(kq + QSIM_OFF(l), rv);\n";
   e += i + "  }\n";
   e += i + "} else {\n";
   e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
   e += i + "    const u64 addr = base + lane + QSIM_OFF(l);\n";
   e += i + "    if (addr >= start && addr < end) {\n";
   e += i + "      " + value + "\n";
-  e += i + "      __stcs(kq + QSIM_OFF(l), rv);\n";
+  e += i + "      QSIM_ST(kq + QSIM_OFF(l), rv);\n";
   e += i + "    }\n";
   e += i + "  }\n";
   e += i + "}\n";
@@ -1001,6 +1007,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     for (int k = 0; k < 5; ++k) keyw.push_back(J[k]);
     keyw.push_back((uint32_t)L);
     keyw.push_back((uint32_t)nv);
+    if (const char* e = std::getenv("QSIM_KRON_ST")) keyw.push_back((uint32_t)e[0] | ((uint32_t)e[1] << 8));
     const uint64_t kind = 0x6b726f6eull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
