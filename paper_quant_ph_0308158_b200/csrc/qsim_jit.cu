@@ -249,12 +249,9 @@ std::string walk_code(const uint32_t* w, int n, int M) {
 // aligned block of 2^L outputs.  Stores stay 128 / 256-byte warp runs.
 std::string thread_defs(const uint8_t* J, int L) {
   char buf[320];
-  std::string st = "#define QSIM_ST(p, v) __stcs(p, v)\n";
-  if (const char* e = std::getenv("QSIM_KRON_ST")) {  // experiment: store policy
-    if (!std::strcmp(e, "wb")) st = "#define QSIM_ST(p, v) (*(p) = (v))\n";
-    else if (!std::strcmp(e, "cg")) st = "#define QSIM_ST(p, v) __stcg(p, v)\n";
-    else if (!std::strcmp(e, "wt")) st = "#define QSIM_ST(p, v) __stwt(p, v)\n";
-  }
+  // streaming stores (write-back / .cg / .wt measured the same for the
+  // on-the-fly input: profiles/r02_kron_store_policy.txt)
+  const std::string st = "#define QSIM_ST(p, v) __stcs(p, v)\n";
   std::snprintf(buf, sizeof buf,
                 "#define QSIM_L %d\n"
                 "#define QSIM_OFF(l) (((l) & 1 ? 1ull << %d : 0ull) | ((l) & 2 ? 1ull << %d : 0ull) | "
@@ -1007,7 +1004,6 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
     for (int k = 0; k < 5; ++k) keyw.push_back(J[k]);
     keyw.push_back((uint32_t)L);
     keyw.push_back((uint32_t)nv);
-    if (const char* e = std::getenv("QSIM_KRON_ST")) keyw.push_back((uint32_t)e[0] | ((uint32_t)e[1] << 8));
     const uint64_t kind = 0x6b726f6eull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
