@@ -50,3 +50,23 @@ def both_chunked(c=256 << 20):
 for name, fn in (("h2d", h2d), ("d2h", d2h), ("both", both), ("both_chunked_256MB", both_chunked)):
     t = run(fn)
     print(json.dumps({"case": name, "s": round(t, 4), "GBps_each_direction": n / t / 1e9}), flush=True)
+
+
+# round 2: more streams per direction, other chunk sizes
+s3, s4 = torch.cuda.Stream(), torch.cuda.Stream()
+
+
+def both_4streams(c=256 << 20):
+    for i, o in enumerate(range(0, n, c)):
+        with torch.cuda.stream(s1 if i % 2 == 0 else s3):
+            d1[o:o + c].copy_(h1[o:o + c], non_blocking=True)
+        with torch.cuda.stream(s2 if i % 2 == 0 else s4):
+            h2[o:o + c].copy_(d2[o:o + c], non_blocking=True)
+
+
+for name, fn in (("both_chunked_64MB", lambda: both_chunked(64 << 20)),
+                 ("both_chunked_1GB", lambda: both_chunked(1 << 30)),
+                 ("both_4streams_256MB", both_4streams),
+                 ("both_4streams_64MB", lambda: both_4streams(64 << 20))):
+    t = run(fn)
+    print(json.dumps({"case": name, "s": round(t, 4), "GBps_each_direction": n / t / 1e9}), flush=True)
