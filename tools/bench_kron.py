@@ -29,6 +29,6 @@ for i in range(6):
     times.append(a.elapsed_time(b))
 ms = min(times[2:])
 e = 8 if dtype == "c64" else 16
-print(f"M={M} count=2^{cl} {dtype} gb_env={os.environ.get('QSIM_KRON_GROUP_BITS', '-')}: {ms:.3f} ms "
+print(f"M={M} count=2^{cl} {dtype} {ms:.3f} ms "
       f"{count / ms * 1e3:.3e} entries/s {count * e / ms / 1e6:.0f} GB/s seed={seed} "
       f"layout={os.environ.get('QSIM_THREAD_BITS', '-')} [{q.last_kernel()}]")

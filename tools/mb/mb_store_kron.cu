@@ -34,6 +34,47 @@ __global__ void __launch_bounds__(256, 2) k_tile_j(uint2* out, uint64_t ntiles, 
   }
 }
 
+// 16-byte stores: a lane holds the two entries (o, o ^ 1) -- lanes on output
+// bits 1..5, in-thread bits {0} + J[1..4]: 16 store instructions of 512 B
+__global__ void __launch_bounds__(256, 2) k_tile_j16(uint4* out, uint64_t ntiles, int j1, int j2, int j3,
+                                                     int j4) {
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const int J[5] = {0, j1, j2, j3, j4};
+  for (uint64_t tile = (uint64_t)blockIdx.x * 8u + warp; tile < ntiles; tile += (uint64_t)gridDim.x * 8u) {
+    uint64_t base = tile << 5;   // in units of entries, bits 1..5 = lane (entry pairs)
+    for (int k = 1; k < 5; ++k) base = (base & ((1ull << J[k]) - 1)) | ((base >> J[k]) << (J[k] + 1));
+    base = (base << 1);          // bit 0 is the pair
+    // base now has lane bits at 6.. -- rebuild: lanes on bits 1..5
+    uint64_t t = tile;
+    uint64_t b2 = 0;
+    int pos = 6, kk = 0;
+    (void)kk;
+    for (int bit = 6; bit < 40 && t; ++bit) {
+      bool inJ = false;
+      for (int k = 1; k < 5; ++k) inJ = inJ || (J[k] == bit);
+      if (inJ) continue;
+      b2 |= (t & 1ull) << bit;
+      t >>= 1;
+      (void)pos;
+    }
+    base = b2 | ((uint64_t)lane << 1);
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      uint64_t off = 0;
+#pragma unroll
+      for (int k = 1; k < 5; ++k)
+        if ((l >> (k - 1)) & 1) off |= 1ull << J[k];
+      __stcs(out + ((base + off) >> 1), make_uint4((uint32_t)l, 1u, 2u, 3u));
+    }
+  }
+}
+
+template <typename V>
+__global__ void k_seqv(V* out, uint64_t n, V v) {
+  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += nthr) __stcs(out + t, v);
+}
+
 __global__ void k_seq(uint2* out, uint64_t n) {
   const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += nthr)
@@ -64,6 +105,19 @@ int main() {
            bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
   };
   run("seq u64 grid=16xSM", [&] { k_seq<<<sms * 16, 256>>>(out, n); });
+  for (int g : {8, 16, 32}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "seq u64 grid=%dxSM", g);
+    run(nm, [&] { k_seqv<uint2><<<sms * g, 256>>>(out, n, make_uint2(1u, 2u)); });
+    snprintf(nm, sizeof nm, "seq u128 grid=%dxSM", g);
+    run(nm, [&] { k_seqv<uint4><<<sms * g, 256>>>(reinterpret_cast<uint4*>(out), n / 2, make_uint4(1u, 2u, 3u, 4u)); });
+  }
+  run("kron tiles 16-B pairs J=0.7.13.26.29", [&] {
+    k_tile_j16<<<sms * 8, 256>>>(reinterpret_cast<uint4*>(out), n >> 10, 7, 13, 26, 29);
+  });
+  run("kron tiles 16-B pairs J=0.6.7.8.9", [&] {
+    k_tile_j16<<<sms * 8, 256>>>(reinterpret_cast<uint4*>(out), n >> 10, 6, 7, 8, 9);
+  });
   const int Js[3][5] = {{7, 8, 13, 26, 29}, {5, 6, 7, 8, 9}, {9, 12, 16, 17, 23}};
   for (int t = 0; t < 3; ++t)
     for (int rot = 0; rot < 3; ++rot) {
