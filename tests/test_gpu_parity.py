@@ -565,6 +565,59 @@ def test_plan_tune_keeps_a_valid_plan(q):
     assert out2.cpu().numpy().tobytes() == ref.tobytes()
 
 
+@pytest.mark.slow
+def test_plan_tune_tail_order_stage(q):
+    """Above the L2 (M = 25, 256 MB state) the tuner's third stage reorders the
+    counter bits above the sector cover at run time: the kept plan is a
+    valid order (a permutation fixing the kept low bits) and every output of
+    map + gather, fused and apply with it equals the oracle."""
+    import oracle.parallel as opar
+    M = 25
+    gates = wl.random_gates(64, M, 4)
+    k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 25))
+    perm_ref = opar.build_map(gates, M)
+    ref = opar.apply_map(perm_ref, k1)
+    k1_d = _to_dev(k1)
+    plan = q.plan_create(gates, M, "c64")
+    assert not (plan.flags & 1)
+    pm, out = _new_perm(1 << M), torch.empty_like(k1_d)
+    q.plan_tune(plan, gates, pm, k1_d, out, q.workspace())
+    sig = list(plan.sigma)[:M]
+    assert sorted(sig) == list(range(M)) and sig[:3] == [0, 1, 2]
+    for run in ("mg", "fu", "ap"):
+        out.fill_(0)
+        if run == "mg":
+            pm.fill_(-1)
+            q.map_gather_planned(plan, gates, pm, k1_d, out, q.workspace())
+        elif run == "fu":
+            q.run_fused_planned(plan, gates, k1_d, out, q.workspace())
+        else:
+            q.apply_map_planned(plan, pm, k1_d, out, q.workspace())
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == ref.tobytes(), run
+        assert np.array_equal(_perm_np(pm), perm_ref)
+
+
+def test_plain_run_fused_concurrent_streams(q):
+    """The plain qsim_run_fused keeps one chunk ticket per stream: two
+    circuits run concurrently on two streams, repeatedly, give the oracle's
+    bytes."""
+    M = 18
+    cases = []
+    for sd in (1, 2):
+        gates = wl.random_gates(60, M, 70 + sd)
+        k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, sd))
+        cases.append((gates, _to_dev(k1), oracle.apply_map(oracle.build_map(gates, M), k1)))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [torch.empty_like(c[1]) for c in cases]
+    for _ in range(3):
+        for (gates, k1_d, _), o, st in zip(cases, outs, streams):
+            q.run_fused(gates, M, k1_d, o, stream=st, dtype="c64")
+        torch.cuda.synchronize()
+        for (_, _, ref), o in zip(cases, outs):
+            assert o.cpu().numpy().tobytes() == ref.tobytes()
+
+
 def test_aot_fallback_launch_shapes(q):
     """Without NVRTC (QSIM_NO_JIT=1, a subprocess: the switch is read once per
     process) the planned calls run the ahead-of-time kernels; every launch
