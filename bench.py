@@ -288,16 +288,6 @@ def other_configs(q, wl, dev, stream, names=("cfg3", "cfg4")):
             "apply_map_planned": (lambda: q.apply_map_planned(plan, perm, k1, k2, ws, stream=stream),
                                   4 + 2 * e),
         }
-        scratches = []
-        for wp in (False, True):
-            nb = q.bucket_scratch_bytes(M, cfg.dtype, wp)
-            if nb:
-                sc = torch.empty(nb, dtype=torch.uint8, device=dev)
-                scratches.append(sc)
-                calls["bucketed" + ("_map_gather" if wp else "_fused")] = (
-                    (lambda sc=sc, wp=wp: q.run_bucketed(g, M, k1, k2, sc, perm_out=perm if wp else None,
-                                                         stream=stream, dtype=cfg.dtype)),
-                    2 * e + (4 if wp else 0))
         res = {"M": M, "dtype": cfg.dtype, "natural_order_plan": bool(plan.flags & 1)}
         for call, (f, bpe) in calls.items():
             ts = []
@@ -315,7 +305,7 @@ def other_configs(q, wl, dev, stream, names=("cfg3", "cfg4")):
             res[call] = {"ms": ms, "entries_per_s": N / (ms * 1e-3), "GBps": gbps,
                          "bytes_per_entry": bpe, "frac_of_peak": gbps / hbm, "kernel": q.last_kernel()}
         out[name] = res
-        del k1, k2, perm, calls, scratches
+        del k1, k2, perm, calls
         torch.cuda.empty_cache()
     return out
 

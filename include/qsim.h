@@ -390,40 +390,6 @@ int qsim_jit_check_compile_kron(const qsim_gate *gates, int32_t n_gates, int32_t
                                 int32_t dtype);
 int qsim_jit_check_compile_planned(const qsim_plan *plan, const qsim_gate *gates,
                                    int32_t n_gates);
-int qsim_jit_check_compile_bucketed(const qsim_gate *gates, int32_t n_gates, int32_t M,
-                                    int32_t dtype, int32_t with_perm);
-/* qsim_run_bucketed -- k2 = U k1 (and, when perm_out != NULL, the map, as
- * qsim_map_gather_planned) in TWO passes through destination buckets, for
- * well-mixed circuits where no traversal order keeps a k1 sector's readers
- * together (the plan's natural-order flag, e.g. BASELINE cfg3: 256 random
- * gates on 26 bits) and a one-pass gather is bound by random 32-byte DRAM
- * accesses:
- *   pass 1 streams k1 in address order, walks each source s forward to its
- *     output d (perm(d) = s; Step 1 first), and appends (k1[s] with the row
- *     value applied, d[, s]) to the scratch region of bucket d / Bk, in runs
- *     per CTA (shared-memory counting sort of 8192 entries);
- *   pass 2 runs persistent thread-block clusters (16 CTAs, else 8), one
- *     bucket at a time each: the bucket's Bk outputs live in the cluster's
- *     distributed shared memory (each CTA holds S = Bk / C of them), the
- *     cluster stores every entry into the CTA that owns its output, then each
- *     CTA writes its S outputs (and map entries) as one contiguous run --
- *     whole k2 lines, never partial sectors -- while the next bucket's
- *     entries are already being loaded.
- * Same bytes as qsim_run_fused / qsim_map_gather_planned.
- *   M        with 16-CTA clusters at most 512 buckets: complex128 M = 17..26,
- *            complex64 M = 18..27 (QSIM_ERANGE otherwise)
- *   k1, k2   device, 2^M entries; perm_out device, 2^M uint32, or NULL
- *   scratch  device, >= qsim_bucket_scratch_bytes(M, dtype, perm_out != NULL)
- *            bytes (2^M * (e + 4 [+ 4]) + cursors), 16-B aligned, caller-owned,
- *            contents undefined afterwards; must not overlap k1 / k2 / perm
- * qsim_bucket_scratch_bytes returns 0 when M / dtype are out of range.
- * Phase steps (R17) are allowed without perm_out (QSIM_EINVAL with it).
- * Without NVRTC the call runs the one-pass kernels (same bytes).            */
-uint64_t qsim_bucket_scratch_bytes(int32_t M, int32_t dtype, int32_t with_perm);
-int qsim_run_bucketed(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t dtype,
-                      const void *k1, void *k2, uint32_t *perm_out, void *scratch,
-                      uint64_t scratch_bytes, void *stream);
-
 /* ABI version of this header / library: 7 (plans with the sector cover,
  * phase / SWAP gates, M > 32 on-the-fly input, batch e2e, graphs, tuning;
  * 7: the measured-slower linear-traversal and lane-pair plan fields removed). */

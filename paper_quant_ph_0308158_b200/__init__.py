@@ -95,8 +95,6 @@ def _load() -> ctypes.CDLL:
     sig["qsim_jit_check_compile_kron"] = [vp, i32, i32, i32]
     sig["qsim_run_fused_kron"] = [vp, i32, i32, i32, vp, u64, u64, vp, i32, vp]
     sig["qsim_jit_check_compile_planned"] = [ctypes.POINTER(Plan), vp, i32]
-    sig["qsim_run_bucketed"] = [vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]
-    sig["qsim_jit_check_compile_bucketed"] = [vp, i32, i32, i32, i32]
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args
@@ -110,8 +108,6 @@ def _load() -> ctypes.CDLL:
     lib.qsim_jit_last_compile_ms.restype = ctypes.c_double
     lib.qsim_last_launch_count.restype = i32
     lib.qsim_last_kernel.restype = ctypes.c_char_p
-    lib.qsim_bucket_scratch_bytes.argtypes = [i32, i32, i32]
-    lib.qsim_bucket_scratch_bytes.restype = u64
     return lib
 
 
@@ -391,26 +387,6 @@ def run_fused_kron(gates, M: int, qubits, k2_out, start: int = 0, count: int | N
     g, gp, n = _gates(gates)
     _check(_lib.qsim_run_fused_kron(gp, n, M, code, qd.ctypes.data, start, count,
                                     _ptr(k2_out), walk, _stream(stream)), "qsim_run_fused_kron")
-
-
-def bucket_scratch_bytes(M: int, dtype="c64", with_perm: bool = False) -> int:
-    """Scratch bytes qsim_run_bucketed needs (0 if M / dtype are out of range)."""
-    return int(_lib.qsim_bucket_scratch_bytes(M, _dtype_code(dtype), 1 if with_perm else 0))
-
-
-def run_bucketed(gates, M: int, k1, k2, scratch, perm_out=None, stream=None, dtype=None) -> None:
-    """k2 = U k1 (and perm_out, if given) in two passes through destination
-    buckets (well-mixed circuits; see qsim_run_bucketed in include/qsim.h)."""
-    g, gp, n = _gates(gates)
-    code = _dtype_code(k1 if dtype is None else dtype)
-    if 1 <= M <= 32 and code in _ELEM:
-        _need(k1, _ELEM[code] << M, "k1")
-        _need(k2, _ELEM[code] << M, "k2")
-        _need(perm_out, 4 << M, "perm_out")
-    _need(scratch, 1, "scratch")
-    nbytes = scratch.numel() * scratch.element_size() if hasattr(scratch, "numel") else int(scratch.nbytes)
-    _check(_lib.qsim_run_bucketed(gp, n, M, code, _ptr(k1), _ptr(k2), _ptr(perm_out), _ptr(scratch),
-                                  nbytes, _stream(stream)), "qsim_run_bucketed")
 
 
 def workspace(device=None):

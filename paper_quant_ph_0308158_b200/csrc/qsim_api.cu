@@ -1311,72 +1311,6 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
 }
 
 
-// ---- Two passes through destination buckets (well-mixed circuits) --------
-// Buckets of C * S outputs held in a thread-block cluster's distributed
-// shared memory (qsim_jit.cu bucket_source); pass 1 needs at most 2^10
-// buckets (clusters of 8), pass 2 at most 2^9 with clusters of 16.
-int bucket_log_count(int32_t M, int32_t dtype, bool with_perm, int C) {
-  int logS = 0;
-  return qsim::bucket_geometry(M, elem_bytes(dtype), with_perm, C, &logS);
-}
-
-bool bucket_supported(int32_t M, int32_t dtype, bool with_perm) {
-  if (M < 13 || M > 32 || elem_bytes(dtype) == 0) return false;
-  const int l16 = bucket_log_count(M, dtype, with_perm, 16);
-  return l16 >= 0 && l16 <= 10;
-}
-
-uint64_t bucket_scratch_bytes(int32_t M, int32_t dtype, bool with_perm) {
-  const uint64_t N = 1ull << M;
-  const uint64_t nb_max = 1ull << bucket_log_count(M, dtype, with_perm, 8);
-  return ((N * (elem_bytes(dtype) + 4 + (with_perm ? 4 : 0)) + 255) & ~255ull) + 4 * nb_max;
-}
-
-int bucketed_impl(const qsim_gate* gates, int32_t n, int32_t M, int32_t dtype, const void* k1,
-                  void* k2, uint32_t* perm_out, void* scratch, uint64_t scratch_bytes,
-                  cudaStream_t st) {
-  g_last_kernel = "";
-  int rc = check_gates(gates, n, M);
-  if (rc) return rc;
-  const int e = elem_bytes(dtype);
-  if (e == 0) return QSIM_EINVAL;
-  const bool wp = perm_out != nullptr;
-  if (!bucket_supported(M, dtype, wp)) return QSIM_ERANGE;
-  if (wp && has_phase(gates, n)) {
-    std::snprintf(g_err, sizeof g_err, "phase gates: the map cannot hold -1 rows");
-    return QSIM_EINVAL;
-  }
-  const uint64_t N = 1ull << M, need = bucket_scratch_bytes(M, dtype, wp);
-  if (!k1 || !k2 || !scratch || !aligned16(k1) || !aligned16(k2) || !aligned16(scratch) ||
-      (wp && !aligned16(perm_out)))
-    return QSIM_EINVAL;
-  if (scratch_bytes < need) return QSIM_EINVAL;
-  if (overlap(k1, N * e, k2, N * e) || overlap(scratch, need, k1, N * e) ||
-      overlap(scratch, need, k2, N * e) ||
-      (wp && (overlap(perm_out, N * 4, k1, N * e) || overlap(perm_out, N * 4, k2, N * e) ||
-              overlap(perm_out, N * 4, scratch, need))))
-    return QSIM_EALIAS;
-  char* sc = static_cast<char*>(scratch);
-  void* bval = sc;
-  uint32_t* bidx = reinterpret_cast<uint32_t*>(sc + N * e);
-  uint32_t* bsrc = wp ? reinterpret_cast<uint32_t*>(sc + N * (e + 4)) : nullptr;
-  uint32_t* cursor = reinterpret_cast<uint32_t*>(sc + ((N * (e + 4 + (wp ? 4 : 0)) + 255) & ~255ull));
-  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
-  pack_gates(gates, n, false, *gl);
-  std::string err;
-  if (qsim::jit_bucketed(gl->w, n, M, e, k1, k2, perm_out, bval, bidx, bsrc, cursor, sm_count(), st,
-                         err) == 0) {
-    g_launches += 2;
-    g_last_kernel = "qsim_bucket_pass1 + qsim_bucket_pass2";
-    return QSIM_OK;
-  }
-  // without NVRTC (or a cluster launch): the one-pass kernels (same bytes)
-  qsim_plan plan;
-  if ((rc = cached_plan(gates, n, M, dtype, &plan))) return rc;
-  if (wp) return map_gather_impl(&plan, gates, n, perm_out, k1, k2, nullptr, st);
-  return fused_planned_impl(&plan, gates, n, k1, k2, nullptr, st);
-}
-
 }  // namespace
 
 extern "C" {
@@ -1505,20 +1439,6 @@ int qsim_map_gather_planned(const qsim_plan* plan, const qsim_gate* gates, int32
   g_last_kernel = "";
   return map_gather_impl(plan, gates, n_gates, perm, k1, k2, workspace,
                          static_cast<cudaStream_t>(stream));
-}
-
-uint64_t qsim_bucket_scratch_bytes(int32_t M, int32_t dtype, int32_t with_perm) {
-  if (!bucket_supported(M, dtype, with_perm != 0)) return 0;
-  return bucket_scratch_bytes(M, dtype, with_perm != 0);
-}
-
-int qsim_run_bucketed(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype,
-                      const void* k1, void* k2, uint32_t* perm_out, void* scratch,
-                      uint64_t scratch_bytes, void* stream) {
-  g_launches = 0;
-  if (M < 1 || M > 32) return QSIM_ERANGE;
-  return bucketed_impl(gates, n_gates, M, dtype, k1, k2, perm_out, scratch, scratch_bytes,
-                       static_cast<cudaStream_t>(stream));
 }
 
 int qsim_run_host(const qsim_gate* gates, int32_t n_gates, int32_t M, int32_t dtype, int32_t mode,
@@ -1970,23 +1890,6 @@ int qsim_jit_check_compile_kron(const qsim_gate* gates, int32_t n_gates, int32_t
   if (qsim::jit_check_compile_kron(gl->w, n_gates, M, elem_bytes(dtype), (int)gb, (int)ng, ly.pos,
                                    ly.J, ly.L, ly.nv, err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
-    return QSIM_ECUDA;
-  }
-  return QSIM_OK;
-}
-
-int qsim_jit_check_compile_bucketed(const qsim_gate* gates, int32_t n_gates, int32_t M,
-                                    int32_t dtype, int32_t with_perm) {
-  g_launches = 0;
-  int rc = check_gates(gates, n_gates, M);
-  if (rc) return rc;
-  if (elem_bytes(dtype) == 0) return QSIM_EINVAL;
-  if (!bucket_supported(M, dtype, with_perm != 0)) return QSIM_ERANGE;
-  std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
-  pack_gates(gates, n_gates, false, *gl);
-  std::string err;
-  if (qsim::jit_check_compile_bucketed(gl->w, n_gates, M, elem_bytes(dtype), with_perm != 0, err) != 0) {
-    std::snprintf(g_err, sizeof g_err, "jit (bucketed): %s", err.c_str());
     return QSIM_ECUDA;
   }
   return QSIM_OK;

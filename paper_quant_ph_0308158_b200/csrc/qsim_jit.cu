@@ -57,9 +57,6 @@ struct Driver {
   PFN_cuModuleGetFunction_v2000 getfn = nullptr;
   PFN_cuLaunchKernel_v4000 launch = nullptr;
   PFN_cuFuncSetAttribute_v9000 setattr = nullptr;
-  // occupancy queries (optional: the bucketed path falls back to fixed grids)
-  CUresult (*occ_blocks)(int*, CUfunction, int, size_t) = nullptr;
-  CUresult (*occ_clusters)(int*, CUfunction, const CUlaunchConfig*) = nullptr;
   bool ok = false;
 };
 
@@ -123,12 +120,6 @@ void init_locked() {
   ok = ok && cudaGetDriverEntryPoint("cuFuncSetAttribute", &p, cudaEnableDefault, &q) ==
                  cudaSuccess && q == cudaDriverEntryPointSuccess;
   g_drv.setattr = reinterpret_cast<PFN_cuFuncSetAttribute_v9000>(p);
-  if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", &p, cudaEnableDefault, &q) ==
-          cudaSuccess && q == cudaDriverEntryPointSuccess)
-    g_drv.occ_blocks = reinterpret_cast<CUresult (*)(int*, CUfunction, int, size_t)>(p);
-  if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveClusters", &p, cudaEnableDefault, &q) == cudaSuccess &&
-      q == cudaDriverEntryPointSuccess)
-    g_drv.occ_clusters = reinterpret_cast<CUresult (*)(int*, CUfunction, const CUlaunchConfig*)>(p);
   g_drv.ok = ok;
   g_status = ok ? "ready (nvrtc " + std::to_string(g_nvrtc.major) + "." + std::to_string(g_nvrtc.minor) + ")"
                : "driver entry points unavailable";
@@ -757,234 +748,6 @@ qsim_jit_local(u64 ntiles, const E* __restrict__ k1, E* __restrict__ k2, u32* __
   return s;
 }
 
-// Two passes for well-mixed circuits (no traversal order keeps a k1
-// sector's readers together, e.g. cfg3: 256 random gates on 26 bits), where
-// a one-pass gather is bound by random 32-byte DRAM accesses.  The second
-// pass must produce WHOLE k2 lines: a scatter of 8- / 16-byte entries makes
-// the L2 fetch a sector from DRAM for every partial write (measured, round
-// 2).  So buckets live in on-chip memory: a thread-block cluster of C CTAs
-// holds one bucket of Bk = C * S outputs in its distributed shared memory.
-//   pass 1 (persistent, one CTA per SM): streams k1 in address order, walks
-//     each source s FORWARD to its output d = g(s) (perm(d) = s; Step 1
-//     first: the gate list reversed into walk_code; each step is an
-//     involution), counting-sorts the CTA's 8192 entries by bucket
-//     d / Bk in shared memory (per-warp histograms) and appends each bucket's
-//     run (value with the row value applied, d [, s]) to the bucket's scratch
-//     region (one atomic cursor per bucket and tile);
-//   pass 2 (one cluster per bucket): the cluster's CTAs stream the bucket's
-//     Bk entries from the scratch and store each value into the shared memory
-//     of the CTA that owns its output (st.shared::cluster after mapa); after a
-//     cluster barrier every CTA writes its S outputs (and map entries) to k2
-//     as one contiguous run.
-// Phase steps (R17): the product of the step values along the forward walk
-// equals the backward walk's (phase steps do not move the address).  Every
-// entry carries its own d, so the bytes do not depend on the atomics' order.
-std::string bucket_source(const uint32_t* w, int n, int M, int elem, int C, int logS, bool with_src,
-                          int w1) {
-  std::string s = kPrelude;
-  char buf[320];
-  const int logBk = logS + __builtin_ctz((unsigned)C);
-  std::snprintf(buf, sizeof buf,
-                "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_LOGBK %d\n#define QSIM_NB %d\n"
-                "#define QSIM_LOGS %d\n#define QSIM_C %d\n#define QSIM_SRC %d\n#define QSIM_W1 %d\n",
-                elem == 8 ? "uint2" : "uint4", M, logBk, 1 << (M - logBk), logS, C, with_src ? 1 : 0, w1);
-  s += buf;
-  s += R"(
-#define QSIM_TILE (QSIM_W1 * 1024u)
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
-extern "C" __global__ void __launch_bounds__(QSIM_W1 * 32)
-qsim_bucket_pass1(const QSIM_T* __restrict__ k1, QSIM_T* __restrict__ bval, u32* __restrict__ bidx,
-                  u32* __restrict__ bsrc, u32* __restrict__ cursor) {
-  extern __shared__ __align__(16) unsigned char bsm[];
-  QSIM_T* sval = reinterpret_cast<QSIM_T*>(bsm);                 // [TILE] values, bucket-sorted
-  u32* sidx = reinterpret_cast<u32*>(sval + QSIM_TILE);          // [TILE] their outputs d
-#if QSIM_SRC
-  u32* ssrc = sidx + QSIM_TILE;                                  // [TILE] their sources s
-  u32* wcnt = ssrc + QSIM_TILE;                                  // [W1][NB] counts per warp
-#else
-  u32* wcnt = sidx + QSIM_TILE;
-#endif
-  u32* start = wcnt + QSIM_W1 * QSIM_NB;                         // [NB] bucket offsets in the tile
-  u32* gbase = start + QSIM_NB;                                  // [NB] run offsets in the scratch
-  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const u64 ntiles = (1ull << QSIM_M) / QSIM_TILE;
-  for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    for (u32 x = threadIdx.x; x < QSIM_W1 * QSIM_NB; x += blockDim.x) wcnt[x] = 0u;
-    __syncthreads();
-    const u64 base = tile * QSIM_TILE + (u64)warp * 1024u;   // this warp's 1024 sources
-    // the 32 values first (coalesced; they arrive while the walk runs)
-    QSIM_T v[32];
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) v[l] = __ldcs(k1 + base + 32u * l + lane);
-)";
-  // planes of the sources base + 32 l + lane: lanes on bits 0..4, the
-  // thread's 32 entries on bits 5..9, the rest constant in the warp
-  const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-  for (int b = 0; b < 32; ++b) {
-    if (b >= M)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = 0u;\n", b);
-    else if (b < 5)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-    else if (b < 10)
-      std::snprintf(buf, sizeof buf, "    u32 p%d = %s;\n", b, pat[b - 5]);
-    else
-      std::snprintf(buf, sizeof buf, "    u32 p%d = ((base >> %d) & 1ull) ? 0xffffffffu : 0u;\n", b, b);
-    s += buf;
-  }
-  s += "    u32 sg = 0u;\n";
-  {  // forward walk: Step 1 first (the list reversed into the last -> first emitter)
-    std::vector<uint32_t> rev(w, w + n);
-    std::reverse(rev.begin(), rev.end());
-    s += walk_code(rev.data(), n, M);
-  }
-  s += "    u32 a[32] = {";
-  for (int b = 0; b < 32; ++b) {
-    std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-    s += buf;
-  }
-  s += R"(
-    QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)
-    QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)
-    // a[l] = d = g(base + 32 l + lane); its rank among this warp's entries of its bucket
-    u32 slot[16];   // two 16-bit ranks per word (< 1024)
-    u32* const wc = wcnt + warp * QSIM_NB;
-    _Pragma("unroll") for (int l = 0; l < 32; l += 2)
-      slot[l >> 1] = atomicAdd(&wc[a[l] >> QSIM_LOGBK], 1u) |
-                     (atomicAdd(&wc[a[l + 1] >> QSIM_LOGBK], 1u) << 16);
-    __syncthreads();
-    // per bucket: warp offsets, tile total; then offsets over the buckets and the scratch runs
-    for (u32 b = threadIdx.x; b < QSIM_NB; b += blockDim.x) {
-      u32 run = 0u;
-      _Pragma("unroll") for (int v = 0; v < QSIM_W1; ++v) {
-        const u32 c = wcnt[v * QSIM_NB + b];
-        wcnt[v * QSIM_NB + b] = run;
-        run += c;
-      }
-      gbase[b] = run;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      u32 carry = 0u;
-      for (u32 b0 = 0; b0 < QSIM_NB; b0 += 32u) {
-        const u32 b = b0 + lane;
-        const u32 c = b < QSIM_NB ? gbase[b] : 0u;
-        u32 x = c;
-        _Pragma("unroll") for (int o = 1; o < 32; o <<= 1) {
-          const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-          if (lane >= (u32)o) x += y;
-        }
-        if (b < QSIM_NB) {
-          start[b] = carry + x - c;
-          gbase[b] = c ? atomicAdd(&cursor[b], c) : 0u;
-        }
-        carry += __shfl_sync(0xffffffffu, x, 31);
-      }
-    }
-    __syncthreads();
-    // values to their bucket-sorted slots
-    _Pragma("unroll") for (int l = 0; l < 32; ++l) {
-      const u32 d = a[l], b = d >> QSIM_LOGBK;
-      const u32 pos = start[b] + wc[b] + ((slot[l >> 1] >> (16 * (l & 1))) & 0xffffu);
-      sval[pos] = negate_if(v[l], (sg >> l) & 1u);
-      sidx[pos] = d;
-#if QSIM_SRC
-      ssrc[pos] = (u32)(base + 32u * l + lane);
-#endif
-    }
-    __syncthreads();
-    // runs out: slot pos of bucket b -> scratch b * Bk + gbase[b] + (pos - start[b])
-    for (u32 pos = threadIdx.x; pos < QSIM_TILE; pos += blockDim.x) {
-      const u32 d = sidx[pos], b = d >> QSIM_LOGBK;
-      const u64 g = ((u64)b << QSIM_LOGBK) + gbase[b] + (pos - start[b]);
-      stcs(bval + g, sval[pos]);
-      __stcs(bidx + g, d);
-#if QSIM_SRC
-      __stcs(bsrc + g, ssrc[pos]);
-#endif
-    }
-    __syncthreads();
-  }
-}
-
-// pass 2 (persistent): cluster c takes buckets c, c + nclusters, ...; each
-// bucket's Bk = C * S outputs live in the cluster's shared memory (S per
-// CTA).  Per bucket: scatter the entries already in registers into the
-// owners' shared memory (mapa + st.shared::cluster), cluster barrier, issue
-// the NEXT bucket's loads, write this CTA's S outputs as one run while they
-// are in flight, cluster barrier.
-#define QSIM_P2T 1024u
-#define QSIM_E2 ((1u << QSIM_LOGBK) / (QSIM_C * QSIM_P2T))   // entries per thread and bucket
-extern "C" __global__ void __cluster_dims__(QSIM_C, 1, 1) __launch_bounds__(1024, 1)
-qsim_bucket_pass2(const QSIM_T* __restrict__ bval, const u32* __restrict__ bidx,
-                  const u32* __restrict__ bsrc, QSIM_T* __restrict__ k2, u32* __restrict__ perm_out) {
-  extern __shared__ __align__(16) unsigned char bsm[];
-  QSIM_T* slv = reinterpret_cast<QSIM_T*>(bsm);                  // [S] this CTA's outputs
-#if QSIM_SRC
-  u32* slp = reinterpret_cast<u32*>(slv + (1u << QSIM_LOGS));    // [S] their map entries
-#endif
-  u32 rank, cid, ncl;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(cid));
-  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(ncl));
-  const u32 S = 1u << QSIM_LOGS;
-  const u32 v_sh = smem_u32(slv);
-#if QSIM_SRC
-  const u32 p_sh = smem_u32(slp);
-#endif
-  const u32 me = rank * QSIM_P2T + threadIdx.x;      // this thread's entries: me + j * C * P2T
-  QSIM_T v[QSIM_E2];
-  u32 d[QSIM_E2];
-#if QSIM_SRC
-  u32 sr[QSIM_E2];
-#endif
-  auto load = [&](u32 b) {
-    const u64 base = (u64)b << QSIM_LOGBK;
-    _Pragma("unroll") for (u32 j = 0; j < QSIM_E2; ++j) {
-      const u64 i = base + me + (u64)j * (QSIM_C * QSIM_P2T);
-      v[j] = __ldcs(bval + i);
-      d[j] = __ldcs(bidx + i);
-#if QSIM_SRC
-      sr[j] = __ldcs(bsrc + i);
-#endif
-    }
-  };
-  if (cid < QSIM_NB) load(cid);
-  for (u32 b = cid; b < QSIM_NB; b += ncl) {
-    const u64 base = (u64)b << QSIM_LOGBK;
-    _Pragma("unroll") for (u32 j = 0; j < QSIM_E2; ++j) {
-      const u32 rel = (u32)(d[j] - base), own = rel >> QSIM_LOGS, off = rel & (S - 1u);
-      u32 ra;   // the owner CTA's slot in the cluster's shared-memory window
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(v_sh + off * (u32)sizeof(QSIM_T)), "r"(own));
-#if QSIM_SRC
-      u32 rpa;
-      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rpa) : "r"(p_sh + off * 4u), "r"(own));
-      asm volatile("st.shared::cluster.u32 [%0], %1;" :: "r"(rpa), "r"(sr[j]) : "memory");
-#endif
-      if (sizeof(QSIM_T) == 16) {
-        const uint4 x = *reinterpret_cast<const uint4*>(&v[j]);
-        asm volatile("st.shared::cluster.v4.u32 [%0], {%1, %2, %3, %4};"
-                     :: "r"(ra), "r"(x.x), "r"(x.y), "r"(x.z), "r"(x.w) : "memory");
-      } else {
-        const uint2 x = *reinterpret_cast<const uint2*>(&v[j]);
-        asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};"
-                     :: "r"(ra), "r"(x.x), "r"(x.y) : "memory");
-      }
-    }
-    if (b + ncl < QSIM_NB) load(b + ncl);            // in flight during the barrier and the write-out
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    const u64 o0 = base + (u64)rank * S;
-    for (u32 j = threadIdx.x; j < S; j += QSIM_P2T) {
-      stcs(k2 + o0 + j, slv[j]);
-#if QSIM_SRC
-      __stcs(perm_out + o0 + j, slp[j]);
-#endif
-    }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-  }
-}
-)";
-  return s;
-}
-
 struct Entry {
   std::vector<uint32_t> words;
   int M;
@@ -1353,133 +1116,6 @@ int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* 
     return -1;
   }
   return 0;
-}
-
-// Two-pass cluster-bucketed gather (bucket_source).  Tries clusters of 16
-// CTAs (non-portable size), then 8.  scratch holds bval (2^M elem bytes),
-// bidx (2^M u32), bsrc (2^M u32 when perm_out) and NB cursors; laid out by
-// the caller.  Returns 0 or -1 with err.
-int bucket_geometry(int M, int elem, bool with_src, int C, int* logS) {
-  // S outputs per CTA: its values (and map entries) in at most 160 KB of smem
-  const int per = elem + (with_src ? 4 : 0);
-  int ls = 0;
-  while ((per << (ls + 1)) <= (160 << 10)) ++ls;
-  *logS = ls;
-  const int logBk = ls + __builtin_ctz((unsigned)C);
-  return M - logBk;  // log2 of the bucket count
-}
-
-int jit_bucketed(const uint32_t* words, int n, int M, int elem, const void* k1, void* k2,
-                 uint32_t* perm_out, void* bval, uint32_t* bidx, uint32_t* bsrc, uint32_t* cursor,
-                 int sms, cudaStream_t st, std::string& err) {
-  const bool with_src = perm_out != nullptr;
-  for (int C : {16, 8}) {
-    int logS = 0;
-    const int lnb = bucket_geometry(M, elem, with_src, C, &logS);
-    if (lnb < 0 || lnb > 11) {
-      err = "bucket count out of range";
-      return -1;
-    }
-    const int NB = 1 << lnb;
-    const int w1 = 4;  // pass-1 tile: 4 warps x 1024 sources (2+ CTAs per SM)
-    const int smem1 = 1024 * w1 * (elem + 4 + (with_src ? 4 : 0)) + 4 * (w1 * NB + 2 * NB);
-    const int smem2 = (1 << logS) * (elem + (with_src ? 4 : 0));
-    CUfunction f1 = nullptr, f2 = nullptr;
-    {
-      std::lock_guard<std::mutex> lk(g_mu);
-      init_locked();
-      if (!(g_nvrtc.ok && g_drv.ok)) {
-        err = g_status;
-        return -1;
-      }
-      std::vector<uint32_t> keyw(words, words + n);
-      keyw.push_back((uint32_t)elem);
-      keyw.push_back((uint32_t)C);
-      keyw.push_back((uint32_t)logS);
-      keyw.push_back(with_src ? 1u : 0u);
-      const uint64_t k1d = 0x62756b31ull, k2d = 0x62756b32ull;
-      const uint64_t h1 = fnv(keyw.data(), (int)keyw.size(), k1d), h2 = fnv(keyw.data(), (int)keyw.size(), k2d);
-      for (const Entry& e : g_cache[h1])
-        if (e.M == M && e.words == keyw) f1 = e.fn;
-      for (const Entry& e : g_cache[h2])
-        if (e.M == M && e.words == keyw) f2 = e.fn;
-      if (!f1 || !f2) {
-        const std::string src = bucket_source(words, n, M, elem, C, logS, with_src, w1);
-        f1 = get_kernel_locked(k1d, keyw, M, src, "qsim_bucket_pass1", err);
-        if (!f1) return -1;
-        f2 = get_kernel_locked(k2d, keyw, M, src, "qsim_bucket_pass2", err);
-        if (!f2) return -1;
-        if (g_drv.setattr(f1, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem1) != CUDA_SUCCESS ||
-            g_drv.setattr(f2, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem2) != CUDA_SUCCESS) {
-          err = "cuFuncSetAttribute(max dynamic smem) failed";
-          return -1;
-        }
-        g_drv.setattr(f1, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
-        g_drv.setattr(f2, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100);
-        if (C > 8) g_drv.setattr(f2, CU_FUNC_ATTRIBUTE_NON_PORTABLE_CLUSTER_SIZE_ALLOWED, 1);
-      }
-    }
-    if (cudaMemsetAsync(cursor, 0, sizeof(uint32_t) * NB, st) != cudaSuccess) {
-      err = "bucket cursor reset failed";
-      return -1;
-    }
-    const uint64_t ntiles = (1ull << M) / (1024ull * w1);
-    int occ1 = 0;  // resident pass-1 CTAs per SM
-    if (!g_drv.occ_blocks || g_drv.occ_blocks(&occ1, f1, 32 * w1, (size_t)smem1) != CUDA_SUCCESS || occ1 < 1)
-      occ1 = 1;
-    const uint64_t b1 = std::min<uint64_t>(ntiles, (uint64_t)sms * occ1);
-    void* a1[] = {const_cast<void**>(&k1), &bval, &bidx, &bsrc, &cursor};
-    if (g_drv.launch(f1, (unsigned)b1, 1, 1, 32 * w1, 1, 1, (unsigned)smem1, (CUstream)st, a1, nullptr) !=
-        CUDA_SUCCESS) {
-      err = "cuLaunchKernel (bucket pass 1) failed";
-      return -1;
-    }
-    // pass 2: as many clusters as can be resident at once (persistent), else sms / C
-    int ncl = 0;
-    if (g_drv.occ_clusters) {
-      CUlaunchConfig cfg;
-      std::memset(&cfg, 0, sizeof cfg);
-      CUlaunchAttribute at;
-      std::memset(&at, 0, sizeof at);
-      at.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-      at.value.clusterDim.x = (unsigned)C;
-      at.value.clusterDim.y = at.value.clusterDim.z = 1;
-      cfg.gridDimX = (unsigned)(C * std::max(1, sms / C));
-      cfg.gridDimY = cfg.gridDimZ = 1;
-      cfg.blockDimX = 1024;
-      cfg.blockDimY = cfg.blockDimZ = 1;
-      cfg.sharedMemBytes = (unsigned)smem2;
-      cfg.hStream = (CUstream)st;
-      cfg.attrs = &at;
-      cfg.numAttrs = 1;
-      if (g_drv.occ_clusters(&ncl, f2, &cfg) != CUDA_SUCCESS) ncl = 0;
-    }
-    if (ncl < 1) ncl = std::max(1, sms / C);
-    ncl = std::min(ncl, NB);
-    void* a2[] = {&bval, &bidx, &bsrc, &k2, &perm_out};
-    if (g_drv.launch(f2, (unsigned)(ncl * C), 1, 1, 1024, 1, 1, (unsigned)smem2, (CUstream)st, a2,
-                     nullptr) == CUDA_SUCCESS)
-      return 0;
-    err = "cuLaunchKernel (bucket pass 2, cluster " + std::to_string(C) + ") failed";
-    // pass 1 ran: retry only pass 2's cluster size by redoing both with C = 8
-    if (C == 8) return -1;
-  }
-  return -1;
-}
-
-int jit_check_compile_bucketed(const uint32_t* words, int n, int M, int elem, bool with_src,
-                               std::string& err) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  init_locked();
-  if (!g_nvrtc.ok) {
-    err = g_status;
-    return -1;
-  }
-  int logS = 0;
-  bucket_geometry(M, elem, with_src, 16, &logS);
-  std::vector<char> cubin;
-  return compile_cubin_locked(bucket_source(words, n, M, elem, 16, logS, with_src, 4), cubin, err) ? 0
-                                                                                                     : -1;
 }
 
 int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T, std::string& err) {

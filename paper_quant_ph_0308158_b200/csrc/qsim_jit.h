@@ -55,14 +55,4 @@ int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& 
 int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,
               uint32_t* perm_out, int sms, cudaStream_t st, std::string& err);
 int jit_check_compile_local(const uint32_t* words, int n, int M, int elem, int T, std::string& err);
-// Well-mixed circuits: two passes through destination buckets held in a
-// thread-block cluster's distributed shared memory (bucket_source).
-// bucket_geometry returns log2 of the bucket count (and log2 of the outputs
-// per CTA) for a cluster of C CTAs.  jit_bucketed returns 0 or -1 with err.
-int bucket_geometry(int M, int elem, bool with_src, int C, int* logS);
-int jit_bucketed(const uint32_t* words, int n, int M, int elem, const void* k1, void* k2,
-                 uint32_t* perm_out, void* bval, uint32_t* bidx, uint32_t* bsrc, uint32_t* cursor,
-                 int sms, cudaStream_t st, std::string& err);
-int jit_check_compile_bucketed(const uint32_t* words, int n, int M, int elem, bool with_src,
-                               std::string& err);
 }  // namespace qsim

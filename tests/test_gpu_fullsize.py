@@ -10,9 +10,8 @@ CPU oracle (perm as uint32, k2 as raw entry bytes; readings R14/R15):
 * the CUDA path runs through the C ABI: the plain calls of the north star
   (qsim_build_map, qsim_apply_map, qsim_run_fused), the planned calls with the
   default plan (qsim_plan_create) AND with the plan qsim_plan_tune keeps (the
-  kernel instance bench.py times), the two-pass cluster-bucketed call
-  (qsim_run_bucketed, where the bucket count allows it: cfg3) and the
-  end-to-end host-buffer call (qsim_run_host);
+  kernel instance bench.py times), and the end-to-end host-buffer call
+  (qsim_run_host);
 * the oracle's perm and k2 are copied to the device once and each mode's
   output is compared with them byte for byte (torch.equal on 512 MiB
   chunks); a failure names the mode and the first mismatching output index.
@@ -136,20 +135,6 @@ def _run_config(q, name):
     check_k2("qsim_run_fused_planned " + label)
     q.apply_map_planned(tuned, perm, k1, k2, ws)
     check_k2("qsim_apply_map_planned " + label)
-    # two passes through cluster-held destination buckets (where the bucket count allows)
-    for wp in (False, True):
-        nb = q.bucket_scratch_bytes(M, cfg.dtype, wp)
-        if nb == 0:
-            continue
-        scratch = torch.empty(nb, dtype=torch.uint8, device=DEV)
-        if wp:
-            perm.fill_(-1)
-        q.run_bucketed(gates, M, k1, k2, scratch, perm_out=perm if wp else None, dtype=cfg.dtype)
-        if wp:
-            check_perm("qsim_run_bucketed (with map)")
-        check_k2(f"qsim_run_bucketed (with map: {wp})")
-        del scratch
-        torch.cuda.empty_cache()
     # end to end from host buffers (the e2e leg of bench.py)
     k2_host = np.empty_like(k1_host)
     for mode in (q.MATERIALISED, q.FUSED):
