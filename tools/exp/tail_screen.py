@@ -28,7 +28,7 @@ def t_of(s, reps):
 t_of(cur, 2)
 print("cur", t_of(cur, 3))
 res = []
-frm = 13
+frm = int(sys.argv[2]) if len(sys.argv) > 2 else 13
 for at in range(frm, M):
     for pos in range(frm, frm + 10):
         if pos == at:
