@@ -1,0 +1,200 @@
+// first_touch.cu -- experiment (NOT the product path).  Question: does the
+// cfg5 gather get faster when the FIRST reader of every 128-byte k1 line (in
+// the plan's counter order) requests the whole line in one warp instruction,
+// so that the line costs one DRAM access instead of ~1.84 sector accesses?
+//
+// Offline (untimed) the "first reader" flags are computed from the stored
+// map: inv = perm^-1; for counter c (output o = sigma(c), source s = perm[o])
+// flag c iff c is the smallest counter among the 16 readers of s's line
+// (mode 0) or its chunk is the smallest chunk among them (mode 1).  The
+// timed kernel is the planned apply (qsim_jit_apply's traversal: lanes =
+// counter bits 0..4, entries = 5..9, tiles = 10..14, chunks from an in-order
+// ticket) with, optionally, warp-cooperative whole-line loads (8 lanes x 16 B
+// per line) for the flagged entries issued before the tile's 32 gathers.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -shared -Xcompiler -fPIC \
+//        -o libft.so first_touch.cu
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+
+struct Tabs { u32 fwd[4][256]; u32 inv[4][256]; };  // sigma (counter->output), sigma^-1
+
+__device__ __forceinline__ u32 lut(const u32 (*t)[256], u32 x) {
+  return t[0][x & 255] | t[1][(x >> 8) & 255] | t[2][(x >> 16) & 255] | t[3][x >> 24];
+}
+
+__global__ void k_inv(const u32* __restrict__ perm, u32* __restrict__ inv, u64 n) {
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x)
+    inv[perm[i]] = (u32)i;
+}
+
+__global__ void k_flags(const u32* __restrict__ perm, const u32* __restrict__ inv, const Tabs* __restrict__ gt,
+                        u32* __restrict__ bitmap, u64 n, int mode, u32 chunk_log2, u64* count) {
+  __shared__ u32 tf[4][256], ti[4][256];
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
+    tf[x >> 8][x & 255] = gt->fwd[x >> 8][x & 255];
+    ti[x >> 8][x & 255] = gt->inv[x >> 8][x & 255];
+  }
+  __syncthreads();
+  for (u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x; c < n; c += (u64)gridDim.x * blockDim.x) {
+    const u32 o = lut(tf, (u32)c), s = perm[o], L = s & ~15u;
+    u32 mn = 0xffffffffu;
+    for (u32 r = 0; r < 16; ++r) {
+      const u32 cr = lut(ti, inv[L + r]);
+      mn = cr < mn ? cr : mn;
+    }
+    const bool f = mode == 0 ? (u32)c == mn : ((u32)c >> chunk_log2) == (mn >> chunk_log2);
+    const u32 w = __ballot_sync(0xffffffffu, f);
+    if ((threadIdx.x & 31) == 0) {
+      bitmap[c >> 5] = w;
+      atomicAdd(count, (u64)__popc(w));
+    }
+  }
+}
+
+__device__ __forceinline__ uint2 ldg2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void stcs2(uint2* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+// asynchronous 16-byte copy into a per-lane dummy shared-memory slot: the
+// request goes out without a register dependency (the warp does not stall)
+template <int CM>
+__device__ __forceinline__ void ld_line16(u32 dst, const uint4* p) {
+  if (CM == 0)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(p) : "memory");
+}
+
+// MODE 0: plain planned apply; 1: flag words read, no extra loads (control);
+// 2: cooperative whole-line .ca loads for flagged entries; 3: the same .cg;
+// 4: prefetch.global.L2 of the flagged entry's line by the flagged lane only
+template <int MODE>
+__global__ void __launch_bounds__(256) k_gather(u64 N, u32 chunk_log2, u64* ticket, const uint2* __restrict__ k1,
+                                                uint2* __restrict__ k2, const u32* __restrict__ perm,
+                                                const u32* __restrict__ bitmap, const Tabs* __restrict__ gt,
+                                                u32* sink) {
+  __shared__ u32 tab[4][256];
+  __shared__ u64 s_chunk;
+  __shared__ __align__(16) uint4 dummy[256];
+  __shared__ u32 s_list[8][1024];
+  const u32 dslot = (u32)__cvta_generic_to_shared(&dummy[threadIdx.x]);
+  for (int x = threadIdx.x; x < 1024; x += blockDim.x) tab[x >> 8][x & 255] = gt->fwd[x >> 8][x & 255];
+  __syncthreads();
+  const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  u32 lt[32];
+#pragma unroll
+  for (int l = 0; l < 32; ++l) lt[l] = tab[0][(l << 5) & 255] | tab[1][(l << 5) >> 8];
+  const u32 lo = tab[0][lane];
+  const u64 nchunks = N >> chunk_log2;
+  const u32 tiles = 1u << (chunk_log2 - 10);
+  u32 acc = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
+    __syncthreads();
+    const u64 ch = s_chunk;
+    if (ch >= nchunks) break;
+    for (u32 tt = warp; tt < tiles; tt += 8u) {
+      const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
+      const u32 ob = lut(tab, (u32)c);
+      u32 a[32];
+#pragma unroll
+      for (int l = 0; l < 32; ++l) a[l] = __ldcs(perm + (ob ^ lt[l] ^ lo));
+      if (MODE >= 1 && MODE <= 4) {
+        const u32 fw = bitmap[(c >> 5) + lane];
+        if (MODE == 1) acc ^= fw;
+#pragma unroll
+        if (MODE == 4) {
+#pragma unroll
+          for (int l = 0; l < 32; ++l) {
+            const bool f = (__shfl_sync(0xffffffffu, fw, l) >> lane) & 1u;
+            if (f) asm volatile("prefetch.global.L2 [%0];" ::"l"(k1 + (a[l] & ~15u)) : "memory");
+          }
+        } else if (MODE >= 2) {
+          // compact the tile's flagged sources (about 64 of 1024) into a
+          // per-warp list, then 8 lanes x 16 B per line, 4 lines per instruction
+          u32* const lst = s_list[warp];
+          u32 fx = 0;
+#pragma unroll
+          for (int l = 0; l < 32; ++l) fx |= ((__shfl_sync(0xffffffffu, fw, l) >> lane) & 1u) << l;
+          const u32 cnt = __popc(fx);
+          u32 off = cnt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, off, d);
+            if (lane >= (u32)d) off += y;
+          }
+          const u32 total = __shfl_sync(0xffffffffu, off, 31);
+          off -= cnt;
+#pragma unroll
+          for (int l = 0; l < 32; ++l)
+            if ((fx >> l) & 1u) lst[off++] = a[l] & ~15u;
+          __syncwarp();
+          for (u32 k = lane >> 3; k < total; k += 4)
+            ld_line16<MODE - 2>(dslot, reinterpret_cast<const uint4*>(k1 + lst[k]) + (lane & 7));
+          __syncwarp();
+        }
+      }
+      if (MODE == 5) {  // perm read and k2 written, no k1 gathers
+#pragma unroll
+        for (int l = 0; l < 32; ++l) stcs2(k2 + (ob ^ lt[l] ^ lo), make_uint2(a[l], 0u));
+      } else if (MODE == 6) {  // perm read and k1 gathered, no k2 stores
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {
+          uint2 v[16];
+#pragma unroll
+          for (int l = 0; l < 16; ++l) v[l] = ldg2(k1 + a[h + l]);
+#pragma unroll
+          for (int l = 0; l < 16; ++l) acc ^= v[l].x ^ v[l].y;
+        }
+      } else {
+#pragma unroll
+      for (int h = 0; h < 32; h += 16) {
+        uint2 v[16];
+#pragma unroll
+        for (int l = 0; l < 16; ++l) v[l] = ldg2(k1 + a[h + l]);
+#pragma unroll
+        for (int l = 0; l < 16; ++l) stcs2(k2 + (ob ^ lt[h + l] ^ lo), v[l]);
+      }
+      }
+      if (MODE == 2 || MODE == 3) asm volatile("cp.async.wait_all;" ::: "memory");
+    }
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
+extern "C" {
+int ft_inv(const u32* perm, u32* inv, u64 n, cudaStream_t st) {
+  k_inv<<<148 * 8, 256, 0, st>>>(perm, inv, n);
+  return (int)cudaGetLastError();
+}
+int ft_flags(const u32* perm, const u32* inv, const Tabs* t, u32* bitmap, u64 n, int mode, u32 chunk_log2,
+             u64* count, cudaStream_t st) {
+  k_flags<<<148 * 8, 256, 0, st>>>(perm, inv, t, bitmap, n, mode, chunk_log2, count);
+  return (int)cudaGetLastError();
+}
+int ft_gather(int mode, u64 N, u32 chunk_log2, u64* ticket, const void* k1, void* k2, const u32* perm,
+              const u32* bitmap, const Tabs* t, u32* sink, int ctas, cudaStream_t st) {
+  cudaMemsetAsync(ticket, 0, 8, st);
+  const uint2* a = (const uint2*)k1;
+  uint2* b = (uint2*)k2;
+  switch (mode) {
+    case 0: k_gather<0><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 1: k_gather<1><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 2: k_gather<2><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 3: k_gather<3><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 4: k_gather<4><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 5: k_gather<5><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 6: k_gather<6><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    default: return -1;
+  }
+  return (int)cudaGetLastError();
+}
+}
