@@ -531,33 +531,6 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   return s;
 }
 
-// CTA-staged stores of the on-the-fly input (complex64): the 8 warps of a
-// CTA hold 8192 outputs -- lanes on output bits 0..4, the in-thread bits J,
-// and as warp bits the 3 lowest remaining bits W.  When those 13 bits hold
-// 0..r-1 with r >= 7, the CTA's outputs are 2^(13-r) runs of 2^r consecutive
-// entries: the values go to shared memory and one thread writes each run
-// with a TMA bulk store (cp.async.bulk, 1-64 KB), overlapped with the next
-// tile's compute.  Returns the mode (0: direct stores; 1: one staging
-// buffer; 2: two) and fills W and r.
-int kron_stage(const uint8_t* J, int L, int M, int elem, uint8_t* W, int* runb) {
-  *runb = 0;
-  const char* e = std::getenv("QSIM_KRON_STAGE");
-  const int mode = e ? std::atoi(e) : 1;
-  if (mode <= 0 || elem != 8 || L < 13) return 0;
-  uint64_t set = 31ull;
-  for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
-  int k = 0;
-  for (int b = 5; b < M && k < 3; ++b)
-    if (!((set >> b) & 1ull)) W[k++] = (uint8_t)b;
-  if (k < 3) return 0;
-  for (int i = 0; i < 3; ++i) set |= 1ull << W[i];
-  int r = 0;
-  while (r < 13 && ((set >> r) & 1ull)) ++r;
-  if (r < 7) return 0;
-  *runb = r;
-  return mode >= 2 ? 2 : 1;
-}
-
 // Fused walk with the input generated on the fly (Appendix 1):
 // k2_out[out - start] = k1(perm(out)) from tables of qubit products, ng
 // groups of gb table positions (same arithmetic and order as
@@ -586,43 +559,6 @@ std::string kron_source(const uint32_t* w, int n, int M, int elem, int gb, int n
                 ng);
   s += buf;
   s += thread_defs(J, L);
-  uint8_t W[3] = {0, 0, 0};
-  int runb = 0;
-  const int stage = kron_stage(J, L, M, elem, W, &runb);
-  std::snprintf(buf, sizeof buf, "#define QSIM_STAGE %d\n", stage);
-  s += buf;
-  if (stage) {
-    // compact index of each staged bit (its rank among the CTA's 13 bits)
-    uint64_t set = 31ull;
-    for (int k = 0; k < 5; ++k) set |= 1ull << J[k];
-    for (int k = 0; k < 3; ++k) set |= 1ull << W[k];
-    auto rank = [&](int b) { return __builtin_popcountll(set & ((1ull << b) - 1)); };
-    std::snprintf(buf, sizeof buf,
-                  "#define QSIM_CIDX(l) (((l) & 1 ? %du : 0u) | ((l) & 2 ? %du : 0u) | ((l) & 4 ? %du : 0u) | "
-                  "((l) & 8 ? %du : 0u) | ((l) & 16 ? %du : 0u))\n",
-                  1 << rank(J[0]), 1 << rank(J[1]), 1 << rank(J[2]), 1 << rank(J[3]), 1 << rank(J[4]));
-    s += buf;
-    std::snprintf(buf, sizeof buf,
-                  "#define QSIM_WIDX(w) (((w) & 1 ? %du : 0u) | ((w) & 2 ? %du : 0u) | ((w) & 4 ? %du : 0u))\n"
-                  "#define QSIM_WMASK %lluull\n#define QSIM_RUNB %d\n#define QSIM_NRUNS %d\n",
-                  1 << rank(W[0]), 1 << rank(W[1]), 1 << rank(W[2]),
-                  (unsigned long long)((1ull << W[0]) | (1ull << W[1]) | (1ull << W[2])), runb,
-                  1 << (13 - runb));
-    s += buf;
-    // output offset of each run: the staged bits ranked >= r
-    std::vector<int> hi;
-    for (int b = 0; b < 64; ++b)
-      if (((set >> b) & 1ull) && rank(b) >= runb) hi.push_back(b);
-    const int nruns = 1 << (13 - runb);
-    s += "__constant__ u64 kRunOff[" + std::to_string(nruns) + "] = {";
-    for (int r = 0; r < nruns; ++r) {
-      uint64_t off = 0;
-      for (size_t i = 0; i < hi.size(); ++i)
-        if ((r >> i) & 1) off |= 1ull << hi[i];
-      std::snprintf(buf, sizeof buf, "%lluull%s", (unsigned long long)off, r < nruns - 1 ? ", " : "};\n");
-      s += buf;
-    }
-  }
   s += f32 ? R"(
 __device__ __forceinline__ C cmul(C a, C b) {
   return make_float2(__fmaf_rn(a.x, b.x, -__fmul_rn(a.y, b.y)),
@@ -654,51 +590,13 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
   }
   __syncthreads();
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-#if QSIM_STAGE
-  C* const stg = T + (QSIM_NG << QSIM_GB);   // [QSIM_STAGE][8192] the CTA's outputs, address order
-  const u32 widx = QSIM_WIDX(warp);
-  u32 it = 0u;
-#endif
   for (u64 tile = tb + (u64)blockIdx.x * 8u + warp; tile < te; tile += (u64)gridDim.x * 8u) {
 )";
   const int np = wide ? 64 : 32;
   s += thread_planes(M, J, np);
   s += "    u32 sg = 0u;\n";
   s += walk_code(w, n, M);
-  // a whole block (CTA-uniform: the CTA's 8 tiles lie in one 2^L block) with
-  // 16-byte aligned runs goes through the staging buffer
-  s += R"(
-#if QSIM_STAGE
-#if QSIM_STAGE == 1
-    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-    __syncthreads();   // the buffer's previous bulk stores have read it
-#endif
-    C* const sb = stg + (QSIM_STAGE == 2 ? ((it & 1u) << 13) : 0u);
-    const bool stg_ok = full && (start & 1ull) == 0ull;
-#else
-    const bool stg_ok = false;
-#endif
-)";
   auto P = [&](int k) { return std::string("p") + std::to_string(pos[k]); };
-  // the 32 values of a thread: staged, stored directly (whole blocks) or
-  // stored inside the range
-  auto stores = [&](const std::string& value, const char* ind) {
-    const std::string i(ind);
-    std::string e;
-    if (stage) {
-      e += i + "if (stg_ok) {\n";
-      e += i + "  _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) {\n";
-      e += i + "    " + value + "\n";
-      e += i + "    sb[lane | QSIM_CIDX(l) | widx] = rv;\n";
-      e += i + "  }\n";
-      e += i + "} else {\n";
-      e += thread_stores("k2", value.c_str(), (i + "  ").c_str());
-      e += i + "}\n";
-      return e;
-    }
-    return thread_stores("k2", value.c_str(), ind);
-  };
-  bool fast_open = false;
 
   if (nv > 0 && ng >= 2) {
     s += "    u32 un = 0u;\n";
@@ -730,9 +628,8 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     }
     s += "      QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
     s += "      QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += stores("const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
-    s += "    } else {\n";
-    fast_open = true;
+    s += thread_stores("k2", "const C rv = negate_if(cmul(cc, T[a[l] | i0]), (sg >> l) & 1u);", "      ");
+    s += "      continue;\n    }\n";
   }
   for (int h = 0; h < (wide ? 2 : 1); ++h) {
     std::snprintf(buf, sizeof buf, "    u32 a%d[32] = {", h);
@@ -759,32 +656,8 @@ qsim_jit_kron(u64 start, u64 end, u64 tb, u64 te, Qubits q, C* __restrict__ k2) 
     gen += buf;
   }
   gen += " const C rv = negate_if(r, (sg >> l) & 1u);";
-  s += stores(gen, "    ");
-  if (fast_open) s += "    }\n";
-  if (stage)  // the CTA's staged outputs to k2: one TMA bulk store per run
-    s += R"(
-    if (stg_ok) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#if QSIM_STAGE == 2
-      if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#endif
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const u64 cbase = base & ~QSIM_WMASK;
-        for (u32 r = 0; r < QSIM_NRUNS; ++r) {
-          const u64 ga = (u64)(k2 + (cbase + kRunOff[r] - start));
-          const u32 sa = (u32)__cvta_generic_to_shared(sb + (r << QSIM_RUNB));
-          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                       :: "l"(ga), "r"(sa), "r"((u32)(sizeof(C) << QSIM_RUNB)) : "memory");
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      ++it;
-    }
-)";
-  s += "  }\n";
-  if (stage) s += "  if (threadIdx.x == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n";
-  s += "}\n";
+  s += thread_stores("k2", gen.c_str(), "    ");
+  s += "  }\n}\n";
   return s;
 }
 
@@ -1114,10 +987,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
              int elem, int gbits, int ngroups, const uint8_t* pos, const uint8_t* J, int L, int nv,
              uint64_t start, uint64_t count, void* k2_out, int sms, cudaStream_t st,
              std::string& err) {
-  uint8_t Wb[3];
-  int runb = 0;
-  const int stage = kron_stage(J, L, M, elem, Wb, &runb);  // + the CTA's staged outputs
-  const int smem = ((ngroups << gbits) + stage * 8192) * (elem == 8 ? 8 : 16);
+  const int smem = (ngroups << gbits) * (elem == 8 ? 8 : 16);
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1127,7 +997,6 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
       return -1;
     }
     std::vector<uint32_t> keyw(words, words + n);
-    keyw.push_back((uint32_t)stage);
     keyw.push_back((uint32_t)elem);
     keyw.push_back((uint32_t)gbits);
     keyw.push_back((uint32_t)ngroups);
@@ -1145,7 +1014,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
       if (!fn) return -1;
       // write-only: shared memory for the tables of several resident CTAs
       // (the gather kernels' 3 % carveout would allow one)
-      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, stage ? 100 : 50);
+      g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 50);
       if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, smem) != CUDA_SUCCESS) {
         err = "cuFuncSetAttribute(max dynamic smem) failed";
         return -1;
