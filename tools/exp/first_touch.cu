@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256) k_gather(u64 N, u32 chunk_log2, u64* tick
   __shared__ u32 tab[4][256];
   __shared__ u64 s_chunk;
   __shared__ __align__(16) uint4 dummy[256];
-  __shared__ u32 s_list[8][1024];
+  __shared__ u32 s_list[8][1024];  // modes 2, 3, 7
   const u32 dslot = (u32)__cvta_generic_to_shared(&dummy[threadIdx.x]);
   for (int x = threadIdx.x; x < 1024; x += blockDim.x) tab[x >> 8][x & 255] = gt->fwd[x >> 8][x & 255];
   __syncthreads();
@@ -154,6 +154,51 @@ __global__ void __launch_bounds__(256) k_gather(u64 N, u32 chunk_log2, u64* tick
 #pragma unroll
           for (int l = 0; l < 16; ++l) acc ^= v[l].x ^ v[l].y;
         }
+      } else if (MODE == 7) {
+        // per half-batch: the half's flagged sources (compacted per warp), then
+        // whole-line plain 16-byte loads (8 lanes per line, 4 lines per
+        // instruction, at most 8 instructions) issued before the half's 16
+        // gathers and consumed after them (no stall before the gathers)
+        u32* const lst = s_list[warp];
+        const u32 fw = bitmap[(c >> 5) + lane];
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {
+          u32 fx = 0;
+#pragma unroll
+          for (int l = 0; l < 16; ++l) fx |= ((__shfl_sync(0xffffffffu, fw, h + l) >> lane) & 1u) << l;
+          const u32 cnt = __popc(fx);
+          u32 off = cnt;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(0xffffffffu, off, d);
+            if (lane >= (u32)d) off += y;
+          }
+          const u32 total = __shfl_sync(0xffffffffu, off, 31);
+          off -= cnt;
+#pragma unroll
+          for (int l = 0; l < 16; ++l)
+            if ((fx >> l) & 1u) lst[off++] = a[h + l] & ~15u;
+          __syncwarp();
+          uint4 cv[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const u32 item = 4u * k + (lane >> 3);
+            if (item < total)
+              asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(cv[k].x), "=r"(cv[k].y), "=r"(cv[k].z), "=r"(cv[k].w)
+                           : "l"(reinterpret_cast<const uint4*>(k1 + lst[item]) + (lane & 7)) : "memory");
+            else
+              cv[k] = make_uint4(0u, 0u, 0u, 0u);
+          }
+          uint2 v[16];
+#pragma unroll
+          for (int l = 0; l < 16; ++l) v[l] = ldg2(k1 + a[h + l]);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc ^= cv[k].x ^ cv[k].w;
+#pragma unroll
+          for (int l = 0; l < 16; ++l) stcs2(k2 + (ob ^ lt[h + l] ^ lo), v[l]);
+          __syncwarp();
+        }
       } else {
 #pragma unroll
       for (int h = 0; h < 32; h += 16) {
@@ -192,6 +237,7 @@ int ft_gather(int mode, u64 N, u32 chunk_log2, u64* ticket, const void* k1, void
     case 3: k_gather<3><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 4: k_gather<4><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 5: k_gather<5><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 7: k_gather<7><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 6: k_gather<6><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     default: return -1;
   }
