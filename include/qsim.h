@@ -244,10 +244,12 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * orders only), then chunks of 2^(c-1) / 2^(c+1) counters for the kept order,
  * then the order of the counter bits above the sector cover (every tail bit
  * at each of the 10 positions next to the cover, best move kept on a >= 0.5 %
- * win, up to 3 rounds; sigma[10..] is a kernel parameter, so no recompiles).
+ * win, up to 3 rounds; sigma[10..] is a kernel parameter, so no recompiles),
+ * then 400 screened random exchanges of two counter positions >= 10 (fixed
+ * seed; a move kept when re-timed >= 0.5 % faster).
  * Each trial runs qsim_map_gather_planned (the first of a variant compiles
  * its kernel), so perm and k2 hold a valid result afterwards; the call
- * synchronises `stream` (cfg5: about 10 s).  plan: in (chunk sizes, residency kept) /
+ * synchronises `stream` (cfg5: about 20 s).  plan: in (chunk sizes, residency kept) /
  * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
  * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit).
  * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */
