@@ -245,8 +245,8 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * then the order of the counter bits above the sector cover (every tail bit
  * at each of the 10 positions next to the cover, best move kept on a >= 0.5 %
  * win, up to 3 rounds; sigma[10..] is a kernel parameter, so no recompiles),
- * then 400 screened random exchanges of two counter positions >= 10 (fixed
- * seed; a move kept when re-timed >= 0.5 % faster).
+ * then exchanges of any two counter positions >= 10 (every pair screened,
+ * the four best re-timed, the best kept on a >= 0.5 % win, up to 2 rounds).
  * Each trial runs qsim_map_gather_planned (the first of a variant compiles
  * its kernel), so perm and k2 hold a valid result afterwards; the call
  * synchronises `stream` (cfg5: about 20 s).  plan: in (chunk sizes, residency kept) /

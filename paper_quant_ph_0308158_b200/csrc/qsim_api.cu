@@ -760,6 +760,18 @@ int plan_validate(const qsim_plan* p) {
 
 bool plan_natural(const qsim_plan* p) { return (p->flags & 1u) || p->M < 10; }
 
+// The NVRTC gather kernels take chunks from the workspace ticket in counter
+// order (an in-order front: k2 / perm written close to their neighbours, k1
+// lines' readers close in time).  A natural-order plan of an L2-resident
+// state (<= 64 MB) gains nothing from it, and resetting the ticket costs a
+// memset per call (cfg2: 14.4 -> 12.3 us per call without it); a
+// natural-order plan of an HBM-resident, well-mixed state keeps it (cfg3:
+// 1.50 ms with the ticket, 1.87 ms round-robin).
+void* ticket_for(const qsim_plan* p, void* workspace) {
+  const uint64_t bytes = (1ull << p->M) * (uint64_t)elem_bytes(p->dtype);
+  return plan_natural(p) && bytes <= (64ull << 20) ? nullptr : workspace;
+}
+
 qsim::SigmaParams plan_params(const qsim_plan* p, void* workspace, bool fused = false) {
   qsim::SigmaParams sp;
   std::memcpy(sp.sigma, p->sigma, 32);
@@ -1149,7 +1161,7 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
     uint64_t blocks = (uint64_t)sm_count() * pp->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
     std::string err;
-    if (qsim::jit_apply(M, pp->sigma, pp->fused_chunk_log2, e, perm, k1, k2, workspace,
+    if (qsim::jit_apply(M, pp->sigma, pp->fused_chunk_log2, e, perm, k1, k2, ticket_for(plan, workspace),
                         (int)blocks, st, err) == 0) {
       ++g_launches;
       g_last_kernel = "qsim_jit_apply";
@@ -1261,7 +1273,8 @@ int fused_planned_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n,
       const qsim_plan nat = natural_view(plan);
       bool jit = false;
       const int launches = g_launches;
-      if (fused_sigma_dispatch(&nat, gates, n, k1, k2, nullptr, workspace, st, &jit) == QSIM_OK && jit)
+      if (fused_sigma_dispatch(&nat, gates, n, k1, k2, nullptr, ticket_for(plan, workspace), st, &jit) ==
+              QSIM_OK && jit)
         return QSIM_OK;
       g_launches = launches;
     }
@@ -1296,7 +1309,7 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
     const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
     bool jit = false;
     int launches = g_launches;
-    rc = fused_sigma_dispatch(pp, gates, n, k1, k2, perm, workspace, st, &jit);
+    rc = fused_sigma_dispatch(pp, gates, n, k1, k2, perm, ticket_for(plan, workspace), st, &jit);
     if (rc == QSIM_OK && jit) return QSIM_OK;
     g_launches = launches;
   }
@@ -1586,8 +1599,8 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
   return QSIM_OK;
 }
 
-// qsim_plan_tune stage 4: random exchanges of two counter positions screened
-constexpr int kTuneSwapScreens = 400;
+// qsim_plan_tune stage 4: rounds of screening every exchange of two counter positions
+constexpr int kTuneSwapRounds = 2;
 
 int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
                    const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
@@ -1746,29 +1759,37 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       cur_t = cand_t;
       cur = cand;
     }
-    // fourth stage: random exchanges of any two counter positions >= 10 (this
-    // also trades the CTA's warp-level cover bits 10..12 against tail bits),
-    // screened with one timed call, a candidate re-timed (best of 3) and kept
-    // on a >= 0.5 % win; a fixed number of screens from a fixed seed.  cfg5:
-    // 19.11 -> 18.81 ms in a 14k-screen experiment whose two accepted moves
-    // came at screens 14 and 293 (tools/exp/tail_climb.py,
+    // fourth stage: exchanges of any two counter positions >= 10 (this also
+    // trades the CTA's warp-level cover bits 10..12 against tail bits): every
+    // pair screened with one timed call, the four best re-timed (best of 3),
+    // the best kept on a >= 0.5 % win; up to 2 rounds.  cfg5: a random-swap
+    // hill climb found 19.11 -> 18.81 ms (tools/exp/tail_climb.py,
     // profiles/r02_tail_climb.txt)
-    uint64_t rs = 0x7a11c1b5ull;
-    const int span = cur.M - 10;
-    for (int s = 0; s < kTuneSwapScreens && rc == QSIM_OK && span >= 2; ++s) {
-      rs = rs * 6364136223846793005ull + 1442695040888963407ull;
-      const int i = 10 + (int)((rs >> 33) % (uint64_t)span);
-      int j = 10 + (int)((rs >> 17) % (uint64_t)(span - 1));
-      if (j >= i) ++j;
-      qsim_plan p = cur;
-      std::swap(p.sigma[i], p.sigma[j]);
-      const float t = time_plan(p, false, 1);
-      if (rc != QSIM_OK || !(t < cur_t * 0.995f)) continue;
-      const float t3 = time_plan(p, false, 3);
-      if (rc == QSIM_OK && t3 < cur_t * 0.995f) {
-        cur = p;
-        cur_t = t3;
+    for (int round = 0; round < kTuneSwapRounds && rc == QSIM_OK; ++round) {
+      std::vector<std::pair<float, qsim_plan>> screened;
+      for (int i = 10; i < cur.M && rc == QSIM_OK; ++i)
+        for (int j = i + 1; j < cur.M && rc == QSIM_OK; ++j) {
+          qsim_plan p = cur;
+          std::swap(p.sigma[i], p.sigma[j]);
+          const float t = time_plan(p, false, 1);
+          if (rc == QSIM_OK) screened.push_back({t, p});
+        }
+      if (rc != QSIM_OK || screened.empty()) break;
+      std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
+                        screened.end(), [](const std::pair<float, qsim_plan>& x,
+                                           const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
+      float cand_t = 1e30f;
+      qsim_plan cand = cur;
+      for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
+        const float t = time_plan(screened[c].second, false, 3);
+        if (rc == QSIM_OK && t < cand_t) {
+          cand_t = t;
+          cand = screened[c].second;
+        }
       }
+      if (rc != QSIM_OK || !(cand_t < cur_t * 0.995f)) break;
+      cur_t = cand_t;
+      cur = cand;
     }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;
