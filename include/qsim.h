@@ -246,10 +246,13 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * at each of the 10 positions next to the cover, best move kept on a >= 0.5 %
  * win, up to 3 rounds; sigma[10..] is a kernel parameter, so no recompiles),
  * then exchanges of any two counter positions >= 10 (every pair screened,
- * the four best re-timed, the best kept on a >= 0.5 % win, up to 2 rounds).
+ * the four best re-timed, the best kept on a >= 0.5 % win, up to 2 rounds),
+ * then exchanges of a compiled position (3..9: lanes and in-thread entries,
+ * a new kernel each) with a position below 17, the same way, up to 2 rounds
+ * (each kept move followed by one more round of runtime exchanges).
  * Each trial runs qsim_map_gather_planned (the first of a variant compiles
  * its kernel), so perm and k2 hold a valid result afterwards; the call
- * synchronises `stream` (cfg5: about 20 s).  plan: in (chunk sizes, residency kept) /
+ * synchronises `stream` (cfg5: about 40 s).  plan: in (chunk sizes, residency kept) /
  * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
  * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit).
  * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */

@@ -1601,6 +1601,9 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
 
 // qsim_plan_tune stage 4: rounds of screening every exchange of two counter positions
 constexpr int kTuneSwapRounds = 2;
+// stage 5: compiled positions exchanged with positions below this one
+constexpr int kTuneCompiledSwapSpan = 17;
+constexpr int kTuneCompiledRounds = 2;
 
 int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
                    const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
@@ -1765,31 +1768,71 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     // the best kept on a >= 0.5 % win; up to 2 rounds.  cfg5: a random-swap
     // hill climb found 19.11 -> 18.81 ms (tools/exp/tail_climb.py,
     // profiles/r02_tail_climb.txt)
-    for (int round = 0; round < kTuneSwapRounds && rc == QSIM_OK; ++round) {
+    auto swap_rounds = [&](int rounds) {
+      for (int round = 0; round < rounds && rc == QSIM_OK; ++round) {
+        std::vector<std::pair<float, qsim_plan>> screened;
+        for (int i = 10; i < cur.M && rc == QSIM_OK; ++i)
+          for (int j = i + 1; j < cur.M && rc == QSIM_OK; ++j) {
+            qsim_plan p = cur;
+            std::swap(p.sigma[i], p.sigma[j]);
+            const float t = time_plan(p, false, 1);
+            if (rc == QSIM_OK) screened.push_back({t, p});
+          }
+        if (rc != QSIM_OK || screened.empty()) break;
+        std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
+                          screened.end(), [](const std::pair<float, qsim_plan>& x,
+                                             const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
+        float cand_t = 1e30f;
+        qsim_plan cand = cur;
+        for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
+          const float t = time_plan(screened[c].second, false, 3);
+          if (rc == QSIM_OK && t < cand_t) {
+            cand_t = t;
+            cand = screened[c].second;
+          }
+        }
+        if (rc != QSIM_OK || !(cand_t < cur_t * 0.995f)) break;
+        cur_t = cand_t;
+        cur = cand;
+      }
+    };
+    swap_rounds(kTuneSwapRounds);
+    // fifth stage: exchanges that move a compiled position (counter bits
+    // plan_keep_bits..9: lanes and in-thread entries; each order is a new
+    // NVRTC kernel) with a position up to 16: screened with one call after
+    // the compile, the four best re-timed, the best kept on a >= 0.5 % win,
+    // then one more round of the fourth stage; up to 2 rounds.  cfg5: lanes
+    // on output bit 11 instead of 3 (output bit 3 in-thread) 18.91 -> 18.35
+    // ms, then output bit 3 to the warp bits 18.20 -> 17.99 ms
+    // (tools/exp/compiled_swaps.py, profiles/r02_compiled_swaps.txt)
+    for (int round = 0; round < kTuneCompiledRounds && rc == QSIM_OK; ++round) {
       std::vector<std::pair<float, qsim_plan>> screened;
-      for (int i = 10; i < cur.M && rc == QSIM_OK; ++i)
-        for (int j = i + 1; j < cur.M && rc == QSIM_OK; ++j) {
+      const int keep = plan_keep_bits(cur.dtype);
+      for (int i = keep; i < 10 && i < cur.M && rc == QSIM_OK; ++i)
+        for (int j = i + 1; j < std::min(cur.M, kTuneCompiledSwapSpan) && rc == QSIM_OK; ++j) {
           qsim_plan p = cur;
           std::swap(p.sigma[i], p.sigma[j]);
-          const float t = time_plan(p, false, 1);
+          const float t = time_plan(p, true, 1);
           if (rc == QSIM_OK) screened.push_back({t, p});
         }
-      if (rc != QSIM_OK || screened.empty()) break;
-      std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
-                        screened.end(), [](const std::pair<float, qsim_plan>& x,
-                                           const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
-      float cand_t = 1e30f;
-      qsim_plan cand = cur;
-      for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
-        const float t = time_plan(screened[c].second, false, 3);
-        if (rc == QSIM_OK && t < cand_t) {
-          cand_t = t;
-          cand = screened[c].second;
+      if (rc == QSIM_OK && !screened.empty()) {
+        std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
+                          screened.end(), [](const std::pair<float, qsim_plan>& x,
+                                             const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
+        float cand_t = 1e30f;
+        qsim_plan cand = cur;
+        for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
+          const float t = time_plan(screened[c].second, false, 3);
+          if (rc == QSIM_OK && t < cand_t) {
+            cand_t = t;
+            cand = screened[c].second;
+          }
         }
+        if (!(rc == QSIM_OK && cand_t < cur_t * 0.995f)) break;
+        cur_t = cand_t;
+        cur = cand;
+        swap_rounds(1);
       }
-      if (rc != QSIM_OK || !(cand_t < cur_t * 0.995f)) break;
-      cur_t = cand_t;
-      cur = cand;
     }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;
