@@ -248,8 +248,9 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * then exchanges of any two counter positions >= 10 (every pair screened,
  * the four best re-timed, the best kept on a >= 0.5 % win, up to 2 rounds),
  * then exchanges of a compiled position (3..9: lanes and in-thread entries,
- * a new kernel each) with a position below 17, the same way, up to 2 rounds
- * (each kept move followed by one more round of runtime exchanges).
+ * a new kernel each, a round's kernels compiled in parallel on the host)
+ * with any later position, the same way, up to 3 rounds (each kept move
+ * followed by one more round of runtime exchanges).
  * Each trial runs qsim_map_gather_planned (the first of a variant compiles
  * its kernel), so perm and k2 hold a valid result afterwards; the call
  * synchronises `stream` (cfg5: about 40 s).  plan: in (chunk sizes, residency kept) /

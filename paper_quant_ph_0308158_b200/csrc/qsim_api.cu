@@ -13,6 +13,7 @@
 #include <mutex>
 #include <algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "qsim.h"
@@ -1601,9 +1602,8 @@ int qsim_run_host_batch(const qsim_gate* gates, int32_t n_gates, int32_t M, int3
 
 // qsim_plan_tune stage 4: rounds of screening every exchange of two counter positions
 constexpr int kTuneSwapRounds = 2;
-// stage 5: compiled positions exchanged with positions below this one
-constexpr int kTuneCompiledSwapSpan = 17;
-constexpr int kTuneCompiledRounds = 2;
+// stage 5: rounds of exchanges of a compiled position with any later one
+constexpr int kTuneCompiledRounds = 3;
 
 int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
                    const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
@@ -1799,22 +1799,36 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     swap_rounds(kTuneSwapRounds);
     // fifth stage: exchanges that move a compiled position (counter bits
     // plan_keep_bits..9: lanes and in-thread entries; each order is a new
-    // NVRTC kernel) with a position up to 16: screened with one call after
-    // the compile, the four best re-timed, the best kept on a >= 0.5 % win,
-    // then one more round of the fourth stage; up to 2 rounds.  cfg5: lanes
+    // NVRTC kernel, all of a round compiled at once on the host's cores) with
+    // any later position: screened with one call, the four best re-timed, the
+    // best kept on a >= 0.5 % win, then one more round of the fourth stage;
+    // up to 3 rounds.  cfg5: lanes
     // on output bit 11 instead of 3 (output bit 3 in-thread) 18.91 -> 18.35
     // ms, then output bit 3 to the warp bits 18.20 -> 17.99 ms
     // (tools/exp/compiled_swaps.py, profiles/r02_compiled_swaps.txt)
+    std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
+    pack_gates(gates, n_gates, false, *gl);
+    const unsigned hw = std::thread::hardware_concurrency();
     for (int round = 0; round < kTuneCompiledRounds && rc == QSIM_OK; ++round) {
-      std::vector<std::pair<float, qsim_plan>> screened;
+      std::vector<qsim_plan> cand_plans;
       const int keep = plan_keep_bits(cur.dtype);
-      for (int i = keep; i < 10 && i < cur.M && rc == QSIM_OK; ++i)
-        for (int j = i + 1; j < std::min(cur.M, kTuneCompiledSwapSpan) && rc == QSIM_OK; ++j) {
+      for (int i = keep; i < 10 && i < cur.M; ++i)
+        for (int j = i + 1; j < cur.M; ++j) {
           qsim_plan p = cur;
           std::swap(p.sigma[i], p.sigma[j]);
-          const float t = time_plan(p, true, 1);
-          if (rc == QSIM_OK) screened.push_back({t, p});
+          cand_plans.push_back(p);
         }
+      {  // every candidate kernel compiled at once on the host's cores
+        std::vector<uint8_t> sg(32 * cand_plans.size());
+        for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
+        qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(),
+                                elem_bytes(cur.dtype), hw ? (int)std::min(hw, 32u) : 8);
+      }
+      std::vector<std::pair<float, qsim_plan>> screened;
+      for (size_t c = 0; c < cand_plans.size() && rc == QSIM_OK; ++c) {
+        const float t = time_plan(cand_plans[c], true, 1);
+        if (rc == QSIM_OK) screened.push_back({t, cand_plans[c]});
+      }
       if (rc == QSIM_OK && !screened.empty()) {
         std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
                           screened.end(), [](const std::pair<float, qsim_plan>& x,

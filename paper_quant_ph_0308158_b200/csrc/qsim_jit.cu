@@ -20,6 +20,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -27,6 +28,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -981,6 +983,59 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     if (!fn) return -1;
   }
   return launch_gather(fn, M, sigma, chunk_log2, k1, k2, perm_out, ticket, blocks, st, err);
+}
+
+// NVRTC programs are independent, so several compile at once (the driver
+// calls that load the modules stay under the lock).
+int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
+                      int threads) {
+  const uint64_t kind = 0x66757365ull;
+  std::vector<std::vector<uint32_t>> keys;
+  std::vector<std::string> srcs;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    init_locked();
+    if (!(g_nvrtc.ok && g_drv.ok)) return -1;
+    for (int i = 0; i < count; ++i) {
+      const uint8_t* sg = sigmas + 32 * i;
+      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem);
+      const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
+      bool have = false;
+      for (const Entry& e : g_cache[key]) have = have || (e.M == M && e.words == keyw);
+      for (const auto& k : keys) have = have || k == keyw;
+      if (have) continue;
+      keys.push_back(keyw);
+      srcs.push_back(fused_source(words, n, M, sg, elem, false));
+    }
+  }
+  const size_t m = keys.size();
+  std::vector<std::vector<char>> cubins(m);
+  std::vector<std::string> errs(m);
+  std::vector<char> ok(m, 0);
+  std::atomic<size_t> next{0};
+  auto work = [&]() {
+    for (size_t i; (i = next.fetch_add(1)) < m;) ok[i] = compile_cubin_locked(srcs[i], cubins[i], errs[i]);
+  };
+  const int nt = (int)std::min<size_t>(m, (size_t)std::max(1, threads));
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  int done = 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (size_t i = 0; i < m; ++i) {
+    if (!ok[i]) continue;  // jit_fused compiles it again and reports the error
+    CUmodule mod = nullptr;
+    CUfunction fn = nullptr;
+    if (g_drv.load(&mod, cubins[i].data()) != CUDA_SUCCESS ||
+        g_drv.getfn(&fn, mod, "qsim_jit_fused") != CUDA_SUCCESS)
+      continue;
+    g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 3);
+    const uint64_t key = fnv(keys[i].data(), (int)keys[i].size(), kind);
+    g_cache[key].push_back(Entry{keys[i], M, fn, 0.0});
+    ++done;
+  }
+  return done;
 }
 
 int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, size_t qbytes,

@@ -29,6 +29,12 @@ int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint
 int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
               cudaStream_t st, std::string& err);
+// Compile (NVRTC, on up to `threads` host threads at once) and cache the fused
+// kernels of `count` orders (32 bytes each, sigmas[32 * i ..]) that are not
+// cached yet, so that later jit_fused calls find them.  Returns the number
+// compiled, or -1 if NVRTC is unavailable.
+int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
+                      int threads);
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
 // k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
 // qsim::Qubits (passed by value as a kernel parameter).
