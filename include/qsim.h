@@ -250,10 +250,13 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * then exchanges of a compiled position (3..9: lanes and in-thread entries,
  * a new kernel each, a round's kernels compiled in parallel on the host)
  * with any later position, the same way, up to 3 rounds (each kept move
- * followed by one more round of runtime exchanges).
+ * followed by one more round of runtime exchanges).  In every stage the four
+ * best screened candidates are re-timed interleaved with the current order
+ * (clock drift under sw_power_cap cancels) and the best ratio is kept on a
+ * >= 0.5 % win.
  * Each trial runs qsim_map_gather_planned (the first of a variant compiles
  * its kernel), so perm and k2 hold a valid result afterwards; the call
- * synchronises `stream` (cfg5: about 40 s).  plan: in (chunk sizes, residency kept) /
+ * synchronises `stream` (cfg5: about 60 s).  plan: in (chunk sizes, residency kept) /
  * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
  * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit).
  * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */

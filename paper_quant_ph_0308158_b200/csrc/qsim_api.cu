@@ -1727,85 +1727,98 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
   qsim_plan cur = cands[best_i];
   const int from = std::max(10, (int)cur.tile_log2);
   if (!(cur.flags & 1u) && cur.M >= from + 4) {
+    const bool trace = std::getenv("QSIM_TUNE_TRACE") != nullptr;  // diagnostics (stderr)
     float cur_t = time_plan(cur, false, 3);
+    // Stages 3-5 share one step: screen every candidate order with one timed
+    // call (the GPU kept busy first, so no screen profits from an idle,
+    // unthrottled start -- the bench state runs into sw_power_cap), then
+    // re-time the four best against the current order interleaved (cur,
+    // cand, cur, cand, ...: best of 3 each, so clock drift cancels) and keep
+    // the best ratio when it is a >= 0.5 % win.  Returns true if cur moved.
+    // (compiled: a candidate's first call may load its kernel -- it is warmed untimed)
+    auto step = [&](const std::vector<qsim_plan>& cand_plans, const char* stage, bool compiled) -> bool {
+      time_plan(cur, false, 2);
+      std::vector<std::pair<float, size_t>> screened;
+      for (size_t c = 0; c < cand_plans.size() && rc == QSIM_OK; ++c) {
+        const float t = time_plan(cand_plans[c], compiled, 1);
+        if (rc == QSIM_OK) screened.push_back({t, c});
+      }
+      if (rc != QSIM_OK || screened.empty()) return false;
+      const size_t top = std::min<size_t>(4, screened.size());
+      std::partial_sort(screened.begin(), screened.begin() + top, screened.end());
+      float best_ratio = 1.0f, best_t = cur_t;
+      size_t best_c = SIZE_MAX;
+      for (size_t c = 0; c < top && rc == QSIM_OK; ++c) {
+        float tc = 1e30f, tx = 1e30f;
+        for (int r = 0; r < 3 && rc == QSIM_OK; ++r) {
+          tc = std::min(tc, time_plan(cur, false, 1));
+          tx = std::min(tx, time_plan(cand_plans[screened[c].second], false, 1));
+        }
+        if (trace)
+          std::fprintf(stderr, "[qsim_plan_tune] %s: screened %.3f, re-timed %.3f vs current %.3f\n", stage,
+                       screened[c].first, tx, tc);
+        if (rc == QSIM_OK && tx / tc < best_ratio) {
+          best_ratio = tx / tc;
+          best_t = tx;
+          best_c = screened[c].second;
+        }
+      }
+      if (rc != QSIM_OK || best_c == SIZE_MAX || !(best_ratio < 0.995f)) return false;
+      cur = cand_plans[best_c];
+      cur_t = best_t;
+      return true;
+    };
+    // third stage: the order of the counter bits above the cover (runtime
+    // kernel parameter, no recompiles).  The plan orders them for the k1 reads
+    // (a line's readers close in time); moving an output bit down next to the
+    // cover changes which k2 / perm lines share a chunk front (their DRAM rows
+    // on write-back) and which k1 lines are read together: every tail bit
+    // tried at each of the 10 positions just above the cover; up to 3 rounds.
+    // The gains depend on the data in the buffers (power: sw_power_cap),
+    // which is why the search runs on the caller's buffers.  cfg5: output bit
+    // 4 moves from counter bit 21 to 15, 19.85 -> 19.3 ms with the bench's
+    // Gaussian state (profiles/r02_sigma_tail_moves.txt, r02_tail_search.txt,
+    // r02_sigma_ab.txt).
     for (int round = 0; round < 3 && rc == QSIM_OK; ++round) {
-      std::vector<std::pair<float, qsim_plan>> screened;  // (one timed call, plan)
-      for (int at = from; at < cur.M && rc == QSIM_OK; ++at) {
-        for (int pos = from; pos < std::min(cur.M, from + 10) && rc == QSIM_OK; ++pos) {
+      std::vector<qsim_plan> moves;
+      for (int at = from; at < cur.M; ++at)
+        for (int pos = from; pos < std::min(cur.M, from + 10); ++pos) {
           if (pos == at) continue;
           qsim_plan p = cur;
           uint8_t rest[32];
           int m = 0;
           for (int k = from; k < cur.M; ++k)
             if (k != at) rest[m++] = cur.sigma[k];
-          for (int k = from, r = 0; k < cur.M; ++k)
-            p.sigma[k] = k == pos ? cur.sigma[at] : rest[r++];
-          const float t = time_plan(p, false, 1);
-          if (rc == QSIM_OK) screened.push_back({t, p});
+          for (int k = from, r = 0; k < cur.M; ++k) p.sigma[k] = k == pos ? cur.sigma[at] : rest[r++];
+          moves.push_back(p);
         }
-      }
-      if (rc != QSIM_OK || screened.empty()) break;
-      // the four best screened moves, re-timed (best of 3), against the current order
-      std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
-                        screened.end(), [](const std::pair<float, qsim_plan>& x,
-                                           const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
-      float cand_t = 1e30f;
-      qsim_plan cand = cur;
-      for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
-        const float t = time_plan(screened[c].second, false, 3);
-        if (rc == QSIM_OK && t < cand_t) {
-          cand_t = t;
-          cand = screened[c].second;
-        }
-      }
-      if (rc != QSIM_OK || !(cand_t < cur_t * 0.995f)) break;
-      cur_t = cand_t;
-      cur = cand;
+      if (!step(moves, "stage 3", false)) break;
     }
     // fourth stage: exchanges of any two counter positions >= 10 (this also
-    // trades the CTA's warp-level cover bits 10..12 against tail bits): every
-    // pair screened with one timed call, the four best re-timed (best of 3),
-    // the best kept on a >= 0.5 % win; up to 2 rounds.  cfg5: a random-swap
-    // hill climb found 19.11 -> 18.81 ms (tools/exp/tail_climb.py,
-    // profiles/r02_tail_climb.txt)
+    // trades the CTA's warp-level cover bits 10..12 against tail bits); up to
+    // 2 rounds.  cfg5: a random-swap hill climb found 19.11 -> 18.81 ms
+    // (tools/exp/tail_climb.py, profiles/r02_tail_climb.txt)
     auto swap_rounds = [&](int rounds) {
       for (int round = 0; round < rounds && rc == QSIM_OK; ++round) {
-        std::vector<std::pair<float, qsim_plan>> screened;
-        for (int i = 10; i < cur.M && rc == QSIM_OK; ++i)
-          for (int j = i + 1; j < cur.M && rc == QSIM_OK; ++j) {
+        std::vector<qsim_plan> swaps;
+        for (int i = 10; i < cur.M; ++i)
+          for (int j = i + 1; j < cur.M; ++j) {
             qsim_plan p = cur;
             std::swap(p.sigma[i], p.sigma[j]);
-            const float t = time_plan(p, false, 1);
-            if (rc == QSIM_OK) screened.push_back({t, p});
+            swaps.push_back(p);
           }
-        if (rc != QSIM_OK || screened.empty()) break;
-        std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
-                          screened.end(), [](const std::pair<float, qsim_plan>& x,
-                                             const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
-        float cand_t = 1e30f;
-        qsim_plan cand = cur;
-        for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
-          const float t = time_plan(screened[c].second, false, 3);
-          if (rc == QSIM_OK && t < cand_t) {
-            cand_t = t;
-            cand = screened[c].second;
-          }
-        }
-        if (rc != QSIM_OK || !(cand_t < cur_t * 0.995f)) break;
-        cur_t = cand_t;
-        cur = cand;
+        if (!step(swaps, "stage 4", false)) break;
       }
     };
     swap_rounds(kTuneSwapRounds);
     // fifth stage: exchanges that move a compiled position (counter bits
     // plan_keep_bits..9: lanes and in-thread entries; each order is a new
-    // NVRTC kernel, all of a round compiled at once on the host's cores) with
-    // any later position: screened with one call, the four best re-timed, the
-    // best kept on a >= 0.5 % win, then one more round of the fourth stage;
-    // up to 3 rounds.  cfg5: lanes
-    // on output bit 11 instead of 3 (output bit 3 in-thread) 18.91 -> 18.35
-    // ms, then output bit 3 to the warp bits 18.20 -> 17.99 ms
-    // (tools/exp/compiled_swaps.py, profiles/r02_compiled_swaps.txt)
+    // NVRTC kernel, a round's kernels compiled at once on the host's cores)
+    // with any later position; each kept move is followed by one more round
+    // of the fourth stage; up to 3 rounds.  cfg5: lanes on output bit 11
+    // instead of 3 (output bit 3 in-thread) 18.91 -> 18.35 ms, then output
+    // bit 3 to the warp bits 18.20 -> 17.99 ms (tools/exp/compiled_swaps.py,
+    // profiles/r02_compiled_swaps.txt)
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n_gates, false, *gl);
     const unsigned hw = std::thread::hardware_concurrency();
@@ -1818,35 +1831,12 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
           std::swap(p.sigma[i], p.sigma[j]);
           cand_plans.push_back(p);
         }
-      {  // every candidate kernel compiled at once on the host's cores
-        std::vector<uint8_t> sg(32 * cand_plans.size());
-        for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
-        qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(),
-                                elem_bytes(cur.dtype), hw ? (int)std::min(hw, 32u) : 8);
-      }
-      std::vector<std::pair<float, qsim_plan>> screened;
-      for (size_t c = 0; c < cand_plans.size() && rc == QSIM_OK; ++c) {
-        const float t = time_plan(cand_plans[c], true, 1);
-        if (rc == QSIM_OK) screened.push_back({t, cand_plans[c]});
-      }
-      if (rc == QSIM_OK && !screened.empty()) {
-        std::partial_sort(screened.begin(), screened.begin() + std::min<size_t>(4, screened.size()),
-                          screened.end(), [](const std::pair<float, qsim_plan>& x,
-                                             const std::pair<float, qsim_plan>& y) { return x.first < y.first; });
-        float cand_t = 1e30f;
-        qsim_plan cand = cur;
-        for (size_t c = 0; c < std::min<size_t>(4, screened.size()) && rc == QSIM_OK; ++c) {
-          const float t = time_plan(screened[c].second, false, 3);
-          if (rc == QSIM_OK && t < cand_t) {
-            cand_t = t;
-            cand = screened[c].second;
-          }
-        }
-        if (!(rc == QSIM_OK && cand_t < cur_t * 0.995f)) break;
-        cur_t = cand_t;
-        cur = cand;
-        swap_rounds(1);
-      }
+      std::vector<uint8_t> sg(32 * cand_plans.size());
+      for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
+      qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
+                              hw ? (int)std::min(hw, 32u) : 8);
+      if (!step(cand_plans, "stage 5", true)) break;
+      swap_rounds(1);
     }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;

@@ -49,10 +49,18 @@ def t(p):
     return best
 
 
-res = {"new": [], "recorded": []}
+sw = q.plan_create(gates, M, "c64")
+ctypes_copy = bytes(plan)
+import ctypes  # noqa: E402
+ctypes.memmove(ctypes.addressof(sw), ctypes_copy, len(ctypes_copy))
+i, j = [int(x) for x in os.environ.get("TC_SWAP", "3,6").split(",")]
+sw.sigma[i], sw.sigma[j] = plan.sigma[j], plan.sigma[i]
+res = {"new": [], "recorded": [], "swapped": []}
 for _ in range(5):
     res["new"].append(t(plan))
     res["recorded"].append(t(old))
+    res["swapped"].append(t(sw))
 print(json.dumps({"tune_s": tune_s, "variant": variant, "sigma": list(plan.sigma),
                   "chunk_log2": plan.chunk_log2, "new_ms": min(res["new"]),
-                  "recorded_ms": min(res["recorded"]), "all": res}), flush=True)
+                  "recorded_ms": min(res["recorded"]), "swapped_ms": min(res["swapped"]),
+                  "swapped_sigma": list(sw.sigma), "all": res}), flush=True)
