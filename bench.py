@@ -375,7 +375,7 @@ def run_qsim(args):
 
     from paper_quant_ph_0308158_b200.dist import barrier, max_over_ranks
 
-    def timed_loop(step_fn, steps, warmup, per_kernel=None):
+    def timed_loop(step_fn, steps, warmup, per_kernel=None, name="step"):
         for _ in range(warmup):
             step_fn(None)
         torch.cuda.synchronize()
@@ -385,11 +385,15 @@ def run_qsim(args):
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         launches = 0
+        # an NVTX range around the timed launches: the ncu launch list and the
+        # full capture of the step select them with --nvtx-include "timed_<name>/"
+        torch.cuda.nvtx.range_push(f"timed_{name}")
         with torch.cuda.stream(stream):
             t0.record(stream)
             for _ in range(steps):
                 launches += step_fn(marks)
             t1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -492,26 +496,26 @@ def run_qsim(args):
     sampler = ClockSampler(local)
     with sampler:
         ms_mg, launches_mg, kern_mg = timed_loop(step_map_gather, args.steps, args.warmup,
-                                                 per_kernel=True)
+                                                 per_kernel=True, name="map_gather")
         # the timed step's own output, checked against the oracle before any
         # other loop overwrites perm / k2
         verified = verify_sample(gates, M, e, perm, k2, k1_host, cfg, dev)
         ms_mat, launches_mat, kern_mat = timed_loop(step_materialised, args.steps, args.warmup,
-                                                    per_kernel=True)
+                                                    per_kernel=True, name="materialised")
         ms_fused, launches_fused, kern_fused = timed_loop(step_fused, args.steps, args.warmup,
-                                                          per_kernel=True)
+                                                          per_kernel=True, name="fused")
         plain_steps = max(2, args.steps // 4)
         ms_pf, launches_pf, kern_pf = timed_loop(step_plain_fused, plain_steps, args.warmup,
-                                                 per_kernel=True)
+                                                 per_kernel=True, name="plain_fused")
         kern_name_pf = q.last_kernel()
         q.build_map(gates, M, perm, stream=stream)
         ms_pa, launches_pa, kern_pa = timed_loop(step_plain_apply, plain_steps, min(args.warmup, 1),
-                                                 per_kernel=True)
+                                                 per_kernel=True, name="plain_apply")
         ms_kron, launches_kron, kern_kron = timed_loop(step_kron, args.steps, args.warmup,
-                                                       per_kernel=True)
+                                                       per_kernel=True, name="kron")
         kern_name_kron = q.last_kernel()
         ms_k40, launches_k40, kern_k40 = timed_loop(step_kron40, max(2, args.steps // 4),
-                                                    args.warmup, per_kernel=True)
+                                                    args.warmup, per_kernel=True, name="kron40")
         kern_name_k40 = q.last_kernel()
         # write-only ceiling for the on-the-fly input's roofline: torch's fill
         # of the same 2^M-entry output buffer (not our kernel; a denominator)
