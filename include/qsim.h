@@ -250,7 +250,8 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * then exchanges of a compiled position (3..9: lanes and in-thread entries,
  * a new kernel each, a round's kernels compiled in parallel on the host)
  * with any later position, the same way, up to 3 rounds (each kept move
- * followed by one more round of runtime exchanges).  In every stage the four
+ * followed by one more round of runtime exchanges), then the chunk size
+ * (2^(c±1)) and 2 CTAs per SM once more for the kept order.  In every stage the four
  * best screened candidates are re-timed interleaved with the current order
  * (clock drift under sw_power_cap cancels) and the best ratio is kept on a
  * >= 0.5 % win.

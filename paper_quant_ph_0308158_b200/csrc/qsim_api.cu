@@ -1838,6 +1838,24 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       if (!step(cand_plans, "stage 5", true)) break;
       swap_rounds(1);
     }
+    // sixth stage: the chunk size and CTAs per SM again, for the order kept
+    // (stage 2 chose the chunk for the stage-1 order)
+    {
+      std::vector<qsim_plan> launch_cands;
+      for (int d = -1; d <= 1; d += 2) {
+        const int cl = (int)cur.fused_chunk_log2 + d;
+        if (cl < 10 || cl > cur.M || ((1ull << cur.M) >> cl) < (uint64_t)sm_count()) continue;
+        qsim_plan p = cur;
+        p.chunk_log2 = p.fused_chunk_log2 = (uint32_t)cl;
+        launch_cands.push_back(p);
+      }
+      if (cur.blocks_per_sm == 1) {
+        qsim_plan p = cur;
+        p.blocks_per_sm = 2;
+        launch_cands.push_back(p);
+      }
+      if (rc == QSIM_OK && !launch_cands.empty()) step(launch_cands, "stage 6", false);
+    }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;
   }
