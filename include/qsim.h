@@ -219,7 +219,8 @@ typedef struct qsim_plan {
                                shared-memory staged kernel (TMA bulk copies of k1
                                tiles, double-buffered), re-checked on the gates given */
     uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
-    uint16_t cta_threads;   /* apply kernel CTA size: 256, 512 or 1024 (0 = 256)    */
+    uint16_t cta_threads;   /* CTA size: 256, 512 or 1024 (0 = 256); the NVRTC
+                               gather kernels run 16 warps for 512, else 8     */
     uint16_t fused_chunk_log2; /* counters per CTA chunk of the fused kernel (default 16) */
     uint16_t reserved_spread;  /* diagnostics: log2 of the 0.9-quantile spread of a line's
                                   readers, natural order (low byte) and sigma order (high) */
@@ -251,7 +252,7 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * a new kernel each, a round's kernels compiled in parallel on the host)
  * with any later position, the same way, up to 3 rounds (each kept move
  * followed by one more round of runtime exchanges), then the chunk size
- * (2^(c±1)) and 2 CTAs per SM once more for the kept order.  In every stage the four
+ * (2^(c±1)), 2 CTAs per SM and 512-thread CTAs once more for the kept order.  In every stage the four
  * best screened candidates are re-timed interleaved with the current order
  * (clock drift under sw_power_cap cancels) and the best ratio is kept on a
  * >= 0.5 % win.

@@ -761,6 +761,10 @@ int plan_validate(const qsim_plan* p) {
 
 bool plan_natural(const qsim_plan* p) { return (p->flags & 1u) || p->M < 10; }
 
+// warps per CTA of the NVRTC gather kernels: 16 for plans with 512-thread
+// CTAs (a block of 2^14 counters per round), else 8
+int jit_warps(const qsim_plan* p) { return p->cta_threads == 512 ? 16 : 8; }
+
 // The NVRTC gather kernels take chunks from the workspace ticket in counter
 // order (an in-order front: k2 / perm written close to their neighbours, k1
 // lines' readers close in time).  A natural-order plan of an L2-resident
@@ -1163,7 +1167,7 @@ int apply_planned_impl(const qsim_plan* plan, const uint32_t* perm, const void* 
     if (blocks > nchunks) blocks = nchunks;
     std::string err;
     if (qsim::jit_apply(M, pp->sigma, pp->fused_chunk_log2, e, perm, k1, k2, ticket_for(plan, workspace),
-                        (int)blocks, st, err) == 0) {
+                        (int)blocks, jit_warps(pp), st, err) == 0) {
       ++g_launches;
       g_last_kernel = "qsim_jit_apply";
       return QSIM_OK;
@@ -1240,7 +1244,7 @@ int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t 
     uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
     if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2, perm_out,
-                        workspace, (int)blocks, st, err) == 0) {
+                        workspace, (int)blocks, jit_warps(plan), st, err) == 0) {
       ++g_launches;
       *used_jit = true;
       g_last_kernel = "qsim_jit_fused";
@@ -1834,12 +1838,14 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
       std::vector<uint8_t> sg(32 * cand_plans.size());
       for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
       qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
-                              hw ? (int)std::min(hw, 32u) : 8);
+                              jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8);
       if (!step(cand_plans, "stage 5", true)) break;
       swap_rounds(1);
     }
-    // sixth stage: the chunk size and CTAs per SM again, for the order kept
-    // (stage 2 chose the chunk for the stage-1 order)
+    // sixth stage: the chunk size, 2 CTAs per SM and 16-warp CTAs, for the
+    // order kept (stage 2 chose the chunk for the stage-1 order; cfg5 keeps
+    // 2^15 counters, 1 CTA of 8 warps: 16 warps 18.7 vs 17.75 ms,
+    // profiles/r02_cta16.txt)
     {
       std::vector<qsim_plan> launch_cands;
       for (int d = -1; d <= 1; d += 2) {
@@ -1854,7 +1860,12 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
         p.blocks_per_sm = 2;
         launch_cands.push_back(p);
       }
-      if (rc == QSIM_OK && !launch_cands.empty()) step(launch_cands, "stage 6", false);
+      if (cur.cta_threads == 256) {  // 16 warps per CTA: a round covers counter bits 0..13
+        qsim_plan p = cur;
+        p.cta_threads = 512;
+        launch_cands.push_back(p);
+      }
+      if (rc == QSIM_OK && !launch_cands.empty()) step(launch_cands, "stage 6", true);
     }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;

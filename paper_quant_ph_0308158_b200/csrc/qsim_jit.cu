@@ -422,16 +422,16 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // built from it), so qsim_plan_tune can try orders of the high counter bits
 // without recompiling.
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem,
-                         bool from_perm) {
+                         bool from_perm, int warps = 8) {
   std::string s = kPrelude;
   char buf[256];
-  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n",
-                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16);
+  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n",
+                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16, warps);
   s += buf;
   s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
   s += R"(
 struct Sigma { unsigned char s[32]; };
-extern "C" __global__ void __launch_bounds__(256)
+extern "C" __global__ void __launch_bounds__(32 * QSIM_W)
 QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
            QSIM_T* __restrict__ k2, u32* __restrict__ perm_out, const Sigma sig) {
   __shared__ u32 tab[4][256];
@@ -460,7 +460,7 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
       ch = (u64)blockIdx.x + it * gridDim.x;
     }
     if (ch >= nchunks) break;
-    for (u32 tt = warp; tt < tiles; tt += 8u) {
+    for (u32 tt = warp; tt < tiles; tt += QSIM_W) {
       const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
       const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
                      tab[3][(c >> 24) & 255];
@@ -932,7 +932,7 @@ struct SigmaArg {
 
 // one chunk ticket reset + launch of a gather kernel (fused / apply)
 int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log2, const void* k1,
-                  void* k2, uint32_t* perm, void* ticket, int blocks, cudaStream_t st,
+                  void* k2, uint32_t* perm, void* ticket, int blocks, int warps, cudaStream_t st,
                   std::string& err) {
   uint64_t N = 1ull << M;
   uint32_t cl = chunk_log2;
@@ -943,7 +943,7 @@ int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log
     err = "ticket reset failed";
     return -1;
   }
-  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) !=
+  if (g_drv.launch(fn, (unsigned)blocks, 1, 1, 32u * (unsigned)warps, 1, 1, 0, (CUstream)st, args, nullptr) !=
       CUDA_SUCCESS) {
     err = "cuLaunchKernel failed";
     return -1;
@@ -953,17 +953,18 @@ int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log
 
 // cache key of a gather kernel: what shapes its code (sigma[0..9], the dtype
 // and, for the fused walk, the gates)
-std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem) {
+std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem, int warps) {
   std::vector<uint32_t> keyw(words, words + n);
   for (int k = 0; k < 10; ++k) keyw.push_back(sigma[k]);
   keyw.push_back((uint32_t)elem);
+  keyw.push_back((uint32_t)warps);
   return keyw;
 }
 }  // namespace
 
 int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
-              cudaStream_t st, std::string& err) {
+              int warps, cudaStream_t st, std::string& err) {
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -972,23 +973,23 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
       err = g_status;
       return -1;
     }
-    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem);
+    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem, warps);
     const uint64_t kind = 0x66757365ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])  // the source is only generated on a cache miss
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps),
                              "qsim_jit_fused", err);
     if (!fn) return -1;
   }
-  return launch_gather(fn, M, sigma, chunk_log2, k1, k2, perm_out, ticket, blocks, st, err);
+  return launch_gather(fn, M, sigma, chunk_log2, k1, k2, perm_out, ticket, blocks, warps, st, err);
 }
 
 // NVRTC programs are independent, so several compile at once (the driver
 // calls that load the modules stay under the lock).
 int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
-                      int threads) {
+                      int warps, int threads) {
   const uint64_t kind = 0x66757365ull;
   std::vector<std::vector<uint32_t>> keys;
   std::vector<std::string> srcs;
@@ -998,14 +999,14 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
     if (!(g_nvrtc.ok && g_drv.ok)) return -1;
     for (int i = 0; i < count; ++i) {
       const uint8_t* sg = sigmas + 32 * i;
-      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem);
+      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem, warps);
       const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
       bool have = false;
       for (const Entry& e : g_cache[key]) have = have || (e.M == M && e.words == keyw);
       for (const auto& k : keys) have = have || k == keyw;
       if (have) continue;
       keys.push_back(keyw);
-      srcs.push_back(fused_source(words, n, M, sg, elem, false));
+      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps));
     }
   }
   const size_t m = keys.size();
@@ -1109,7 +1110,7 @@ int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gb
 // The planned apply from a materialised map: the fused kernel's traversal and
 // batching with the sources read from perm (k2[o] = k1[perm[o]]).
 int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,
-              const void* k1, void* k2, void* ticket, int blocks, cudaStream_t st,
+              const void* k1, void* k2, void* ticket, int blocks, int warps, cudaStream_t st,
               std::string& err) {
   CUfunction fn = nullptr;
   {
@@ -1119,18 +1120,18 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
       err = g_status;
       return -1;
     }
-    const std::vector<uint32_t> keyw = gather_key(nullptr, 0, sigma, elem);
+    const std::vector<uint32_t> keyw = gather_key(nullptr, 0, sigma, elem, warps);
     const uint64_t kind = 0x6170706c79ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true, warps),
                              "qsim_jit_apply", err);
     if (!fn) return -1;
   }
   return launch_gather(fn, M, sigma, chunk_log2, k1, k2, const_cast<uint32_t*>(perm), ticket,
-                       blocks, st, err);
+                       blocks, warps, st, err);
 }
 
 int jit_local(const uint32_t* words, int n, int M, int elem, int T, const void* k1, void* k2,

@@ -165,9 +165,10 @@ def test_planned_apply_and_fused(q, M, dtype):
     plan.flags = 0                                       # force the sigma kernels
     ws = q.workspace()
     for cl in sorted({10, min(M, 12), M}):
-        for bps in (1, 2, 8):
+        for bps, thr in ((1, 256), (2, 256), (8, 256), (1, 512)):   # 512: 16-warp NVRTC kernels
             for w in (ws, None):
                 plan.chunk_log2, plan.blocks_per_sm, plan.fused_chunk_log2 = cl, bps, cl
+                plan.cta_threads = thr
                 out = torch.empty_like(k1_d)
                 q.apply_map_planned(plan, perm, k1_d, out, w)
                 outf = torch.empty_like(k1_d)
@@ -176,10 +177,10 @@ def test_planned_apply_and_fused(q, M, dtype):
                 pm = _new_perm(1 << M)
                 q.map_gather_planned(plan, gates, pm, k1_d, outm, w)
                 torch.cuda.synchronize()
-                assert out.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
-                assert outf.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
-                assert outm.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps)
-                assert np.array_equal(_perm_np(pm), _perm_np(perm)), (cl, bps)
+                assert out.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps, thr)
+                assert outf.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps, thr)
+                assert outm.cpu().numpy().tobytes() == ref.tobytes(), (cl, bps, thr)
+                assert np.array_equal(_perm_np(pm), _perm_np(perm)), (cl, bps, thr)
 
 
 @pytest.mark.parametrize("dtype,M", [("c64", 12), ("c64", 14), ("c64", 17), ("c128", 11),
