@@ -265,6 +265,18 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
 int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
                    const void *k1, void *k2, void *workspace, void *stream, int32_t *chosen);
 
+/* qsim_plan_tune_ex -- qsim_plan_tune with a search effort (like FFTW's
+ * planner flags):
+ *   QSIM_TUNE_MEASURE  stages 1-3 (cover variants, chunk size, moves of the
+ *                      runtime counter bits): cfg5 about 10 s, 19.1-19.3 ms
+ *   QSIM_TUNE_PATIENT  all six stages (= qsim_plan_tune): cfg5 about 60 s,
+ *                      17.6-18.0 ms (profiles/r02_tune_trace_cfg5.txt)
+ * Any other effort: QSIM_EINVAL (nothing runs).                            */
+enum { QSIM_TUNE_MEASURE = 1, QSIM_TUNE_PATIENT = 2 };
+int qsim_plan_tune_ex(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
+                      const void *k1, void *k2, void *workspace, void *stream, int32_t effort,
+                      int32_t *chosen);
+
 /* qsim_apply_map_planned -- qsim_apply_map (the same k2, bit for bit) in the
  * traversal order of `plan` (M and dtype are plan->M, plan->dtype).
  *   workspace  device scratch of QSIM_WORKSPACE_BYTES (16-B aligned), reset

@@ -33,6 +33,7 @@ WALK_AUTO, WALK_PER_LANE, WALK_BITSLICED, WALK_JIT = 0, 1, 2, 3
 NOT, CNOT, CCNOT, Z, CZ, CCZ, SWAP = 0, 1, 2, 3, 4, 5, 6
 MAX_GATES = 4096
 MATERIALISED, FUSED = 0, 1
+TUNE_MEASURE, TUNE_PATIENT = 1, 2      # qsim_plan_tune_ex search effort
 
 
 class QsimError(RuntimeError):
@@ -85,6 +86,8 @@ def _load() -> ctypes.CDLL:
     sig["qsim_graph_launch"] = [vp, vp]
     sig["qsim_plan_tune"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp, vp,
                              ctypes.POINTER(i32)]
+    sig["qsim_plan_tune_ex"] = [ctypes.POINTER(Plan), vp, i32, vp, vp, vp, vp, vp, i32,
+                                ctypes.POINTER(i32)]
     sig["qsim_graph_destroy"] = [vp]
     sig["qsim_apply_map_signed"] = [vp, vp, u64, i32, i32, vp, vp, vp]
     sig["qsim_plan_create"] = [vp, i32, i32, i32, ctypes.POINTER(Plan)]
@@ -319,14 +322,22 @@ def plan_create(gates, M: int, dtype="c64") -> Plan:
     return plan
 
 
-def plan_tune(plan: Plan, gates, perm, k1, k2, workspace, stream=None) -> int:
+def plan_tune(plan: Plan, gates, perm, k1, k2, workspace, stream=None, effort=None) -> int:
     """Measure plan variants on these buffers and keep the fastest map + gather
-    in `plan` (returns the variant index; see qsim_plan_tune)."""
+    in `plan` (returns the variant index; see qsim_plan_tune).  effort:
+    None / TUNE_PATIENT (all stages, qsim_plan_tune) or TUNE_MEASURE (stages
+    1-3, qsim_plan_tune_ex)."""
     g, gp, n = _gates(gates)
     chosen = ctypes.c_int32(-1)
-    _check(_lib.qsim_plan_tune(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
-                               _ptr(workspace), _stream(stream), ctypes.byref(chosen)),
-           "qsim_plan_tune")
+    if effort is None:
+        _check(_lib.qsim_plan_tune(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
+                                   _ptr(workspace), _stream(stream), ctypes.byref(chosen)),
+               "qsim_plan_tune")
+    else:
+        _check(_lib.qsim_plan_tune_ex(ctypes.byref(plan), gp, n, _ptr(perm), _ptr(k1), _ptr(k2),
+                                      _ptr(workspace), _stream(stream), int(effort),
+                                      ctypes.byref(chosen)),
+               "qsim_plan_tune_ex")
     return chosen.value
 
 

@@ -1611,8 +1611,16 @@ constexpr int kTuneCompiledRounds = 3;
 
 int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
                    const void* k1, void* k2, void* workspace, void* stream, int32_t* chosen) {
+  return qsim_plan_tune_ex(plan, gates, n_gates, perm, k1, k2, workspace, stream, QSIM_TUNE_PATIENT,
+                           chosen);
+}
+
+int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uint32_t* perm,
+                      const void* k1, void* k2, void* workspace, void* stream, int32_t effort,
+                      int32_t* chosen) {
   g_launches = 0;
   if (!plan || !workspace || !aligned16(workspace)) return QSIM_EINVAL;
+  if (effort != QSIM_TUNE_MEASURE && effort != QSIM_TUNE_PATIENT) return QSIM_EINVAL;
   int rc = plan_validate(plan);
   if (rc) return rc;
   if ((rc = check_gates(gates, n_gates, plan->M))) return rc;
@@ -1814,7 +1822,7 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
         if (!step(swaps, "stage 4", false)) break;
       }
     };
-    swap_rounds(kTuneSwapRounds);
+    if (effort == QSIM_TUNE_PATIENT) swap_rounds(kTuneSwapRounds);
     // fifth stage: exchanges that move a compiled position (counter bits
     // plan_keep_bits..9: lanes and in-thread entries; each order is a new
     // NVRTC kernel, a round's kernels compiled at once on the host's cores)
@@ -1826,7 +1834,8 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
     std::unique_ptr<qsim::GateList<qsim::kMaxGates>> gl(new qsim::GateList<qsim::kMaxGates>);
     pack_gates(gates, n_gates, false, *gl);
     const unsigned hw = std::thread::hardware_concurrency();
-    for (int round = 0; round < kTuneCompiledRounds && rc == QSIM_OK; ++round) {
+    for (int round = 0; effort == QSIM_TUNE_PATIENT && round < kTuneCompiledRounds && rc == QSIM_OK;
+         ++round) {
       std::vector<qsim_plan> cand_plans;
       const int keep = plan_keep_bits(cur.dtype);
       for (int i = keep; i < 10 && i < cur.M; ++i)
@@ -1865,7 +1874,8 @@ int qsim_plan_tune(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, uin
         p.cta_threads = 512;
         launch_cands.push_back(p);
       }
-      if (rc == QSIM_OK && !launch_cands.empty()) step(launch_cands, "stage 6", true);
+      if (effort == QSIM_TUNE_PATIENT && rc == QSIM_OK && !launch_cands.empty())
+        step(launch_cands, "stage 6", true);
     }
     best = std::min(best, cur_t);
     if (rc == QSIM_OK) cands[best_i] = cur;

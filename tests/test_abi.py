@@ -360,6 +360,11 @@ def test_plan_tune_validation(q):
     plan2 = q.plan_create(ph, 16, "c64")
     assert L.qsim_plan_tune(ctypes.byref(plan2), ph.ctypes.data, 1, FAKE, FAKE * 4, FAKE * 8,
                             FAKE * 16, None, None) == q.EINVAL                # phase circuit
+    for effort in (0, 3, -1):                                                 # no such effort
+        assert L.qsim_plan_tune_ex(ctypes.byref(plan), g.ctypes.data, 20, FAKE, FAKE * 4, FAKE * 8,
+                                   FAKE * 16, None, effort, ctypes.byref(chosen)) == q.EINVAL
+    assert L.qsim_plan_tune_ex(ctypes.byref(plan), g.ctypes.data, 20, FAKE, FAKE * 4, FAKE * 8,
+                               None, None, q.TUNE_MEASURE, None) == q.EINVAL  # needs a workspace
 
 
 def test_binding_checks_before_the_c_call(q):

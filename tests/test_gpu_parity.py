@@ -543,7 +543,8 @@ def test_local_tiles_staged_in_shared_memory(q, M, dtype):
     assert out3.cpu().numpy().tobytes() == oracle.apply_map(oracle.build_map(far, M), k1).tobytes()
 
 
-def test_plan_tune_keeps_a_valid_plan(q):
+@pytest.mark.parametrize("effort", [None, 1])   # qsim_plan_tune / qsim_plan_tune_ex MEASURE
+def test_plan_tune_keeps_a_valid_plan(q, effort):
     """qsim_plan_tune measures plan variants and keeps one: the result of its
     own runs and of the tuned plan afterwards equal the oracle's bytes."""
     M = 20
@@ -555,7 +556,7 @@ def test_plan_tune_keeps_a_valid_plan(q):
     plan = q.plan_create(gates, M, "c64")
     plan.flags &= ~1
     pm, out = _new_perm(1 << M), torch.empty_like(k1_d)
-    chosen = q.plan_tune(plan, gates, pm, k1_d, out, q.workspace())
+    chosen = q.plan_tune(plan, gates, pm, k1_d, out, q.workspace(), effort=effort)
     assert 0 <= chosen <= 5
     torch.cuda.synchronize()
     assert out.cpu().numpy().tobytes() == ref.tobytes()
