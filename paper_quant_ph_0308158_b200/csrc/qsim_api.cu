@@ -259,7 +259,7 @@ int range_block_bits(int M, uint64_t start, uint64_t count) {
 
 // jmax: in-thread bits are chosen below min(L, jmax)
 void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t count, int maxv,
-                 bool require_affine, ThreadBits* tb, int jmax = 64) {
+                 bool require_affine, ThreadBits* tb, int jmax = 64, bool store_order = false) {
   for (int k = 0; k < 5; ++k) tb->J[k] = (uint8_t)(5 + k);
   tb->L = 10;
   tb->V = 0;
@@ -301,6 +301,47 @@ void thread_bits(const qsim_gate* g, int n, int M, uint64_t start, uint64_t coun
     J[k] = best;
     Jm |= 1ull << best;
     V |= infl[best];
+  }
+  if (store_order) {
+    // the on-the-fly input is bound by its store pattern: every 5-subset of
+    // in-thread bits whose sources vary in at most maxv bits, preferring one
+    // that holds output bit 6 (then 7), then the fewest varying bits, then
+    // the lowest bits.  The stores alone (tools/mb/mb_store_kron.cu): J with
+    // bit 6 -- 6.7.8.13.26, 6.7.26.29.30 -- 5.00 ms like J = 5..9, J without
+    // it 5.18-5.26 ms (profiles/r02_mb_store_kron_j.jsonl); the kernel:
+    // cfg5 5.35 -> 5.15 ms, the M = 40 portion 5.36 -> 5.19 ms
+    // (profiles/r02_kron_j_ab.txt)
+    long best_key = -1;
+    int bj[5] = {0, 0, 0, 0, 0};
+    const int lo = 5, hi = jtop;
+    for (int a = lo; a < hi; ++a)
+      for (int b = a + 1; b < hi; ++b)
+        for (int c = b + 1; c < hi; ++c) {
+          const uint64_t vabc = infl[a] | infl[b] | infl[c];
+          if (__builtin_popcountll(vabc) > maxv) continue;
+          for (int d = c + 1; d < hi; ++d) {
+            const uint64_t vabcd = vabc | infl[d];
+            if (__builtin_popcountll(vabcd) > maxv) continue;
+            for (int e = d + 1; e < hi; ++e) {
+              const int nv = __builtin_popcountll(vabcd | infl[e]);
+              if (nv > maxv) continue;
+              const uint64_t jm = (1ull << a) | (1ull << b) | (1ull << c) | (1ull << d) | (1ull << e);
+              const long key = ((long)(!((jm >> 6) & 1ull)) << 40) | ((long)(!((jm >> 7) & 1ull)) << 32) |
+                               ((long)nv << 16) | (long)(a + b + c + d + e);
+              if (best_key < 0 || key < best_key) {
+                best_key = key;
+                bj[0] = a, bj[1] = b, bj[2] = c, bj[3] = d, bj[4] = e;
+              }
+            }
+          }
+        }
+    if (best_key >= 0) {
+      V = 0;
+      for (int k = 0; k < 5; ++k) {
+        J[k] = bj[k];
+        V |= infl[bj[k]];
+      }
+    }
   }
   std::sort(J, J + 5);
   V = 0;
@@ -426,7 +467,7 @@ void kron_layout(const qsim_gate* g, int n, int M, int gb, int ng, uint64_t star
     const bool hit = c.env == env && c.M == M && c.maxv == gb && c.gates.size() == (size_t)n &&
                      (n == 0 || std::memcmp(c.gates.data(), g, sizeof(qsim_gate) * n) == 0);
     if (!hit) {
-      thread_bits(g, n, M, 0, 1ull << M, gb, false, &c.tb, M > 32 ? 28 : 64);
+      thread_bits(g, n, M, 0, 1ull << M, gb, false, &c.tb, M > 32 ? 28 : 64, true);
       c.gates.assign(g, g + n);
       c.env = env;
       c.M = M, c.maxv = gb, c.start = 0, c.count = 1ull << M;

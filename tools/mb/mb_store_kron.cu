@@ -81,7 +81,7 @@ __global__ void k_seq(uint2* out, uint64_t n) {
     __stcs(out + t, make_uint2(1u, 2u));
 }
 
-int main() {
+int main(int argc, char** argv) {
   const uint64_t n = 1ull << 32, bytes = n * 8;
   uint2* out;
   if (cudaMalloc(&out, bytes) != cudaSuccess) return 1;
@@ -104,6 +104,17 @@ int main() {
     printf("{\"case\": \"%s\", \"ms\": %.3f, \"GBps\": %.0f, \"err\": \"%s\"}\n", name, best,
            bytes / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
   };
+  if (argc > 1) {  // J sets given as a.b.c.d.e: the kernel's store pattern for each (rot none)
+    for (int i = 1; i < argc; ++i) {
+      int J[5];
+      if (sscanf(argv[i], "%d.%d.%d.%d.%d", &J[0], &J[1], &J[2], &J[3], &J[4]) != 5) continue;
+      char nm[128];
+      snprintf(nm, sizeof nm, "kron tiles J=%s", argv[i]);
+      run(nm, [&] { k_tile_j<<<sms * 8, 256>>>(out, n >> 10, J[0], J[1], J[2], J[3], J[4], 0); });
+    }
+    cudaFree(out);
+    return 0;
+  }
   run("seq u64 grid=16xSM", [&] { k_seq<<<sms * 16, 256>>>(out, n); });
   for (int g : {8, 16, 32}) {
     char nm[64];
