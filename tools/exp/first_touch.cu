@@ -59,6 +59,17 @@ __device__ __forceinline__ uint2 ldg2(const uint2* p) {
   asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
   return r;
 }
+template <int Q>
+__device__ __forceinline__ uint2 ldq2(const uint2* p) {
+  uint2 r;
+  if (Q == 0)
+    asm volatile("ld.global.nc.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  else if (Q == 1)
+    asm volatile("ld.global.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  else
+    asm volatile("ld.global.nc.L1::evict_last.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p) : "memory");
+  return r;
+}
 __device__ __forceinline__ void stcs2(uint2* p, uint2 v) {
   asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
@@ -199,6 +210,15 @@ __global__ void __launch_bounds__(256) k_gather(u64 N, u32 chunk_log2, u64* tick
           for (int l = 0; l < 16; ++l) stcs2(k2 + (ob ^ lt[h + l] ^ lo), v[l]);
           __syncwarp();
         }
+      } else if (MODE >= 8) {  // k1 gathers with other load flavours
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {
+          uint2 v[16];
+#pragma unroll
+          for (int l = 0; l < 16; ++l) v[l] = ldq2<MODE - 8>(k1 + a[h + l]);
+#pragma unroll
+          for (int l = 0; l < 16; ++l) stcs2(k2 + (ob ^ lt[h + l] ^ lo), v[l]);
+        }
       } else {
 #pragma unroll
       for (int h = 0; h < 32; h += 16) {
@@ -237,6 +257,9 @@ int ft_gather(int mode, u64 N, u32 chunk_log2, u64* ticket, const void* k1, void
     case 3: k_gather<3><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 4: k_gather<4><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 5: k_gather<5><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 8: k_gather<8><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 9: k_gather<9><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
+    case 10: k_gather<10><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 7: k_gather<7><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     case 6: k_gather<6><<<ctas, 256, 0, st>>>(N, chunk_log2, ticket, a, b, perm, bitmap, t, sink); break;
     default: return -1;

@@ -36,8 +36,8 @@ def main():
     perm = torch.empty(N, dtype=torch.int32, device=dev)
     q.build_map(gates, M, perm)
     tuned = json.load(open(os.path.join(ROOT, "profiles", "r02_tuned_plan_cfg5.json")))["sigma"]
-    orders = {"tuned": tuned}
-    for k in [int(x) for x in os.environ.get("OS_FORCE", "5,6,7,8,9,10").split(",")]:
+    orders = {} if os.environ.get("OS_NO_TUNED") == "1" else {"tuned": tuned}
+    for k in [int(x) for x in os.environ.get("OS_FORCE", "5,6,7,8,9,10").split(",") if x]:
         orders[f"low{k}"] = list(range(k)) + [b for b in tuned if b >= k]
     extra = os.environ.get("OS_SIGMA")
     if extra:
