@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--mmin", type=int, default=20)
     ap.add_argument("--mmax", type=int, default=32)
     ap.add_argument("--kron-max", type=int, default=40)
+    ap.add_argument("--tune", default="none", choices=["none", "measure", "patient"],
+                    help="qsim_plan_tune_ex effort per M (outside the timings)")
     args = ap.parse_args()
     print("M,entries,map_gather_ms,build_ms,apply_ms,fused_ms,entries_per_s,growth_per_bit,"
           "plan_natural")
@@ -46,6 +48,9 @@ def main():
         perm = torch.empty(N, dtype=torch.int32, device="cuda")
         ws = q.workspace()
         plan = q.plan_create(gates, M, "c64")
+        if args.tune != "none" and not (plan.flags & 1):
+            q.plan_tune(plan, gates, perm, k1, k2, ws,
+                        effort=q.TUNE_MEASURE if args.tune == "measure" else q.TUNE_PATIENT)
         t_mg = timeit(lambda: q.map_gather_planned(plan, gates, perm, k1, k2, ws))
         t_b = timeit(lambda: q.build_map(gates, M, perm))
         t_a = timeit(lambda: q.apply_map_planned(plan, perm, k1, k2, ws))
