@@ -271,7 +271,9 @@ int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uin
  *                      runtime counter bits): cfg5 about 10 s, 19.1-19.3 ms
  *   QSIM_TUNE_PATIENT  all six stages (= qsim_plan_tune): cfg5 about 60 s,
  *                      17.6-18.0 ms (profiles/r02_tune_trace_cfg5.txt)
- * Any other effort: QSIM_EINVAL (nothing runs).                            */
+ * Any other effort: QSIM_EINVAL (nothing runs).  The kernels compiled for
+ * the candidates stay in the process's JIT cache (PATIENT at M = 32: about
+ * 500 modules of tens of KB of device code each).                          */
 enum { QSIM_TUNE_MEASURE = 1, QSIM_TUNE_PATIENT = 2 };
 int qsim_plan_tune_ex(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
                       const void *k1, void *k2, void *workspace, void *stream, int32_t effort,
