@@ -422,7 +422,7 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // built from it), so qsim_plan_tune can try orders of the high counter bits
 // without recompiling.
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem,
-                         bool from_perm, int warps = 8, bool store_ex = true) {
+                         bool from_perm, int warps = 8) {
   std::string s = kPrelude;
   char buf[256];
   std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n",
@@ -507,124 +507,24 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   s += R"(
       const u32 lo = tab[0][lane];   // output bits of the lane: sigma(lane)
 )";
-  // Store layout.  The plan picks the lanes for the k1 reads; before the
-  // stores, lane bits are exchanged with in-thread entry bits (warp shuffles:
-  // lane position p <-> entry bit w-5) so that the lanes hold the 5 lowest
-  // output bits of the warp tile -- the longest contiguous runs per store
-  // instruction.  ss = the store order, ex = the exchanges.
-  uint8_t ss[10];
-  for (int k = 0; k < 10; ++k) ss[k] = sigma[k];
-  std::vector<std::pair<int, int>> ex;
-  if (store_ex && M >= 10) {
-    uint8_t srt[10];
-    std::memcpy(srt, sigma, 10);
-    std::sort(srt, srt + 10);
-    auto low = [&](uint8_t b) { return std::find(srt, srt + 5, b) != srt + 5; };
-    const int wmax = elem == 8 ? 10 : 9;  // complex128: exchanges inside 16-entry batches
-    for (int p = 0; p < 5; ++p) {
-      if (low(ss[p])) continue;
-      for (int w = 5; w < wmax; ++w)
-        if (low(ss[w])) {
-          std::swap(ss[p], ss[w]);
-          ex.push_back({p, w});
-          break;
-        }
-    }
-  }
-  const bool exch = !ex.empty();
-  if (exch) {
-    s += "      const u32 lts[32] = {";
-    for (int l = 0; l < 32; ++l) {
-      uint32_t o = 0u;
-      for (int j = 0; j < 5; ++j)
-        if ((l >> j) & 1) o ^= 1u << ss[5 + j];
-      std::snprintf(buf, sizeof buf, "%uu%s", o, l < 31 ? ", " : "};\n");
-      s += buf;
-    }
-    std::snprintf(buf, sizeof buf,
-                  "      const u32 los = ((lane & 1u) ? %uu : 0u) | ((lane & 2u) ? %uu : 0u) | "
-                  "((lane & 4u) ? %uu : 0u) | ((lane & 8u) ? %uu : 0u) | ((lane & 16u) ? %uu : 0u);\n",
-                  1u << ss[0], 1u << ss[1], 1u << ss[2], 1u << ss[3], 1u << ss[4]);
-    s += buf;
-  }
-  // the exchanges on an array X[0..n) of entries (entry index bit j = word bit j)
-  auto exchange = [&](const char* X, int nent, bool vec, int comps) {
-    std::string e;
-    for (const auto& pw : ex) {
-      const int p = pw.first, wb = pw.second - 5;
-      if ((1 << wb) >= nent) continue;
-      std::snprintf(buf, sizeof buf, "      { const bool hi = (lane >> %d) & 1u;\n", p);
-      e += buf;
-      for (int l0 = 0; l0 < nent; ++l0) {
-        if ((l0 >> wb) & 1) continue;
-        const int l1 = l0 | (1 << wb);
-        if (!vec) {
-          std::snprintf(buf, sizeof buf,
-                        "        { const u32 t = __shfl_xor_sync(0xffffffffu, hi ? %s[%d] : %s[%d], %d);"
-                        " if (hi) %s[%d] = t; else %s[%d] = t; }\n",
-                        X, l0, X, l1, 1 << p, X, l0, X, l1);
-          e += buf;
-        } else {
-          const char* cn[4] = {"x", "y", "z", "w"};
-          std::snprintf(buf, sizeof buf, "        { QSIM_T t = hi ? %s[%d] : %s[%d];", X, l0, X, l1);
-          e += buf;
-          for (int c = 0; c < comps; ++c) {
-            std::snprintf(buf, sizeof buf, " t.%s = __shfl_xor_sync(0xffffffffu, t.%s, %d);", cn[c], cn[c], 1 << p);
-            e += buf;
-          }
-          std::snprintf(buf, sizeof buf, " if (hi) %s[%d] = t; else %s[%d] = t; }\n", X, l0, X, l1);
-          e += buf;
-        }
-      }
-      e += "      }\n";
-    }
-    return e;
-  };
-  const int comps = elem == 8 ? 2 : 4;
   if (from_perm)  // the apply: sources read from the materialised map (32-B runs)
     s += R"(
       u32 a[32];
       const u32 sg = 0u;
       _Pragma("unroll") for (int l = 0; l < 32; ++l) a[l] = __ldcs(perm_out + (ob ^ lt[l] ^ lo));
 )";
-  else if (!(exch && elem == 8))
+  else
     s += R"(
       if (perm_out) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob ^ lt[l] ^ lo), a[l]);
       }
 )";
-  if (!exch) {
-    s += R"(
+  s += R"(
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
           stcs(k2 + (ob ^ lt[h + l] ^ lo), negate_if(v[l], (sg >> (h + l)) & 1u));
-      }
-    }
-  }
-}
-)";
-    return s;
-  }
-  // exchanged stores: the loads first (they consume a[]), then -- complex64,
-  // one batch of 32 -- the map in the store layout while the loads are in
-  // flight, then k2
-  s += R"(
-      _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
-        QSIM_T v[QSIM_B];
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
-)";
-  if (!from_perm && elem == 8) {
-    s += "        if (perm_out) {\n";
-    s += exchange("a", 32, false, 1);
-    s += "          _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob ^ lts[l] ^ los), a[l]);\n";
-    s += "        }\n";
-  }
-  s += "        _Pragma(\"unroll\") for (int l = 0; l < QSIM_B; ++l) v[l] = negate_if(v[l], (sg >> (h + l)) & 1u);\n";
-  s += exchange("v", elem == 8 ? 32 : 16, true, comps);
-  s += R"(
-        _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) stcs(k2 + (ob ^ lts[h + l] ^ los), v[l]);
       }
     }
   }
@@ -1053,15 +953,8 @@ int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log
 
 // cache key of a gather kernel: what shapes its code (sigma[0..9], the dtype
 // and, for the fused walk, the gates)
-// A/B switch of the exchanged store layout (fused_source); part of the key
-bool store_ex_enabled() {
-  const char* e = std::getenv("QSIM_STORE_EX");
-  return !(e && e[0] == '0');
-}
-
 std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem, int warps) {
   std::vector<uint32_t> keyw(words, words + n);
-  keyw.push_back(store_ex_enabled() ? 1u : 0u);
   for (int k = 0; k < 10; ++k) keyw.push_back(sigma[k]);
   keyw.push_back((uint32_t)elem);
   keyw.push_back((uint32_t)warps);
@@ -1086,7 +979,7 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
     for (const Entry& e : g_cache[key])  // the source is only generated on a cache miss
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps, store_ex_enabled()),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps),
                              "qsim_jit_fused", err);
     if (!fn) return -1;
   }
@@ -1113,7 +1006,7 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
       for (const auto& k : keys) have = have || k == keyw;
       if (have) continue;
       keys.push_back(keyw);
-      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps, store_ex_enabled()));
+      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps));
     }
   }
   const size_t m = keys.size();
@@ -1233,7 +1126,7 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true, warps, store_ex_enabled()),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true, warps),
                              "qsim_jit_apply", err);
     if (!fn) return -1;
   }
