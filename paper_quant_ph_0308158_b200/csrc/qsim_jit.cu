@@ -1019,7 +1019,13 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
   };
   const int nt = (int)std::min<size_t>(m, (size_t)std::max(1, threads));
   std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+  for (int t = 1; t < nt; ++t) {
+    try {
+      pool.emplace_back(work);
+    } catch (...) {  // no more threads: the ones running (and this one) finish the list
+      break;
+    }
+  }
   work();
   for (auto& t : pool) t.join();
   int done = 0;
