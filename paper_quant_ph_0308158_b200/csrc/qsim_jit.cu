@@ -421,12 +421,15 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // kernel parameter (the tile offset `ob` comes from 4 shared-memory tables
 // built from it), so qsim_plan_tune can try orders of the high counter bits
 // without recompiling.
+// ident: sigma is the identity over all M positions (natural order; the
+// kernel then skips the order tables -- the runtime tail is ignored)
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem,
-                         bool from_perm, int warps = 8) {
+                         bool from_perm, int warps = 8, bool ident = false) {
   std::string s = kPrelude;
   char buf[256];
-  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n",
-                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16, warps);
+  std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n"
+                "#define QSIM_IDENT %d\n",
+                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16, warps, ident ? 1 : 0);
   s += buf;
   s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
   s += R"(
@@ -434,8 +437,11 @@ struct Sigma { unsigned char s[32]; };
 extern "C" __global__ void __launch_bounds__(32 * QSIM_W)
 QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
            QSIM_T* __restrict__ k2, u32* __restrict__ perm_out, const Sigma sig) {
-  __shared__ u32 tab[4][256];
   __shared__ u64 s_chunk;
+#if QSIM_IDENT   // natural order: output = counter, no tables
+  (void)sig;
+#else
+  __shared__ u32 tab[4][256];
   for (int x = threadIdx.x; x < 1024; x += blockDim.x) {
     const int b = x >> 8, v = x & 255;
     u32 r = 0;
@@ -444,6 +450,7 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
     tab[b][v] = r;
   }
   __syncthreads();
+#endif
   const u32 lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const u64 nchunks = N >> chunk_log2;
   const u32 tiles = 1u << (chunk_log2 - 10);
@@ -462,8 +469,12 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
     if (ch >= nchunks) break;
     for (u32 tt = warp; tt < tiles; tt += QSIM_W) {
       const u64 c = (ch << chunk_log2) + ((u64)tt << 10);
+#if QSIM_IDENT
+      const u32 ob = (u32)c;
+#else
       const u32 ob = tab[0][c & 255] | tab[1][(c >> 8) & 255] | tab[2][(c >> 16) & 255] |
                      tab[3][(c >> 24) & 255];
+#endif
 )";
   if (!from_perm) {
     // plane initialisation: output bit b comes from counter bit inv[b]: a
@@ -505,7 +516,11 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
     s += buf;
   }
   s += R"(
+#if QSIM_IDENT
+      const u32 lo = lane;
+#else
       const u32 lo = tab[0][lane];   // output bits of the lane: sigma(lane)
+#endif
 )";
   if (from_perm)  // the apply: sources read from the materialised map (32-B runs)
     s += R"(
@@ -953,8 +968,16 @@ int launch_gather(CUfunction fn, int M, const uint8_t* sigma, uint32_t chunk_log
 
 // cache key of a gather kernel: what shapes its code (sigma[0..9], the dtype
 // and, for the fused walk, the gates)
-std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem, int warps) {
+bool sigma_ident(const uint8_t* sigma, int M) {
+  for (int k = 0; k < M && k < 32; ++k)
+    if (sigma[k] != k) return false;
+  return true;
+}
+
+std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem, int warps,
+                                 int M) {
   std::vector<uint32_t> keyw(words, words + n);
+  keyw.push_back(sigma_ident(sigma, M) ? 1u : 0u);
   for (int k = 0; k < 10; ++k) keyw.push_back(sigma[k]);
   keyw.push_back((uint32_t)elem);
   keyw.push_back((uint32_t)warps);
@@ -973,13 +996,13 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
       err = g_status;
       return -1;
     }
-    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem, warps);
+    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem, warps, M);
     const uint64_t kind = 0x66757365ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])  // the source is only generated on a cache miss
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps, sigma_ident(sigma, M)),
                              "qsim_jit_fused", err);
     if (!fn) return -1;
   }
@@ -999,14 +1022,14 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
     if (!(g_nvrtc.ok && g_drv.ok)) return -1;
     for (int i = 0; i < count; ++i) {
       const uint8_t* sg = sigmas + 32 * i;
-      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem, warps);
+      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem, warps, M);
       const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
       bool have = false;
       for (const Entry& e : g_cache[key]) have = have || (e.M == M && e.words == keyw);
       for (const auto& k : keys) have = have || k == keyw;
       if (have) continue;
       keys.push_back(keyw);
-      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps));
+      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps, sigma_ident(sg, M)));
     }
   }
   const size_t m = keys.size();
@@ -1126,13 +1149,13 @@ int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const 
       err = g_status;
       return -1;
     }
-    const std::vector<uint32_t> keyw = gather_key(nullptr, 0, sigma, elem, warps);
+    const std::vector<uint32_t> keyw = gather_key(nullptr, 0, sigma, elem, warps, M);
     const uint64_t kind = 0x6170706c79ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true, warps),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(nullptr, 0, M, sigma, elem, true, warps, sigma_ident(sigma, M)),
                              "qsim_jit_apply", err);
     if (!fn) return -1;
   }
@@ -1199,7 +1222,7 @@ int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(nullptr, 0, M, sigma, elem, true), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(nullptr, 0, M, sigma, elem, true, 8, sigma_ident(sigma, M)), cubin, err) ? 0 : -1;
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
@@ -1211,7 +1234,7 @@ int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(words, n, M, sigma, elem, false), cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(words, n, M, sigma, elem, false, 8, sigma_ident(sigma, M)), cubin, err) ? 0 : -1;
 }
 
 }  // namespace qsim
