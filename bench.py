@@ -497,6 +497,7 @@ def run_qsim(args):
     with sampler:
         ms_mg, launches_mg, kern_mg = timed_loop(step_map_gather, args.steps, args.warmup,
                                                  per_kernel=True, name="map_gather")
+        kern_name_mg = q.last_kernel()
         # the timed step's own output, checked against the oracle before any
         # other loop overwrites perm / k2
         verified = verify_sample(gates, M, e, perm, k2, k1_host, cfg, dev)
@@ -676,8 +677,13 @@ def run_qsim(args):
     k40_ms = statistics.mean(kern_k40["fused_kron40"])
     ms_step = ms_mg / args.steps
     achieved = bytes_mg / (mg_ms * 1e-3) / 1e9
-    mg_kernel = ("qsim_jit_fused (NVRTC, circuit-specialised, perm + gather)"
-                 if launches_mg == args.steps else "k_build/k_apply_sigma (no JIT)")
+    split = bool(plan.flags & q.PLAN_SPLIT)
+    if split:
+        mg_kernel = (f"{kern_name_mg}: the planned gather (NVRTC, circuit-specialised, k2 only) "
+                     "then the natural-order build (perm), two launches per step")
+    else:
+        mg_kernel = (f"{kern_name_mg} (NVRTC, circuit-specialised, perm + gather, one launch)"
+                     if launches_mg == args.steps else f"{kern_name_mg} (no JIT)")
 
     def gbps(b, ms):
         return b / (ms * 1e-3) / 1e9
@@ -699,7 +705,9 @@ def run_qsim(args):
                    "n_gates": int(gates.shape[0]), "state_dtype": "complex64" if e == 8 else
                    "complex128",
                    "step": "qsim_map_gather_planned: materialised map (perm, uint32) + gather "
-                           "k2 = k1[perm], one kernel",
+                           "k2 = k1[perm]" + (" -- two kernels (plan flag QSIM_PLAN_SPLIT: "
+                                              "planned gather, then natural-order build)"
+                                              if split else ", one kernel"),
                    "l2": "inputs larger than L2 (k1, k2 %d GiB each; perm %d GiB)"
                    % (N * e >> 30, N * 4 >> 30), "parallelism": f"replicas x{world}"},
         "achieved_GBps": gbps(bytes_mg, ms_step),
@@ -707,7 +715,20 @@ def run_qsim(args):
         "roofline": {"bound": "hbm", "kernel": mg_kernel, "achieved": achieved,
                      "peak": hbm, "peak_source": hbm_src, "unit": "GB/s",
                      "frac": achieved / hbm, "frac_of_8TBps": achieved * 1e9 / 8e12,
-                     "traffic": ncu_traffic(args.config, "map_gather"),
+                     "traffic": ncu_traffic(args.config, "map_gather_split" if split
+                                            else "map_gather"),
+                     "scope": ("the step's two launches together (the call's CUDA-event "
+                               "duration); per launch in per_kernel" if split else
+                               "the step's one launch"),
+                     "per_kernel": ({
+                         "gather": {"kernel": "qsim_jit_fused (same plan, same kernel instance as "
+                                              "modes.run_fused)", "ms": fused_ms,
+                                    "bytes_per_entry": 2 * e, "GBps": gbps(bytes_fused, fused_ms),
+                                    "frac": gbps(bytes_fused, fused_ms) / hbm},
+                         "build": {"kernel": "qsim_jit_build (natural order, as modes.build_map)",
+                                   "ms": build_ms, "bytes_per_entry": 4,
+                                   "GBps": gbps(bytes_build, build_ms),
+                                   "frac": gbps(bytes_build, build_ms) / hbm}} if split else None),
                      "algorithmic_bytes_per_launch": bytes_mg,
                      "algorithmic_bytes_per_entry": 4 + 2 * e,
                      "note": "DRAM traffic ~1.04x algorithmic (ncu); bound: the random k1 reads, "
@@ -774,7 +795,9 @@ def run_qsim(args):
         "plan": {"seconds": t_plan, "tune_seconds": t_tune, "tuned_variant": tuned,
                  "sigma": list(plan.sigma)[:M], "chunk_log2": plan.chunk_log2,
                  "fused_chunk_log2": plan.fused_chunk_log2, "blocks_per_sm": plan.blocks_per_sm,
-                 "natural_order": bool(plan.flags & 1), "sector_cover_bits": plan.tile_log2,
+                 "natural_order": bool(plan.flags & 1), "split": split,
+                 "cta_threads": plan.cta_threads, "flags": plan.flags,
+                 "sector_cover_bits": plan.tile_log2,
                  "sector_pairs_contained": plan.tile_contained,
                  "note": "qsim_plan_create (host sampling of the circuit) and qsim_plan_tune "
                          "(measured variants) run once per circuit, outside the timed region, "

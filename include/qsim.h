@@ -203,6 +203,7 @@ int qsim_run_fused_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
  * and fills `plan`, a plain value owned by the caller.  chunk_log2 and
  * blocks_per_sm may be edited before use (tuning).                          */
 #define QSIM_WORKSPACE_BYTES 256
+#define QSIM_PLAN_SPLIT 4u  /* qsim_plan.flags bit 2 (below) */
 
 typedef struct qsim_plan {
     int32_t M;
@@ -217,7 +218,15 @@ typedef struct qsim_plan {
                                (complex128), so each aligned tile of 2^T outputs reads
                                its own tile of k1: map+gather and fused use the
                                shared-memory staged kernel (TMA bulk copies of k1
-                               tiles, double-buffered), re-checked on the gates given */
+                               tiles, double-buffered), re-checked on the gates given.
+                               bit 2 (QSIM_PLAN_SPLIT, sigma plans only): the map +
+                               gather step runs as two kernels -- the planned gather
+                               with the map recomputed in registers (k2 only), then
+                               the natural-order build (perm in coalesced runs) --
+                               instead of one kernel storing perm in plan order;
+                               same bytes, set by qsim_plan_tune when it measures
+                               faster (the scattered perm runs cost a DRAM row
+                               activation each)                                   */
     uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
     uint16_t cta_threads;   /* CTA size: 256, 512 or 1024 (0 = 256); the NVRTC
                                gather kernels run 16 warps for 512, else 8     */
@@ -260,7 +269,9 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * its kernel), so perm and k2 hold a valid result afterwards; the call
  * synchronises `stream` (cfg5: about 60 s).  plan: in (chunk sizes, residency kept) /
  * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
- * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit).
+ * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit;
+ * + 8: the same order as the two-kernel step, flag QSIM_PLAN_SPLIT -- every
+ * sigma variant is also timed that way in the first stage).
  * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */
 int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
                    const void *k1, void *k2, void *workspace, void *stream, int32_t *chosen);

@@ -47,6 +47,7 @@ class QsimError(RuntimeError):
 
 
 WORKSPACE_BYTES = 256
+PLAN_SPLIT = 4                         # qsim_plan.flags bit 2 (QSIM_PLAN_SPLIT)
 
 
 class Plan(ctypes.Structure):

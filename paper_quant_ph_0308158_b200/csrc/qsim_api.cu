@@ -1350,6 +1350,17 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
       overlap(perm, N * 4, k1, N * e))
     return QSIM_EALIAS;
   if (local_dispatch(plan, gates, n, k1, k2, perm, workspace, st)) return QSIM_OK;
+  if ((plan->flags & QSIM_PLAN_SPLIT) && !plan_natural(plan)) {
+    // two kernels, each at its own best pattern: the planned gather with the
+    // map recomputed in registers (k2 only), then the natural-order build
+    // (perm written in coalesced runs instead of the gather's scattered
+    // 64-128-byte runs, which cost one DRAM row activation each)
+    bool jit = false;
+    if ((rc = fused_sigma_dispatch(plan, gates, n, k1, k2, nullptr, workspace, st, &jit))) return rc;
+    if ((rc = build_impl(gates, n, M, 0, N, perm, QSIM_WALK_AUTO, st))) return rc;
+    g_last_kernel = jit ? "qsim_jit_fused + qsim_jit_build" : "k_fused_sigma + build";
+    return QSIM_OK;
+  }
   if (!plan_natural(plan) || M >= 13) {
     const qsim_plan nat = natural_view(plan);
     const qsim_plan* pp = plan_natural(plan) ? &nat : plan;
@@ -1710,6 +1721,16 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
       idx.push_back((int)i);
     }
   }
+  // each sigma variant also as the two-kernel step (planned gather, then the
+  // natural-order build): cfg5 14.9 + 2.7 ms against 18.0 ms for one kernel
+  // storing perm in plan order (profiles/r02_concurrent_build.txt)
+  for (size_t i = 0, nc = cands.size(); i < nc; ++i)
+    if (!plan_natural(&cands[i]) && !(cands[i].flags & 2u)) {
+      qsim_plan p = cands[i];
+      p.flags |= QSIM_PLAN_SPLIT;
+      cands.push_back(p);
+      idx.push_back(idx[i] + 8);
+    }
   cudaEvent_t a = nullptr, b = nullptr;
   cudaError_t ce;
   if ((ce = cudaEventCreate(&a)) != cudaSuccess || (ce = cudaEventCreate(&b)) != cudaSuccess) {
