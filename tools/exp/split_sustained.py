@@ -43,9 +43,11 @@ variant = q.plan_tune(plan, gates, perm, k1, k2, ws)
 tune_s = time.time() - t0
 ref_perm, ref_k2 = perm.clone(), k2.clone()
 
-toggled = q.Plan.from_buffer_copy(plan)
-toggled.flags ^= q.PLAN_SPLIT
-plans = {"tuned": plan, "toggled": toggled}
+plans = {"tuned": plan}
+for nm, form in (("one_kernel", 0), ("split", q.PLAN_SPLIT), ("natmap", q.PLAN_NATMAP)):
+    o = q.Plan.from_buffer_copy(plan)
+    o.flags = (o.flags & ~(q.PLAN_SPLIT | q.PLAN_NATMAP)) | form
+    plans[nm + "(same order)"] = o
 rec_path = os.path.join(ROOT, "profiles", "r02_tuned_plan_cfg5_s6.json")
 if cfg is wl.CONFIGS["cfg5"] and os.path.exists(rec_path):
     rec = json.load(open(rec_path))
@@ -87,6 +89,13 @@ def fused_loop(p):
     return a.elapsed_time(b) / STEPS
 
 
+ok = {}
+for name, p in plans.items():               # warm (compiles) + byte check against the tuner's result
+    perm.fill_(-1)
+    k2.fill_(0)
+    q.map_gather_planned(p, gates, perm, k1, k2, ws)
+    torch.cuda.synchronize()
+    ok[name] = bool(torch.equal(perm, ref_perm) and torch.equal(k2, ref_k2))
 res = {n: [] for n in plans}
 res["fused(tuned)"] = []
 for _ in range(int(os.environ.get("SC_REPS", "4"))):
@@ -94,6 +103,6 @@ for _ in range(int(os.environ.get("SC_REPS", "4"))):
         res[n].append(loop(p))
     res["fused(tuned)"].append(fused_loop(plan))
 out = {"variant": variant, "tune_s": tune_s, "flags": plan.flags, "sigma": list(plan.sigma)[:M],
-       "steps_per_loop": STEPS, "ms_per_step_each_loop": res,
+       "bytes_equal": ok, "steps_per_loop": STEPS, "ms_per_step_each_loop": res,
        "ms_mean": {n: sum(v) / len(v) for n, v in res.items()}}
 print(json.dumps(out))
