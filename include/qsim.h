@@ -204,7 +204,6 @@ int qsim_run_fused_ex(const qsim_gate *gates, int32_t n_gates, int32_t M,
  * blocks_per_sm may be edited before use (tuning).                          */
 #define QSIM_WORKSPACE_BYTES 256
 #define QSIM_PLAN_SPLIT 4u  /* qsim_plan.flags bit 2 (below) */
-#define QSIM_PLAN_NATMAP 8u /* qsim_plan.flags bit 3 (below) */
 
 typedef struct qsim_plan {
     int32_t M;
@@ -227,14 +226,7 @@ typedef struct qsim_plan {
                                instead of one kernel storing perm in plan order;
                                same bytes, set by qsim_plan_tune when it measures
                                faster (the scattered perm runs cost a DRAM row
-                               activation each).
-                               bit 3 (QSIM_PLAN_NATMAP, sigma plans only, NVRTC): one
-                               kernel that gathers in plan order and, per counter
-                               tile c, walks the natural tile [c, c + 1024) a second
-                               time and stores its map in coalesced runs (perm's
-                               sequential writes interleave with the gather); same
-                               bytes, set by qsim_plan_tune when it measures faster.
-                               SPLIT wins if both are set.                        */
+                               activation each)                                   */
     uint16_t ilp;           /* gathers in flight per thread: 8, 16 or 32 (0 = 16) */
     uint16_t cta_threads;   /* CTA size: 256, 512 or 1024 (0 = 256); the NVRTC
                                gather kernels run 16 warps for 512, else 8     */
@@ -278,9 +270,8 @@ int qsim_plan_create(const qsim_gate *gates, int32_t n_gates, int32_t M, int32_t
  * synchronises `stream` (cfg5: about 60 s).  plan: in (chunk sizes, residency kept) /
  * out; chosen (may be NULL): index of the variant kept (0 default rule, 1
  * rule + lanes 0..4, 2 full cover, 3 full + lanes, 4/5 full 11/12-bit;
- * + 8: the same order as the two-kernel step, flag QSIM_PLAN_SPLIT; + 16:
- * as one kernel storing the map in natural order, QSIM_PLAN_NATMAP -- every
- * sigma variant is also timed those two ways in the first stage).
+ * + 8: the same order as the two-kernel step, flag QSIM_PLAN_SPLIT -- every
+ * sigma variant is also timed that way in the first stage).
  * QSIM_EINVAL for phase circuits (the map + gather step refuses them).     */
 int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
                    const void *k1, void *k2, void *workspace, void *stream, int32_t *chosen);

@@ -48,7 +48,6 @@ class QsimError(RuntimeError):
 
 WORKSPACE_BYTES = 256
 PLAN_SPLIT = 4                         # qsim_plan.flags bit 2 (QSIM_PLAN_SPLIT)
-PLAN_NATMAP = 8                        # qsim_plan.flags bit 3 (QSIM_PLAN_NATMAP)
 
 
 class Plan(ctypes.Structure):

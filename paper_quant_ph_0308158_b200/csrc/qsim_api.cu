@@ -1274,7 +1274,7 @@ int fused_planned_t(const qsim_plan* plan, const qsim_gate* gates, int32_t n, co
 // stores the map (one-pass map + gather).
 int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t n, const void* k1,
                          void* k2, uint32_t* perm_out, void* workspace, cudaStream_t st,
-                         bool* used_jit, bool nat_map = false) {
+                         bool* used_jit) {
   *used_jit = false;
   const int e = elem_bytes(plan->dtype);
   {  // workspace == nullptr: the kernel takes its chunks round-robin by CTA
@@ -1285,7 +1285,7 @@ int fused_sigma_dispatch(const qsim_plan* plan, const qsim_gate* gates, int32_t 
     uint64_t blocks = (uint64_t)sm_count() * plan->blocks_per_sm;
     if (blocks > nchunks) blocks = nchunks;
     if (qsim::jit_fused(gl->w, n, plan->M, plan->sigma, plan->fused_chunk_log2, e, k1, k2, perm_out,
-                        workspace, (int)blocks, jit_warps(plan), st, err, nat_map) == 0) {
+                        workspace, (int)blocks, jit_warps(plan), st, err) == 0) {
       ++g_launches;
       *used_jit = true;
       g_last_kernel = "qsim_jit_fused";
@@ -1360,19 +1360,6 @@ int map_gather_impl(const qsim_plan* plan, const qsim_gate* gates, int32_t n, ui
     if ((rc = build_impl(gates, n, M, 0, N, perm, QSIM_WALK_AUTO, st))) return rc;
     g_last_kernel = jit ? "qsim_jit_fused + qsim_jit_build" : "k_fused_sigma + build";
     return QSIM_OK;
-  }
-  if ((plan->flags & QSIM_PLAN_NATMAP) && !plan_natural(plan)) {
-    // one kernel: the planned gather, and per counter tile the natural tile's
-    // map walked a second time and stored in coalesced runs (perm's sequential
-    // writes interleave with the gather's scattered accesses)
-    bool jit = false;
-    const int launches = g_launches;
-    rc = fused_sigma_dispatch(plan, gates, n, k1, k2, perm, workspace, st, &jit, true);
-    if (rc == QSIM_OK && jit) {
-      g_last_kernel = "qsim_jit_fused (natural-order map)";
-      return QSIM_OK;
-    }
-    g_launches = launches;  // no NVRTC: the two-kernel path below
   }
   if (!plan_natural(plan) || M >= 13) {
     const qsim_plan nat = natural_view(plan);
@@ -1737,16 +1724,12 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
   // each sigma variant also as the two-kernel step (planned gather, then the
   // natural-order build): cfg5 14.9 + 2.7 ms against 18.0 ms for one kernel
   // storing perm in plan order (profiles/r02_concurrent_build.txt)
-  // and as one kernel storing the map in natural order (QSIM_PLAN_NATMAP)
   for (size_t i = 0, nc = cands.size(); i < nc; ++i)
     if (!plan_natural(&cands[i]) && !(cands[i].flags & 2u)) {
       qsim_plan p = cands[i];
       p.flags |= QSIM_PLAN_SPLIT;
       cands.push_back(p);
       idx.push_back(idx[i] + 8);
-      p.flags = (p.flags & ~QSIM_PLAN_SPLIT) | QSIM_PLAN_NATMAP;
-      cands.push_back(p);
-      idx.push_back(idx[i] + 16);
     }
   cudaEvent_t a = nullptr, b = nullptr;
   cudaError_t ce;
@@ -1926,8 +1909,7 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
       std::vector<uint8_t> sg(32 * cand_plans.size());
       for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
       qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
-                              jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8,
-                              (cur.flags & QSIM_PLAN_NATMAP) && !(cur.flags & QSIM_PLAN_SPLIT));
+                              jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8);
       if (!step(cand_plans, "stage 5", true)) break;
       swap_rounds(1);
     }
@@ -2071,7 +2053,7 @@ int qsim_jit_check_compile_planned(const qsim_plan* plan, const qsim_gate* gates
   pack_gates(gates, n_gates, false, *gl);
   std::string err;
   if (qsim::jit_check_compile_fused(gl->w, n_gates, plan->M, plan->sigma, elem_bytes(plan->dtype),
-                                    err, (plan->flags & QSIM_PLAN_NATMAP) != 0) != 0) {
+                                    err) != 0) {
     std::snprintf(g_err, sizeof g_err, "jit: %s", err.c_str());
     return QSIM_ECUDA;
   }

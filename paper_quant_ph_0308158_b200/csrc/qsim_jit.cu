@@ -424,7 +424,7 @@ qsim_jit_build(u64 start, u64 end, u64 tb, u64 te, u32* __restrict__ perm_out) {
 // ident: sigma is the identity over all M positions (natural order; the
 // kernel then skips the order tables -- the runtime tail is ignored)
 std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, int elem,
-                         bool from_perm, int warps = 8, bool ident = false, bool nat_map = false) {
+                         bool from_perm, int warps = 8, bool ident = false) {
   std::string s = kPrelude;
   char buf[256];
   std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n"
@@ -528,7 +528,7 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
       const u32 sg = 0u;
       _Pragma("unroll") for (int l = 0; l < 32; ++l) a[l] = __ldcs(perm_out + (ob ^ lt[l] ^ lo));
 )";
-  else if (!nat_map)
+  else
     s += R"(
       if (perm_out) {
         _Pragma("unroll") for (int l = 0; l < 32; ++l) __stcs(perm_out + (ob ^ lt[l] ^ lo), a[l]);
@@ -538,39 +538,6 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
       _Pragma("unroll") for (int h = 0; h < 32; h += QSIM_B) {
         QSIM_T v[QSIM_B];
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l) v[l] = ldg(k1 + a[h + l]);
-)";
-  if (nat_map && !from_perm) {
-    // the map in NATURAL order, in the same launch: counter tile c is also
-    // the natural output tile [c, c + 1024) -- chunks x tiles enumerate every
-    // counter once, so every natural tile once -- walked with identity
-    // planes (lanes on output bits 0..4, the 32 entries on 5..9) and stored
-    // as 128-byte warp runs while this tile's gathers are in flight
-    s += "        if (h == 0) {\n          const u32 nb = (u32)c;\n";
-    const char* pat[5] = {"0xaaaaaaaau", "0xccccccccu", "0xf0f0f0f0u", "0xff00ff00u", "0xffff0000u"};
-    for (int b = 0; b < 32; ++b) {
-      if (b < 5)
-        std::snprintf(buf, sizeof buf, "          u32 p%d = ((lane >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-      else if (b < 10)
-        std::snprintf(buf, sizeof buf, "          u32 p%d = %s;\n", b, pat[b - 5]);
-      else if (b < M)
-        std::snprintf(buf, sizeof buf, "          u32 p%d = ((nb >> %d) & 1u) ? 0xffffffffu : 0u;\n", b, b);
-      else
-        std::snprintf(buf, sizeof buf, "          u32 p%d = 0u;\n", b);
-      s += buf;
-    }
-    s += "          u32 sg = 0u;\n";
-    s += walk_code(w, n, M);
-    s += "          (void)sg;\n          u32 a[32] = {";
-    for (int b = 0; b < 32; ++b) {
-      std::snprintf(buf, sizeof buf, "p%d%s", b, b < 31 ? ", " : "};\n");
-      s += buf;
-    }
-    s += "          QSIM_TS(16, 0x0000ffffu, a) QSIM_TS(8, 0x00ff00ffu, a) QSIM_TS(4, 0x0f0f0f0fu, a)\n";
-    s += "          QSIM_TS(2, 0x33333333u, a) QSIM_TS(1, 0x55555555u, a)\n";
-    s += "          _Pragma(\"unroll\") for (int l = 0; l < 32; ++l) __stcs(perm_out + (nb + 32u * l + lane), a[l]);\n";
-    s += "        }\n";
-  }
-  s += R"(
         _Pragma("unroll") for (int l = 0; l < QSIM_B; ++l)
           stcs(k2 + (ob ^ lt[h + l] ^ lo), negate_if(v[l], (sg >> (h + l)) & 1u));
       }
@@ -1008,9 +975,8 @@ bool sigma_ident(const uint8_t* sigma, int M) {
 }
 
 std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* sigma, int elem, int warps,
-                                 int M, bool nat_map = false) {
+                                 int M) {
   std::vector<uint32_t> keyw(words, words + n);
-  keyw.push_back(nat_map ? 0x6e61u : 0u);
   keyw.push_back(sigma_ident(sigma, M) ? 1u : 0u);
   for (int k = 0; k < 10; ++k) keyw.push_back(sigma[k]);
   keyw.push_back((uint32_t)elem);
@@ -1021,8 +987,7 @@ std::vector<uint32_t> gather_key(const uint32_t* words, int n, const uint8_t* si
 
 int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
-              int warps, cudaStream_t st, std::string& err, bool nat_map) {
-  nat_map = nat_map && perm_out != nullptr && M >= 10;
+              int warps, cudaStream_t st, std::string& err) {
   CUfunction fn = nullptr;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -1031,14 +996,13 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
       err = g_status;
       return -1;
     }
-    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem, warps, M, nat_map);
+    const std::vector<uint32_t> keyw = gather_key(words, n, sigma, elem, warps, M);
     const uint64_t kind = 0x66757365ull;
     const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
     for (const Entry& e : g_cache[key])  // the source is only generated on a cache miss
       if (e.M == M && e.words == keyw) fn = e.fn;
     if (!fn)
-      fn = get_kernel_locked(kind, keyw, M,
-                             fused_source(words, n, M, sigma, elem, false, warps, sigma_ident(sigma, M), nat_map),
+      fn = get_kernel_locked(kind, keyw, M, fused_source(words, n, M, sigma, elem, false, warps, sigma_ident(sigma, M)),
                              "qsim_jit_fused", err);
     if (!fn) return -1;
   }
@@ -1048,8 +1012,7 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
 // NVRTC programs are independent, so several compile at once (the driver
 // calls that load the modules stay under the lock).
 int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
-                      int warps, int threads, bool nat_map) {
-  nat_map = nat_map && M >= 10;
+                      int warps, int threads) {
   const uint64_t kind = 0x66757365ull;
   std::vector<std::vector<uint32_t>> keys;
   std::vector<std::string> srcs;
@@ -1059,14 +1022,14 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
     if (!(g_nvrtc.ok && g_drv.ok)) return -1;
     for (int i = 0; i < count; ++i) {
       const uint8_t* sg = sigmas + 32 * i;
-      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem, warps, M, nat_map);
+      std::vector<uint32_t> keyw = gather_key(words, n, sg, elem, warps, M);
       const uint64_t key = fnv(keyw.data(), (int)keyw.size(), kind);
       bool have = false;
       for (const Entry& e : g_cache[key]) have = have || (e.M == M && e.words == keyw);
       for (const auto& k : keys) have = have || k == keyw;
       if (have) continue;
       keys.push_back(keyw);
-      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps, sigma_ident(sg, M), nat_map));
+      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps, sigma_ident(sg, M)));
     }
   }
   const size_t m = keys.size();
@@ -1263,7 +1226,7 @@ int jit_check_compile_apply(int M, const uint8_t* sigma, int elem, std::string& 
 }
 
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
-                            std::string& err, bool nat_map) {
+                            std::string& err) {
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nvrtc.ok) {
@@ -1271,9 +1234,7 @@ int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* 
     return -1;
   }
   std::vector<char> cubin;
-  return compile_cubin_locked(fused_source(words, n, M, sigma, elem, false, 8, sigma_ident(sigma, M),
-                                           nat_map && M >= 10),
-                              cubin, err) ? 0 : -1;
+  return compile_cubin_locked(fused_source(words, n, M, sigma, elem, false, 8, sigma_ident(sigma, M)), cubin, err) ? 0 : -1;
 }
 
 }  // namespace qsim

@@ -26,18 +26,16 @@ int jit_build(const uint32_t* words, int n, int M, const uint8_t* J, int L, uint
 // compiled for (circuit, sigma[0..9], element size, warps per CTA: 8 or 16,
 // tiles of 1024 counters striding by it); sigma[10..] is a kernel
 // parameter.  If perm_out != null the map is stored as well (one-pass map +
-// gather; nat_map: perm_out is written in NATURAL order by a second,
-// identity-plane walk of each counter tile in the same launch, instead of in
-// plan order).  ticket: device scratch (reset on st).  Returns 0 or -1 with err.
+// gather).  ticket: device scratch (reset on st).  Returns 0 or -1 with err.
 int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_t chunk_log2,
               int elem, const void* k1, void* k2, uint32_t* perm_out, void* ticket, int blocks,
-              int warps, cudaStream_t st, std::string& err, bool nat_map = false);
+              int warps, cudaStream_t st, std::string& err);
 // Compile (NVRTC, on up to `threads` host threads at once) and cache the fused
 // kernels of `count` orders (32 bytes each, sigmas[32 * i ..]) that are not
 // cached yet, so that later jit_fused calls find them.  Returns the number
 // compiled, or -1 if NVRTC is unavailable.
 int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
-                      int warps, int threads, bool nat_map = false);
+                      int warps, int threads);
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
 // k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
 // qsim::Qubits (passed by value as a kernel parameter).
@@ -52,8 +50,7 @@ int jit_kron(const uint32_t* words, int n, int M, const void* qubits_struct, siz
 int jit_check_compile_kron(const uint32_t* words, int n, int M, int elem, int gbits, int ngroups,
                            const uint8_t* pos, const uint8_t* J, int L, int nv, std::string& err);
 int jit_check_compile_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, int elem,
-                            std::string& err,
-                            bool nat_map = false);
+                            std::string& err);
 // Planned apply from a materialised map (NVRTC; sigma order, the fused
 // kernel's batching).  Returns 0 or -1 with err.
 int jit_apply(int M, const uint8_t* sigma, uint32_t chunk_log2, int elem, const uint32_t* perm,

@@ -194,12 +194,10 @@ def test_jit_fused_source_compiles_without_gpu(q):
         cfg = wl.CONFIGS[name]
         g = np.ascontiguousarray(cfg.gates())
         plan = q.plan_create(g, cfg.M, cfg.dtype)
-        for flags in (plan.flags, plan.flags | q.PLAN_NATMAP):   # + the natural-order map variant
-            plan.flags = flags
-            rc = L.qsim_jit_check_compile_planned(ctypes.byref(plan), g.ctypes.data, len(g))
-            if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
-                pytest.skip("NVRTC not available here")
-            assert rc == q.OK, L.qsim_last_error().decode()
+        rc = L.qsim_jit_check_compile_planned(ctypes.byref(plan), g.ctypes.data, len(g))
+        if rc != q.OK and "libnvrtc" in L.qsim_last_error().decode():
+            pytest.skip("NVRTC not available here")
+        assert rc == q.OK, L.qsim_last_error().decode()
 
 
 def test_jit_kron_source_compiles_without_gpu(q):

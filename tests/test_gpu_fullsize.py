@@ -132,18 +132,14 @@ def _run_config(q, name):
     check_perm("qsim_map_gather_planned " + label)
     check_k2("qsim_map_gather_planned " + label)
     if not (tuned.flags & 1):
-        # the tuned order in the other map + gather forms: one kernel storing perm
-        # in plan order, gather then natural-order build (QSIM_PLAN_SPLIT), one
-        # kernel storing perm in natural order (QSIM_PLAN_NATMAP)
-        for form in (0, q.PLAN_SPLIT, q.PLAN_NATMAP):
-            other = q.Plan.from_buffer_copy(tuned)
-            other.flags = (other.flags & ~(q.PLAN_SPLIT | q.PLAN_NATMAP)) | form
-            if other.flags == tuned.flags:
-                continue
-            perm.fill_(-1)
-            q.map_gather_planned(other, gates, perm, k1, k2, ws)
-            check_perm(f"qsim_map_gather_planned (flags {other.flags}) " + label)
-            check_k2(f"qsim_map_gather_planned (flags {other.flags}) " + label)
+        # the tuned order in the other map + gather mode (one kernel storing perm
+        # in plan order <-> gather then natural-order build, QSIM_PLAN_SPLIT)
+        other = q.Plan.from_buffer_copy(tuned)
+        other.flags ^= q.PLAN_SPLIT
+        perm.fill_(-1)
+        q.map_gather_planned(other, gates, perm, k1, k2, ws)
+        check_perm(f"qsim_map_gather_planned (flags {other.flags}) " + label)
+        check_k2(f"qsim_map_gather_planned (flags {other.flags}) " + label)
     q.run_fused_planned(tuned, gates, k1, k2, ws)
     check_k2("qsim_run_fused_planned " + label)
     q.apply_map_planned(tuned, perm, k1, k2, ws)

@@ -44,9 +44,12 @@ tune_s = time.time() - t0
 ref_perm, ref_k2 = perm.clone(), k2.clone()
 
 plans = {"tuned": plan}
-for nm, form in (("one_kernel", 0), ("split", q.PLAN_SPLIT), ("natmap", q.PLAN_NATMAP)):
+# QSIM_PLAN_NATMAP (8) existed only in commit dd6f732 (measured slower, removed)
+NATMAP = getattr(q, "PLAN_NATMAP", None)
+forms = (("one_kernel", 0), ("split", q.PLAN_SPLIT)) + ((("natmap", NATMAP),) if NATMAP else ())
+for nm, form in forms:
     o = q.Plan.from_buffer_copy(plan)
-    o.flags = (o.flags & ~(q.PLAN_SPLIT | q.PLAN_NATMAP)) | form
+    o.flags = (o.flags & ~(q.PLAN_SPLIT | (NATMAP or 0))) | form
     plans[nm + "(same order)"] = o
 rec_path = os.path.join(ROOT, "profiles", "r02_tuned_plan_cfg5_s6.json")
 if cfg is wl.CONFIGS["cfg5"] and os.path.exists(rec_path):
