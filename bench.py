@@ -735,8 +735,11 @@ def run_qsim(args):
                              "fetched by L2 as separate 32-B sectors unless a line's sectors share "
                              "one warp instruction (DESIGN.md section 6, profiles/r01_mb_window.jsonl)"},
         "modes": {
-            "map_gather_1pass": {"ms": mg_ms, "GBps": achieved, "entries_per_s": N / (mg_ms * 1e-3),
-                                 "launches_per_step": launches_mg / args.steps},
+            "map_gather": {"ms": mg_ms, "GBps": achieved, "entries_per_s": N / (mg_ms * 1e-3),
+                           "launches_per_step": launches_mg / args.steps,
+                           "form": ("two kernels: planned gather, natural-order build (QSIM_PLAN_SPLIT)"
+                                    if split else "one kernel: perm stored in plan order + gather"),
+                           "kernel": kern_name_mg},
             "two_call": {"ms": ms_mat / args.steps, "entries_per_s": N / (ms_mat / args.steps * 1e-3),
                          "calls": "qsim_build_map + qsim_apply_map_planned"},
             "build_map": {"ms": build_ms, "GBps": gbps(bytes_build, build_ms),
