@@ -285,7 +285,11 @@ int qsim_plan_tune(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uin
  * Any other effort: QSIM_EINVAL (nothing runs).  The kernels compiled for
  * the candidates stay in the process's JIT cache (PATIENT at M = 32: about
  * 500 modules of tens of KB of device code each).                          */
-enum { QSIM_TUNE_MEASURE = 1, QSIM_TUNE_PATIENT = 2 };
+enum { QSIM_TUNE_MEASURE = 1, QSIM_TUNE_PATIENT = 2,
+       QSIM_TUNE_APPLY = 0x100 /* OR-ed into effort: tune qsim_apply_map_planned
+                                  instead -- perm is built first (the map of gates),
+                                  the trials time the planned apply on it (k2
+                                  written); the two-kernel form is not tried   */ };
 int qsim_plan_tune_ex(qsim_plan *plan, const qsim_gate *gates, int32_t n_gates, uint32_t *perm,
                       const void *k1, void *k2, void *workspace, void *stream, int32_t effort,
                       int32_t *chosen);

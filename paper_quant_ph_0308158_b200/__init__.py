@@ -34,6 +34,7 @@ NOT, CNOT, CCNOT, Z, CZ, CCZ, SWAP = 0, 1, 2, 3, 4, 5, 6
 MAX_GATES = 4096
 MATERIALISED, FUSED = 0, 1
 TUNE_MEASURE, TUNE_PATIENT = 1, 2      # qsim_plan_tune_ex search effort
+TUNE_APPLY = 0x100                     # | effort: tune the planned apply (perm built first)
 
 
 class QsimError(RuntimeError):

@@ -1672,6 +1672,10 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
                       int32_t* chosen) {
   g_launches = 0;
   if (!plan || !workspace || !aligned16(workspace)) return QSIM_EINVAL;
+  // QSIM_TUNE_APPLY: the trials time qsim_apply_map_planned on the map in perm
+  // (built once here) instead of the map + gather step
+  const bool for_apply = (effort & QSIM_TUNE_APPLY) != 0;
+  effort &= ~QSIM_TUNE_APPLY;
   if (effort != QSIM_TUNE_MEASURE && effort != QSIM_TUNE_PATIENT) return QSIM_EINVAL;
   int rc = plan_validate(plan);
   if (rc) return rc;
@@ -1687,6 +1691,8 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
       return QSIM_EALIAS;
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (for_apply && (rc = build_impl(gates, n_gates, plan->M, 0, 1ull << plan->M, perm, QSIM_WALK_AUTO, st)))
+    return rc;
   // candidates: the default rule, the full cover, each with lanes on output bits 0..4,
   // and smaller full covers
   const PlanOpts base;
@@ -1724,7 +1730,7 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
   // each sigma variant also as the two-kernel step (planned gather, then the
   // natural-order build): cfg5 14.9 + 2.7 ms against 18.0 ms for one kernel
   // storing perm in plan order (profiles/r02_concurrent_build.txt)
-  for (size_t i = 0, nc = cands.size(); i < nc; ++i)
+  for (size_t i = 0, nc = for_apply ? 0 : cands.size(); i < nc; ++i)
     if (!plan_natural(&cands[i]) && !(cands[i].flags & 2u)) {
       qsim_plan p = cands[i];
       p.flags |= QSIM_PLAN_SPLIT;
@@ -1739,12 +1745,16 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
   }
   // best of `reps` timed map + gather calls with plan p (one untimed call
   // first when `warm`: it compiles the kernel)
+  auto trial = [&](const qsim_plan& p) -> int {
+    return for_apply ? apply_planned_impl(&p, perm, k1, k2, workspace, st)
+                     : map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st);
+  };
   auto time_plan = [&](const qsim_plan& p, bool warm, int reps) -> float {
-    if (warm && (rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st))) return 1e30f;
+    if (warm && (rc = trial(p))) return 1e30f;
     float t_best = 1e30f;
     for (int r = 0; r < reps && rc == QSIM_OK; ++r) {
       cudaEventRecord(a, st);
-      rc = map_gather_impl(&p, gates, n_gates, perm, k1, k2, workspace, st);
+      rc = trial(p);
       cudaEventRecord(b, st);
       if ((ce = cudaEventSynchronize(b)) != cudaSuccess) {
         rc = cuda_fail(ce, "tune sync");
@@ -1908,7 +1918,8 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
         }
       std::vector<uint8_t> sg(32 * cand_plans.size());
       for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
-      qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
+      if (!for_apply)  // (the apply kernels compile on their first, untimed trial)
+        qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
                               jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8);
       if (!step(cand_plans, "stage 5", true)) break;
       swap_rounds(1);

@@ -144,6 +144,15 @@ def _run_config(q, name):
     check_k2("qsim_run_fused_planned " + label)
     q.apply_map_planned(tuned, perm, k1, k2, ws)
     check_k2("qsim_apply_map_planned " + label)
+    # the plan bench.py's two-call mode times (tuned for the planned apply)
+    ap = q.plan_create(gates, M, cfg.dtype)
+    if not (ap.flags & 1):
+        perm.fill_(-1)
+        q.plan_tune(ap, gates, perm, k1, k2, ws, effort=q.TUNE_MEASURE | q.TUNE_APPLY)
+        check_perm("qsim_plan_tune_ex(APPLY) map")
+        k2.fill_(0xA5)
+        q.apply_map_planned(ap, perm, k1, k2, ws)
+        check_k2(f"qsim_apply_map_planned (apply-tuned plan, sigma {list(ap.sigma)[:13]})")
     # end to end from host buffers (the e2e leg of bench.py)
     k2_host = np.empty_like(k1_host)
     for mode in (q.MATERIALISED, q.FUSED):

@@ -551,7 +551,8 @@ def test_local_tiles_staged_in_shared_memory(q, M, dtype):
     assert out3.cpu().numpy().tobytes() == oracle.apply_map(oracle.build_map(far, M), k1).tobytes()
 
 
-@pytest.mark.parametrize("effort", [None, 1])   # qsim_plan_tune / qsim_plan_tune_ex MEASURE
+# qsim_plan_tune / qsim_plan_tune_ex MEASURE / MEASURE for the planned apply
+@pytest.mark.parametrize("effort", [None, 1, 0x101])
 def test_plan_tune_keeps_a_valid_plan(q, effort):
     """qsim_plan_tune measures plan variants and keeps one: the result of its
     own runs and of the tuned plan afterwards equal the oracle's bytes."""
