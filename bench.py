@@ -371,12 +371,12 @@ def run_qsim(args):
     tuned = q.plan_tune(plan, gates, perm, k1, k2, ws, stream=stream) if not (plan.flags & 1) else -1
     t_tune = time.perf_counter() - t_tune
     # the planned apply (two-call mode) gets its own measured order: it reads
-    # perm in plan order instead of writing it (stages 1-3, about 10 s)
+    # perm in plan order instead of writing it (all stages, about 60 s)
     t_tune_ap = time.perf_counter()
     plan_ap = q.plan_create(gates, M, cfg.dtype)
     if not (plan_ap.flags & 1):
         q.plan_tune(plan_ap, gates, perm, k1, k2, ws, stream=stream,
-                    effort=q.TUNE_MEASURE | q.TUNE_APPLY)
+                    effort=q.TUNE_PATIENT | q.TUNE_APPLY)
     t_tune_ap = time.perf_counter() - t_tune_ap
     torch.cuda.synchronize()
     t_setup = time.perf_counter() - t_setup
@@ -806,7 +806,7 @@ def run_qsim(args):
         "plan_apply": {"tune_seconds": t_tune_ap, "sigma": list(plan_ap.sigma)[:M],
                        "chunk_log2": plan_ap.chunk_log2, "blocks_per_sm": plan_ap.blocks_per_sm,
                        "note": "the two-call mode's qsim_apply_map_planned uses its own plan, "
-                               "qsim_plan_tune_ex(QSIM_TUNE_MEASURE | QSIM_TUNE_APPLY)"},
+                               "qsim_plan_tune_ex(QSIM_TUNE_PATIENT | QSIM_TUNE_APPLY)"},
         "plan": {"seconds": t_plan, "tune_seconds": t_tune, "tuned_variant": tuned,
                  "sigma": list(plan.sigma)[:M], "chunk_log2": plan.chunk_log2,
                  "fused_chunk_log2": plan.fused_chunk_log2, "blocks_per_sm": plan.blocks_per_sm,

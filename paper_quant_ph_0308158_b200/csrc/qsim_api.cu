@@ -1918,9 +1918,8 @@ int qsim_plan_tune_ex(qsim_plan* plan, const qsim_gate* gates, int32_t n_gates, 
         }
       std::vector<uint8_t> sg(32 * cand_plans.size());
       for (size_t c = 0; c < cand_plans.size(); ++c) std::memcpy(&sg[32 * c], cand_plans[c].sigma, 32);
-      if (!for_apply)  // (the apply kernels compile on their first, untimed trial)
-        qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
-                              jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8);
+      qsim::jit_fused_prepare(gl->w, n_gates, cur.M, sg.data(), (int)cand_plans.size(), elem_bytes(cur.dtype),
+                              jit_warps(&cur), hw ? (int)std::min(hw, 32u) : 8, for_apply);
       if (!step(cand_plans, "stage 5", true)) break;
       swap_rounds(1);
     }

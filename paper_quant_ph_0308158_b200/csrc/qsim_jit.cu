@@ -1012,8 +1012,13 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
 // NVRTC programs are independent, so several compile at once (the driver
 // calls that load the modules stay under the lock).
 int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
-                      int warps, int threads) {
-  const uint64_t kind = 0x66757365ull;
+                      int warps, int threads, bool apply) {
+  // apply: the planned-apply kernels of those orders (jit_apply's key / source)
+  const uint64_t kind = apply ? 0x6170706c79ull : 0x66757365ull;
+  if (apply) {
+    words = nullptr;
+    n = 0;
+  }
   std::vector<std::vector<uint32_t>> keys;
   std::vector<std::string> srcs;
   {
@@ -1029,7 +1034,7 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
       for (const auto& k : keys) have = have || k == keyw;
       if (have) continue;
       keys.push_back(keyw);
-      srcs.push_back(fused_source(words, n, M, sg, elem, false, warps, sigma_ident(sg, M)));
+      srcs.push_back(fused_source(words, n, M, sg, elem, apply, warps, sigma_ident(sg, M)));
     }
   }
   const size_t m = keys.size();
@@ -1058,7 +1063,7 @@ int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas
     CUmodule mod = nullptr;
     CUfunction fn = nullptr;
     if (g_drv.load(&mod, cubins[i].data()) != CUDA_SUCCESS ||
-        g_drv.getfn(&fn, mod, "qsim_jit_fused") != CUDA_SUCCESS)
+        g_drv.getfn(&fn, mod, apply ? "qsim_jit_apply" : "qsim_jit_fused") != CUDA_SUCCESS)
       continue;
     g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 3);
     const uint64_t key = fnv(keys[i].data(), (int)keys[i].size(), kind);

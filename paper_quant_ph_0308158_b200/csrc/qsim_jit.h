@@ -35,7 +35,7 @@ int jit_fused(const uint32_t* words, int n, int M, const uint8_t* sigma, uint32_
 // cached yet, so that later jit_fused calls find them.  Returns the number
 // compiled, or -1 if NVRTC is unavailable.
 int jit_fused_prepare(const uint32_t* words, int n, int M, const uint8_t* sigmas, int count, int elem,
-                      int warps, int threads);
+                      int warps, int threads, bool apply = false);
 // Natural-order fused walk with the input generated on the fly (Appendix 1):
 // k2_out[r] = k1(perm(start + r)); qubits_struct points to a host
 // qsim::Qubits (passed by value as a kernel parameter).
