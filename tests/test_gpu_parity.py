@@ -470,11 +470,11 @@ def test_structured_circuits(q, M):
                 assert np.array_equal(_perm_np(pm), perm_ref), (name, dtype, natural)
 
 
-@pytest.mark.parametrize("M,natural", [(16, 1), (16, 0), (20, 1)])
+@pytest.mark.parametrize("M,natural", [(16, 1), (16, 0), (20, 1), (18, 4)])   # 4: two-kernel step
 def test_graphs_replay_planned_calls(q, M, natural):
     """CUDA graphs of repeated planned calls (launch-bound small states):
     replaying the recorded steps gives the oracle's bytes, for map + gather,
-    fused and apply, natural and plan order."""
+    fused and apply, natural and plan order, one- and two-kernel map + gather."""
     gates = wl.random_gates(64, M, 1700 + M)
     k1 = wl.make_state(wl.StateSpec(M, "c64", wl.GAUSS, 4 + M))
     perm_ref = oracle.build_map(gates, M)
@@ -498,6 +498,13 @@ def test_graphs_replay_planned_calls(q, M, natural):
         if call == q.GRAPH_MAP_GATHER:
             assert np.array_equal(_perm_np(pm), perm_ref)
         g.close()
+    if natural & q.PLAN_SPLIT:                            # no workspace: round-robin chunks
+        out, pm2 = torch.empty_like(k1_d), _new_perm(1 << M)
+        q.map_gather_planned(plan, gates, pm2, k1_d, out, None)
+        assert q.last_launch_count() == 2
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == ref.tobytes()
+        assert np.array_equal(_perm_np(pm2), perm_ref)
 
 
 @pytest.mark.parametrize("dtype,M", [("c64", 13), ("c64", 17), ("c64", 22), ("c128", 12),
