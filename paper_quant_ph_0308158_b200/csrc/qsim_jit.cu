@@ -428,8 +428,9 @@ std::string fused_source(const uint32_t* w, int n, int M, const uint8_t* sigma, 
   std::string s = kPrelude;
   char buf[256];
   std::snprintf(buf, sizeof buf, "#define QSIM_T %s\n#define QSIM_M %d\n#define QSIM_B %d\n#define QSIM_W %du\n"
-                "#define QSIM_IDENT %d\n",
-                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16, warps, ident ? 1 : 0);
+                "#define QSIM_IDENT %d\n#define QSIM_TICKET_AHEAD %d\n",
+                elem == 8 ? "uint2" : "uint4", M, elem == 8 ? 32 : 16, warps, ident ? 1 : 0,
+                from_perm ? 0 : 1);  // ticket ahead: gather -1.5 %, apply +1.5 % (r02_ticket_ahead_ab.json)
   s += buf;
   s += from_perm ? "#define QSIM_KNAME qsim_jit_apply\n" : "#define QSIM_KNAME qsim_jit_fused\n";
   s += R"(
@@ -437,7 +438,7 @@ struct Sigma { unsigned char s[32]; };
 extern "C" __global__ void __launch_bounds__(32 * QSIM_W)
 QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
            QSIM_T* __restrict__ k2, u32* __restrict__ perm_out, const Sigma sig) {
-  __shared__ u64 s_chunk;
+  __shared__ u64 s_chunk[2];
 #if QSIM_IDENT   // natural order: output = counter, no tables
   (void)sig;
 #else
@@ -456,13 +457,24 @@ QSIM_KNAME(u64 N, u32 chunk_log2, u64* ticket, const QSIM_T* __restrict__ k1,
   const u32 tiles = 1u << (chunk_log2 - 10);
   // chunks in counter order: from a device ticket (dynamic), or without a
   // workspace round-robin by CTA (static; the front still moves in order)
+#if QSIM_TICKET_AHEAD
+  // the ticket of the next chunk is taken while this one is worked on (one
+  // barrier per chunk; the atomic's round trip is not waited for by the CTA)
+  if (ticket && threadIdx.x == 0) s_chunk[0] = atomicAdd(ticket, 1ull);
+#endif
   for (u64 it = 0;; ++it) {
     u64 ch;
     if (ticket) {
+#if QSIM_TICKET_AHEAD
+      __syncthreads();  // chunk it-1 done by every warp, slot it&1 written
+      ch = s_chunk[it & 1];
+      if (threadIdx.x == 0 && ch < nchunks) s_chunk[(it + 1) & 1] = atomicAdd(ticket, 1ull);
+#else
       __syncthreads();
-      if (threadIdx.x == 0) s_chunk = atomicAdd(ticket, 1ull);
+      if (threadIdx.x == 0) s_chunk[0] = atomicAdd(ticket, 1ull);
       __syncthreads();
-      ch = s_chunk;
+      ch = s_chunk[0];
+#endif
     } else {
       ch = (u64)blockIdx.x + it * gridDim.x;
     }
