@@ -57,6 +57,7 @@ for nm, form in forms:
 
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 STEPS = int(os.environ.get("SC_STEPS", "20"))
+SWITCH = os.environ.get("AB_SWITCH", "QSIM_TICKET_AHEAD")   # a generated-source A/B switch
 calls = {
     "map_gather": lambda: q.map_gather_planned(plan, gates, perm, k1, k2, ws),
     "fused": lambda: q.run_fused_planned(plan, gates, k1, k2, ws),
@@ -78,18 +79,18 @@ def loop(fn):
 
 ok = {}
 for mode in ("0", "1"):                      # compile both variants, check bytes
-    os.environ["QSIM_TICKET_AHEAD"] = mode
+    os.environ[SWITCH] = mode
     perm.fill_(-1)
     k2.fill_(0)
     calls["map_gather"]()
     torch.cuda.synchronize()
     ok[mode] = bool(torch.equal(perm, ref_perm) and torch.equal(k2, ref_k2))
-res = {f"{c}/ahead={m}": [] for c in calls for m in ("0", "1")}
+res = {f"{c}/{SWITCH}={m}": [] for c in calls for m in ("0", "1")}
 for _ in range(int(os.environ.get("SC_REPS", "4"))):
     for c, fn in calls.items():
         for m in ("0", "1"):
-            os.environ["QSIM_TICKET_AHEAD"] = m
-            res[f"{c}/ahead={m}"].append(loop(fn))
+            os.environ[SWITCH] = m
+            res[f"{c}/{SWITCH}={m}"].append(loop(fn))
 print(json.dumps({"variant": variant, "flags": plan.flags, "bytes_equal": ok, "steps_per_loop": STEPS,
                   "ms_per_step_each_loop": res,
                   "ms_mean": {n: sum(v) / len(v) for n, v in res.items()}}))
