@@ -1,5 +1,6 @@
-"""Experiment (sustained) -- chunk-ticket prefetch A/B.  The QSIM_TICKET_AHEAD
-switch it toggles existed only in the experiment build (a generated-source
+"""Experiment (sustained) -- chunk-ticket prefetch A/B.  AB_SWITCH names the
+generated-source switch (QSIM_TICKET_AHEAD, QSIM_TILE_DYN, QSIM_GATHER_PIPE);
+each existed only in its experiment build. QSIM_TICKET_AHEAD (a generated-source
 macro, now fixed: on for the gathers, off for the apply); result in
 profiles/r02_ticket_ahead_ab.json.  (Header of split_sustained.py follows.) cfg5 map + gather as one kernel (perm stored in plan order) vs
 two kernels (QSIM_PLAN_SPLIT: the planned gather, then the natural-order
