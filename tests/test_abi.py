@@ -360,7 +360,7 @@ def test_plan_tune_validation(q):
     plan2 = q.plan_create(ph, 16, "c64")
     assert L.qsim_plan_tune(ctypes.byref(plan2), ph.ctypes.data, 1, FAKE, FAKE * 4, FAKE * 8,
                             FAKE * 16, None, None) == q.EINVAL                # phase circuit
-    for effort in (0, 3, -1):                                                 # no such effort
+    for effort in (0, 3, -1, q.TUNE_APPLY, q.TUNE_APPLY | 3, 0x200 | q.TUNE_MEASURE):  # no such effort
         assert L.qsim_plan_tune_ex(ctypes.byref(plan), g.ctypes.data, 20, FAKE, FAKE * 4, FAKE * 8,
                                    FAKE * 16, None, effort, ctypes.byref(chosen)) == q.EINVAL
     assert L.qsim_plan_tune_ex(ctypes.byref(plan), g.ctypes.data, 20, FAKE, FAKE * 4, FAKE * 8,
@@ -400,3 +400,13 @@ def test_binding_wrappers_reach_their_checks(q):
     for c in calls:
         with pytest.raises(ValueError):
             c()
+
+
+def test_header_constants_match_the_binding(q):
+    """The plan flag and tuner-effort values the binding uses are the header's."""
+    h = open(os.path.join(ROOT, "include", "qsim.h")).read()
+    assert int(re.search(r"#define QSIM_PLAN_SPLIT (\d+)u", h).group(1)) == q.PLAN_SPLIT
+    assert int(re.search(r"#define QSIM_WORKSPACE_BYTES (\d+)", h).group(1)) == q.WORKSPACE_BYTES
+    assert int(re.search(r"QSIM_TUNE_MEASURE = (\d+)", h).group(1)) == q.TUNE_MEASURE
+    assert int(re.search(r"QSIM_TUNE_PATIENT = (\d+)", h).group(1)) == q.TUNE_PATIENT
+    assert int(re.search(r"QSIM_TUNE_APPLY = (0x[0-9a-f]+)", h).group(1), 16) == q.TUNE_APPLY
