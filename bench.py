@@ -8,7 +8,10 @@ NOT/CNOT/CCNOT gates, seed 4, complex64 Gaussian normalised state).
 One step = the whole hot path over the 2^32-entry state, materialised:
 qsim_map_gather_planned computes the composite map perm (uint32, stored:
 "save information about the unitary matrix") and the state transform
-k2[i] = k1[perm[i]] in one kernel compiled for the circuit.  The
+k2[i] = k1[perm[i]] with kernels compiled for the circuit -- one
+kernel storing perm in plan order, or (plan flag QSIM_PLAN_SPLIT, what
+qsim_plan_tune keeps on cfg5) the planned gather then the natural-order
+build; the plan is measured once, outside the timed region.  The
 two-call form (qsim_build_map then qsim_apply_map_planned) and the fused
 mode (qsim_run_fused_planned: the map recomputed, no perm) are timed in
 their own loops and reported under "modes".  Inputs are larger than L2
